@@ -1,0 +1,212 @@
+// Thin extern "C" wrapper over the *unmodified* reference library (qcsim,
+// /root/reference/proj/src/*.cpp), compiled by oracle/Makefile into
+// oracle/_ref/libqcsref.so.  TEST INFRASTRUCTURE ONLY: it is the checker that
+// pins oracle/qcs_oracle.c and generates tests/golden/, and bench.py's
+// `--impl reference` arm times it.  Nothing in the product path loads it.
+//
+// Every entry point calls only public reference API:
+//   compress / decompress_into / serialize_block / parse_block  (codec.hpp:80-105)
+//   parse_circuit / print_circuit / build_qft / build_grover / build_random
+//                                                            (circuit.hpp:47-70)
+//   run_program / CompressedState::{to_amplitudes, compressed_bytes,
+//   min_stride_ratio, norm_sq_tracked, stride_scale}           (aalc.hpp:110-209)
+//   run_dense / fidelity                                        (dense.hpp)
+//   emit_csv                                                    (metrics.hpp:66)
+
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "qcs/aalc.hpp"
+#include "qcs/circuit.hpp"
+#include "qcs/codec.hpp"
+#include "qcs/dense.hpp"
+#include "qcs/metrics.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg)
+{
+    g_err = msg;
+    return code;
+}
+
+// Return-code convention shared with include/qcs_b200.h (QCS_E_*).
+int classify(const std::exception& e)
+{
+    if (auto* c = dynamic_cast<const qcs::CodecError*>(&e)) {
+        switch (c->kind()) {
+            case qcs::CodecError::Kind::bad_magic: return 10;
+            case qcs::CodecError::Kind::truncated: return 11;
+            case qcs::CodecError::Kind::unknown_codec: return 12;
+            case qcs::CodecError::Kind::bad_value: return 13;
+        }
+    }
+    if (dynamic_cast<const std::out_of_range*>(&e)) return 3;
+    if (dynamic_cast<const std::invalid_argument*>(&e)) return 2;
+    return 1;
+}
+
+int copy_text(const std::string& s, char* out, std::uint64_t cap, std::uint64_t* len)
+{
+    if (len) *len = s.size();
+    if (!out) return 0;
+    if (s.size() + 1 > cap) return fail(4, "output buffer too small");
+    std::memcpy(out, s.data(), s.size());
+    out[s.size()] = '\0';
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+int ref_max_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+// Serialized QCS1 block (29-byte header + payload) of compress(x, delta).
+int ref_codec_compress(const double* x, std::uint64_t n, double delta,
+                       std::uint8_t* out, std::uint64_t cap, std::uint64_t* len)
+{
+    try {
+        const qcs::CompressedBlock b =
+            qcs::compress(std::span<const double>(x, n), qcs::ErrorBound(delta));
+        const std::vector<std::uint8_t> bytes = qcs::serialize_block(b);
+        *len = bytes.size();
+        if (out) {
+            if (bytes.size() > cap) return fail(4, "output buffer too small");
+            std::memcpy(out, bytes.data(), bytes.size());
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(classify(e), e.what());
+    }
+}
+
+// Parses one serialized block and decodes it into out[n].
+int ref_codec_decompress(const std::uint8_t* blk, std::uint64_t len, double* out,
+                         std::uint64_t n)
+{
+    try {
+        std::size_t off = 0;
+        const qcs::CompressedBlock b =
+            qcs::parse_block(std::span<const std::uint8_t>(blk, len), off);
+        if (b.scalar_count != n) return fail(2, "scalar count mismatch");
+        qcs::decompress_into(b, std::span<double>(out, n));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(classify(e), e.what());
+    }
+}
+
+// Text of a reference-built circuit: kind 0 = build_qft(n),
+// 1 = build_grover(n, arg, iters), 2 = build_random(n, iters, arg).
+int ref_builtin_circuit(int kind, int n, std::uint64_t arg, int iters, char* out,
+                        std::uint64_t cap, std::uint64_t* len)
+{
+    try {
+        qcs::CircuitProgram p;
+        if (kind == 0) p = qcs::build_qft(n);
+        else if (kind == 1) p = qcs::build_grover(n, arg, iters);
+        else p = qcs::build_random(n, iters, arg);
+        return copy_text(qcs::print_circuit(p), out, cap, len);
+    } catch (const std::exception& e) {
+        return fail(classify(e), e.what());
+    }
+}
+
+// run_program on a circuit given in the reference text format.
+//   stop_after < 0 runs the whole program.
+//   csv (optional) receives emit_csv(records).
+//   amps (optional) receives to_amplitudes() as interleaved re/im doubles.
+//   summary[10]: gate-loop ns, amplitude updates (sum bytes_before/16),
+//     init_min_ratio, threshold_violations, compressed_bytes,
+//     min_stride_ratio, norm_sq_tracked, overall_min_ratio, n_records,
+//     wall ns of run_program (incl. basis_state).
+int ref_run(const char* circuit_text, int stride_bits, std::uint64_t basis,
+            const double* ladder, int n_levels, double theta, int workers,
+            std::int64_t stop_after, char* csv, std::uint64_t csv_cap,
+            std::uint64_t* csv_len, double* amps, double* summary)
+{
+    try {
+        const qcs::CircuitProgram p = qcs::parse_circuit(circuit_text);
+        const qcs::StateGeometry geom = qcs::StateGeometry::make(p.n_qubits, stride_bits);
+        const qcs::ErrorBoundLadder lad = qcs::ErrorBoundLadder::make(
+            std::vector<double>(ladder, ladder + n_levels));
+        qcs::RunOptions opt;
+        opt.basis = basis;
+        opt.workers = workers;
+        if (stop_after >= 0) opt.stop_after = static_cast<std::size_t>(stop_after);
+        const auto t0 = std::chrono::steady_clock::now();
+        const qcs::RunResult r =
+            qcs::run_program(p, lad, qcs::RatioThreshold(theta), geom, opt);
+        const auto t1 = std::chrono::steady_clock::now();
+        std::uint64_t loop_ns = 0, upd = 0;
+        for (const qcs::GateRecord& g : r.metrics.records) {
+            loop_ns += g.elapsed_ns;
+            upd += g.bytes_before / 16;
+        }
+        if (summary) {
+            summary[0] = static_cast<double>(loop_ns);
+            summary[1] = static_cast<double>(upd);
+            summary[2] = r.metrics.init_min_ratio;
+            summary[3] = static_cast<double>(r.metrics.threshold_violations);
+            summary[4] = static_cast<double>(r.state.compressed_bytes());
+            summary[5] = r.state.min_stride_ratio();
+            summary[6] = r.state.norm_sq_tracked();
+            summary[7] = r.metrics.overall_min_ratio();
+            summary[8] = static_cast<double>(r.metrics.records.size());
+            summary[9] = static_cast<double>(
+                std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
+        }
+        if (amps) {
+            const std::vector<qcs::Amplitude> a = r.state.to_amplitudes();
+            for (std::size_t i = 0; i < a.size(); ++i) {
+                amps[2 * i] = a[i].real();
+                amps[2 * i + 1] = a[i].imag();
+            }
+        }
+        if (csv || csv_len) {
+            int rc = copy_text(qcs::emit_csv(r.metrics.records), csv, csv_cap, csv_len);
+            if (rc) return rc;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(classify(e), e.what());
+    }
+}
+
+// Dense serial simulation (run_dense) of the circuit; amps interleaved re/im.
+int ref_dense(const char* circuit_text, std::uint64_t basis, double* amps)
+{
+    try {
+        const qcs::CircuitProgram p = qcs::parse_circuit(circuit_text);
+        const qcs::DenseState d = qcs::run_dense(p, basis, 30);
+        for (std::size_t i = 0; i < d.amplitudes.size(); ++i) {
+            amps[2 * i] = d.amplitudes[i].real();
+            amps[2 * i + 1] = d.amplitudes[i].imag();
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(classify(e), e.what());
+    }
+}
+
+}  // extern "C"
