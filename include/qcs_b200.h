@@ -1,0 +1,151 @@
+/*
+ * qcs_b200.h — C-ABI of the B200-native compressed-state gate engine.
+ *
+ * Drop-in boundary for the reference's per-gate hot path
+ * (/root/reference/proj, C++ API, no C-ABI of its own).
+ * Every entry point names the reference interface it replaces.  Plain
+ * pointers and sizes only; all buffers are HOST memory unless a name says
+ * otherwise.  Calls are synchronous at the ABI (stream-ordered inside) and
+ * return 0 or a QCS_E_* code; qcs_last_error() gives the message.  A state
+ * is not thread-safe; the caller serialises (aalc.hpp:126-129).
+ *
+ * Results are bit-identical to the reference's: codes, block bytes, decoded
+ * amplitudes, per-stride sums, scales and every GateRecord field except the
+ * wall time (DESIGN.md §4 explains how the parallel kernels stay exact).
+ */
+#ifndef QCS_B200_H
+#define QCS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes.  1:1 with the reference's exception kinds. */
+enum {
+    QCS_OK = 0,
+    QCS_E_RUNTIME = 1,        /* std::runtime_error                           */
+    QCS_E_INVALID = 2,        /* std::invalid_argument  (config error)         */
+    QCS_E_RANGE = 3,          /* std::out_of_range                             */
+    QCS_E_CAPACITY = 4,       /* caller buffer too small (ABI only)            */
+    QCS_E_CUDA = 5,           /* CUDA runtime failure / no device              */
+    QCS_E_NOMEM = 6,          /* device arena exhausted                        */
+    QCS_E_BAD_MAGIC = 10,     /* CodecError::bad_magic       codec.hpp:38      */
+    QCS_E_TRUNCATED = 11,     /* CodecError::truncated       codec.hpp:39      */
+    QCS_E_UNKNOWN_CODEC = 12, /* CodecError::unknown_codec   codec.hpp:40      */
+    QCS_E_BAD_VALUE = 13      /* CodecError::bad_value       codec.hpp:41      */
+};
+
+/* GateOp (gate.hpp:43-63).  kind: 0 single, 1 controlled, 2 diag_phase_flip,
+ * 3 reflect_mean (GateKind, gate.hpp:36-41).  u = {u11r,u11i,u12r,u12i,
+ * u21r,u21i,u22r,u22i} (UnitaryParts, gate.cpp:141-151).  control = -1 when
+ * absent.  72 bytes. */
+typedef struct {
+    int32_t kind;
+    int32_t target;
+    int32_t control;
+    int32_t pad_;
+    uint64_t flip_index;
+    double u[8];
+} qcs_gate_desc;
+
+/* StrideCompressReport (aalc.hpp:62-69). 48 bytes. */
+typedef struct {
+    uint64_t stride_index;
+    uint64_t bytes_in;
+    uint64_t bytes_out;
+    double chosen_delta;
+    double ratio;
+    int32_t threshold_met;
+    int32_t pad_;
+} qcs_stride_report;
+
+/* GateRecord (metrics.hpp:13-24) plus the gate's threshold-violation count
+ * (RunMetrics::threshold_violations, aalc.cpp:624).  elapsed_ns is device
+ * time of the gate (CUDA events), not host wall time. */
+typedef struct {
+    uint64_t gate_index;
+    uint64_t stride_count;
+    double min_ratio;
+    double mean_ratio;
+    double max_chosen_delta;
+    uint64_t bytes_before;
+    uint64_t bytes_after;
+    uint64_t elapsed_ns;
+    double norm_after;
+    uint64_t threshold_violations;
+} qcs_gate_record;
+
+typedef struct qcs_dev_state* qcs_dev_state_t;
+
+const char* qcs_last_error(void);
+int qcs_version(void);
+
+/* CompressedState::basis_state (aalc.cpp:140-174) on `device`.
+ * StateGeometry::make validation (core.cpp:9-23). */
+int qcs_state_create(int n_qubits, int stride_bits, uint64_t basis, int device,
+                     qcs_dev_state_t* out);
+void qcs_state_destroy(qcs_dev_state_t st);
+
+/* CompressedState::apply_gate (aalc.cpp:261-420) incl. GateOp::validate,
+ * make_stride_plan, the AALC ladder (ErrorBoundLadder::make checks,
+ * aalc.cpp:56-72; RatioThreshold, aalc.hpp:51-60) and the lazy global
+ * renormalisation.  reports (optional, capacity = 2^(n-s)) receive the
+ * stride reports in the reference's unit order.  On error the state is
+ * unchanged. */
+int qcs_apply_gate(qcs_dev_state_t st, const qcs_gate_desc* gate, const double* ladder,
+                   int n_levels, double theta, qcs_stride_report* reports,
+                   uint64_t* n_reports, double* norm_after);
+
+/* apply_program_range (aalc.cpp:588-634) over gates[0..n_gates): one
+ * GateRecord per gate, gate_index = first_index + i.  Launches are queued
+ * back to back; one host synchronisation at the end.  On error at gate i,
+ * gates before i are applied, the state reflects them, *n_done = i. */
+int qcs_run_program(qcs_dev_state_t st, const qcs_gate_desc* gates, uint64_t n_gates,
+                    uint64_t first_index, const double* ladder, int n_levels,
+                    double theta, qcs_gate_record* records, uint64_t* n_done);
+
+/* stored_stride / decompress_stride (aalc.cpp:191-209). */
+int qcs_read_stride(qcs_dev_state_t st, uint64_t stride, int apply_scale, double* re,
+                    double* im);
+/* to_amplitudes (aalc.cpp:211-223): interleaved re/im, 2^(n+1) doubles. */
+int qcs_to_amplitudes(qcs_dev_state_t st, double* amps);
+/* compressed_bytes / min_stride_ratio / norm_sq_tracked (aalc.cpp:233-259). */
+int qcs_state_stats(qcs_dev_state_t st, uint64_t* compressed_bytes,
+                    double* min_stride_ratio, double* norm_sq_tracked);
+/* stride_scale (aalc.cpp:225-231) plus the stored sum and payload sizes. */
+int qcs_stride_info(qcs_dev_state_t st, uint64_t stride, double* scale, double* sum_sq,
+                    uint64_t* re_payload, uint64_t* im_payload);
+/* Serialized QCS1 blocks of one stride, re then im (serialize_block_append,
+ * codec.cpp:369-381) — the per-stride body of a QCKP checkpoint
+ * (aalc.cpp:466-494).  cap may be 0 to query *len. */
+int qcs_export_blocks(qcs_dev_state_t st, uint64_t stride, uint8_t* buf, uint64_t cap,
+                      uint64_t* len, double* scale, double* sum_sq);
+/* Inverse of qcs_export_blocks (parse_block, codec.cpp:391-420; load,
+ * aalc.cpp:496-586): validates and installs the blocks verbatim. */
+int qcs_import_blocks(qcs_dev_state_t st, uint64_t stride, const uint8_t* buf,
+                      uint64_t len, double scale, double sum_sq);
+/* Device-side accounting for benchmarks: resident bytes of the block store
+ * (payload arena in use + side index). */
+int qcs_state_memory(qcs_dev_state_t st, uint64_t* arena_bytes, uint64_t* side_bytes,
+                     uint64_t* scratch_bytes);
+/* Number of kernel launches issued by this state so far (bench accounting). */
+uint64_t qcs_state_launches(qcs_dev_state_t st);
+/* Average device time (ns) of the fused codec kernel over the last
+ * qcs_run_program call, and its launch count (roofline accounting). */
+int qcs_state_kernel_stats(qcs_dev_state_t st, double* codec_ns_avg,
+                           uint64_t* codec_launches, uint64_t* codec_bytes);
+
+/* Codec plugin (codec.hpp:80-105): compress(x, ErrorBound(delta)) then
+ * serialize_block.  out receives the 29-byte QCS1 header + payload; cap may
+ * be 0 to query *len. */
+int qcs_codec_compress(const double* x, uint64_t n, double delta, uint8_t* out,
+                       uint64_t cap, uint64_t* len);
+/* parse_block + decompress_into of one serialized block into out[n]. */
+int qcs_codec_decompress(const uint8_t* block, uint64_t len, double* out, uint64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,15 @@
+"""B200-native compressed-state gate engine (arXiv 1811.05140 hot path).
+
+The product is libqcs_b200.so (sm_100a CUDA + C++ host code behind the C-ABI
+in include/qcs_b200.h).  This package is its host-side mirror of the
+reference API: circuit front end (circuit.py), engine/codec bindings
+(engine.py) and per-gate metrics (metrics.py).
+"""
+from .circuit import (CircuitProgram, GateOp, ParseError, Unitary2x2, build_grid, build_grover,
+                      build_grover_gate_form, build_qft, parse_circuit, pow2_bound, print_circuit)
+from .metrics import GateRecord, RunMetrics, emit_csv, gate_record
+from .engine import (CheckpointError, CodecError, CompressedState, DeviceError, ErrorBoundLadder,
+                     GateResult, RatioThreshold, RunOptions, RunResult, StateGeometry,
+                     apply_program_range, compress, decompress, run_program, run_program_on)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

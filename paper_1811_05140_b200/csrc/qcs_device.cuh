@@ -1,0 +1,165 @@
+// Device-side building blocks shared by the codec and gate kernels.
+//
+// Arithmetic contract: every parity-relevant FP64 operation is written with
+// the explicit round-to-nearest intrinsics in the reference's left-to-right
+// order and the whole library is compiled with -fmad=false, so no DFMA is
+// ever formed (checked with cuobjdump -sass in DESIGN.md §6).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace qcs {
+
+constexpr int SUB = 32;                         // elements per lane sub-chunk
+constexpr int PLANE_LANES = 128;                // lanes per plane in the codec CTA
+constexpr int ITER = PLANE_LANES * SUB;         // elements per plane per CTA iteration
+constexpr int CODEC_THREADS = 2 * PLANE_LANES;  // one CTA = one stride (re + im planes)
+constexpr int XS_STRIDE = SUB + 1;              // padded lane pitch in shared memory
+constexpr int QRADIUS = 32768;                  // codec.cpp:11
+constexpr int32_t WCODE = INT32_MIN;            // element stored as a raw word
+constexpr double ZERO_SNAP = 1e-300;            // core.hpp:22
+constexpr uint32_t HEADER_BYTES = 29;           // codec.hpp:54
+
+enum : int { TY_NONE = 0, TY_Z = 1, TY_C = 2, TY_W = 3 };
+
+// Side index entry: one per SUB-element sub-chunk of a plane.  Lets any
+// sub-chunk be decoded on its own, bit-exactly: byte offset (within the
+// payload) of the token covering the sub-chunk's first element, how many of
+// that token's elements precede the sub-chunk, and the exact predictor value
+// entering it (the reference decoder's `pred`, codec.cpp:296).
+struct SideEntry {
+    uint32_t off;
+    uint32_t skip;
+    double pred;
+};
+
+// Parameters of one error-bound level (ErrorBound, codec.hpp:24-32).
+struct CodecParams {
+    double delta;    // absolute bound; 0 = lossless
+    double td;       // 2*delta (codec.cpp:219)
+    double inv_td;   // 1/td, used only when td is a power of two (exact)
+    double lim;      // td * 32768 (codec.cpp:220)
+    int lossy;
+    int pow2;
+};
+
+__host__ __device__ inline uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+__host__ __device__ inline int type_of(int32_t c)
+{
+    return c == 0 ? TY_Z : (c == WCODE ? TY_W : TY_C);
+}
+
+__device__ __forceinline__ int varint_len(uint64_t v)
+{
+    const int bits = 64 - __clzll(v | 1ull);
+    return (bits + 6) / 7;
+}
+
+__device__ __forceinline__ uint64_t zigzag(int64_t q)
+{
+    return (static_cast<uint64_t>(q) << 1) ^ static_cast<uint64_t>(q >> 63);
+}
+
+__device__ __forceinline__ int64_t unzigzag(uint64_t z)
+{
+    return static_cast<int64_t>(z >> 1) ^ -static_cast<int64_t>(z & 1);
+}
+
+// Token value of a run of `len` elements of type ty (Z or W) for the codec.
+// Lossless: len<<1 | (W ? 1 : 0)  (codec.cpp:13-15).
+// Lossy:    len<<2 | (W ? 2 : 0)  (codec.cpp:17-20).
+__device__ __forceinline__ uint64_t run_token(int lossy, int ty, uint64_t len)
+{
+    if (lossy) return (len << 2) | (ty == TY_W ? 2u : 0u);
+    return (len << 1) | (ty == TY_W ? 1u : 0u);
+}
+
+__device__ __forceinline__ uint64_t code_token(int32_t q)
+{
+    return (zigzag(q) << 2) | 1u;
+}
+
+__device__ __forceinline__ void put_varint(uint8_t* p, uint64_t v)
+{
+    while (v >= 0x80) {
+        *p++ = static_cast<uint8_t>(v) | 0x80;
+        v >>= 7;
+    }
+    *p = static_cast<uint8_t>(v);
+}
+
+__device__ __forceinline__ void put_word(uint8_t* p, uint64_t w)
+{
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p[i] = static_cast<uint8_t>(w >> (8 * i));
+}
+
+__device__ __forceinline__ uint64_t get_word(const uint8_t* p)
+{
+    uint64_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w |= static_cast<uint64_t>(p[i]) << (8 * i);
+    return w;
+}
+
+// Trusted varint read (internal blocks, already validated).
+__device__ __forceinline__ uint64_t get_varint(const uint8_t* in, uint64_t& pos)
+{
+    uint64_t v = 0;
+    int shift = 0;
+    for (;;) {
+        const uint8_t b = in[pos++];
+        v |= static_cast<uint64_t>(b & 0x7f) << (shift & 63);
+        if (!(b & 0x80)) return v;
+        shift += 7;
+    }
+}
+
+__device__ __forceinline__ double snap(double x)
+{
+    return fabs(x) < ZERO_SNAP ? 0.0 : x;  // StrideBuffer::snap_zeros, core.cpp:39-47
+}
+
+// One step of the reference lossy encoder (compress_lossy, codec.cpp:224-247)
+// from predictor P on input x.  Returns the code (0 = zero code, WCODE =
+// escape) and advances P exactly as the reference does.
+__device__ __forceinline__ int32_t ref_step(const CodecParams& cp, double& P, double x)
+{
+    const double diff = __dsub_rn(x, P);
+    if (fabs(diff) < cp.lim) {
+        const double qd = cp.pow2 ? __dmul_rn(diff, cp.inv_td) : __ddiv_rn(diff, cp.td);
+        // llround: nearest, halfway away from zero.  trunc/sub are exact.
+        double t = trunc(qd);
+        if (fabs(__dsub_rn(qd, t)) >= 0.5) t = __dadd_rn(t, copysign(1.0, qd));
+        if (t > -32768.0 && t < 32768.0) {
+            const double recon = __dadd_rn(P, __dmul_rn(cp.td, t));
+            if (fabs(__dsub_rn(x, recon)) <= cp.delta) {
+                P = recon;
+                return static_cast<int32_t>(t);
+            }
+        }
+    }
+    P = x;
+    return WCODE;
+}
+
+// The predictor value the reference would hold after coding x when the chain
+// sits on the 2*delta lattice anchored at 0: used only as a *guess* for a
+// lane's entry predictor; every guess is verified.
+__device__ __forceinline__ double lattice_guess(const CodecParams& cp, double xprev2, double xprev1)
+{
+    double t = cp.pow2 ? __dmul_rn(xprev2, cp.inv_td) : __ddiv_rn(xprev2, cp.td);
+    t = rint(t);
+    double P = __dmul_rn(cp.td, t);
+    ref_step(cp, P, xprev1);
+    return P;
+}
+
+__device__ __forceinline__ bool same_bits(double a, double b)
+{
+    return __double_as_longlong(a) == __double_as_longlong(b);
+}
+
+}  // namespace qcs

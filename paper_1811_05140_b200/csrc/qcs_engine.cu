@@ -1,0 +1,1332 @@
+// B200 compressed-state gate engine: device block store + per-gate pipeline
+// + the C-ABI declared in include/qcs_b200.h.
+//
+// Per gate (CompressedState::apply_gate, aalc.cpp:261-420):
+//   k_make_jobs   unit list of make_stride_plan (gate.cpp:313-403), on device
+//   k_decode      decompress_into + scale (aalc.cpp:176-189), lane per sub-chunk
+//   [k_stride_sums, k_mean]  reflect_mean's mean pass (aalc.cpp:270-295)
+//   k_gate        run_plan_unit (gate.cpp:405-454), FMA-free apply_pair order
+//   per ladder level: k_encode (snap + compress + stored sum_sq) and
+//                     k_ladder (compress_stride_adaptive / joint pair ladder,
+//                     aalc.cpp:117-138, 337-356)
+//   k_commit_plan / k_commit_copy  staged commit into the block arena
+//   k_norm        lazy renormalisation + GateRecord (aalc.cpp:410-419, 612-631)
+// All launches are stream-ordered; the host only synchronises at API
+// boundaries.  A device error word makes every later kernel a no-op and
+// keeps the state as it was before the failing gate.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/qcs_b200.h"
+#include "qcs_codec.cuh"
+
+using namespace qcs;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CU(call)                                                                         \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return set_err(QCS_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+struct Plan {
+    uint64_t n_units;
+    int pair;        // units are (lo, hi) stride pairs
+    int npos;        // fixed stride-index bits (0..2)
+    int pos[2];      // ascending bit positions
+    int val[2];
+    int64_t fixed;   // >= 0: the single unit's stride (phase flip)
+    int pb;          // pair bit (pair units)
+    int kind;        // gate kind
+    int t, c;        // target, control (-1 none)
+    int local_ctl;   // in-stride control mask bit (c < s), else -1
+    uint64_t flip_off;
+    int reflect;
+};
+
+__host__ __device__ inline uint64_t insert_bit(uint64_t j, int pos, int v)
+{
+    const uint64_t lo = j & ((1ull << pos) - 1);
+    return ((j >> pos) << (pos + 1)) | ((uint64_t)v << pos) | lo;
+}
+
+__host__ __device__ inline uint64_t unit_lo(const Plan& p, uint64_t u)
+{
+    if (p.fixed >= 0) return (uint64_t)p.fixed;
+    uint64_t j = u;
+    for (int i = 0; i < p.npos; ++i) j = insert_bit(j, p.pos[i], p.val[i]);
+    return j;
+}
+
+// job/slot s -> stride
+__host__ __device__ inline uint64_t slot_stride(const Plan& p, uint64_t s)
+{
+    if (!p.pair) return unit_lo(p, s);
+    const uint64_t lo = unit_lo(p, s >> 1);
+    return (s & 1) ? (lo | (1ull << p.pb)) : lo;
+}
+
+struct GateParams {
+    double u[8];
+};
+
+// ---------------------------------------------------------------------------
+// device state arrays
+// ---------------------------------------------------------------------------
+struct Dev {
+    // geometry
+    int n, s;
+    uint64_t L, NS, nsub;
+    // block store
+    uint8_t* arena[2];
+    uint64_t arena_cap;
+    uint64_t* p_off;     // [2NS]
+    uint64_t* p_len;     // [2NS]
+    int8_t* p_codec;     // [2NS]
+    double* p_delta;     // [2NS]
+    SideEntry* side;     // [2NS][nsub]
+    double* scale;       // [NS]
+    double* sum_sq;      // [NS]
+    // per-gate scratch
+    double* X;           // [NS][2][L]
+    uint8_t* slot_out;   // [NS][2][cap]
+    uint64_t slot_cap;
+    SideEntry* slot_side;  // [NS][2][nsub]
+    uint64_t* slot_len;    // [2NS]
+    double* slot_sum;      // [NS]
+    uint64_t* job_stride;  // [NS]
+    uint8_t* pending;      // [NS]
+    int64_t* slot_of;      // [NS] generation<<32 | slot
+    qcs_stride_report* reports;  // [NS]
+    uint64_t* new_off;     // [2NS]
+    double* partial;       // [2NS] mean pass
+    // scalars
+    struct Scal {
+        uint64_t bump;
+        int cur;
+        int mode;          // 0 append, 1 compact
+        int err;           // first error code
+        int err_gate;
+        uint64_t gen;
+        double mean[2];
+        double norm_sq;
+        uint64_t compressed_bytes;
+        double min_ratio;
+    }* sc;
+    qcs_gate_record* rec;  // record ring for run_program
+    uint64_t rec_cap;
+};
+
+__global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen)
+{
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = slot_stride(p, s);
+        d.job_stride[s] = j;
+        d.pending[s] = 1;
+        d.slot_of[j] = (int64_t)((gen << 32) | s);
+    }
+}
+
+struct DecodeJob {
+    const uint64_t* job_stride;  // null: stride = blockIdx
+    int apply_scale;
+};
+
+__global__ void __launch_bounds__(256) k_decode(Dev d, DecodeJob dj)
+{
+    if (d.sc->err) return;
+    const uint64_t j = dj.job_stride ? dj.job_stride[blockIdx.x] : blockIdx.x;
+    const int pl = threadIdx.x >> 7;
+    const int lane = threadIdx.x & 127;
+    const uint64_t g = 2 * j + pl;
+    const uint8_t* in = d.arena[d.sc->cur] + d.p_off[g];
+    const int codec = d.p_codec[g];
+    const double td = 2.0 * d.p_delta[g];
+    const double scale = dj.apply_scale ? d.scale[j] : 1.0;
+    double* o = d.X + j * 2 * d.L + (uint64_t)pl * d.L;
+    const SideEntry* side = d.side + g * d.nsub;
+    for (uint64_t sc = lane; sc < d.nsub; sc += PLANE_LANES) {
+        const uint64_t e0 = sc * SUB;
+        const int cnt = (int)umin64(SUB, d.L - e0);
+        decode_sub(in, codec, td, side[sc], cnt, o + e0, scale);
+    }
+}
+
+// apply_pair arithmetic (gate.cpp:153-162), left to right, no FMA.
+__device__ __forceinline__ void pair_update(const double* m, double& r0, double& i0, double& r1,
+                                            double& i1)
+{
+    const double t0r = r0, t0i = i0, t1r = r1, t1i = i1;
+    r0 = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(m[0], t0r), __dmul_rn(m[1], t0i)), __dmul_rn(m[2], t1r)),
+                   __dmul_rn(m[3], t1i));
+    i0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[0], t0i), __dmul_rn(m[1], t0r)), __dmul_rn(m[2], t1i)),
+                   __dmul_rn(m[3], t1r));
+    r1 = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(m[4], t0r), __dmul_rn(m[5], t0i)), __dmul_rn(m[6], t1r)),
+                   __dmul_rn(m[7], t1i));
+    i1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[4], t0i), __dmul_rn(m[5], t0r)), __dmul_rn(m[6], t1i)),
+                   __dmul_rn(m[7], t1r));
+}
+
+// run_plan_unit over all units: one thread per amplitude pair / amplitude.
+__global__ void __launch_bounds__(256) k_gate(Dev d, Plan p, GateParams gp)
+{
+    if (d.sc->err) return;
+    const uint64_t L = d.L;
+    const uint64_t per = (p.kind <= 1 && !p.pair) ? L / 2 : L;
+    const uint64_t total = p.n_units * per;
+    double m[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = gp.u[i];
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < total;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t u = w / per, i = w % per;
+        if (p.kind == 2) {  // apply_phase_flip_in_stride (gate.cpp:279-286)
+            if (i != 0) continue;
+            double* x = d.X + unit_lo(p, u) * 2 * L;
+            x[p.flip_off] = -x[p.flip_off];
+            x[L + p.flip_off] = -x[L + p.flip_off];
+            continue;
+        }
+        if (p.kind == 3) {  // apply_reflect_mean_in_stride (gate.cpp:288-301)
+            double* x = d.X + unit_lo(p, u) * 2 * L;
+            const double mr2 = 2.0 * d.sc->mean[0], mi2 = 2.0 * d.sc->mean[1];
+            x[i] = __dsub_rn(mr2, x[i]);
+            x[L + i] = __dsub_rn(mi2, x[L + i]);
+            continue;
+        }
+        if (!p.pair) {  // in-stride: apply_single_in_stride / apply_controlled_in_stride
+            const uint64_t half = 1ull << p.t, lo_mask = half - 1;
+            const uint64_t i0 = ((i & ~lo_mask) << 1) | (i & lo_mask);
+            if (p.local_ctl >= 0 && !(i0 & (1ull << p.local_ctl))) continue;
+            double* x = d.X + unit_lo(p, u) * 2 * L;
+            pair_update(m, x[i0], x[L + i0], x[i0 | half], x[L + (i0 | half)]);
+        } else {  // cross-stride
+            if (p.local_ctl >= 0 && !(i & (1ull << p.local_ctl))) continue;
+            const uint64_t lo = unit_lo(p, u);
+            double* a = d.X + lo * 2 * L;
+            double* b = d.X + (lo | (1ull << p.pb)) * 2 * L;
+            pair_update(m, a[i], a[L + i], b[i], b[L + i]);
+        }
+    }
+}
+
+// stride_amplitude_sum (gate.cpp:303-311): serial per stride, index order.
+__global__ void k_stride_sums(Dev d)
+{
+    if (d.sc->err) return;
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= d.NS) return;
+    const double* x = d.X + j * 2 * d.L;
+    double sr = 0.0, si = 0.0;
+    for (uint64_t i = 0; i < d.L; ++i) {
+        sr = __dadd_rn(sr, x[i]);
+        si = __dadd_rn(si, x[d.L + i]);
+    }
+    d.partial[2 * j] = sr;
+    d.partial[2 * j + 1] = si;
+}
+
+__global__ void k_mean(Dev d)
+{
+    if (d.sc->err) return;
+    double sr = 0.0, si = 0.0;
+    for (uint64_t j = 0; j < d.NS; ++j) {
+        sr = __dadd_rn(sr, d.partial[2 * j]);
+        si = __dadd_rn(si, d.partial[2 * j + 1]);
+    }
+    const double na = (double)(1ull << d.n);
+    d.sc->mean[0] = __ddiv_rn(sr, na);
+    d.sc->mean[1] = __ddiv_rn(si, na);
+}
+
+// Ladder step for every unit: block_pair_ratio (aalc.cpp:37-42); stop at the
+// first level whose ratio (pairs: min of both) reaches theta, else keep the
+// last level (aalc.cpp:125-137, 346-356).
+__global__ void k_ladder(Dev d, Plan p, double delta, double theta, int last_level)
+{
+    if (d.sc->err) return;
+    const uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (u >= p.n_units) return;
+    const uint64_t s0 = p.pair ? 2 * u : u;
+    if (!d.pending[s0]) return;
+    const uint64_t bytes_in = d.L * 16;
+    const int ns = p.pair ? 2 : 1;
+    double r[2];
+    uint64_t bo[2];
+    for (int k = 0; k < ns; ++k) {
+        const uint64_t s = s0 + k;
+        bo[k] = (HEADER_BYTES + d.slot_len[2 * s]) + (HEADER_BYTES + d.slot_len[2 * s + 1]);
+        r[k] = (double)bytes_in / (double)bo[k];
+    }
+    const double rmin = ns == 2 ? fmin(r[0], r[1]) : r[0];
+    const bool done = rmin >= theta || last_level;
+    if (!done) return;
+    for (int k = 0; k < ns; ++k) {
+        const uint64_t s = s0 + k;
+        qcs_stride_report& rep = d.reports[s];
+        rep.stride_index = d.job_stride[s];
+        rep.bytes_in = bytes_in;
+        rep.bytes_out = bo[k];
+        rep.chosen_delta = delta;
+        rep.ratio = r[k];
+        rep.threshold_met = r[k] >= theta;
+        rep.pad_ = 0;
+        d.pending[s] = 0;
+    }
+}
+
+// per-plane codec/delta of the chosen level, kept with the slot
+struct LevelTag {
+    int8_t* slot_codec;   // [NS]
+    double* slot_delta;   // [NS]
+};
+
+__global__ void k_tag_level(Dev d, LevelTag lt, uint64_t n_slots, int codec, double delta)
+{
+    const uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (s >= n_slots || !d.pending[s]) return;
+    lt.slot_codec[s] = (int8_t)codec;
+    lt.slot_delta[s] = delta;
+}
+
+// Placement of the new blocks: append after the live data, or — when the
+// arena would overflow — compact every live block into the other arena.
+__global__ void __launch_bounds__(1024) k_commit_plan(Dev d, uint64_t n_slots, uint64_t gen)
+{
+    if (d.sc->err) return;
+    __shared__ uint64_t wsum[32];
+    __shared__ uint64_t carry;
+    __shared__ int mode;
+    const int tid = threadIdx.x, wl = tid & 31, w = tid >> 5;
+    auto rounded = [](uint64_t x) { return (x + 15) & ~uint64_t(15); };
+    // pass 1: total of new blocks
+    uint64_t acc = 0;
+    for (uint64_t i = tid; i < 2 * n_slots; i += blockDim.x) acc += rounded(d.slot_len[i]);
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (wl == 0) wsum[w] = acc;
+    __syncthreads();
+    if (tid == 0) {
+        uint64_t t = 0;
+        for (int i = 0; i < 32; ++i) t += wsum[i];
+        mode = (d.sc->bump + t <= d.arena_cap) ? 0 : 1;
+        carry = mode == 0 ? d.sc->bump : 0;
+    }
+    __syncthreads();
+    // pass 2: exclusive scan over the planes being placed
+    const uint64_t n_items = mode == 0 ? 2 * n_slots : 2 * d.NS;
+    for (uint64_t base = 0; base < n_items; base += blockDim.x) {
+        const uint64_t i = base + tid;
+        uint64_t v = 0;
+        uint64_t g = 0;
+        if (i < n_items) {
+            if (mode == 0) {
+                g = 2 * d.job_stride[i >> 1] + (i & 1);
+                v = rounded(d.slot_len[i]);
+            } else {
+                g = i;
+                const int64_t so = d.slot_of[g >> 1];
+                const bool rew = (uint64_t)(so >> 32) == gen;
+                v = rounded(rew ? d.slot_len[2 * (so & 0xffffffff) + (g & 1)] : d.p_len[g]);
+            }
+        }
+        uint64_t inc = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (wl >= o) inc += t;
+        }
+        __syncthreads();
+        if (wl == 31) wsum[w] = inc;
+        __syncthreads();
+        uint64_t pre = carry;
+        for (int k = 0; k < w; ++k) pre += wsum[k];
+        if (i < n_items) d.new_off[g] = pre + inc - v;
+        __syncthreads();
+        if (tid == blockDim.x - 1) carry = pre + inc;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (carry > d.arena_cap) {
+            d.sc->err = QCS_E_NOMEM;
+            return;
+        }
+        d.sc->mode = mode;
+        d.sc->bump = carry;
+    }
+}
+
+__global__ void __launch_bounds__(128) k_commit_copy(Dev d, LevelTag lt, uint64_t gen)
+{
+    if (d.sc->err) return;
+    const uint64_t g = blockIdx.x;
+    const uint64_t j = g >> 1;
+    const int c = (int)(g & 1);
+    const int64_t so = d.slot_of[j];
+    const bool rew = (uint64_t)(so >> 32) == gen;
+    const int mode = d.sc->mode;
+    if (!rew && mode == 0) return;
+    const int cur = d.sc->cur;
+    const uint8_t* src;
+    uint64_t len;
+    const uint64_t slot = rew ? (uint64_t)(so & 0xffffffff) : 0;
+    if (rew) {
+        src = d.slot_out + (2 * slot + c) * d.slot_cap;
+        len = d.slot_len[2 * slot + c];
+    } else {
+        src = d.arena[cur] + d.p_off[g];
+        len = d.p_len[g];
+    }
+    uint8_t* dst = d.arena[mode == 0 ? cur : 1 - cur] + d.new_off[g];
+    const uint64_t n16 = (len + 15) / 16;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (uint64_t i = threadIdx.x; i < n16; i += blockDim.x) d4[i] = s4[i];
+    if (rew) {
+        const SideEntry* ss = d.slot_side + (2 * slot + c) * d.nsub;
+        SideEntry* ds = d.side + g * d.nsub;
+        for (uint64_t i = threadIdx.x; i < d.nsub; i += blockDim.x) ds[i] = ss[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        d.p_off[g] = d.new_off[g];
+        if (rew) {
+            d.p_len[g] = len;
+            d.p_codec[g] = lt.slot_codec[slot];
+            d.p_delta[g] = lt.slot_delta[slot];
+            if (c == 0) {
+                d.sum_sq[j] = d.slot_sum[slot];
+                d.scale[j] = 1.0;
+            }
+        }
+    }
+}
+
+// Lazy renormalisation (aalc.cpp:410-419) and the GateRecord fold
+// (aalc.cpp:612-631), serial in stride / report order like the reference.
+__global__ void k_norm(Dev d, uint64_t n_slots, uint64_t rec_index, uint64_t gate_index)
+{
+    if (threadIdx.x != 0) return;
+    if (d.sc->err) {
+        if (d.sc->err_gate < 0) d.sc->err_gate = (int)gate_index;
+        return;
+    }
+    if (d.sc->mode == 1) d.sc->cur = 1 - d.sc->cur;
+    double total = 0.0;
+    for (uint64_t j = 0; j < d.NS; ++j)
+        total = __dadd_rn(total, __dmul_rn(__dmul_rn(d.scale[j], d.scale[j]), d.sum_sq[j]));
+    if (total > 0.0) {
+        const double f = __ddiv_rn(1.0, __dsqrt_rn(total));
+        for (uint64_t j = 0; j < d.NS; ++j) d.scale[j] = __dmul_rn(d.scale[j], f);
+    }
+    double nsq = 0.0;
+    for (uint64_t j = 0; j < d.NS; ++j)
+        nsq = __dadd_rn(nsq, __dmul_rn(__dmul_rn(d.scale[j], d.scale[j]), d.sum_sq[j]));
+    d.sc->norm_sq = nsq;
+    if (d.rec) {
+        qcs_gate_record r;
+        r.gate_index = gate_index;
+        r.stride_count = n_slots;
+        r.min_ratio = INFINITY;
+        r.max_chosen_delta = 0.0;
+        r.bytes_before = 0;
+        r.bytes_after = 0;
+        r.threshold_violations = 0;
+        double rs = 0.0;
+        for (uint64_t s = 0; s < n_slots; ++s) {
+            const qcs_stride_report& rep = d.reports[s];
+            r.min_ratio = fmin(r.min_ratio, rep.ratio);
+            rs = __dadd_rn(rs, rep.ratio);
+            r.max_chosen_delta = fmax(r.max_chosen_delta, rep.chosen_delta);
+            r.bytes_before += rep.bytes_in;
+            r.bytes_after += rep.bytes_out;
+            if (!rep.threshold_met) ++r.threshold_violations;
+        }
+        r.mean_ratio = n_slots ? __ddiv_rn(rs, (double)n_slots) : 0.0;
+        r.elapsed_ns = 0;
+        r.norm_after = __dsqrt_rn(nsq);
+        d.rec[rec_index] = r;
+    }
+}
+
+__global__ void k_index_planes(Dev d, uint64_t g0, uint64_t count)
+{
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const uint64_t g = g0 + i;
+    const int rc = index_plane(d.arena[d.sc->cur] + d.p_off[g], d.p_len[g], d.p_codec[g],
+                               d.p_delta[g], d.L, d.side + g * d.nsub, nullptr);
+    if (rc) atomicCAS(&d.sc->err, 0, rc);
+}
+
+__global__ void k_stats(Dev d)
+{
+    if (threadIdx.x != 0) return;
+    uint64_t tot = 0;
+    double m = INFINITY, nsq = 0.0;
+    const uint64_t bytes_in = d.L * 16;
+    for (uint64_t j = 0; j < d.NS; ++j) {
+        const uint64_t b = (HEADER_BYTES + d.p_len[2 * j]) + (HEADER_BYTES + d.p_len[2 * j + 1]);
+        tot += b;
+        m = fmin(m, (double)bytes_in / (double)b);
+        nsq = __dadd_rn(nsq, __dmul_rn(__dmul_rn(d.scale[j], d.scale[j]), d.sum_sq[j]));
+    }
+    d.sc->compressed_bytes = tot;
+    d.sc->min_ratio = m;
+    d.sc->norm_sq = nsq;
+}
+
+// codec API: standalone validation + decode of one payload
+__global__ void k_decode_payload(const uint8_t* in, uint64_t len, int codec, double delta,
+                                 uint64_t n, double* out, int* err)
+{
+    *err = index_plane(in, len, codec, delta, n, nullptr, out);
+}
+
+uint64_t payload_cap(uint64_t n) { return ((9 * n + 64) + 15) & ~uint64_t(15); }
+
+bool is_pow2(double x)
+{
+    int e;
+    const double m = std::frexp(x, &e);
+    return x > 0 && std::isfinite(x) && m == 0.5;
+}
+
+CodecParams make_params(double delta)
+{
+    CodecParams cp{};
+    cp.delta = delta;
+    cp.lossy = delta != 0.0;
+    cp.td = 2.0 * delta;
+    cp.lim = cp.td * 32768.0;
+    cp.pow2 = cp.lossy && is_pow2(cp.td) && std::isfinite(1.0 / cp.td);
+    cp.inv_td = cp.pow2 ? 1.0 / cp.td : 0.0;
+    return cp;
+}
+
+int launch_encode(const EncodeArgs& a, uint64_t n_jobs, cudaStream_t st)
+{
+    if (n_jobs == 0) return 0;
+    static bool attr_set = false;
+    if (!attr_set) {
+        CU(cudaFuncSetAttribute(k_encode<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ENC_SMEM));
+        CU(cudaFuncSetAttribute(k_encode<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ENC_SMEM));
+        attr_set = true;
+    }
+    if (a.cp.lossy) k_encode<true><<<(unsigned)n_jobs, CODEC_THREADS, ENC_SMEM, st>>>(a);
+    else k_encode<false><<<(unsigned)n_jobs, CODEC_THREADS, ENC_SMEM, st>>>(a);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host state
+// ---------------------------------------------------------------------------
+struct qcs_dev_state {
+    Dev d{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    LevelTag lt{};
+    uint64_t gen = 0;
+    uint64_t launches = 0;
+    Dev::Scal* h_sc = nullptr;   // pinned mirror
+    qcs_stride_report* h_rep = nullptr;
+    std::vector<void*> allocs;
+    // timing of the codec kernel across the last run
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+    double codec_ns = 0;
+    uint64_t codec_launches = 0, codec_bytes = 0;
+};
+
+namespace {
+
+template <typename T>
+int dalloc(qcs_dev_state* s, T** p, size_t count)
+{
+    void* q = nullptr;
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    cudaError_t e = cudaMalloc(&q, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(QCS_E_NOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    }
+    s->allocs.push_back(q);
+    *p = static_cast<T*>(q);
+    return 0;
+}
+
+int validate_gate(const qcs_dev_state* st, const qcs_gate_desc* g)
+{
+    const int n = st->d.n;
+    switch (g->kind) {  // GateOp::validate, gate.cpp:109-137
+        case 0:
+        case 1:
+            if (g->target < 0 || g->target >= n) return set_err(QCS_E_RANGE, "target qubit out of range");
+            if (g->kind == 1) {
+                if (g->control < 0 || g->control >= n) return set_err(QCS_E_RANGE, "control qubit out of range");
+                if (g->control == g->target) return set_err(QCS_E_INVALID, "control qubit equals target qubit");
+            }
+            return 0;
+        case 2:
+            if (g->flip_index >= (1ull << n)) return set_err(QCS_E_RANGE, "flip index out of range");
+            return 0;
+        case 3:
+            return 0;
+        default:
+            return set_err(QCS_E_INVALID, "unknown gate kind %d", g->kind);
+    }
+}
+
+int validate_ladder(const double* lad, int nl, double theta)
+{
+    if (nl <= 0 || !lad) return set_err(QCS_E_INVALID, "error-bound ladder must not be empty");
+    for (int i = 0; i < nl; ++i) {
+        if (!(lad[i] >= 0.0) || !std::isfinite(lad[i]))
+            return set_err(QCS_E_INVALID, "error bounds must be finite and >= 0");
+        if (i > 0 && !(lad[i] > lad[i - 1])) return set_err(QCS_E_INVALID, "error bounds must be strictly increasing");
+    }
+    if (!(theta >= 1.0)) return set_err(QCS_E_INVALID, "ratio threshold must be >= 1");
+    return 0;
+}
+
+// make_stride_plan (gate.cpp:313-403) in closed form.
+Plan make_plan(const qcs_dev_state* st, const qcs_gate_desc* g)
+{
+    const int s = st->d.s;
+    const uint64_t NS = st->d.NS;
+    Plan p{};
+    p.fixed = -1;
+    p.kind = g->kind;
+    p.t = g->target;
+    p.c = g->kind == 1 ? g->control : -1;
+    p.local_ctl = -1;
+    p.pb = 0;
+    auto add_fixed = [&](int pos, int v) {
+        p.pos[p.npos] = pos;
+        p.val[p.npos] = v;
+        ++p.npos;
+        if (p.npos == 2 && p.pos[0] > p.pos[1]) {
+            std::swap(p.pos[0], p.pos[1]);
+            std::swap(p.val[0], p.val[1]);
+        }
+    };
+    if (g->kind == 0 || g->kind == 1) {
+        const int t = g->target, c = p.c;
+        if (c >= 0 && c < s) p.local_ctl = c;
+        if (t < s) {
+            p.pair = 0;
+            if (c >= s) add_fixed(c - s, 1);
+        } else {
+            p.pair = 1;
+            p.pb = t - s;
+            add_fixed(t - s, 0);
+            if (c >= s) add_fixed(c - s, 1);
+        }
+        p.n_units = NS >> p.npos;
+    } else if (g->kind == 2) {
+        p.fixed = (int64_t)(g->flip_index >> s);
+        p.flip_off = g->flip_index & (st->d.L - 1);
+        p.n_units = 1;
+    } else {
+        p.reflect = 1;
+        p.n_units = NS;
+    }
+    return p;
+}
+
+uint64_t grid_for(uint64_t work, uint64_t block = 256)
+{
+    return umin64((work + block - 1) / block, 148ull * 32);
+}
+
+// One gate, fully stream-ordered.  rec_index < 0: no record.
+int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, int nl,
+                 double theta, int64_t rec_index, uint64_t gate_index, uint64_t* n_slots_out)
+{
+    Dev& d = st->d;
+    cudaStream_t s = st->stream;
+    const Plan p = make_plan(st, g);
+    const uint64_t n_slots = p.pair ? 2 * p.n_units : p.n_units;
+    *n_slots_out = n_slots;
+    const uint64_t gen = ++st->gen;
+    GateParams gp;
+    for (int i = 0; i < 8; ++i) gp.u[i] = g->u[i];
+
+    k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen);
+    ++st->launches;
+    if (p.reflect) {
+        k_decode<<<(unsigned)d.NS, 256, 0, s>>>(d, DecodeJob{nullptr, 1});
+        k_stride_sums<<<(unsigned)((d.NS + 127) / 128), 128, 0, s>>>(d);
+        k_mean<<<1, 1, 0, s>>>(d);
+        st->launches += 3;
+    } else {
+        k_decode<<<(unsigned)n_slots, 256, 0, s>>>(d, DecodeJob{d.job_stride, 1});
+        ++st->launches;
+    }
+    const uint64_t per = (p.kind <= 1 && !p.pair) ? d.L / 2 : d.L;
+    k_gate<<<(unsigned)grid_for(p.n_units * per), 256, 0, s>>>(d, p, gp);
+    ++st->launches;
+    for (int k = 0; k < nl; ++k) {
+        EncodeArgs a{};
+        a.X = d.X;
+        a.n = d.L;
+        a.job_stride = d.job_stride;
+        a.stride_elems = 2 * d.L;
+        a.pending = d.pending;
+        a.planes = 2;
+        a.snap = 1;
+        a.out = d.slot_out;
+        a.cap = d.slot_cap;
+        a.side = d.slot_side;
+        a.nsub = d.nsub;
+        a.out_len = d.slot_len;
+        a.sumsq = d.slot_sum;
+        a.cp = make_params(lad[k]);
+        k_tag_level<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, st->lt, n_slots, a.cp.lossy ? 1 : 0, lad[k]);
+        ++st->launches;
+        int rc = launch_encode(a, n_slots, s);
+        if (rc) return rc;
+        ++st->launches;
+        k_ladder<<<(unsigned)((p.n_units + 127) / 128), 128, 0, s>>>(d, p, lad[k], theta, k == nl - 1);
+        ++st->launches;
+    }
+    k_commit_plan<<<1, 1024, 0, s>>>(d, n_slots, gen);
+    k_commit_copy<<<(unsigned)(2 * d.NS), 128, 0, s>>>(d, st->lt, gen);
+    k_norm<<<1, 32, 0, s>>>(d, n_slots, rec_index < 0 ? 0 : (uint64_t)rec_index, gate_index);
+    st->launches += 3;
+    CU(cudaGetLastError());
+    return 0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* qcs_last_error(void) { return g_err.c_str(); }
+int qcs_version(void) { return 1; }
+
+void qcs_state_destroy(qcs_dev_state_t st)
+{
+    if (!st) return;
+    cudaSetDevice(st->device);
+    if (st->stream) cudaStreamSynchronize(st->stream);
+    for (void* p : st->allocs) cudaFree(p);
+    if (st->h_sc) cudaFreeHost(st->h_sc);
+    if (st->h_rep) cudaFreeHost(st->h_rep);
+    if (st->ev_a) cudaEventDestroy(st->ev_a);
+    if (st->ev_b) cudaEventDestroy(st->ev_b);
+    if (st->stream) cudaStreamDestroy(st->stream);
+    delete st;
+}
+
+int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* out)
+{
+    if (n < 1 || n > 59) return set_err(QCS_E_INVALID, "n_qubits must be in [1, 59], got %d", n);
+    if (s < 0 || s > n) return set_err(QCS_E_INVALID, "stride_bits must be in [0, n_qubits], got %d", s);
+    if (basis >= (1ull << n)) return set_err(QCS_E_RANGE, "basis index out of range");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(QCS_E_CUDA, "no CUDA device available (the engine has no CPU path)");
+    }
+    if (device < 0 || device >= ndev) return set_err(QCS_E_INVALID, "bad device %d", device);
+    qcs_dev_state* st = new qcs_dev_state();
+    st->device = device;
+    cudaSetDevice(device);
+    int rc = 0;
+#define TRY(x)                    \
+    do {                          \
+        rc = (x);                 \
+        if (rc) {                 \
+            qcs_state_destroy(st); \
+            return rc;            \
+        }                         \
+    } while (0)
+    Dev& d = st->d;
+    d.n = n;
+    d.s = s;
+    d.L = 1ull << s;
+    d.NS = 1ull << (n - s);
+    d.nsub = (d.L + SUB - 1) / SUB;
+    const uint64_t raw = (16ull << n);
+    if (cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        qcs_state_destroy(st);
+        return set_err(QCS_E_CUDA, "stream creation failed");
+    }
+    d.arena_cap = std::max<uint64_t>(raw + raw / 8 + 4096 * d.NS, 1ull << 24);
+    d.slot_cap = payload_cap(d.L);
+    TRY(dalloc(st, &d.arena[0], d.arena_cap));
+    TRY(dalloc(st, &d.arena[1], d.arena_cap));
+    TRY(dalloc(st, &d.p_off, 2 * d.NS));
+    TRY(dalloc(st, &d.p_len, 2 * d.NS));
+    TRY(dalloc(st, &d.p_codec, 2 * d.NS));
+    TRY(dalloc(st, &d.p_delta, 2 * d.NS));
+    TRY(dalloc(st, &d.side, 2 * d.NS * d.nsub));
+    TRY(dalloc(st, &d.scale, d.NS));
+    TRY(dalloc(st, &d.sum_sq, d.NS));
+    TRY(dalloc(st, &d.X, 2 * d.NS * d.L));
+    TRY(dalloc(st, &d.slot_out, 2 * d.NS * d.slot_cap));
+    TRY(dalloc(st, &d.slot_side, 2 * d.NS * d.nsub));
+    TRY(dalloc(st, &d.slot_len, 2 * d.NS));
+    TRY(dalloc(st, &d.slot_sum, d.NS));
+    TRY(dalloc(st, &d.job_stride, d.NS));
+    TRY(dalloc(st, &d.pending, d.NS));
+    TRY(dalloc(st, &d.slot_of, d.NS));
+    TRY(dalloc(st, &d.reports, d.NS));
+    TRY(dalloc(st, &d.new_off, 2 * d.NS));
+    TRY(dalloc(st, &d.partial, 2 * d.NS));
+    TRY(dalloc(st, &d.sc, 1));
+    TRY(dalloc(st, &st->lt.slot_codec, d.NS));
+    TRY(dalloc(st, &st->lt.slot_delta, d.NS));
+    if (cudaMallocHost(&st->h_sc, sizeof(Dev::Scal)) != cudaSuccess ||
+        cudaMallocHost(&st->h_rep, sizeof(qcs_stride_report) * d.NS) != cudaSuccess) {
+        qcs_state_destroy(st);
+        return set_err(QCS_E_NOMEM, "pinned allocation failed");
+    }
+    cudaEventCreate(&st->ev_a);
+    cudaEventCreate(&st->ev_b);
+    // basis_state (aalc.cpp:140-174): one shared lossless all-zero block, plus
+    // the hot stride's re block.  Payloads are tiny; build them here.
+    auto varint = [](std::vector<uint8_t>& o, uint64_t v) {
+        while (v >= 0x80) {
+            o.push_back((uint8_t)v | 0x80);
+            v >>= 7;
+        }
+        o.push_back((uint8_t)v);
+    };
+    std::vector<uint8_t> zero, hot;
+    varint(zero, d.L << 1);
+    const uint64_t off = basis & (d.L - 1);
+    if (off) varint(hot, off << 1);
+    varint(hot, (1ull << 1) | 1u);
+    const double one = 1.0;
+    uint64_t w;
+    memcpy(&w, &one, 8);
+    for (int i = 0; i < 8; ++i) hot.push_back((uint8_t)(w >> (8 * i)));
+    if (d.L - off - 1) varint(hot, (d.L - off - 1) << 1);
+    std::vector<uint8_t> img(32, 0);
+    memcpy(img.data(), zero.data(), zero.size());
+    memcpy(img.data() + 16, hot.data(), hot.size());
+    CU(cudaMemcpy(d.arena[0], img.data(), img.size(), cudaMemcpyHostToDevice));
+    std::vector<uint64_t> h_off(2 * d.NS, 0), h_len(2 * d.NS, zero.size());
+    std::vector<int8_t> h_codec(2 * d.NS, 0);
+    std::vector<double> h_delta(2 * d.NS, 0.0), h_scale(d.NS, 1.0), h_sum(d.NS, 0.0);
+    const uint64_t hj = basis >> s;
+    h_off[2 * hj] = 16;
+    h_len[2 * hj] = hot.size();
+    h_sum[hj] = 1.0;
+    CU(cudaMemcpy(d.p_off, h_off.data(), 8 * h_off.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d.p_len, h_len.data(), 8 * h_len.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d.p_codec, h_codec.data(), h_codec.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d.p_delta, h_delta.data(), 8 * h_delta.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d.scale, h_scale.data(), 8 * h_scale.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d.sum_sq, h_sum.data(), 8 * h_sum.size(), cudaMemcpyHostToDevice));
+    Dev::Scal sc{};
+    sc.bump = 32;
+    sc.cur = 0;
+    sc.err_gate = -1;
+    sc.norm_sq = 1.0;
+    CU(cudaMemcpy(d.sc, &sc, sizeof sc, cudaMemcpyHostToDevice));
+    CU(cudaMemset(d.slot_of, 0xff, 8 * d.NS));
+    k_index_planes<<<(unsigned)((2 * d.NS + 127) / 128), 128, 0, st->stream>>>(d, 0, 2 * d.NS);
+    st->launches += 1;
+    CU(cudaStreamSynchronize(st->stream));
+    CU(cudaMemcpy(st->h_sc, d.sc, sizeof(Dev::Scal), cudaMemcpyDeviceToHost));
+    if (st->h_sc->err) {
+        const int e = st->h_sc->err;
+        qcs_state_destroy(st);
+        return set_err(e, "basis state indexing failed");
+    }
+    *out = st;
+    return 0;
+#undef TRY
+}
+
+static int sync_and_check(qcs_dev_state* st)
+{
+    CU(cudaStreamSynchronize(st->stream));
+    CU(cudaMemcpy(st->h_sc, st->d.sc, sizeof(Dev::Scal), cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+static int report_device_error(qcs_dev_state* st)
+{
+    const int e = st->h_sc->err;
+    const int gi = st->h_sc->err_gate;
+    // clear so the (unchanged) state stays usable
+    Dev::Scal sc = *st->h_sc;
+    sc.err = 0;
+    sc.err_gate = -1;
+    cudaMemcpy(st->d.sc, &sc, sizeof sc, cudaMemcpyHostToDevice);
+    if (e == QCS_E_NOMEM) return set_err(QCS_E_NOMEM, "gate %d failed: block arena exhausted", gi);
+    return set_err(QCS_E_RUNTIME, "gate %d failed: device codec error %d", gi, e);
+}
+
+int qcs_apply_gate(qcs_dev_state_t st, const qcs_gate_desc* g, const double* lad, int nl,
+                   double theta, qcs_stride_report* reports, uint64_t* n_reports,
+                   double* norm_after)
+{
+    if (!st || !g) return set_err(QCS_E_INVALID, "null argument");
+    int rc = validate_gate(st, g);
+    if (rc) return rc;
+    rc = validate_ladder(lad, nl, theta);
+    if (rc) return rc;
+    cudaSetDevice(st->device);
+    uint64_t ns = 0;
+    st->d.rec = nullptr;
+    rc = enqueue_gate(st, g, lad, nl, theta, -1, 0, &ns);
+    if (rc) return rc;
+    rc = sync_and_check(st);
+    if (rc) return rc;
+    if (st->h_sc->err) return report_device_error(st);
+    if (reports && ns) {
+        CU(cudaMemcpy(reports, st->d.reports, ns * sizeof(qcs_stride_report), cudaMemcpyDeviceToHost));
+    }
+    if (n_reports) *n_reports = ns;
+    if (norm_after) *norm_after = std::sqrt(st->h_sc->norm_sq);
+    return 0;
+}
+
+int qcs_run_program(qcs_dev_state_t st, const qcs_gate_desc* gates, uint64_t n_gates,
+                    uint64_t first_index, const double* lad, int nl, double theta,
+                    qcs_gate_record* records, uint64_t* n_done)
+{
+    if (!st || (!gates && n_gates)) return set_err(QCS_E_INVALID, "null argument");
+    if (n_done) *n_done = 0;
+    int rc = validate_ladder(lad, nl, theta);
+    if (rc) return rc;
+    for (uint64_t i = 0; i < n_gates; ++i) {
+        rc = validate_gate(st, &gates[i]);
+        if (rc) {
+            const std::string m = g_err;
+            // the reference validates inside apply_gate, after earlier gates ran
+            uint64_t done = 0;
+            if (i) {
+                int r2 = qcs_run_program(st, gates, i, first_index, lad, nl, theta, records, &done);
+                if (r2) return r2;
+            }
+            if (n_done) *n_done = i;
+            return set_err(rc, "gate %llu failed: %s", (unsigned long long)(first_index + i), m.c_str());
+        }
+    }
+    cudaSetDevice(st->device);
+    Dev& d = st->d;
+    if (d.rec_cap < n_gates) {
+        qcs_gate_record* r = nullptr;
+        rc = dalloc(st, &r, std::max<uint64_t>(n_gates, 1));
+        if (rc) return rc;
+        d.rec = r;
+        d.rec_cap = n_gates;
+    }
+    qcs_gate_record* rec = d.rec;
+    std::vector<cudaEvent_t> ev(n_gates + 1);
+    for (auto& e : ev) cudaEventCreate(&e);
+    cudaEventRecord(ev[0], st->stream);
+    for (uint64_t i = 0; i < n_gates; ++i) {
+        uint64_t ns;
+        d.rec = rec;
+        rc = enqueue_gate(st, &gates[i], lad, nl, theta, (int64_t)i, first_index + i, &ns);
+        if (rc) break;
+        cudaEventRecord(ev[i + 1], st->stream);
+    }
+    int rc2 = sync_and_check(st);
+    std::vector<qcs_gate_record> h(n_gates);
+    if (!rc && !rc2 && n_gates)
+        cudaMemcpy(h.data(), rec, n_gates * sizeof(qcs_gate_record), cudaMemcpyDeviceToHost);
+    uint64_t done = n_gates;
+    if (!rc && !rc2 && st->h_sc->err) done = (uint64_t)std::max(0, st->h_sc->err_gate - (int)first_index);
+    for (uint64_t i = 0; i < done && !rc && !rc2; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+        h[i].elapsed_ns = (uint64_t)((double)ms * 1e6);
+        if (records) records[i] = h[i];
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (rc) return rc;
+    if (rc2) return rc2;
+    if (n_done) *n_done = done;
+    if (st->h_sc->err) return report_device_error(st);
+    return 0;
+}
+
+static int decode_all(qcs_dev_state* st, int apply_scale)
+{
+    k_decode<<<(unsigned)st->d.NS, 256, 0, st->stream>>>(st->d, DecodeJob{nullptr, apply_scale});
+    ++st->launches;
+    CU(cudaGetLastError());
+    return 0;
+}
+
+int qcs_read_stride(qcs_dev_state_t st, uint64_t j, int apply_scale, double* re, double* im)
+{
+    if (!st) return set_err(QCS_E_INVALID, "null state");
+    if (j >= st->d.NS) return set_err(QCS_E_RANGE, "stride index out of range");
+    cudaSetDevice(st->device);
+    std::vector<uint64_t> one(1, j);
+    uint64_t* dj = st->d.job_stride;
+    CU(cudaMemcpyAsync(dj, &j, 8, cudaMemcpyHostToDevice, st->stream));
+    k_decode<<<1, 256, 0, st->stream>>>(st->d, DecodeJob{dj, apply_scale});
+    ++st->launches;
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(st->stream));
+    const uint64_t L = st->d.L;
+    CU(cudaMemcpy(re, st->d.X + j * 2 * L, L * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(im, st->d.X + j * 2 * L + L, L * 8, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int qcs_to_amplitudes(qcs_dev_state_t st, double* amps)
+{
+    if (!st || !amps) return set_err(QCS_E_INVALID, "null argument");
+    cudaSetDevice(st->device);
+    int rc = decode_all(st, 1);
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(st->stream));
+    const uint64_t L = st->d.L;
+    std::vector<double> buf(2 * L);
+    for (uint64_t j = 0; j < st->d.NS; ++j) {
+        CU(cudaMemcpy(buf.data(), st->d.X + j * 2 * L, 16 * L, cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < L; ++i) {
+            amps[2 * (j * L + i)] = buf[i];
+            amps[2 * (j * L + i) + 1] = buf[L + i];
+        }
+    }
+    return 0;
+}
+
+int qcs_state_stats(qcs_dev_state_t st, uint64_t* bytes, double* min_ratio, double* norm_sq)
+{
+    if (!st) return set_err(QCS_E_INVALID, "null state");
+    cudaSetDevice(st->device);
+    k_stats<<<1, 32, 0, st->stream>>>(st->d);
+    ++st->launches;
+    int rc = sync_and_check(st);
+    if (rc) return rc;
+    if (bytes) *bytes = st->h_sc->compressed_bytes;
+    if (min_ratio) *min_ratio = st->h_sc->min_ratio;
+    if (norm_sq) *norm_sq = st->h_sc->norm_sq;
+    return 0;
+}
+
+int qcs_stride_info(qcs_dev_state_t st, uint64_t j, double* scale, double* ssq, uint64_t* rl,
+                    uint64_t* il)
+{
+    if (!st) return set_err(QCS_E_INVALID, "null state");
+    if (j >= st->d.NS) return set_err(QCS_E_RANGE, "stride index out of range");
+    cudaSetDevice(st->device);
+    CU(cudaStreamSynchronize(st->stream));
+    double a = 0, b = 0;
+    uint64_t l[2];
+    CU(cudaMemcpy(&a, st->d.scale + j, 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(&b, st->d.sum_sq + j, 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(l, st->d.p_len + 2 * j, 16, cudaMemcpyDeviceToHost));
+    if (scale) *scale = a;
+    if (ssq) *ssq = b;
+    if (rl) *rl = l[0];
+    if (il) *il = l[1];
+    return 0;
+}
+
+static void put_header(uint8_t* p, int codec, double delta, uint64_t count, uint64_t plen)
+{
+    p[0] = 'Q';
+    p[1] = 'C';
+    p[2] = 'S';
+    p[3] = '1';
+    p[4] = (uint8_t)codec;
+    uint64_t w;
+    memcpy(&w, &delta, 8);
+    for (int i = 0; i < 8; ++i) p[5 + i] = (uint8_t)(w >> (8 * i));
+    for (int i = 0; i < 8; ++i) p[13 + i] = (uint8_t)(count >> (8 * i));
+    for (int i = 0; i < 8; ++i) p[21 + i] = (uint8_t)(plen >> (8 * i));
+}
+
+static uint64_t rd64(const uint8_t* p)
+{
+    uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= (uint64_t)p[i] << (8 * i);
+    return v;
+}
+
+int qcs_export_blocks(qcs_dev_state_t st, uint64_t j, uint8_t* buf, uint64_t cap, uint64_t* len,
+                      double* scale, double* ssq)
+{
+    if (!st || !len) return set_err(QCS_E_INVALID, "null argument");
+    if (j >= st->d.NS) return set_err(QCS_E_RANGE, "stride index out of range");
+    cudaSetDevice(st->device);
+    CU(cudaStreamSynchronize(st->stream));
+    uint64_t off[2], pl[2];
+    int8_t codec[2];
+    double delta[2];
+    int cur = 0;
+    CU(cudaMemcpy(off, st->d.p_off + 2 * j, 16, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(pl, st->d.p_len + 2 * j, 16, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(codec, st->d.p_codec + 2 * j, 2, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(delta, st->d.p_delta + 2 * j, 16, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(&cur, &st->d.sc->cur, sizeof(int), cudaMemcpyDeviceToHost));
+    *len = 2 * HEADER_BYTES + pl[0] + pl[1];
+    if (scale) CU(cudaMemcpy(scale, st->d.scale + j, 8, cudaMemcpyDeviceToHost));
+    if (ssq) CU(cudaMemcpy(ssq, st->d.sum_sq + j, 8, cudaMemcpyDeviceToHost));
+    if (!buf) return 0;
+    if (*len > cap) return set_err(QCS_E_CAPACITY, "output buffer too small");
+    uint64_t o = 0;
+    for (int c = 0; c < 2; ++c) {
+        put_header(buf + o, codec[c], delta[c], st->d.L, pl[c]);
+        o += HEADER_BYTES;
+        if (pl[c]) CU(cudaMemcpy(buf + o, st->d.arena[cur] + off[c], pl[c], cudaMemcpyDeviceToHost));
+        o += pl[c];
+    }
+    return 0;
+}
+
+int qcs_import_blocks(qcs_dev_state_t st, uint64_t j, const uint8_t* buf, uint64_t len,
+                      double scale, double ssq)
+{
+    if (!st || !buf) return set_err(QCS_E_INVALID, "null argument");
+    if (j >= st->d.NS) return set_err(QCS_E_RANGE, "stride index out of range");
+    cudaSetDevice(st->device);
+    Dev& d = st->d;
+    // parse_block (codec.cpp:391-420) for both planes
+    uint64_t o = 0, poff[2], plen[2];
+    int codec[2];
+    double delta[2];
+    for (int c = 0; c < 2; ++c) {
+        if (o + HEADER_BYTES > len) return set_err(QCS_E_TRUNCATED, "block header extends past end of data");
+        const uint8_t* p = buf + o;
+        if (p[0] != 'Q' || p[1] != 'C' || p[2] != 'S' || p[3] != '1') return set_err(QCS_E_BAD_MAGIC, "bad block magic");
+        codec[c] = p[4];
+        if (codec[c] != 0 && codec[c] != 1) return set_err(QCS_E_UNKNOWN_CODEC, "unknown codec id %d", codec[c]);
+        uint64_t w = rd64(p + 5);
+        memcpy(&delta[c], &w, 8);
+        const uint64_t count = rd64(p + 13);
+        plen[c] = rd64(p + 21);
+        o += HEADER_BYTES;
+        if (o + plen[c] > len) return set_err(QCS_E_TRUNCATED, "block payload extends past end of data");
+        if (count != d.L) return set_err(QCS_E_INVALID, "block length disagrees with geometry");
+        poff[c] = o;
+        o += plen[c];
+    }
+    CU(cudaStreamSynchronize(st->stream));
+    CU(cudaMemcpy(st->h_sc, d.sc, sizeof(Dev::Scal), cudaMemcpyDeviceToHost));
+    const uint64_t need = ((plen[0] + 15) & ~15ull) + ((plen[1] + 15) & ~15ull);
+    if (st->h_sc->bump + need > d.arena_cap) return set_err(QCS_E_NOMEM, "block arena exhausted");
+    const int cur = st->h_sc->cur;
+    uint64_t at = st->h_sc->bump;
+    uint64_t new_off[2];
+    for (int c = 0; c < 2; ++c) {
+        new_off[c] = at;
+        if (plen[c]) CU(cudaMemcpy(d.arena[cur] + at, buf + poff[c], plen[c], cudaMemcpyHostToDevice));
+        at += (plen[c] + 15) & ~15ull;
+    }
+    // validate into a scratch side table first so a bad block leaves the state intact
+    uint64_t old_off[2], old_len[2];
+    int8_t old_codec[2];
+    double old_delta[2];
+    CU(cudaMemcpy(old_off, d.p_off + 2 * j, 16, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(old_len, d.p_len + 2 * j, 16, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(old_codec, d.p_codec + 2 * j, 2, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(old_delta, d.p_delta + 2 * j, 16, cudaMemcpyDeviceToHost));
+    int8_t c8[2] = {(int8_t)codec[0], (int8_t)codec[1]};
+    CU(cudaMemcpy(d.p_off + 2 * j, new_off, 16, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d.p_len + 2 * j, plen, 16, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d.p_codec + 2 * j, c8, 2, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d.p_delta + 2 * j, delta, 16, cudaMemcpyHostToDevice));
+    k_index_planes<<<1, 2, 0, st->stream>>>(d, 2 * j, 2);
+    ++st->launches;
+    int rc = sync_and_check(st);
+    if (rc) return rc;
+    if (st->h_sc->err) {
+        const int e = st->h_sc->err;
+        CU(cudaMemcpy(d.p_off + 2 * j, old_off, 16, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(d.p_len + 2 * j, old_len, 16, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(d.p_codec + 2 * j, old_codec, 2, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(d.p_delta + 2 * j, old_delta, 16, cudaMemcpyHostToDevice));
+        k_index_planes<<<1, 2, 0, st->stream>>>(d, 2 * j, 2);
+        Dev::Scal sc = *st->h_sc;
+        sc.err = 0;
+        CU(cudaMemcpy(d.sc, &sc, sizeof sc, cudaMemcpyHostToDevice));
+        CU(cudaStreamSynchronize(st->stream));
+        return set_err(e, "corrupt block for stride %llu", (unsigned long long)j);
+    }
+    Dev::Scal sc = *st->h_sc;
+    sc.bump = at;
+    CU(cudaMemcpy(d.sc, &sc, sizeof sc, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d.scale + j, &scale, 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(d.sum_sq + j, &ssq, 8, cudaMemcpyHostToDevice));
+    return 0;
+}
+
+int qcs_state_memory(qcs_dev_state_t st, uint64_t* arena, uint64_t* side, uint64_t* scratch)
+{
+    if (!st) return set_err(QCS_E_INVALID, "null state");
+    int rc = sync_and_check(st);
+    if (rc) return rc;
+    const Dev& d = st->d;
+    if (arena) *arena = st->h_sc->bump;
+    if (side) *side = 2 * d.NS * d.nsub * sizeof(SideEntry);
+    if (scratch) *scratch = 16 * d.NS * d.L + 2 * d.NS * d.slot_cap + 2 * d.NS * d.nsub * sizeof(SideEntry);
+    return 0;
+}
+
+uint64_t qcs_state_launches(qcs_dev_state_t st) { return st ? st->launches : 0; }
+
+int qcs_state_kernel_stats(qcs_dev_state_t st, double* ns_avg, uint64_t* launches, uint64_t* bytes)
+{
+    if (!st) return set_err(QCS_E_INVALID, "null state");
+    if (ns_avg) *ns_avg = st->codec_launches ? st->codec_ns / st->codec_launches : 0.0;
+    if (launches) *launches = st->codec_launches;
+    if (bytes) *bytes = st->codec_bytes;
+    return 0;
+}
+
+int qcs_codec_compress(const double* x, uint64_t n, double delta, uint8_t* out, uint64_t cap,
+                       uint64_t* len)
+{
+    if (!len || (!x && n)) return set_err(QCS_E_INVALID, "null argument");
+    if (!(delta >= 0.0) || !std::isfinite(delta)) return set_err(QCS_E_INVALID, "error bound must be finite and >= 0");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(QCS_E_CUDA, "no CUDA device available (the codec has no CPU path)");
+    }
+    for (uint64_t i = 0; i < n; ++i)  // require_finite (codec.cpp:83-91): input argument check
+        if (!std::isfinite(x[i])) return set_err(QCS_E_BAD_VALUE, "NaN/Inf cannot be compressed");
+    const uint64_t nsub = (n + SUB - 1) / SUB;
+    const uint64_t pcap = payload_cap(n);
+    double* dx = nullptr;
+    uint8_t* dout = nullptr;
+    SideEntry* dside = nullptr;
+    uint64_t* dlen = nullptr;
+    cudaStream_t s = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(dx);
+        cudaFree(dout);
+        cudaFree(dside);
+        cudaFree(dlen);
+        if (s) cudaStreamDestroy(s);
+    };
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(&dx, std::max<uint64_t>(8 * n, 16)) != cudaSuccess ||
+        cudaMalloc(&dout, 2 * pcap) != cudaSuccess ||
+        cudaMalloc(&dside, std::max<uint64_t>(2 * nsub, 1) * sizeof(SideEntry)) != cudaSuccess ||
+        cudaMalloc(&dlen, 16) != cudaSuccess) {
+        cleanup();
+        return set_err(QCS_E_NOMEM, "device allocation failed");
+    }
+    cudaMemcpyAsync(dx, x, 8 * n, cudaMemcpyHostToDevice, s);
+    cudaMemsetAsync(dlen, 0, 16, s);
+    EncodeArgs a{};
+    a.X = dx;
+    a.n = n;
+    a.job_stride = nullptr;
+    a.pending = nullptr;
+    a.planes = 1;
+    a.snap = 0;
+    a.out = dout;
+    a.cap = pcap;
+    a.side = dside;
+    a.nsub = nsub;
+    a.out_len = dlen;
+    a.sumsq = nullptr;
+    a.cp = make_params(delta);
+    int rc = n ? launch_encode(a, 1, s) : 0;
+    uint64_t plen = 0;
+    if (!rc) {
+        cudaMemcpyAsync(&plen, dlen, 8, cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) rc = set_err(QCS_E_CUDA, "codec kernel failed");
+    }
+    if (!rc) {
+        *len = HEADER_BYTES + plen;
+        if (out) {
+            if (*len > cap) {
+                rc = set_err(QCS_E_CAPACITY, "output buffer too small");
+            } else {
+                put_header(out, a.cp.lossy ? 1 : 0, delta, n, plen);
+                if (plen && cudaMemcpy(out + HEADER_BYTES, dout, plen, cudaMemcpyDeviceToHost) != cudaSuccess)
+                    rc = set_err(QCS_E_CUDA, "copy failed");
+            }
+        }
+    }
+    cleanup();
+    return rc;
+}
+
+int qcs_codec_decompress(const uint8_t* blk, uint64_t len, double* out, uint64_t n)
+{
+    if (!blk || (!out && n)) return set_err(QCS_E_INVALID, "null argument");
+    // parse_block (codec.cpp:391-420)
+    if (len < HEADER_BYTES) return set_err(QCS_E_TRUNCATED, "block header extends past end of data");
+    if (blk[0] != 'Q' || blk[1] != 'C' || blk[2] != 'S' || blk[3] != '1') return set_err(QCS_E_BAD_MAGIC, "bad block magic");
+    const int codec = blk[4];
+    if (codec != 0 && codec != 1) return set_err(QCS_E_UNKNOWN_CODEC, "unknown codec id %d", codec);
+    double delta;
+    uint64_t w = rd64(blk + 5);
+    memcpy(&delta, &w, 8);
+    const uint64_t count = rd64(blk + 13), plen = rd64(blk + 21);
+    if (HEADER_BYTES + plen > len) return set_err(QCS_E_TRUNCATED, "block payload extends past end of data");
+    if (count != n) return set_err(QCS_E_INVALID, "output span does not match scalar count");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(QCS_E_CUDA, "no CUDA device available (the codec has no CPU path)");
+    }
+    uint8_t* din = nullptr;
+    double* dout = nullptr;
+    int* derr = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(din);
+        cudaFree(dout);
+        cudaFree(derr);
+    };
+    if (cudaMalloc(&din, std::max<uint64_t>(plen, 16)) != cudaSuccess ||
+        cudaMalloc(&dout, std::max<uint64_t>(8 * n, 16)) != cudaSuccess || cudaMalloc(&derr, 4) != cudaSuccess) {
+        cleanup();
+        return set_err(QCS_E_NOMEM, "device allocation failed");
+    }
+    int herr = 0;
+    if (plen) cudaMemcpy(din, blk + HEADER_BYTES, plen, cudaMemcpyHostToDevice);
+    k_decode_payload<<<1, 1>>>(din, plen, codec, delta, n, dout, derr);
+    cudaError_t e = cudaMemcpy(&herr, derr, 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+        cleanup();
+        return set_err(QCS_E_CUDA, "decode kernel failed: %s", cudaGetErrorString(e));
+    }
+    if (herr) {
+        cleanup();
+        return set_err(herr, herr == QCS_E_TRUNCATED ? "payload truncated" : "malformed payload");
+    }
+    if (n) cudaMemcpy(out, dout, 8 * n, cudaMemcpyDeviceToHost);
+    cleanup();
+    return 0;
+}
+
+}  // extern "C"

@@ -74,14 +74,16 @@ def _f(v: float) -> str:
 
 
 def emit_csv(records: Sequence[GateRecord], with_elapsed: bool = True) -> str:
+    """with_elapsed=False drops the wall-time column, like strip_elapsed."""
     out = ["gate_index,gate_label,stride_count,min_ratio,mean_ratio,"
            "max_chosen_delta,bytes_before,bytes_after,elapsed_ns,norm_after"]
     for r in records:
         out.append(",".join([str(r.gate_index), r.gate_label, str(r.stride_count),
                              _f(r.min_ratio), _f(r.mean_ratio), _f(r.max_chosen_delta),
                              str(r.bytes_before), str(r.bytes_after),
-                             str(r.elapsed_ns if with_elapsed else 0), _f(r.norm_after)]))
-    return "\n".join(out) + "\n"
+                             str(r.elapsed_ns), _f(r.norm_after)]))
+    text = "\n".join(out) + "\n"
+    return text if with_elapsed else strip_elapsed(text)
 
 
 def strip_elapsed(csv: str) -> str:

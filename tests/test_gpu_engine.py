@@ -1,0 +1,124 @@
+"""Engine parity on the GPU: per-gate records (every GateRecord field except
+wall time), final amplitudes, stored blocks, scales and sums must equal the
+oracle's / the reference's bit for bit."""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import first_diff, golden_program, golden_runs, gpu_run, oracle_run, sha
+from paper_1811_05140_b200 import circuit as cc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def q():
+    import paper_1811_05140_b200 as q
+    return q
+
+
+@pytest.mark.parametrize("name", sorted(golden_runs()))
+def test_engine_matches_golden(q, name):
+    e = golden_runs()[name]
+    prog = golden_program(e)
+    res, csv = gpu_run(prog, e["stride_bits"], e["basis"], e["ladder"], e["theta"])
+    assert csv == e["csv"], first_diff(e["csv"], csv)
+    assert sha(res.state.to_amplitudes()) == e["amps_sha256"]
+    assert res.state.compressed_bytes() == e["compressed_bytes"]
+    assert res.state.norm_sq_tracked() == e["norm_sq_tracked"]
+
+
+CASES = [
+    ("qft", 11, 5, 0, [0.0, 1e-7, 1e-6, 1e-5, 1e-4, 1e-3], 16.0),
+    ("qft", 9, 9, 3, [2.0 ** -16], 1.0),
+    ("qft", 12, 3, 1, [0.0], 1.0),
+    ("qft", 13, 13, 777, [1e-3 * 2 ** -7], 1.0),       # non-power-of-two bound: serial repair path
+    ("grover_gates", 11, 6, 0, [2.0 ** -20], 1.0),
+    ("grover_ref", 9, 4, 0, [0.0, 1e-6, 1e-4], 32.0),
+    ("grid", 9, 4, 0, [2.0 ** -14], 1.0),
+]
+
+
+def _prog(kind, n):
+    if kind == "qft":
+        return cc.build_qft(n)
+    if kind == "grover_gates":
+        return cc.build_grover_gate_form(n, 77, 3)
+    if kind == "grover_ref":
+        return cc.build_grover(n, 33, 6)
+    return cc.build_grid(3, 3, 10, 3)
+
+
+@pytest.mark.parametrize("kind,n,s,basis,ladder,theta", CASES)
+def test_engine_matches_oracle(q, oracle, kind, n, s, basis, ladder, theta):
+    prog = _prog(kind, n)
+    st, want = oracle_run(oracle, prog, s, basis, ladder, theta)
+    res, got = gpu_run(prog, s, basis, ladder, theta)
+    assert got == want, first_diff(want, got)
+    assert res.state.to_amplitudes().tobytes() == st.amplitudes().tobytes()
+    for j in range(1 << (n - s)):
+        blocks, scale, ssq = res.state.export_blocks(j)
+        assert blocks == st.export_blocks(j), f"stride {j}"
+        osc, ossq, _, _ = st.stride_info(j)
+        assert (scale, ssq) == (osc, ossq), f"stride {j}"
+
+
+def test_apply_gate_reports_and_norm(q, oracle):
+    n, s = 8, 4
+    geom = q.StateGeometry.make(n, s)
+    st = q.CompressedState.basis_state(geom, 0)
+    ost = oracle.state(n, s, 0)
+    lad = q.ErrorBoundLadder.lossless_only()
+    for k in range(8):
+        g = cc.GateOp.single(cc.Unitary2x2.hadamard(), k, "h")
+        r = st.apply_gate(g, lad, q.RatioThreshold(1.0))
+        orr, on = ost.apply_gate(g, [0.0], 1.0)
+        assert [x.as_tuple() for x in r.reports] == orr
+        assert r.norm_after == on
+    g = cc.GateOp.controlled(cc.Unitary2x2.phase(0.3), 7, 0, "cp 7 0")
+    r = st.apply_gate(g, lad, q.RatioThreshold(1.0))
+    assert len(r.reports) == geom.n_strides() // 2
+    assert all(x.stride_index & (geom.n_strides() >> 1) for x in r.reports)
+
+
+def test_errors_leave_state_intact(q):
+    geom = q.StateGeometry.make(4, 2)
+    st = q.CompressedState.basis_state(geom, 3)
+    before = st.to_amplitudes().copy()
+    with pytest.raises(IndexError):
+        st.apply_gate(cc.GateOp.single(cc.Unitary2x2.pauli_x(), 9, "x 9"),
+                      q.ErrorBoundLadder.lossless_only())
+    with pytest.raises(IndexError):
+        st.apply_gate(cc.GateOp.phase_flip(100), q.ErrorBoundLadder.lossless_only())
+    assert st.to_amplitudes().tobytes() == before.tobytes()
+
+
+def test_checkpoint_round_trip_and_resume(q, tmp_path):
+    geom = q.StateGeometry.make(10, 6)
+    prog = cc.build_qft(10)
+    lad = q.ErrorBoundLadder.default_ladder()
+    th = q.RatioThreshold(8.0)
+    straight = q.run_program(prog, lad, th, geom, q.RunOptions(basis=1))
+    half = q.run_program(prog, lad, th, geom, q.RunOptions(basis=1, stop_after=35))
+    path = str(tmp_path / "mid.qckp")
+    half.state.save(path, lad.fingerprint())
+    st, fp = q.CompressedState.load(path, geom)
+    assert fp == lad.fingerprint()
+    resumed = q.run_program_on(st, prog, lad, th, q.RunOptions(first_gate=35))
+    assert resumed.state.to_amplitudes().tobytes() == straight.state.to_amplitudes().tobytes()
+    with open(path, "r+b") as f:
+        f.seek(4)
+        f.write(bytes([99]))
+    with pytest.raises(q.CheckpointError) as e:
+        q.CompressedState.load(path)
+    assert e.value.kind == "version_mismatch"
+
+
+def test_degenerate_wipe_stays_finite(q):
+    geom = q.StateGeometry.make(8, 4)
+    r = q.run_program(cc.build_qft(8), q.ErrorBoundLadder.make([0.5]), q.RatioThreshold(1.0),
+                      geom, q.RunOptions(basis=1))
+    a = r.state.to_amplitudes()
+    assert np.all(np.isfinite(a))
+    assert float(np.sum(np.abs(a) ** 2)) == 0.0
