@@ -166,7 +166,10 @@ __device__ __forceinline__ uint64_t block_scan_sat(uint64_t v, uint64_t* wsum, u
         tot = sat_add(tot, wsum[i]);
     }
     total = tot;
-    return sat_add(pre, inc - v);  // inc - v is exact: no saturation inside one warp of <=2^57
+    // exclusive prefix from the neighbour's inclusive value (inc - v would be
+    // wrong once this thread's own value saturated)
+    const uint64_t prev = __shfl_up_sync(0xffffffffu, inc, 1);
+    return sat_add(pre, wl ? prev : 0);
 }
 
 // t_k = fl(fl(re^2) + fl(im^2)) at iteration-local element k.
@@ -234,6 +237,9 @@ __device__ void sumsq_iteration(double* xs, int n_it, EncShared& S)
             if (ms + run >= (1ull << 53)) bad = k;
         }
         const long long kstar = block_min_ll(bad, S.wmin);
+#ifdef SUMSQ_TRACE
+        if (tid == 0) printf("k0=%d s=%.17g e=%d ms=%llu total=%llu kstar=%lld\n", k0, s, e, (unsigned long long)ms, (unsigned long long)total, kstar);
+#endif
         if (kstar == LLONG_MAX) {
             if (tid == 0) S.s = (double)(ms + total) / to_units;  // exact
             break;
@@ -297,7 +303,8 @@ __device__ __forceinline__ uint64_t plane_sum_scan(uint64_t v, EncShared& S, int
 // the lane closes it (emit_tail).
 template <typename FR, typename FC, typename FW>
 __device__ __forceinline__ void lane_walk(const int16_t* cl, int cnt, uint64_t e0, int in_ty,
-                                          uint64_t in_st, bool tail_closes, FR on_run,
+                                          uint64_t in_st, bool tail_closes, bool close_carried,
+                                          FR on_run,
                                           FC on_code, FW on_word)
 {
     int cur = TY_NONE;
@@ -305,6 +312,9 @@ __device__ __forceinline__ void lane_walk(const int16_t* cl, int cnt, uint64_t e
     if (cnt > 0 && in_ty != TY_NONE && ty16(cl[0]) == in_ty) {
         cur = in_ty;
         cst = in_st;
+    } else if (close_carried && in_ty != TY_NONE) {
+        // run carried over from the previous CTA iteration ends right here
+        on_run(in_ty, in_st, e0);
     }
     for (int i = 0; i < cnt; ++i) {
         const uint64_t k = e0 + i;
@@ -498,7 +508,7 @@ __global__ void __launch_bounds__(CODEC_THREADS, 2) k_encode(EncodeArgs a)
             tail_st = cst;
             if (lane + 1 < active) tail_closes = (cur != TY_NONE) && (next_ft != cur);
             lane_walk(
-                cl, cnt, e0, in_ty, in_st, tail_closes,
+                cl, cnt, e0, in_ty, in_st, tail_closes, lane == 0,
                 [&](int t, uint64_t st, uint64_t end) {
                     const uint64_t len = end - st;
                     const int vl = varint_len(run_token(LOSSY, t, len));
@@ -556,19 +566,25 @@ __global__ void __launch_bounds__(CODEC_THREADS, 2) k_encode(EncodeArgs a)
             __syncthreads();
         }
 
-        // 9. write tokens; record where runs that span lanes live
+        // 9. write tokens.  The lane that closes a run writes its varint and
+        //    the words of its own elements; runs that span lanes publish their
+        //    token/word position under the lane they started in (unique: a
+        //    lane has at most one run reaching past its end).
         {
             uint64_t pos = bstart;
-            const int lane_lo_start = (int)(e0 >= base ? (e0 - base) / SUB : 0);
-            (void)lane_lo_start;
             lane_walk(
-                cl, cnt, e0, in_ty, in_st, tail_closes,
+                cl, cnt, e0, in_ty, in_st, tail_closes, lane == 0,
                 [&](int t, uint64_t st, uint64_t end) {
                     const uint64_t len = end - st;
                     const uint64_t v = run_token(LOSSY, t, len);
                     const int vl = varint_len(v);
                     put_varint(out + pos, v);
-                    if (st >= base) {
+                    if (t == TY_W) {
+                        for (uint64_t k = (st > e0 ? st : e0); k < end; ++k)
+                            put_word(out + pos + vl + 8 * (k - st),
+                                     (uint64_t)__double_as_longlong(xl[k - e0]));
+                    }
+                    if (st < e0 && st >= base) {
                         const int sl = (int)((st - base) / SUB);
                         S.runtok[pl][sl] = pos;
                         S.runw[pl][sl] = pos + vl;
@@ -592,15 +608,13 @@ __global__ void __launch_bounds__(CODEC_THREADS, 2) k_encode(EncodeArgs a)
         }
         __syncthreads();
 
-        // 10. words of W runs, placed by the lane that owns each element
-        lane_walk(
-            cl, cnt, e0, in_ty, in_st, tail_closes, [&](int, uint64_t, uint64_t) {},
-            [&](int16_t) {},
-            [&](uint64_t k, uint64_t st) {
-                const uint64_t wb = st < base ? C.carry_w : S.runw[pl][(st - base) / SUB];
-                put_word(out + wb + 8 * (k - st),
-                         (uint64_t)__double_as_longlong(xl[k - e0]));
-            });
+        // 10. words of a W run that reaches past this lane (closed later, or
+        //     carried into the next iteration)
+        if (cnt > 0 && tail_ty == TY_W && !tail_closes) {
+            const uint64_t wb = tail_st < base ? C.carry_w : S.runw[pl][(tail_st - base) / SUB];
+            for (uint64_t k = (tail_st > e0 ? tail_st : e0); k < e0 + cnt; ++k)
+                put_word(out + wb + 8 * (k - tail_st), (uint64_t)__double_as_longlong(xl[k - e0]));
+        }
 
         // 11. side index
         if (cnt > 0) {
@@ -613,7 +627,12 @@ __global__ void __launch_bounds__(CODEC_THREADS, 2) k_encode(EncodeArgs a)
                 bool full = t0 != TY_C;
                 for (int i = 1; i < cnt && full; ++i) full = ty16(cl[i]) == t0;
                 const bool emitted_here = !full || tail_closes;
-                se.off = (uint32_t)(emitted_here ? bstart : S.runtok[pl][lane]);
+                uint64_t cover = bstart;
+                if (lane == 0 && in_ty != TY_NONE) {  // carried run closed at e0 precedes us
+                    const uint64_t len = e0 - in_st;
+                    cover += varint_len(run_token(LOSSY, in_ty, len)) + (in_ty == TY_W ? 8 * len : 0);
+                }
+                se.off = (uint32_t)(emitted_here ? cover : S.runtok[pl][lane]);
                 se.skip = 0;
             }
             se.pred = LOSSY ? S.entryP[pl][lane] : 0.0;
@@ -668,7 +687,9 @@ __device__ __forceinline__ void decode_sub(const uint8_t* in, int codec, double 
     double P = se.pred;
     int produced = 0;
     const bool sc = scale != 1.0;
+    int guard = 0;
     while (produced < cnt) {
+        if (++guard > 4 * SUB + 8) break;  // corrupt side index: never spin
         const uint64_t v = get_varint(in, pos);
         if (codec == 1) {
             const unsigned tag = (unsigned)(v & 3u);

@@ -1329,4 +1329,32 @@ int qcs_codec_decompress(const uint8_t* blk, uint64_t len, double* out, uint64_t
     return 0;
 }
 
+
+// Test hook: lossless-encode a (re, im) stride pair and return the stored
+// sum of squares the engine would record (StrideBuffer::sum_sq, core.cpp:30-37).
+int qcs_debug_stride_sumsq(const double* re, const double* im, uint64_t n, double* out)
+{
+    const uint64_t nsub = (n + SUB - 1) / SUB, pcap = payload_cap(n);
+    double *dx = nullptr, *dsum = nullptr;
+    uint8_t* dout = nullptr;
+    SideEntry* dside = nullptr;
+    uint64_t* dlen = nullptr;
+    int rc = 0;
+    if (cudaMalloc(&dx, 16 * n + 16) != cudaSuccess || cudaMalloc(&dsum, 8) != cudaSuccess ||
+        cudaMalloc(&dout, 2 * pcap) != cudaSuccess || cudaMalloc(&dside, 2 * nsub * sizeof(SideEntry) + 16) != cudaSuccess ||
+        cudaMalloc(&dlen, 16) != cudaSuccess) {
+        rc = set_err(QCS_E_NOMEM, "device allocation failed");
+    } else {
+        cudaMemcpy(dx, re, 8 * n, cudaMemcpyHostToDevice);
+        cudaMemcpy(dx + n, im, 8 * n, cudaMemcpyHostToDevice);
+        EncodeArgs a{};
+        a.X = dx; a.n = n; a.planes = 2; a.snap = 0; a.out = dout; a.cap = pcap;
+        a.side = dside; a.nsub = nsub; a.out_len = dlen; a.sumsq = dsum; a.cp = make_params(0.0);
+        rc = launch_encode(a, 1, 0);
+        if (!rc && cudaMemcpy(out, dsum, 8, cudaMemcpyDeviceToHost) != cudaSuccess) rc = set_err(QCS_E_CUDA, "copy failed");
+    }
+    cudaFree(dx); cudaFree(dsum); cudaFree(dout); cudaFree(dside); cudaFree(dlen);
+    return rc;
+}
+
 }  // extern "C"

@@ -43,7 +43,7 @@ def test_codec_fuzz_vs_oracle(q, oracle, n):
         for d in (0.0, 1e-6, 2.0 ** -20, 2.0 ** -12, 0.37):
             want = oracle.compress(x, d)
             got = q.compress(x, d)
-            assert got == want, f"n={n} d={d}: first diff at byte " + str(
+            assert got == want, f"n={n} d={d} kind={x[:3]}: len {len(got)} vs {len(want)}, first diff at byte " + str(
                 next((i for i, (a, b) in enumerate(zip(got, want)) if a != b), min(len(got), len(want))))
             y = q.decompress(got, n)
             assert y.tobytes() == oracle.decompress(want, n).tobytes()
