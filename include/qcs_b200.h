@@ -75,6 +75,8 @@ typedef struct {
     uint64_t elapsed_ns;
     double norm_after;
     uint64_t threshold_violations;
+    uint64_t compressed_in;  /* stored bytes (headers included) of the blocks the
+                                gate read and rewrote: the roofline's C_in */
 } qcs_gate_record;
 
 typedef struct qcs_dev_state* qcs_dev_state_t;
@@ -132,10 +134,17 @@ int qcs_state_memory(qcs_dev_state_t st, uint64_t* arena_bytes, uint64_t* side_b
                      uint64_t* scratch_bytes);
 /* Number of kernel launches issued by this state so far (bench accounting). */
 uint64_t qcs_state_launches(qcs_dev_state_t st);
-/* Average device time (ns) of the fused codec kernel over the last
- * qcs_run_program call, and its launch count (roofline accounting). */
-int qcs_state_kernel_stats(qcs_dev_state_t st, double* codec_ns_avg,
-                           uint64_t* codec_launches, uint64_t* codec_bytes);
+/* Per-kernel-class device timing with CUDA events on the engine's stream
+ * (bench roofline accounting).  Classes: 0 decode, 1 gate, 2 encode,
+ * 3 commit+norm, 4 mean pass, 5 bookkeeping.  Enabling resets the totals;
+ * totals cover every gate enqueued while enabled. */
+int qcs_state_profile(qcs_dev_state_t st, int enable);
+int qcs_state_kernel_time(qcs_dev_state_t st, int kernel_class, double* total_ns,
+                          uint64_t* launches);
+/* Cumulative device diagnostics of the codec kernel: [0] lanes whose entry
+ * predictor guess was wrong and were re-run serially, [1] passes of the exact
+ * sum-of-squares emulation, [2] bytes slid to close carried word runs. */
+int qcs_state_counters(qcs_dev_state_t st, uint64_t* out, int n);
 
 /* Codec plugin (codec.hpp:80-105): compress(x, ErrorBound(delta)) then
  * serialize_block.  out receives the 29-byte QCS1 header + payload; cap may

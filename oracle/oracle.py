@@ -203,6 +203,35 @@ class Reference:
         if rc:
             raise OracleError(rc, self.lib.ref_last_error().decode())
 
+    def state(self, text: str, stride_bits: int, basis: int):
+        self.lib.ref_state_create.restype = C.c_void_p
+        self.lib.ref_state_create.argtypes = [C.c_char_p, C.c_int, C.c_uint64]
+        self.lib.ref_state_apply.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_double),
+                                             C.c_int, C.c_double, C.c_int, C.POINTER(C.c_double)]
+        self.lib.ref_state_stats.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+        self.lib.ref_state_destroy.argtypes = [C.c_void_p]
+        h = self.lib.ref_state_create(text.encode(), stride_bits, C.c_uint64(basis))
+        if not h:
+            raise OracleError(1, self.lib.ref_last_error().decode())
+        ref = self
+
+        class _S:
+            def apply(s, first, last, ladder, theta, workers=0):
+                lad = (C.c_double * len(ladder))(*ladder)
+                out = (C.c_double * 4)()
+                ref._check(ref.lib.ref_state_apply(h, first, last, lad, len(ladder),
+                                                   C.c_double(theta), workers, out))
+                return dict(gate_ns=out[0], amp_updates=out[1], min_ratio=out[2], norm=out[3])
+
+            def stats(s):
+                out = (C.c_double * 3)()
+                ref.lib.ref_state_stats(h, out)
+                return dict(compressed_bytes=out[0], min_ratio=out[1], norm_sq=out[2])
+
+            def __del__(s):
+                ref.lib.ref_state_destroy(h)
+        return _S()
+
     def max_threads(self) -> int:
         return self.lib.ref_max_threads()
 

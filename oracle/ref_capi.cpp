@@ -13,6 +13,7 @@
 //   run_dense / fidelity                                        (dense.hpp)
 //   emit_csv                                                    (metrics.hpp:66)
 
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -207,6 +208,67 @@ int ref_dense(const char* circuit_text, std::uint64_t basis, double* amps)
     } catch (const std::exception& e) {
         return fail(classify(e), e.what());
     }
+}
+
+// Persistent reference state for windowed timing (bench.py --impl reference):
+// CompressedState::basis_state then apply_program_range over [first, last).
+struct RefState {
+    qcs::CircuitProgram prog;
+    qcs::CompressedState state;
+};
+
+void* ref_state_create(const char* circuit_text, int stride_bits, std::uint64_t basis)
+{
+    try {
+        auto* r = new RefState();
+        r->prog = qcs::parse_circuit(circuit_text);
+        r->state = qcs::CompressedState::basis_state(
+            qcs::StateGeometry::make(r->prog.n_qubits, stride_bits), basis);
+        return r;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+void ref_state_destroy(void* h) { delete static_cast<RefState*>(h); }
+
+// summary[4]: sum of GateRecord.elapsed_ns, amplitude updates, min ratio,
+// norm_after of the last gate.
+int ref_state_apply(void* h, std::uint64_t first, std::uint64_t last, const double* ladder,
+                    int n_levels, double theta, int workers, double* summary)
+{
+    try {
+        auto* r = static_cast<RefState*>(h);
+        const qcs::ErrorBoundLadder lad = qcs::ErrorBoundLadder::make(
+            std::vector<double>(ladder, ladder + n_levels));
+        const qcs::RunMetrics m = qcs::apply_program_range(
+            r->state, r->prog, first, last, lad, qcs::RatioThreshold(theta), workers);
+        std::uint64_t ns = 0, upd = 0;
+        double mn = 1e300, norm = 0.0;
+        for (const qcs::GateRecord& g : m.records) {
+            ns += g.elapsed_ns;
+            upd += g.bytes_before / 16;
+            mn = std::min(mn, g.min_ratio);
+            norm = g.norm_after;
+        }
+        summary[0] = static_cast<double>(ns);
+        summary[1] = static_cast<double>(upd);
+        summary[2] = mn;
+        summary[3] = norm;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(classify(e), e.what());
+    }
+}
+
+int ref_state_stats(void* h, double* out)
+{
+    auto* r = static_cast<RefState*>(h);
+    out[0] = static_cast<double>(r->state.compressed_bytes());
+    out[1] = r->state.min_stride_ratio();
+    out[2] = r->state.norm_sq_tracked();
+    return 0;
 }
 
 }  // extern "C"

@@ -69,6 +69,8 @@ __device__ __forceinline__ void fn_apply(RunFn F, int& ty, uint64_t& st)
 // ---------------------------------------------------------------------------
 struct PlaneCarry {
     double P;            // exact predictor entering the next iteration
+    double xprev;        // last input of the previous iteration (escape prediction)
+    double xprev_next;
     uint64_t out_pos;    // payload bytes of closed tokens
     int open_ty;         // run still open at the end of the last iteration
     uint64_t open_start;
@@ -85,6 +87,8 @@ struct PlaneCarry {
     uint64_t mv_shift;
 };
 
+constexpr int MAXPIN = 96;  // pinned exact steps per plane and iteration
+
 struct EncShared {
     double entryP[2][PLANE_LANES];
     double exitP[2][PLANE_LANES];
@@ -95,16 +99,26 @@ struct EncShared {
     uint32_t bytes[2][PLANE_LANES];
     int8_t ftype[2][PLANE_LANES + 1];
     RunFn wfn[8];
+    long long wesc_i[8];
+    double wesc_v[8];
     uint64_t wsum[8];
     long long wmin[8];
     PlaneCarry carry[2];
+    long long pin_idx[2][MAXPIN];
+    double pin_val[2][MAXPIN];
+    int16_t pin_code[2][MAXPIN];
+    int npin[2];
+    int pin_over[2];
+    long long wfail[8];
+    double fail_prev[2];
     double s;            // exact running sum of squares of the stride
     long long kstar;
     uint64_t mvmax;
 };
 
-constexpr size_t ENC_SMEM = sizeof(double) * 2 * PLANE_LANES * XS_STRIDE +
-                            sizeof(int16_t) * 2 * ITER + sizeof(EncShared) + 64;
+constexpr size_t ENC_S_OFF = ((sizeof(double) * 2 * PLANE_LANES * XS_STRIDE +
+                               sizeof(int16_t) * 2 * ITER) + 15) & ~size_t(15);
+constexpr size_t ENC_SMEM = ENC_S_OFF + sizeof(EncShared);
 
 struct EncodeArgs {
     const double* X;          // input planes
@@ -121,6 +135,8 @@ struct EncodeArgs {
     uint64_t* out_len;        // [2b+c]
     double* sumsq;            // [b] or null
     CodecParams cp;
+    unsigned long long* counters;  // optional: [0] repaired lanes, [1] exact-sum passes,
+                                   // [2] slid bytes, [3] lanes that fell back to the serial chain
 };
 
 __device__ __forceinline__ double& xs_at(double* xs, int pl, int k)
@@ -181,7 +197,7 @@ __device__ __forceinline__ double tsq(double* xs, int k)
 
 // Exact emulation of `for k: s += t_k` (core.cpp:33-35) over this iteration's
 // n_it elements; S.s holds s in and out.  Must be called by all 256 threads.
-__device__ void sumsq_iteration(double* xs, int n_it, EncShared& S)
+__device__ __forceinline__ void sumsq_iteration(double* xs, int n_it, EncShared& S, unsigned long long* counters)
 {
     constexpr int PER = ITER / CODEC_THREADS;  // 16 elements per thread
     const int tid = threadIdx.x;
@@ -191,6 +207,7 @@ __device__ void sumsq_iteration(double* xs, int n_it, EncShared& S)
         __syncthreads();
         const double s = S.s;
         if (k0 >= n_it) break;
+        if (counters && tid == 0) atomicAdd(&counters[1], 1ull);
         if (s == 0.0) {
             long long mine = LLONG_MAX;
             for (int i = 0; i < PER; ++i) {
@@ -274,6 +291,45 @@ __device__ __forceinline__ RunFn plane_fn_scan(RunFn F, EncShared& S, int pl)
     return fn_compose(pre, inc);
 }
 
+// Exclusive "last predicted escape" scan over the plane's lanes: returns the
+// index (or -1) and input value of the last escape before this lane.
+__device__ __forceinline__ long long plane_last_scan(long long idx, double val, EncShared& S, int pl,
+                                                     double& out_val)
+{
+    const int wl = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long ii = idx;
+    double vv = val;
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long ui = __shfl_up_sync(0xffffffffu, ii, o);
+        const double uv = __shfl_up_sync(0xffffffffu, vv, o);
+        if (wl >= o && ii < 0) {
+            ii = ui;
+            vv = uv;
+        }
+    }
+    // exclusive within the warp
+    long long ei = __shfl_up_sync(0xffffffffu, ii, 1);
+    double ev = __shfl_up_sync(0xffffffffu, vv, 1);
+    if (wl == 0) ei = -1;
+    __syncthreads();
+    if (wl == 31) {
+        S.wesc_i[w] = ii;
+        S.wesc_v[w] = vv;
+    }
+    __syncthreads();
+    if (ei < 0) {
+        for (int k = w - 1; k >= pl * 4; --k) {
+            if (S.wesc_i[k] >= 0) {
+                ei = S.wesc_i[k];
+                ev = S.wesc_v[k];
+                break;
+            }
+        }
+    }
+    out_val = ev;
+    return ei;
+}
+
 __device__ __forceinline__ uint64_t plane_sum_scan(uint64_t v, EncShared& S, int pl, uint64_t& total)
 {
     const int wl = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -344,8 +400,7 @@ __global__ void __launch_bounds__(CODEC_THREADS, 2) k_encode(EncodeArgs a)
     extern __shared__ __align__(16) unsigned char smem[];
     double* xs = reinterpret_cast<double*>(smem);
     int16_t* code = reinterpret_cast<int16_t*>(xs + 2 * PLANE_LANES * XS_STRIDE);
-    EncShared& S = *reinterpret_cast<EncShared*>(
-        (reinterpret_cast<uintptr_t>(code + 2 * ITER) + 15) & ~uintptr_t(15));
+    EncShared& S = *reinterpret_cast<EncShared*>(smem + ENC_S_OFF);
 
     const CodecParams cp = a.cp;
     const int tid = threadIdx.x;
@@ -363,6 +418,7 @@ __global__ void __launch_bounds__(CODEC_THREADS, 2) k_encode(EncodeArgs a)
 
     if (lane == 0) {
         C.P = 0.0;
+        C.xprev = 0.0;
         C.out_pos = 0;
         C.open_ty = TY_NONE;
         C.open_start = 0;
@@ -379,73 +435,395 @@ __global__ void __launch_bounds__(CODEC_THREADS, 2) k_encode(EncodeArgs a)
         const int active = pact ? (int)umin64(PLANE_LANES, (n - base + SUB - 1) / SUB) : 0;
         const int n_it = (int)umin64(ITER, n - base);
 
-        // 1. coalesced load (+ snap_zeros)
+        // 1. coalesced asynchronous load (cp.async: every copy of the
+        //    iteration in flight at once), then snap_zeros in shared memory
+#pragma unroll 8
         for (int i = lane; i < ITER; i += PLANE_LANES) {
-            double v = 0.0;
+            double* dst = &xs_at(xs, pl, i);
             if (pact && base + i < n) {
-                v = xg[base + i];
-                if (a.snap) v = snap(v);
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(xg + base + i)
+                             : "memory");
+            } else {
+                *dst = 0.0;
             }
-            xs_at(xs, pl, i) = v;
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        if (a.snap && cnt > 0) {
+            for (int i = 0; i < cnt; ++i) xl[i] = snap(xl[i]);
         }
         __syncthreads();
 
-        // 2. entry predictor: exact for lane 0, guessed for the others
-        double entry = 0.0;
-        if (LOSSY && cnt > 0) {
-            entry = lane == 0 ? C.P
-                              : lattice_guess(cp, xs_at(xs, pl, lane * SUB - 2), xs_at(xs, pl, lane * SUB - 1));
-            S.entryP[pl][lane] = entry;
-        }
-        __syncthreads();
-
-        // 3. every lane runs the reference step over its sub-chunk
-        if (cnt > 0) {
-            double P = entry;
-            for (int i = 0; i < cnt; ++i) {
-                const double x = xl[i];
-                int32_t c;
-                if (LOSSY) {
-                    c = ref_step(cp, P, x);
-                } else {
-                    c = __double_as_longlong(x) == 0 ? 0 : WCODE;
-                    P = x;
+        if (LOSSY && cp.pow2) {
+            // 2-4 (power-of-two bound).  Event rounds: the reference's predictor
+            // after element k is, unless something special happens, the point of
+            // the current anchor's 2*delta lattice nearest x_k.  Anchors are
+            // *events*: the exact predictor carried into the iteration, predicted
+            // escapes (a jump beyond the escape limit + 2*delta escapes whatever
+            // the predictor), and pinned exact steps.  Every non-pinned element
+            // is verified by one reference step from the speculated predictor of
+            // its left neighbour; all elements verified => the speculation IS the
+            // reference chain (induction from the exact carried predictor).  The
+            // first element that fails (rounding drift off the lattice, a missed
+            // or phantom escape, a tie) is pinned with its exact reference step
+            // and the plane is re-verified.  Verification is element-parallel.
+            if (lane == 0) {
+                S.npin[pl] = 0;
+                S.pin_over[pl] = 0;
+            }
+            if (cnt > 0 && lane + 1 == active) C.xprev_next = xl[cnt - 1];
+            __syncthreads();
+            long long f = LLONG_MAX;
+            for (int round = 0;; ++round) {
+                const int np = S.npin[pl];
+                // (a) last event of every lane, then the event entering each lane
+                long long my_last = -1;
+                double my_val = 0.0;
+                if (cnt > 0) {
+                    double xp = lane == 0 ? C.xprev : xs_at(xs, pl, lane * SUB - 1);
+                    int pp = 0;
+                    while (pp < np && S.pin_idx[pl][pp] < (long long)e0) ++pp;
+                    for (int i = 0; i < cnt; ++i) {
+                        const long long k = (long long)e0 + i;
+                        const double x = xl[i];
+                        if (pp < np && S.pin_idx[pl][pp] == k) {
+                            my_last = k;
+                            my_val = S.pin_val[pl][pp];
+                            ++pp;
+                        } else if (predict_escape(cp, x, xp)) {
+                            my_last = k;
+                            my_val = x;
+                        }
+                        xp = x;
+                    }
                 }
-                xl[i] = P;
-                cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
+                double aval;
+                const long long aidx = plane_last_scan(my_last, my_val, S, pl, aval);
+                // (b) speculate and verify every element
+                long long fail = LLONG_MAX;
+                double fprev = 0.0;
+                if (cnt > 0) {
+                    double A = aidx >= 0 ? aval : C.P;
+                    const long long Aidx = aidx >= 0 ? aidx : (long long)base - 1;
+                    double Pprev = (Aidx == (long long)e0 - 1) ? A
+                                   : lattice_point(cp, A, xs_at(xs, pl, lane * SUB - 1));
+                    double xp = lane == 0 ? C.xprev : xs_at(xs, pl, lane * SUB - 1);
+                    int pp = 0;
+                    while (pp < np && S.pin_idx[pl][pp] < (long long)e0) ++pp;
+#pragma unroll 4
+                    for (int i = 0; i < cnt; ++i) {
+                        const long long k = (long long)e0 + i;
+                        const double x = xl[i];
+                        double Ph;
+                        int16_t c16;
+                        if (pp < np && S.pin_idx[pl][pp] == k) {
+                            Ph = S.pin_val[pl][pp];
+                            c16 = S.pin_code[pl][pp];
+                            A = Ph;
+                            ++pp;
+                        } else {
+                            if (predict_escape(cp, x, xp)) {
+                                Ph = x;
+                                A = x;
+                            } else {
+                                Ph = lattice_step(cp, A, x);
+                            }
+                            double P2 = Pprev;
+                            const int32_t c = ref_step(cp, P2, x);
+                            c16 = c == WCODE ? WCODE16 : (int16_t)c;
+                            if (!same_bits(P2, Ph) && fail == LLONG_MAX) {
+                                fail = k;
+                                fprev = Pprev;
+                            }
+                        }
+                        cl[i] = c16;
+                        xp = x;
+                        Pprev = Ph;
+                    }
+                }
+                // (c) first failure of the plane
+                long long m = fail;
+                for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+                if ((threadIdx.x & 31) == 0) S.wfail[threadIdx.x >> 5] = m;
+                __syncthreads();
+                f = LLONG_MAX;
+                for (int w = pl * 4; w < pl * 4 + 4; ++w) f = min(f, S.wfail[w]);
+                if (fail != LLONG_MAX && fail == f) S.fail_prev[pl] = fprev;
+                const bool more = f != LLONG_MAX && S.npin[pl] < MAXPIN;
+                if (!__syncthreads_or(more)) break;
+                if (lane == 0 && more) {  // pin the exact reference step at f
+                    double P = S.fail_prev[pl];
+                    const int32_t c = ref_step(cp, P, xs_at(xs, pl, (int)(f - (long long)base)));
+                    const int q = S.npin[pl];
+                    S.pin_idx[pl][q] = f;
+                    S.pin_val[pl][q] = P;
+                    S.pin_code[pl][q] = c == WCODE ? WCODE16 : (int16_t)c;
+                    S.npin[pl] = q + 1;
+                    if (a.counters) atomicAdd(&a.counters[0], 1ull);
+                }
+                __syncthreads();
             }
-            S.exitP[pl][lane] = P;
+            // (d) pin budget exhausted (e.g. a bound whose lattice never holds):
+            //     the reference's serial chain from the first unverified element.
+            const long long fser = f;  // LLONG_MAX unless the budget ran out
+            // (e) final values: predictor of every element into xs, lane entries
+            {
+                const int np = S.npin[pl];
+                double Pprev = 0.0, xp = 0.0, A = 0.0;
+                if (cnt > 0) {
+                    long long my_last = -1;
+                    double my_val = 0.0;
+                    (void)my_last;
+                    (void)my_val;
+                }
+                // recompute the entering event (same as (a)) before anyone overwrites x
+                long long my_last = -1;
+                double my_val = 0.0;
+                if (cnt > 0) {
+                    double xq = lane == 0 ? C.xprev : xs_at(xs, pl, lane * SUB - 1);
+                    int pp = 0;
+                    while (pp < np && S.pin_idx[pl][pp] < (long long)e0) ++pp;
+                    for (int i = 0; i < cnt; ++i) {
+                        const long long k = (long long)e0 + i;
+                        const double x = xl[i];
+                        if (pp < np && S.pin_idx[pl][pp] == k) {
+                            my_last = k;
+                            my_val = S.pin_val[pl][pp];
+                            ++pp;
+                        } else if (predict_escape(cp, x, xq)) {
+                            my_last = k;
+                            my_val = x;
+                        }
+                        xq = x;
+                    }
+                }
+                double aval;
+                const long long aidx = plane_last_scan(my_last, my_val, S, pl, aval);
+                if (cnt > 0) {
+                    A = aidx >= 0 ? aval : C.P;
+                    const long long Aidx = aidx >= 0 ? aidx : (long long)base - 1;
+                    Pprev = (Aidx == (long long)e0 - 1) ? A
+                            : lattice_point(cp, A, xs_at(xs, pl, lane * SUB - 1));
+                    xp = lane == 0 ? C.xprev : xs_at(xs, pl, lane * SUB - 1);
+                }
+                __syncthreads();  // neighbours' x read; now overwrite with predictors
+                if (cnt > 0) {
+                    S.entryP[pl][lane] = Pprev;
+                    int pp = 0;
+                    while (pp < np && S.pin_idx[pl][pp] < (long long)e0) ++pp;
+                    for (int i = 0; i < cnt; ++i) {
+                        const long long k = (long long)e0 + i;
+                        if (k >= fser) break;
+                        const double x = xl[i];
+                        double Ph;
+                        if (pp < np && S.pin_idx[pl][pp] == k) {
+                            Ph = S.pin_val[pl][pp];
+                            A = Ph;
+                            ++pp;
+                        } else if (predict_escape(cp, x, xp)) {
+                            Ph = x;
+                            A = x;
+                        } else {
+                            Ph = lattice_step(cp, A, x);
+                        }
+                        xp = x;
+                        xl[i] = Ph;
+                        Pprev = Ph;
+                    }
+                    S.exitP[pl][lane] = Pprev;
+                }
+                __syncthreads();
+                if (lane == 0 && fser != LLONG_MAX) {
+                    // serial tail: x of elements >= fser is still in xs
+                    if (a.counters) atomicAdd(&a.counters[3], 1ull);
+                    const int k0 = (int)(fser - (long long)base);
+                    double P = S.fail_prev[pl];
+                    for (int k = k0; k < n_it; ++k) {
+                        if ((k & (SUB - 1)) == 0) S.entryP[pl][k / SUB] = P;
+                        const int32_t c = ref_step(cp, P, xs_at(xs, pl, k));
+                        code[pl * ITER + k] = c == WCODE ? WCODE16 : (int16_t)c;
+                        xs_at(xs, pl, k) = P;
+                    }
+                    S.exitP[pl][active - 1] = P;
+                }
+                if (lane == 0 && active > 0) C.Pnext = S.exitP[pl][active - 1];
+                __syncthreads();
+            }
+        } else {
+        // 2. entry predictor: exact for lane 0; for the others a guess on the
+        //    lattice of the last *predicted* escape (|x_k - x_k-1| beyond the
+        //    escape limit by more than 2*delta escapes whatever the predictor
+        //    is) or, if none in this iteration, of the exact carried predictor.
+        double entry = 0.0;
+        double lane_anchor = C.P;
+        if (LOSSY) {
+            long long my_last = -1;
+            double my_val = 0.0;
+            if (cnt > 0) {
+                const double thr = __dmul_rn(cp.td, 32769.0);
+                double xp = lane == 0 ? C.xprev : xs_at(xs, pl, lane * SUB - 1);
+                for (int i = 0; i < cnt; ++i) {
+                    const double x = xl[i];
+                    if (fabs(__dsub_rn(x, xp)) > thr) {
+                        my_last = (long long)(e0 + i);
+                        my_val = x;
+                    }
+                    xp = x;
+                }
+                if (lane + 1 == active) C.xprev_next = xl[cnt - 1];
+            }
+            double aval;
+            const long long aidx = plane_last_scan(my_last, my_val, S, pl, aval);
+            if (cnt > 0) {
+                if (lane == 0) {
+                    entry = C.P;
+                } else if (aidx == (long long)e0 - 1) {
+                    entry = aval;
+                } else {
+                    const double anchor = aidx >= 0 ? aval : C.P;
+                    entry = anchored_guess(cp, anchor, xs_at(xs, pl, lane * SUB - 2),
+                                           xs_at(xs, pl, lane * SUB - 1));
+                }
+                if (lane > 0 && aidx >= 0) lane_anchor = aval;
+                S.entryP[pl][lane] = entry;
+            }
         }
         __syncthreads();
 
-        // 4. verify guesses in lane order; re-run any lane whose entry was wrong
+        // 3. lane encode.  Lossy: every element is speculated independently
+        //    (the reference's predictor after coding x_k is the point of the
+        //    current anchor's 2*delta lattice nearest x_k, or x_k itself on an
+        //    escape) and verified by one reference step from the speculated
+        //    predictor of x_k-1.  No dependency chain, so the loop pipelines.
+        //    From the first element that fails, the reference's serial chain
+        //    takes over for the rest of the lane.  Codes only: x stays in shared
+        //    memory for the repair passes.
+        if (cnt > 0) {
+            if (LOSSY) {
+                const double thr = __dmul_rn(cp.td, 32769.0);
+                double xp = lane == 0 ? C.xprev : xs_at(xs, pl, lane * SUB - 1);
+                double anc = lane_anchor;
+                double Pprev = entry, Pfail = 0.0;
+                int fpos = cnt;
+#pragma unroll 4
+                for (int i = 0; i < cnt; ++i) {
+                    const double x = xl[i];
+                    const bool esc = fabs(__dsub_rn(x, xp)) > thr;
+                    xp = x;
+                    double Ph;
+                    if (esc) {
+                        Ph = x;
+                        anc = x;
+                    } else {
+                        const double d = __dsub_rn(x, anc);
+                        const double M = rint(cp.pow2 ? __dmul_rn(d, cp.inv_td) : __ddiv_rn(d, cp.td));
+                        Ph = __dadd_rn(anc, __dmul_rn(cp.td, M));
+                    }
+                    double P2 = Pprev;
+                    const int32_t c = ref_step(cp, P2, x);
+                    cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
+                    if (!same_bits(P2, Ph) && i < fpos) {
+                        fpos = i;
+                        Pfail = Pprev;
+                    }
+                    Pprev = Ph;
+                }
+                if (fpos < cnt) {
+                    if (a.counters) atomicAdd(&a.counters[3], 1ull);
+                    double P = Pfail;
+                    for (int i = fpos; i < cnt; ++i) {
+                        const int32_t c = ref_step(cp, P, xl[i]);
+                        cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
+                    }
+                    Pprev = P;
+                }
+                S.exitP[pl][lane] = Pprev;
+            } else {
+                for (int i = 0; i < cnt; ++i)
+                    cl[i] = __double_as_longlong(xl[i]) == 0 ? (int16_t)0 : WCODE16;
+            }
+        }
+        __syncthreads();
+
         if (LOSSY) {
+            // 4a. parallel repair passes: a lane whose guessed entry differs from
+            //     its left neighbour's exit re-runs from that exit.  The old
+            //     speculative chain is replayed in lock step; once both hold the
+            //     same predictor the rest of the lane is already exact.
+            for (int pass = 0; pass < 4; ++pass) {
+                const bool bad = cnt > 0 && lane > 0 && !same_bits(S.entryP[pl][lane], S.exitP[pl][lane - 1]);
+                const double want = bad ? S.exitP[pl][lane - 1] : 0.0;
+                if (!__syncthreads_or(bad)) break;
+                if (bad) {
+                    if (a.counters) atomicAdd(&a.counters[0], 1ull);
+                    double Pn = want, Po = S.entryP[pl][lane];
+                    bool resync = false;
+                    for (int i = 0; i < cnt; ++i) {
+                        const double x = xl[i];
+                        const int16_t co = cl[i];
+                        if (co == WCODE16) Po = x;
+                        else if (co != 0) Po = __dadd_rn(Po, __dmul_rn(cp.td, (double)co));
+                        const int32_t c = ref_step(cp, Pn, x);
+                        cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
+                        if (same_bits(Pn, Po)) {
+                            resync = true;
+                            break;
+                        }
+                    }
+                    S.entryP[pl][lane] = want;
+                    if (!resync) S.exitP[pl][lane] = Pn;
+                }
+                __syncthreads();
+            }
+            // 4b. whatever is left (long dependency chains, e.g. a bound that
+            //     is not a power of two): the reference's serial order
             if (lane == 0 && active > 0) {
                 for (int l = 1; l < active; ++l) {
                     const double want = S.exitP[pl][l - 1];
                     if (same_bits(want, S.entryP[pl][l])) continue;
+                    if (a.counters) atomicAdd(&a.counters[0], 1ull);
+                    double Pn = want, Po = S.entryP[pl][l];
                     S.entryP[pl][l] = want;
-                    double P = want;
-                    const uint64_t f0 = base + (uint64_t)l * SUB;
-                    const int c2 = (int)umin64(SUB, n - f0);
-                    double* xl2 = xs + pl * PLANE_LANES * XS_STRIDE + l * XS_STRIDE;
+                    const int c2 = (int)umin64(SUB, n - (base + (uint64_t)l * SUB));
+                    const double* xl2 = xs + pl * PLANE_LANES * XS_STRIDE + l * XS_STRIDE;
                     int16_t* cl2 = code + pl * ITER + l * SUB;
+                    bool resync = false;
                     for (int i = 0; i < c2; ++i) {
-                        double x = xg[f0 + i];
-                        if (a.snap) x = snap(x);
-                        const int32_t c = ref_step(cp, P, x);
-                        xl2[i] = P;
+                        const double x = xl2[i];
+                        const int16_t co = cl2[i];
+                        if (co == WCODE16) Po = x;
+                        else if (co != 0) Po = __dadd_rn(Po, __dmul_rn(cp.td, (double)co));
+                        const int32_t c = ref_step(cp, Pn, x);
                         cl2[i] = c == WCODE ? WCODE16 : (int16_t)c;
+                        if (same_bits(Pn, Po)) {
+                            resync = true;
+                            break;
+                        }
                     }
-                    S.exitP[pl][l] = P;
+                    if (!resync) S.exitP[pl][l] = Pn;
                 }
                 C.Pnext = S.exitP[pl][active - 1];
             }
             __syncthreads();
+            // 4c. replace x by the stored (reconstructed) values: the decoder's
+            //     chain from the verified entry (codec.cpp:296-335)
+            if (cnt > 0) {
+                double P = S.entryP[pl][lane];
+                for (int i = 0; i < cnt; ++i) {
+                    const int16_t co = cl[i];
+                    if (co == WCODE16) P = xl[i];
+                    else if (co != 0) P = __dadd_rn(P, __dmul_rn(cp.td, (double)co));
+                    xl[i] = P;
+                }
+            }
+            __syncthreads();
+        }
+
         }
 
         // 5. stored sum of squares (needs both planes' final values)
-        if (a.sumsq) sumsq_iteration(xs, n_it, S);
+        if (a.sumsq) sumsq_iteration(xs, n_it, S, a.counters);
 
         // 6. run summary of each lane and the run entering it
         S.ftype[pl][lane] = cnt > 0 ? (int8_t)ty16(cl[0]) : (int8_t)TY_NONE;
@@ -551,7 +929,10 @@ __global__ void __launch_bounds__(CODEC_THREADS, 2) k_encode(EncodeArgs a)
         __syncthreads();
 
         // 8. slide words of a carried W run left if its varint came out shorter
-        if (tid == 0) S.mvmax = max(S.carry[0].mv_bytes, a.planes > 1 ? S.carry[1].mv_bytes : 0);
+        if (tid == 0) {
+            S.mvmax = max(S.carry[0].mv_bytes, a.planes > 1 ? S.carry[1].mv_bytes : 0);
+            if (a.counters && S.mvmax) atomicAdd(&a.counters[2], (unsigned long long)S.mvmax);
+        }
         __syncthreads();
         for (uint64_t o = 0; o < S.mvmax; o += PLANE_LANES * 8) {
             uint8_t tmp[8];
@@ -644,6 +1025,7 @@ __global__ void __launch_bounds__(CODEC_THREADS, 2) k_encode(EncodeArgs a)
         if (lane == 0 && active > 0) {
             const int last = active - 1;
             C.P = LOSSY ? C.Pnext : 0.0;
+            C.xprev = C.xprev_next;
             const uint64_t new_pos = C.out_pos + C.iter_bytes;
             // state of the run open after the last lane
             int oty = C.open_ty;

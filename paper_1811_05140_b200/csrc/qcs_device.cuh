@@ -157,6 +157,48 @@ __device__ __forceinline__ double lattice_guess(const CodecParams& cp, double xp
     return P;
 }
 
+// Guess for the predictor entering a lane when the chain is anchored at `a`
+// (the last escape before the lane, or any exact predictor on the same
+// lattice): the lattice point a + 2*delta*M nearest to x2, then one exact
+// reference step onto x1.  Only a guess; verified bit-for-bit.
+__device__ __forceinline__ double anchored_guess(const CodecParams& cp, double a, double x2, double x1)
+{
+    const double d = __dsub_rn(x2, a);
+    const double M = rint(cp.pow2 ? __dmul_rn(d, cp.inv_td) : __ddiv_rn(d, cp.td));
+    double P = __dadd_rn(a, __dmul_rn(cp.td, M));
+    ref_step(cp, P, x1);
+    return P;
+}
+
+// Point of the lattice a + 2*delta*Z nearest x (power-of-two delta).
+__device__ __forceinline__ double lattice_point(const CodecParams& cp, double a, double x)
+{
+    const double M = rint(__dmul_rn(__dsub_rn(x, a), cp.inv_td));
+    return __dadd_rn(a, __dmul_rn(cp.td, M));
+}
+
+// lattice_point with rounding emulation: if a + 2*delta*M is not exact the
+// reference chain rounds right here, and the rounded value anchors what
+// follows (a heuristic for the speculation; verification decides).
+__device__ __forceinline__ double lattice_step(const CodecParams& cp, double& a, double x)
+{
+    const double M = rint(__dmul_rn(__dsub_rn(x, a), cp.inv_td));
+    const double y = __dmul_rn(cp.td, M);
+    const double v = __dadd_rn(a, y);
+    // Fast2Sum error of a + y: non-zero exactly when the chain rounds here
+    const double err = fabs(a) >= fabs(y) ? __dsub_rn(y, __dsub_rn(v, a)) : __dsub_rn(a, __dsub_rn(v, y));
+    if (err != 0.0) a = v;
+    return v;
+}
+
+// Escape prediction from the previous input (exact whenever the previous
+// element escaped, since the predictor then IS that input): the reference
+// escapes when llround((x - P)/2delta) leaves (-32768, 32768).
+__device__ __forceinline__ bool predict_escape(const CodecParams& cp, double x, double xprev)
+{
+    return fabs(__dmul_rn(__dsub_rn(x, xprev), cp.inv_td)) >= 32767.5;
+}
+
 __device__ __forceinline__ bool same_bits(double a, double b)
 {
     return __double_as_longlong(a) == __double_as_longlong(b);

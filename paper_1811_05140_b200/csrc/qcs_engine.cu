@@ -137,9 +137,11 @@ struct Dev {
         double norm_sq;
         uint64_t compressed_bytes;
         double min_ratio;
+        uint64_t gate_cin;
     }* sc;
     qcs_gate_record* rec;  // record ring for run_program
     uint64_t rec_cap;
+    unsigned long long* counters;  // [8] device diagnostics
 };
 
 __global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen)
@@ -326,14 +328,26 @@ __global__ void __launch_bounds__(1024) k_commit_plan(Dev d, uint64_t n_slots, u
     const int tid = threadIdx.x, wl = tid & 31, w = tid >> 5;
     auto rounded = [](uint64_t x) { return (x + 15) & ~uint64_t(15); };
     // pass 1: total of new blocks
-    uint64_t acc = 0;
-    for (uint64_t i = tid; i < 2 * n_slots; i += blockDim.x) acc += rounded(d.slot_len[i]);
+    uint64_t acc = 0, cin = 0;
+    for (uint64_t i = tid; i < 2 * n_slots; i += blockDim.x) {
+        acc += rounded(d.slot_len[i]);
+        cin += HEADER_BYTES + d.p_len[2 * d.job_stride[i >> 1] + (i & 1)];
+    }
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (wl == 0) wsum[w] = acc;
+    for (int o = 16; o; o >>= 1) cin += __shfl_xor_sync(0xffffffffu, cin, o);
+    __shared__ uint64_t csum[32];
+    if (wl == 0) {
+        wsum[w] = acc;
+        csum[w] = cin;
+    }
     __syncthreads();
     if (tid == 0) {
-        uint64_t t = 0;
-        for (int i = 0; i < 32; ++i) t += wsum[i];
+        uint64_t t = 0, c = 0;
+        for (int i = 0; i < 32; ++i) {
+            t += wsum[i];
+            c += csum[i];
+        }
+        d.sc->gate_cin = c;
         mode = (d.sc->bump + t <= d.arena_cap) ? 0 : 1;
         carry = mode == 0 ? d.sc->bump : 0;
     }
@@ -469,6 +483,7 @@ __global__ void k_norm(Dev d, uint64_t n_slots, uint64_t rec_index, uint64_t gat
         r.mean_ratio = n_slots ? __ddiv_rn(rs, (double)n_slots) : 0.0;
         r.elapsed_ns = 0;
         r.norm_after = __dsqrt_rn(nsq);
+        r.compressed_in = d.sc->gate_cin;
         d.rec[rec_index] = r;
     }
 }
@@ -558,13 +573,61 @@ struct qcs_dev_state {
     Dev::Scal* h_sc = nullptr;   // pinned mirror
     qcs_stride_report* h_rep = nullptr;
     std::vector<void*> allocs;
-    // timing of the codec kernel across the last run
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;
-    double codec_ns = 0;
-    uint64_t codec_launches = 0, codec_bytes = 0;
+    // per-kernel-class profiling (qcs_state_profile)
+    bool prof = false;
+    struct Mark {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<Mark> marks;
+    std::vector<cudaEvent_t> pool;
+    double cls_ns[6] = {0, 0, 0, 0, 0, 0};
+    uint64_t cls_n[6] = {0, 0, 0, 0, 0, 0};
 };
 
 namespace {
+
+cudaEvent_t pool_event(qcs_dev_state* st)
+{
+    if (!st->pool.empty()) {
+        cudaEvent_t e = st->pool.back();
+        st->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void prof_start(qcs_dev_state* st, int cls)
+{
+    if (!st->prof) return;
+    qcs_dev_state::Mark m{cls, pool_event(st), pool_event(st)};
+    cudaEventRecord(m.a, st->stream);
+    st->marks.push_back(m);
+}
+
+void prof_stop(qcs_dev_state* st)
+{
+    if (!st->prof || st->marks.empty()) return;
+    cudaEventRecord(st->marks.back().b, st->stream);
+}
+
+void prof_collect(qcs_dev_state* st)
+{
+    for (auto& m : st->marks) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, m.a, m.b) == cudaSuccess) {
+            st->cls_ns[m.cls] += (double)ms * 1e6;
+            st->cls_n[m.cls] += 1;
+        }
+        st->pool.push_back(m.a);
+        st->pool.push_back(m.b);
+    }
+    st->marks.clear();
+    cudaGetLastError();
+}
 
 template <typename T>
 int dalloc(qcs_dev_state* s, T** p, size_t count)
@@ -678,19 +741,29 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     GateParams gp;
     for (int i = 0; i < 8; ++i) gp.u[i] = g->u[i];
 
+    prof_start(st, 5);
     k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen);
+    prof_stop(st);
     ++st->launches;
     if (p.reflect) {
+        prof_start(st, 0);
         k_decode<<<(unsigned)d.NS, 256, 0, s>>>(d, DecodeJob{nullptr, 1});
+        prof_stop(st);
+        prof_start(st, 4);
         k_stride_sums<<<(unsigned)((d.NS + 127) / 128), 128, 0, s>>>(d);
         k_mean<<<1, 1, 0, s>>>(d);
+        prof_stop(st);
         st->launches += 3;
     } else {
+        prof_start(st, 0);
         k_decode<<<(unsigned)n_slots, 256, 0, s>>>(d, DecodeJob{d.job_stride, 1});
+        prof_stop(st);
         ++st->launches;
     }
     const uint64_t per = (p.kind <= 1 && !p.pair) ? d.L / 2 : d.L;
+    prof_start(st, 1);
     k_gate<<<(unsigned)grid_for(p.n_units * per), 256, 0, s>>>(d, p, gp);
+    prof_stop(st);
     ++st->launches;
     for (int k = 0; k < nl; ++k) {
         EncodeArgs a{};
@@ -708,17 +781,26 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         a.out_len = d.slot_len;
         a.sumsq = d.slot_sum;
         a.cp = make_params(lad[k]);
+        a.counters = d.counters;
+        prof_start(st, 5);
         k_tag_level<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, st->lt, n_slots, a.cp.lossy ? 1 : 0, lad[k]);
+        prof_stop(st);
         ++st->launches;
+        prof_start(st, 2);
         int rc = launch_encode(a, n_slots, s);
+        prof_stop(st);
         if (rc) return rc;
         ++st->launches;
+        prof_start(st, 5);
         k_ladder<<<(unsigned)((p.n_units + 127) / 128), 128, 0, s>>>(d, p, lad[k], theta, k == nl - 1);
+        prof_stop(st);
         ++st->launches;
     }
+    prof_start(st, 3);
     k_commit_plan<<<1, 1024, 0, s>>>(d, n_slots, gen);
     k_commit_copy<<<(unsigned)(2 * d.NS), 128, 0, s>>>(d, st->lt, gen);
     k_norm<<<1, 32, 0, s>>>(d, n_slots, rec_index < 0 ? 0 : (uint64_t)rec_index, gate_index);
+    prof_stop(st);
     st->launches += 3;
     CU(cudaGetLastError());
     return 0;
@@ -742,6 +824,11 @@ void qcs_state_destroy(qcs_dev_state_t st)
     for (void* p : st->allocs) cudaFree(p);
     if (st->h_sc) cudaFreeHost(st->h_sc);
     if (st->h_rep) cudaFreeHost(st->h_rep);
+    for (auto& m : st->marks) {
+        cudaEventDestroy(m.a);
+        cudaEventDestroy(m.b);
+    }
+    for (auto e : st->pool) cudaEventDestroy(e);
     if (st->ev_a) cudaEventDestroy(st->ev_a);
     if (st->ev_b) cudaEventDestroy(st->ev_b);
     if (st->stream) cudaStreamDestroy(st->stream);
@@ -805,6 +892,8 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     TRY(dalloc(st, &d.new_off, 2 * d.NS));
     TRY(dalloc(st, &d.partial, 2 * d.NS));
     TRY(dalloc(st, &d.sc, 1));
+    TRY(dalloc(st, &d.counters, 8));
+    CU(cudaMemset(d.counters, 0, 64));
     TRY(dalloc(st, &st->lt.slot_codec, d.NS));
     TRY(dalloc(st, &st->lt.slot_delta, d.NS));
     if (cudaMallocHost(&st->h_sc, sizeof(Dev::Scal)) != cudaSuccess ||
@@ -874,6 +963,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
 static int sync_and_check(qcs_dev_state* st)
 {
     CU(cudaStreamSynchronize(st->stream));
+    prof_collect(st);
     CU(cudaMemcpy(st->h_sc, st->d.sc, sizeof(Dev::Scal), cudaMemcpyDeviceToHost));
     return 0;
 }
@@ -1199,12 +1289,36 @@ int qcs_state_memory(qcs_dev_state_t st, uint64_t* arena, uint64_t* side, uint64
 
 uint64_t qcs_state_launches(qcs_dev_state_t st) { return st ? st->launches : 0; }
 
-int qcs_state_kernel_stats(qcs_dev_state_t st, double* ns_avg, uint64_t* launches, uint64_t* bytes)
+int qcs_state_profile(qcs_dev_state_t st, int enable)
 {
     if (!st) return set_err(QCS_E_INVALID, "null state");
-    if (ns_avg) *ns_avg = st->codec_launches ? st->codec_ns / st->codec_launches : 0.0;
-    if (launches) *launches = st->codec_launches;
-    if (bytes) *bytes = st->codec_bytes;
+    int rc = sync_and_check(st);
+    if (rc) return rc;
+    st->prof = enable != 0;
+    for (int i = 0; i < 6; ++i) {
+        st->cls_ns[i] = 0;
+        st->cls_n[i] = 0;
+    }
+    return 0;
+}
+
+int qcs_state_counters(qcs_dev_state_t st, uint64_t* out, int n)
+{
+    if (!st || !out || n < 0 || n > 8) return set_err(QCS_E_INVALID, "bad argument");
+    int rc = sync_and_check(st);
+    if (rc) return rc;
+    CU(cudaMemcpy(out, st->d.counters, 8 * n, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int qcs_state_kernel_time(qcs_dev_state_t st, int cls, double* total_ns, uint64_t* launches)
+{
+    if (!st) return set_err(QCS_E_INVALID, "null state");
+    if (cls < 0 || cls >= 6) return set_err(QCS_E_RANGE, "kernel class out of range");
+    int rc = sync_and_check(st);
+    if (rc) return rc;
+    if (total_ns) *total_ns = st->cls_ns[cls];
+    if (launches) *launches = st->cls_n[cls];
     return 0;
 }
 

@@ -84,6 +84,10 @@ def lib() -> C.CDLL:
         L.qcs_state_memory.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                        C.POINTER(C.c_uint64)]
         L.qcs_state_launches.argtypes = [C.c_void_p]
+        L.qcs_state_counters.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+        L.qcs_state_profile.argtypes = [C.c_void_p, C.c_int]
+        L.qcs_state_kernel_time.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double),
+                                            C.POINTER(C.c_uint64)]
         L.qcs_codec_compress.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_void_p,
                                          C.c_uint64, C.POINTER(C.c_uint64)]
         L.qcs_codec_decompress.argtypes = [C.c_char_p, C.c_uint64, C.c_void_p, C.c_uint64]
@@ -120,7 +124,8 @@ class Record(C.Structure):
                 ("min_ratio", C.c_double), ("mean_ratio", C.c_double),
                 ("max_chosen_delta", C.c_double), ("bytes_before", C.c_uint64),
                 ("bytes_after", C.c_uint64), ("elapsed_ns", C.c_uint64),
-                ("norm_after", C.c_double), ("threshold_violations", C.c_uint64)]
+                ("norm_after", C.c_double), ("threshold_violations", C.c_uint64),
+                ("compressed_in", C.c_uint64)]
 
 
 # ---------------------------------------------------------------------------
@@ -342,6 +347,25 @@ class CompressedState:
                                        C.byref(ss)))
         return buf.raw[: n.value], sc.value, ss.value
 
+    KERNEL_CLASSES = ("decode", "gate", "encode", "commit", "mean", "bookkeeping")
+
+    def profile(self, enable: bool) -> None:
+        _check(lib().qcs_state_profile(self._h, 1 if enable else 0))
+
+    def kernel_times(self) -> dict:
+        out = {}
+        for i, name in enumerate(self.KERNEL_CLASSES):
+            t, n = C.c_double(), C.c_uint64()
+            _check(lib().qcs_state_kernel_time(self._h, i, C.byref(t), C.byref(n)))
+            out[name] = (t.value, n.value)
+        return out
+
+    def counters(self) -> dict:
+        buf = (C.c_uint64 * 4)()
+        _check(lib().qcs_state_counters(self._h, buf, 4))
+        return {"repaired_lanes": buf[0], "sum_passes": buf[1], "slid_bytes": buf[2],
+                "serial_fallback_lanes": buf[3]}
+
     def launches(self) -> int:
         return lib().qcs_state_launches(self._h)
 
@@ -470,6 +494,7 @@ def apply_program_range(state: CompressedState, program: CircuitProgram, first: 
             min_ratio=r.min_ratio, mean_ratio=r.mean_ratio, max_chosen_delta=r.max_chosen_delta,
             bytes_before=r.bytes_before, bytes_after=r.bytes_after, elapsed_ns=r.elapsed_ns,
             norm_after=r.norm_after))
+        metrics.records[-1].compressed_in = r.compressed_in
         metrics.threshold_violations += r.threshold_violations
         metrics.total_elapsed_ns += r.elapsed_ns
     if rc:

@@ -8,12 +8,12 @@ __global__ void k(const double* re, const double* im, int n, double* out) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* xs = reinterpret_cast<double*>(smem);
   int16_t* code = reinterpret_cast<int16_t*>(xs + 2 * PLANE_LANES * XS_STRIDE);
-  EncShared& S = *reinterpret_cast<EncShared*>((reinterpret_cast<uintptr_t>(code + 2 * ITER) + 15) & ~uintptr_t(15));
+  EncShared& S = *reinterpret_cast<EncShared*>(smem + ENC_S_OFF);
   int pl = threadIdx.x >> 7, lane = threadIdx.x & 127;
   for (int i = lane; i < ITER; i += 128) xs_at(xs, pl, i) = i < n ? (pl ? im[i] : re[i]) : 0.0;
   if (threadIdx.x == 0) S.s = 0.0;
   __syncthreads();
-  sumsq_iteration(xs, n, S);
+  sumsq_iteration(xs, n, S, nullptr);
   __syncthreads();
   if (threadIdx.x == 0) *out = S.s;
 }
