@@ -6,6 +6,7 @@ reference's FMA-free x86-64 build bit-for-bit.
 """
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -14,8 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libqcs_b200.so")
 SOURCES = [os.path.join(HERE, "csrc", "qcs_engine.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("qcs_codec.cuh", "qcs_device.cuh")] + [
-    os.path.join(ROOT, "include", "qcs_b200.h")]
+DEPS = sorted(glob.glob(os.path.join(HERE, "csrc", "*"))) + [os.path.join(ROOT, "include", "qcs_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
          "-std=c++17", "-Xcompiler", "-fPIC", "-shared"]

@@ -392,6 +392,62 @@ __device__ __forceinline__ void lane_walk(const int16_t* cl, int cnt, uint64_t e
     if (cur != TY_NONE && tail_closes) on_run(cur, cst, e0 + cnt);
 }
 
+
+// ---- bitmask view of a lane's codes (zero codes / raw words / nonzero codes)
+struct LaneMasks {
+    uint32_t z, w, valid;
+};
+
+__device__ __forceinline__ LaneMasks lane_masks(const int16_t* cl, int cnt)
+{
+    LaneMasks m{0u, 0u, cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u)};
+    const uint32_t* c2 = reinterpret_cast<const uint32_t*>(cl);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const uint32_t v = c2[j];
+        const uint32_t lo = v & 0xffffu, hi = v >> 16;
+        m.z |= ((uint32_t)(lo == 0u) << (2 * j)) | ((uint32_t)(hi == 0u) << (2 * j + 1));
+        m.w |= ((uint32_t)(lo == 0x8000u) << (2 * j)) | ((uint32_t)(hi == 0x8000u) << (2 * j + 1));
+    }
+    m.z &= m.valid;
+    m.w &= m.valid;
+    return m;
+}
+
+__device__ __forceinline__ int mask_type(const LaneMasks& m, int p)
+{
+    return ((m.z >> p) & 1u) ? TY_Z : (((m.w >> p) & 1u) ? TY_W : TY_C);
+}
+
+// Token enumeration over a lane with bitmasks: the same contract as
+// lane_walk (runs closed by this lane -> on_run, nonzero codes -> on_code) but
+// the loop runs once per token, not once per element.
+template <typename FR, typename FC>
+__device__ __forceinline__ void lane_tokens(const LaneMasks& m, const int16_t* cl, int cnt, uint64_t e0,
+                                            int in_ty, uint64_t in_st, bool tail_closes,
+                                            bool close_carried, FR on_run, FC on_code)
+{
+    if (cnt <= 0) return;
+    const int t0 = mask_type(m, 0);
+    const bool cont = in_ty != TY_NONE && t0 == in_ty;
+    if (!cont && close_carried && in_ty != TY_NONE) on_run(in_ty, in_st, e0);
+    const uint32_t cm = m.valid & ~(m.z | m.w);
+    uint32_t rest = (cm | (m.z & ~(m.z << 1)) | (m.w & ~(m.w << 1))) & m.valid & ~1u;
+    int cur = 0;
+    int ty = cont ? in_ty : t0;
+    uint64_t rst = cont ? in_st : e0;
+    for (;;) {
+        const int next = rest ? __ffs(rest) - 1 : cnt;
+        if (ty == TY_C) on_code(cl[cur]);
+        else if (next < cnt || tail_closes) on_run(ty, rst, e0 + next);
+        if (next >= cnt) break;
+        rest &= rest - 1u;
+        cur = next;
+        ty = mask_type(m, next);
+        rst = e0 + next;
+    }
+}
+
 template <bool LOSSY>
 __global__ void __launch_bounds__(CODEC_THREADS, 2) k_encode(EncodeArgs a)
 {

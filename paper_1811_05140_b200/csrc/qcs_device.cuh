@@ -199,9 +199,64 @@ __device__ __forceinline__ bool predict_escape(const CodecParams& cp, double x, 
     return fabs(__dmul_rn(__dsub_rn(x, xprev), cp.inv_td)) >= 32767.5;
 }
 
+// lattice_step that also returns M (relative to the anchor it used) and
+// whether the reference step is provably equal to the lattice step:
+//   with P_prev = a + 2d*M_prev exactly, y = fl(x-a)/2d, |y| < 2^30 and y at
+//   least 2^-19 away from a half-integer, the reference's
+//   llround(fl(x-P_prev)/2d) equals rint(y) - M_prev (both subtractions err by
+//   < 2^-21 in units of 2d), its recon fl(P_prev + 2d*q) rounds the same real
+//   a + 2d*M as we do, and its bound check |x-recon| <= delta holds.
+__device__ __forceinline__ double lattice_step_m(const CodecParams& cp, double& a, double x, double& M,
+                                                 bool& safe)
+{
+    const double y = __dmul_rn(__dsub_rn(x, a), cp.inv_td);
+    M = rint(y);
+    const double fr = fabs(__dsub_rn(y, M));
+    safe = fabs(y) < 1073741824.0 && fr < 0.5 - 1.9073486328125e-06;  // 2^30, 0.5 - 2^-19
+    const double yv = __dmul_rn(cp.td, M);
+    const double v = __dadd_rn(a, yv);
+    const double err = fabs(a) >= fabs(yv) ? __dsub_rn(yv, __dsub_rn(v, a)) : __dsub_rn(a, __dsub_rn(v, yv));
+    if (err != 0.0) a = v;  // the chain rounds here: re-anchor (M relative to v is 0)
+    return v;
+}
+
 __device__ __forceinline__ bool same_bits(double a, double b)
 {
     return __double_as_longlong(a) == __double_as_longlong(b);
+}
+
+// apply_pair arithmetic (gate.cpp:153-162), left to right, no FMA.
+__device__ __forceinline__ void pair_update(const double* m, double& r0, double& i0, double& r1,
+                                            double& i1)
+{
+    const double t0r = r0, t0i = i0, t1r = r1, t1i = i1;
+    r0 = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(m[0], t0r), __dmul_rn(m[1], t0i)), __dmul_rn(m[2], t1r)),
+                   __dmul_rn(m[3], t1i));
+    i0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[0], t0i), __dmul_rn(m[1], t0r)), __dmul_rn(m[2], t1i)),
+                   __dmul_rn(m[3], t1r));
+    r1 = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(m[4], t0r), __dmul_rn(m[5], t0i)), __dmul_rn(m[6], t1r)),
+                   __dmul_rn(m[7], t1i));
+    i1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[4], t0i), __dmul_rn(m[5], t0r)), __dmul_rn(m[6], t1i)),
+                   __dmul_rn(m[7], t1r));
+}
+
+// Row halves of apply_pair: the lo output from (t0, t1) and the hi output.
+__device__ __forceinline__ void pair_lo(const double* m, double t0r, double t0i, double t1r, double t1i,
+                                        double& r, double& i)
+{
+    r = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(m[0], t0r), __dmul_rn(m[1], t0i)), __dmul_rn(m[2], t1r)),
+                  __dmul_rn(m[3], t1i));
+    i = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[0], t0i), __dmul_rn(m[1], t0r)), __dmul_rn(m[2], t1i)),
+                  __dmul_rn(m[3], t1r));
+}
+
+__device__ __forceinline__ void pair_hi(const double* m, double t0r, double t0i, double t1r, double t1i,
+                                        double& r, double& i)
+{
+    r = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(m[4], t0r), __dmul_rn(m[5], t0i)), __dmul_rn(m[6], t1r)),
+                  __dmul_rn(m[7], t1i));
+    i = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[4], t0i), __dmul_rn(m[5], t0r)), __dmul_rn(m[6], t1i)),
+                  __dmul_rn(m[7], t1r));
 }
 
 }  // namespace qcs

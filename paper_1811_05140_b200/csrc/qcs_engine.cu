@@ -25,7 +25,7 @@
 #include <vector>
 
 #include "../../include/qcs_b200.h"
-#include "qcs_codec.cuh"
+#include "qcs_fused.cuh"
 
 using namespace qcs;
 
@@ -141,7 +141,7 @@ struct Dev {
     }* sc;
     qcs_gate_record* rec;  // record ring for run_program
     uint64_t rec_cap;
-    unsigned long long* counters;  // [8] device diagnostics
+    unsigned long long* counters;  // [16] device diagnostics
 };
 
 __global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen)
@@ -178,21 +178,6 @@ __global__ void __launch_bounds__(256) k_decode(Dev d, DecodeJob dj)
         const int cnt = (int)umin64(SUB, d.L - e0);
         decode_sub(in, codec, td, side[sc], cnt, o + e0, scale);
     }
-}
-
-// apply_pair arithmetic (gate.cpp:153-162), left to right, no FMA.
-__device__ __forceinline__ void pair_update(const double* m, double& r0, double& i0, double& r1,
-                                            double& i1)
-{
-    const double t0r = r0, t0i = i0, t1r = r1, t1i = i1;
-    r0 = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(m[0], t0r), __dmul_rn(m[1], t0i)), __dmul_rn(m[2], t1r)),
-                   __dmul_rn(m[3], t1i));
-    i0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[0], t0i), __dmul_rn(m[1], t0r)), __dmul_rn(m[2], t1i)),
-                   __dmul_rn(m[3], t1r));
-    r1 = __dsub_rn(__dadd_rn(__dsub_rn(__dmul_rn(m[4], t0r), __dmul_rn(m[5], t0i)), __dmul_rn(m[6], t1r)),
-                   __dmul_rn(m[7], t1i));
-    i1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[4], t0i), __dmul_rn(m[5], t0r)), __dmul_rn(m[6], t1i)),
-                   __dmul_rn(m[7], t1r));
 }
 
 // run_plan_unit over all units: one thread per amplitude pair / amplitude.
@@ -558,6 +543,36 @@ int launch_encode(const EncodeArgs& a, uint64_t n_jobs, cudaStream_t st)
     return 0;
 }
 
+
+template <bool L, int NPL, int LPL, int MODE>
+int launch_fused_t(const FusedArgs& a, uint64_t grid, cudaStream_t s)
+{
+    static bool set = false;
+    if (!set) {
+        CU(cudaFuncSetAttribute(k_fused<L, NPL, LPL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)FUSED_SMEM));
+        set = true;
+    }
+    if (grid == 0) return 0;
+    k_fused<L, NPL, LPL, MODE><<<(unsigned)grid, NPL * LPL, FUSED_SMEM, s>>>(a);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+enum { FM_LOCAL = 0, FM_FAR = 1, FM_PAIR = 2, FM_RAW1 = 3, FM_RAW2 = 4 };
+
+int launch_fused(const FusedArgs& a, int fm, uint64_t grid, cudaStream_t s)
+{
+    const bool L = a.cp.lossy != 0;
+    switch (fm) {
+        case FM_LOCAL: return L ? launch_fused_t<true, 2, 128, MODE_LOCAL>(a, grid, s) : launch_fused_t<false, 2, 128, MODE_LOCAL>(a, grid, s);
+        case FM_FAR: return L ? launch_fused_t<true, 2, 64, MODE_FAR>(a, grid, s) : launch_fused_t<false, 2, 64, MODE_FAR>(a, grid, s);
+        case FM_PAIR: return L ? launch_fused_t<true, 4, 64, MODE_PAIR>(a, grid, s) : launch_fused_t<false, 4, 64, MODE_PAIR>(a, grid, s);
+        case FM_RAW1: return L ? launch_fused_t<true, 1, 256, MODE_RAW>(a, grid, s) : launch_fused_t<false, 1, 256, MODE_RAW>(a, grid, s);
+        default: return L ? launch_fused_t<true, 2, 128, MODE_RAW>(a, grid, s) : launch_fused_t<false, 2, 128, MODE_RAW>(a, grid, s);
+    }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -738,41 +753,46 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     const uint64_t n_slots = p.pair ? 2 * p.n_units : p.n_units;
     *n_slots_out = n_slots;
     const uint64_t gen = ++st->gen;
-    GateParams gp;
-    for (int i = 0; i < 8; ++i) gp.u[i] = g->u[i];
 
     prof_start(st, 5);
     k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen);
     prof_stop(st);
     ++st->launches;
-    if (p.reflect) {
-        prof_start(st, 0);
-        k_decode<<<(unsigned)d.NS, 256, 0, s>>>(d, DecodeJob{nullptr, 1});
-        prof_stop(st);
+    if (p.reflect) {  // mean pass (aalc.cpp:270-295) needs every stride first
         prof_start(st, 4);
+        k_decode<<<(unsigned)d.NS, 256, 0, s>>>(d, DecodeJob{nullptr, 1});
         k_stride_sums<<<(unsigned)((d.NS + 127) / 128), 128, 0, s>>>(d);
         k_mean<<<1, 1, 0, s>>>(d);
         prof_stop(st);
         st->launches += 3;
-    } else {
-        prof_start(st, 0);
-        k_decode<<<(unsigned)n_slots, 256, 0, s>>>(d, DecodeJob{d.job_stride, 1});
-        prof_stop(st);
-        ++st->launches;
     }
-    const uint64_t per = (p.kind <= 1 && !p.pair) ? d.L / 2 : d.L;
-    prof_start(st, 1);
-    k_gate<<<(unsigned)grid_for(p.n_units * per), 256, 0, s>>>(d, p, gp);
-    prof_stop(st);
-    ++st->launches;
+    int fm = FM_LOCAL;
+    uint64_t grid = n_slots;
+    if (p.pair) {
+        fm = FM_PAIR;
+        grid = p.n_units;
+    } else if (p.kind <= 1 && (1ull << p.t) >= 4096) {
+        fm = FM_FAR;
+    }
     for (int k = 0; k < nl; ++k) {
-        EncodeArgs a{};
-        a.X = d.X;
-        a.n = d.L;
+        FusedArgs a{};
+        a.arena0 = d.arena[0];
+        a.arena1 = d.arena[1];
+        a.arena_cur = &d.sc->cur;
+        a.p_off = d.p_off;
+        a.p_codec = d.p_codec;
+        a.p_delta = d.p_delta;
+        a.side_in = d.side;
+        a.scale = d.scale;
         a.job_stride = d.job_stride;
-        a.stride_elems = 2 * d.L;
+        for (int i = 0; i < 8; ++i) a.u[i] = g->u[i];
+        a.kind = p.kind;
+        a.t = p.t;
+        a.local_ctl = p.local_ctl;
+        a.flip_off = p.flip_off;
+        a.mean = d.sc->mean;
+        a.n = d.L;
         a.pending = d.pending;
-        a.planes = 2;
         a.snap = 1;
         a.out = d.slot_out;
         a.cap = d.slot_cap;
@@ -787,7 +807,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         prof_stop(st);
         ++st->launches;
         prof_start(st, 2);
-        int rc = launch_encode(a, n_slots, s);
+        int rc = launch_fused(a, fm, grid, s);
         prof_stop(st);
         if (rc) return rc;
         ++st->launches;
@@ -892,8 +912,8 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     TRY(dalloc(st, &d.new_off, 2 * d.NS));
     TRY(dalloc(st, &d.partial, 2 * d.NS));
     TRY(dalloc(st, &d.sc, 1));
-    TRY(dalloc(st, &d.counters, 8));
-    CU(cudaMemset(d.counters, 0, 64));
+    TRY(dalloc(st, &d.counters, 16));
+    CU(cudaMemset(d.counters, 0, 128));
     TRY(dalloc(st, &st->lt.slot_codec, d.NS));
     TRY(dalloc(st, &st->lt.slot_delta, d.NS));
     if (cudaMallocHost(&st->h_sc, sizeof(Dev::Scal)) != cudaSuccess ||
@@ -1304,7 +1324,7 @@ int qcs_state_profile(qcs_dev_state_t st, int enable)
 
 int qcs_state_counters(qcs_dev_state_t st, uint64_t* out, int n)
 {
-    if (!st || !out || n < 0 || n > 8) return set_err(QCS_E_INVALID, "bad argument");
+    if (!st || !out || n < 0 || n > 16) return set_err(QCS_E_INVALID, "bad argument");
     int rc = sync_and_check(st);
     if (rc) return rc;
     CU(cudaMemcpy(out, st->d.counters, 8 * n, cudaMemcpyDeviceToHost));
@@ -1358,12 +1378,11 @@ int qcs_codec_compress(const double* x, uint64_t n, double delta, uint8_t* out, 
     }
     cudaMemcpyAsync(dx, x, 8 * n, cudaMemcpyHostToDevice, s);
     cudaMemsetAsync(dlen, 0, 16, s);
-    EncodeArgs a{};
+    FusedArgs a{};
     a.X = dx;
+    a.x_plane_stride = n;
     a.n = n;
-    a.job_stride = nullptr;
     a.pending = nullptr;
-    a.planes = 1;
     a.snap = 0;
     a.out = dout;
     a.cap = pcap;
@@ -1372,7 +1391,7 @@ int qcs_codec_compress(const double* x, uint64_t n, double delta, uint8_t* out, 
     a.out_len = dlen;
     a.sumsq = nullptr;
     a.cp = make_params(delta);
-    int rc = n ? launch_encode(a, 1, s) : 0;
+    int rc = n ? launch_fused(a, FM_RAW1, 1, s) : 0;
     uint64_t plen = 0;
     if (!rc) {
         cudaMemcpyAsync(&plen, dlen, 8, cudaMemcpyDeviceToHost, s);
@@ -1461,10 +1480,10 @@ int qcs_debug_stride_sumsq(const double* re, const double* im, uint64_t n, doubl
     } else {
         cudaMemcpy(dx, re, 8 * n, cudaMemcpyHostToDevice);
         cudaMemcpy(dx + n, im, 8 * n, cudaMemcpyHostToDevice);
-        EncodeArgs a{};
-        a.X = dx; a.n = n; a.planes = 2; a.snap = 0; a.out = dout; a.cap = pcap;
+        FusedArgs a{};
+        a.X = dx; a.x_plane_stride = n; a.n = n; a.snap = 0; a.out = dout; a.cap = pcap;
         a.side = dside; a.nsub = nsub; a.out_len = dlen; a.sumsq = dsum; a.cp = make_params(0.0);
-        rc = launch_encode(a, 1, 0);
+        rc = launch_fused(a, FM_RAW2, 1, 0);
         if (!rc && cudaMemcpy(out, dsum, 8, cudaMemcpyDeviceToHost) != cudaSuccess) rc = set_err(QCS_E_CUDA, "copy failed");
     }
     cudaFree(dx); cudaFree(dsum); cudaFree(dout); cudaFree(dside); cudaFree(dlen);

@@ -1,0 +1,943 @@
+// Fused per-gate kernel: decompress -> scale -> gate -> snap -> recompress
+// (+ stored sum of squares, side index) in ONE kernel per ladder level.
+//
+// Restates, per unit of make_stride_plan (gate.cpp:313-403), the body of
+// CompressedState::apply_gate's worker loop (aalc.cpp:315-382):
+//   decompress_into + scale   aalc.cpp:176-189, codec.cpp:288-340
+//   run_plan_unit             gate.cpp:405-454 (apply_pair order, no FMA)
+//   snap_zeros                core.cpp:39-47
+//   compress (one ladder level) codec.cpp:118-250
+//   stored_sum_sq             aalc.cpp:46-52, core.cpp:30-37
+// Everything stays on chip between the compressed input and the compressed
+// output; nothing uncompressed goes back to HBM.
+//
+// CTA shapes (template NPL planes x LPL lanes, SUB=32 elements per lane):
+//   MODE_LOCAL  2 x 128  one stride, gate partner inside the 4096-element chunk
+//                        (or flip / reflect / plain_single)
+//   MODE_FAR    2 x 64   one stride, partner chunk 2^t away (t >= 11) decoded
+//                        into the spare half of the chunk buffer
+//   MODE_PAIR   4 x 64   lo + hi stride of a cross-stride pair unit
+//   MODE_RAW    1|2 x .  input already uncompressed in HBM (codec API)
+// The encoder half is the verified-speculation codec of qcs_codec.cuh
+// generalised to NPL planes.
+#pragma once
+
+#include "qcs_codec.cuh"
+
+namespace qcs {
+
+enum : int { MODE_RAW = 0, MODE_LOCAL = 1, MODE_FAR = 2, MODE_PAIR = 3 };
+
+struct FusedShared {
+    double entryP[256];
+    double exitP[256];
+    RunFn fincl[256];
+    uint64_t bstart[256];
+    uint64_t runtok[256];
+    uint64_t runw[256];
+    int8_t ftype[264];
+    RunFn wfn[8];
+    long long wesc_i[8];
+    double wesc_v[8];
+    uint64_t wsum[8];
+    long long wmin[8];
+    long long wfail[8];
+    PlaneCarry carry[4];
+    long long pin_idx[4][MAXPIN];
+    double pin_val[4][MAXPIN];
+    int16_t pin_code[4][MAXPIN];
+    int npin[4];
+    double fail_prev[4];
+    double s[2];  // exact running sum of squares per stride
+    uint64_t mvmax;
+};
+
+constexpr size_t FUSED_XS_BYTES = sizeof(double) * 256 * XS_STRIDE;
+constexpr size_t FUSED_CODE_BYTES = sizeof(int16_t) * 256 * SUB;
+constexpr size_t FUSED_S_OFF = (FUSED_XS_BYTES + FUSED_CODE_BYTES + 15) & ~size_t(15);
+constexpr size_t FUSED_SMEM = FUSED_S_OFF + sizeof(FusedShared);
+
+struct FusedArgs {
+    // ---- input: block store (MODE_LOCAL/FAR/PAIR) ----
+    const uint8_t* arena0;        // the two payload arenas
+    const uint8_t* arena1;
+    const int* arena_cur;         // device scalar: which one is live
+    const uint64_t* p_off;
+    const int8_t* p_codec;
+    const double* p_delta;
+    const SideEntry* side_in;     // [plane][nsub]
+    const double* scale;          // [stride]
+    const uint64_t* job_stride;   // [slot]
+    // ---- input: raw planes (MODE_RAW) ----
+    const double* X;
+    uint64_t x_plane_stride;      // elements between a CTA's planes
+    // ---- gate ----
+    double u[8];
+    int kind;                     // GateKind
+    int t;                        // target (in-stride bit for LOCAL/FAR)
+    int local_ctl;                // in-stride control bit, -1 none
+    uint64_t flip_off;
+    const double* mean;           // reflect_mean: {re, im}
+    // ---- encoder ----
+    uint64_t n;                   // elements per plane (stride length)
+    const uint8_t* pending;       // per slot (null = all)
+    int snap;
+    uint8_t* out;
+    uint64_t cap;
+    SideEntry* side;              // output side entries per slot plane
+    uint64_t nsub;
+    uint64_t* out_len;
+    double* sumsq;
+    CodecParams cp;
+    unsigned long long* counters;
+};
+
+template <int LPL>
+__device__ __forceinline__ double& xrow(double* xs, int row_plane, int k)
+{
+    return xs[(row_plane * LPL + (k >> 5)) * XS_STRIDE + (k & 31)];
+}
+
+// ---- scans over the WPL warps of one plane --------------------------------
+template <int WPL>
+__device__ __forceinline__ RunFn fscan_fn(RunFn F, FusedShared& S, int pl)
+{
+    const int wl = threadIdx.x & 31, w = threadIdx.x >> 5;
+    RunFn inc = F;
+    for (int o = 1; o < 32; o <<= 1) {
+        RunFn u;
+        u.kt = __shfl_up_sync(0xffffffffu, inc.kt, o);
+        u.st = __shfl_up_sync(0xffffffffu, inc.st, o);
+        if (wl >= o) inc = fn_compose(u, inc);
+    }
+    __syncthreads();
+    if (wl == 31) S.wfn[w] = inc;
+    __syncthreads();
+    RunFn pre{0, 0};
+    for (int i = pl * WPL; i < w; ++i) pre = fn_compose(pre, S.wfn[i]);
+    return fn_compose(pre, inc);
+}
+
+template <int WPL>
+__device__ __forceinline__ uint64_t fscan_sum(uint64_t v, FusedShared& S, int pl, uint64_t& total)
+{
+    const int wl = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint64_t inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (wl >= o) inc += u;
+    }
+    __syncthreads();
+    if (wl == 31) S.wsum[w] = inc;
+    __syncthreads();
+    uint64_t pre = 0, tot = 0;
+    for (int i = pl * WPL; i < pl * WPL + WPL; ++i) {
+        if (i < w) pre += S.wsum[i];
+        tot += S.wsum[i];
+    }
+    total = tot;
+    return pre + inc - v;
+}
+
+template <int WPL>
+__device__ __forceinline__ long long fscan_last(long long idx, double val, FusedShared& S, int pl,
+                                                double& out_val)
+{
+    const int wl = threadIdx.x & 31, w = threadIdx.x >> 5;
+    long long ii = idx;
+    double vv = val;
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long ui = __shfl_up_sync(0xffffffffu, ii, o);
+        const double uv = __shfl_up_sync(0xffffffffu, vv, o);
+        if (wl >= o && ii < 0) {
+            ii = ui;
+            vv = uv;
+        }
+    }
+    long long ei = __shfl_up_sync(0xffffffffu, ii, 1);
+    double ev = __shfl_up_sync(0xffffffffu, vv, 1);
+    if (wl == 0) ei = -1;
+    __syncthreads();
+    if (wl == 31) {
+        S.wesc_i[w] = ii;
+        S.wesc_v[w] = vv;
+    }
+    __syncthreads();
+    if (ei < 0) {
+        for (int k = w - 1; k >= pl * WPL; --k) {
+            if (S.wesc_i[k] >= 0) {
+                ei = S.wesc_i[k];
+                ev = S.wesc_v[k];
+                break;
+            }
+        }
+    }
+    out_val = ev;
+    return ei;
+}
+
+// ---- exact stored sum of squares over a stride group ------------------------
+// group g = planes (2g, 2g+1), threads [g*GT, (g+1)*GT), GT = 2*LPL; each thread
+// owns 16 consecutive elements of the chunk.  Same algorithm as
+// sumsq_iteration (qcs_codec.cuh), restricted to the group's warps.
+template <int LPL>
+__device__ __forceinline__ double tsq_g(double* xs, int g, int k)
+{
+    const double r = xrow<LPL>(xs, 2 * g, k), i = xrow<LPL>(xs, 2 * g + 1, k);
+    return __dadd_rn(__dmul_rn(r, r), __dmul_rn(i, i));
+}
+
+template <int LPL, int NG>
+__device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FusedShared& S, unsigned long long* counters)
+{
+    constexpr int GT = 2 * LPL;          // threads per group
+    constexpr int GW = GT / 32;          // warps per group
+    constexpr int PER = (LPL * SUB) / GT;  // 16
+    const int tid = threadIdx.x;
+    const int g = tid / GT;
+    const int gt = tid % GT;
+    const int wl = tid & 31, w = tid >> 5;
+    const int kb = gt * PER;
+    int k0 = 0;
+    bool done = false;
+    for (;;) {
+        __syncthreads();
+        const double s = S.s[g];
+        if (k0 >= n_it) done = true;
+        const bool all_done = !__syncthreads_or(!done);
+        if (all_done) break;
+        if (counters && gt == 0 && !done) atomicAdd(&counters[1], 1ull);
+        // --- phase A: decide per group what to do (uniform within the group)
+        long long mine = LLONG_MAX;   // min-reduction candidate
+        uint64_t loc = 0;
+        int e = 0;
+        double to_units = 0.0;
+        uint64_t ms = 0;
+        const int state = done ? 0 : (s == 0.0 ? 1 : (ilogb(s) < -960 ? 2 : 3));
+        if (state == 1) {
+            for (int i = 0; i < PER; ++i) {
+                const int k = kb + i;
+                if (k >= k0 && k < n_it && tsq_g<LPL>(xs, g, k) != 0.0) {
+                    mine = k;
+                    break;
+                }
+            }
+        } else if (state == 3) {
+            e = ilogb(s);
+            to_units = ldexp(1.0, 52 - e);
+            ms = (uint64_t)(s * to_units);
+            for (int i = 0; i < PER; ++i) {
+                const int k = kb + i;
+                if (k < k0 || k >= n_it) continue;
+                const double y = tsq_g<LPL>(xs, g, k) * to_units;
+                // a tie (or an element beyond the binade) saturates the total, which
+                // forces the exact second pass below
+                loc = sat_add(loc, (y >= 9007199254740992.0 || y - floor(y) == 0.5) ? (1ull << 62)
+                                                                                   : (uint64_t)rint(y));
+            }
+        }
+        // group exclusive scan of loc (saturating)
+        uint64_t inc = loc;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (wl >= o) inc = sat_add(inc, u);
+        }
+        const uint64_t prev = __shfl_up_sync(0xffffffffu, inc, 1);
+        __syncthreads();
+        if (wl == 31) S.wsum[w] = inc;
+        __syncthreads();
+        uint64_t pre = 0, total = 0;
+        for (int i = g * GW; i < (g + 1) * GW; ++i) {
+            if (i < w) pre = sat_add(pre, S.wsum[i]);
+            total = sat_add(total, S.wsum[i]);
+        }
+        const uint64_t off = sat_add(pre, wl ? prev : 0);
+        // pass 2 only if the group total may cross the binade (or hit a tie)
+        if (state == 3 && ms + total >= (1ull << 53)) {
+            uint64_t run = off;
+            for (int i = 0; i < PER && mine == LLONG_MAX; ++i) {
+                const int k = kb + i;
+                if (k < k0 || k >= n_it) continue;
+                const double y = tsq_g<LPL>(xs, g, k) * to_units;
+                if (y >= 9007199254740992.0 || y - floor(y) == 0.5) {
+                    mine = k;
+                    break;
+                }
+                run = sat_add(run, (uint64_t)rint(y));
+                if (ms + run >= (1ull << 53)) mine = k;
+            }
+        } else if (state == 2) {
+            if (gt == 0) mine = k0;
+        }
+        // group min
+        long long m = mine;
+        for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+        __syncthreads();
+        if (wl == 0) S.wmin[w] = m;
+        __syncthreads();
+        long long kstar = LLONG_MAX;
+        for (int i = g * GW; i < (g + 1) * GW; ++i) kstar = min(kstar, S.wmin[i]);
+        if (state == 0) continue;
+        if (state == 1) {
+            if (kstar == LLONG_MAX) {
+                k0 = n_it;
+            } else {
+                if (gt == 0) S.s[g] = tsq_g<LPL>(xs, g, (int)kstar);
+                k0 = (int)kstar + 1;
+            }
+            continue;
+        }
+        if (state == 2) {
+            if (gt == 0) S.s[g] = __dadd_rn(s, tsq_g<LPL>(xs, g, k0));
+            ++k0;
+            continue;
+        }
+        if (kstar == LLONG_MAX) {
+            if (gt == 0) S.s[g] = (double)(ms + total) / to_units;
+            k0 = n_it;
+            continue;
+        }
+        if (kstar >= kb && kstar < kb + PER) {
+            uint64_t r2 = off;
+            for (int k = max(kb, k0); k < (int)kstar; ++k) r2 += (uint64_t)rint(tsq_g<LPL>(xs, g, k) * to_units);
+            const double before = (double)(ms + r2) / to_units;
+            S.s[g] = __dadd_rn(before, tsq_g<LPL>(xs, g, (int)kstar));
+        }
+        k0 = (int)kstar + 1;
+    }
+}
+
+// Per-phase cycle accounting (thread 0 of each CTA) into counters[8..15].
+#define QCS_PHASE(id)                                                        \
+    do {                                                                     \
+        if (tid == 0 && a.counters) {                                        \
+            const long long now_ = clock64();                                \
+            ph_acc[id] += (unsigned long long)(now_ - ph_t);                 \
+            ph_t = now_;                                                     \
+        }                                                                    \
+    } while (0)
+
+template <bool LOSSY, int NPL, int LPL, int MODE>
+__global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
+{
+    unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long ph_t = clock64();
+    constexpr int ITP = LPL * SUB;   // elements per plane per CTA iteration
+    constexpr int WPL = LPL / 32;    // warps per plane
+    const int b = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int pl = tid / LPL;
+    const int lane = tid % LPL;
+    // output slot of this plane
+    const uint64_t slot = MODE == MODE_PAIR ? 2ull * b + (pl >> 1) : (uint64_t)b;
+    const int comp = MODE == MODE_PAIR ? (pl & 1) : pl;
+    if (a.pending && !a.pending[MODE == MODE_PAIR ? 2ull * b : (uint64_t)b]) return;
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* xs = reinterpret_cast<double*>(smem);
+    int16_t* code = reinterpret_cast<int16_t*>(smem + FUSED_XS_BYTES);
+    FusedShared& S = *reinterpret_cast<FusedShared*>(smem + FUSED_S_OFF);
+
+    const CodecParams cp = a.cp;
+    const uint64_t n = a.n;
+    uint8_t* out = a.out + (2 * slot + comp) * a.cap;
+    SideEntry* side = a.side + (2 * slot + comp) * a.nsub;
+    double* xl = xs + (pl * LPL + lane) * XS_STRIDE;
+    int16_t* cl = code + pl * ITP + lane * SUB;
+    PlaneCarry& C = S.carry[pl];
+
+    // input plane of this thread (block store modes)
+    uint64_t in_stride = 0;
+    const uint8_t* in_bytes = nullptr;
+    int in_codec = 0;
+    double in_td = 0.0, in_scale = 1.0;
+    const SideEntry* in_side = nullptr;
+    const double* xg = nullptr;
+    if (MODE == MODE_RAW) {
+        xg = a.X + (uint64_t)b * NPL * a.x_plane_stride + (uint64_t)pl * a.x_plane_stride;
+    } else {
+        in_stride = a.job_stride[MODE == MODE_PAIR ? 2ull * b + (pl >> 1) : (uint64_t)b];
+        const uint64_t gpl = 2 * in_stride + comp;
+        in_bytes = (*a.arena_cur ? a.arena1 : a.arena0) + a.p_off[gpl];
+        in_codec = a.p_codec[gpl];
+        in_td = 2.0 * a.p_delta[gpl];
+        in_scale = a.scale[in_stride];
+        in_side = a.side_in + gpl * a.nsub;
+    }
+    double m8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m8[i] = a.u[i];
+    const uint64_t hb = (MODE == MODE_LOCAL || MODE == MODE_FAR) && a.kind <= 1 ? (1ull << a.t) : 0;
+
+    if (lane == 0) {
+        C.P = 0.0;
+        C.xprev = 0.0;
+        C.out_pos = 0;
+        C.open_ty = TY_NONE;
+        C.open_start = 0;
+        C.open_vmax = 0;
+        C.open_w = 0;
+        C.closes_open = 0;
+    }
+    if (tid < 2) S.s[tid] = 0.0;
+    __syncthreads();
+
+    for (uint64_t base = 0; base < n; base += ITP) {
+        const uint64_t e0 = base + (uint64_t)lane * SUB;
+        const int cnt = e0 < n ? (int)umin64(SUB, n - e0) : 0;
+        const bool final_iter = base + ITP >= n;
+        const int active = (int)umin64(LPL, (n - base + SUB - 1) / SUB);
+        const int n_it = (int)umin64(ITP, n - base);
+
+        // 1. input: decode (+ gate) or raw load, then snap_zeros
+        if (MODE == MODE_RAW) {
+#pragma unroll 8
+            for (int i = lane; i < ITP; i += LPL) {
+                double* dst = &xrow<LPL>(xs, pl, i);
+                if (base + i < n) {
+                    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(xg + base + i)
+                                 : "memory");
+                } else {
+                    *dst = 0.0;
+                }
+            }
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            __syncthreads();
+        } else {
+            if (cnt > 0) decode_sub(in_bytes, in_codec, in_td, in_side[e0 / SUB], cnt, xl, in_scale);
+            if (MODE == MODE_FAR && cnt > 0) {
+                const uint64_t pe0 = e0 ^ hb;
+                decode_sub(in_bytes, in_codec, in_td, in_side[pe0 / SUB], cnt,
+                           xs + ((pl + 2) * LPL + lane) * XS_STRIDE, in_scale);
+            }
+            __syncthreads();
+            // gate (run_plan_unit, gate.cpp:405-454)
+            if (MODE == MODE_PAIR) {
+                for (int i = tid; i < n_it; i += NPL * LPL) {
+                    if (a.local_ctl >= 0 && !(((base + i) >> a.local_ctl) & 1)) continue;
+                    pair_update(m8, xrow<LPL>(xs, 0, i), xrow<LPL>(xs, 1, i), xrow<LPL>(xs, 2, i),
+                                xrow<LPL>(xs, 3, i));
+                }
+            } else if (MODE == MODE_FAR) {
+                for (int i = tid; i < n_it; i += NPL * LPL) {
+                    const uint64_t gi = base + i;
+                    const uint64_t lo_idx = gi & ~hb;
+                    if (a.local_ctl >= 0 && !((lo_idx >> a.local_ctl) & 1)) continue;
+                    const double sr = xrow<LPL>(xs, 0, i), si = xrow<LPL>(xs, 1, i);
+                    const double pr = xrow<LPL>(xs, 2, i), pi = xrow<LPL>(xs, 3, i);
+                    double r, im;
+                    if (!(gi & hb)) pair_lo(m8, sr, si, pr, pi, r, im);
+                    else pair_hi(m8, pr, pi, sr, si, r, im);
+                    xrow<LPL>(xs, 0, i) = r;
+                    xrow<LPL>(xs, 1, i) = im;
+                }
+            } else {  // MODE_LOCAL
+                if (a.kind <= 1) {
+                    const uint64_t lo_mask = hb - 1;
+                    for (int q = tid; q < n_it / 2; q += NPL * LPL) {
+                        const int i0 = (int)((((uint64_t)q & ~lo_mask) << 1) | ((uint64_t)q & lo_mask));
+                        const int i1 = i0 | (int)hb;
+                        if (a.local_ctl >= 0 && !(((base + i0) >> a.local_ctl) & 1)) continue;
+                        pair_update(m8, xrow<LPL>(xs, 0, i0), xrow<LPL>(xs, 1, i0), xrow<LPL>(xs, 0, i1),
+                                    xrow<LPL>(xs, 1, i1));
+                    }
+                } else if (a.kind == 2) {
+                    if (tid == 0 && a.flip_off >= base && a.flip_off < base + n_it) {
+                        const int k = (int)(a.flip_off - base);
+                        xrow<LPL>(xs, 0, k) = -xrow<LPL>(xs, 0, k);
+                        xrow<LPL>(xs, 1, k) = -xrow<LPL>(xs, 1, k);
+                    }
+                } else {
+                    const double mr2 = 2.0 * a.mean[0], mi2 = 2.0 * a.mean[1];
+                    for (int i = tid; i < n_it; i += NPL * LPL) {
+                        xrow<LPL>(xs, 0, i) = __dsub_rn(mr2, xrow<LPL>(xs, 0, i));
+                        xrow<LPL>(xs, 1, i) = __dsub_rn(mi2, xrow<LPL>(xs, 1, i));
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (a.snap && cnt > 0) {
+            for (int i = 0; i < cnt; ++i) xl[i] = snap(xl[i]);
+        }
+        __syncthreads();
+
+        QCS_PHASE(0);
+        // 2-4. codes and exact predictors
+        if (LOSSY && cp.pow2) {
+            // event rounds (see qcs_codec.cuh k_encode for the argument)
+            if (lane == 0) S.npin[pl] = 0;
+            if (cnt > 0 && lane + 1 == active) C.xprev_next = xl[cnt - 1];
+            const double x_left = cnt > 0 ? (lane == 0 ? C.xprev : xrow<LPL>(xs, pl, lane * SUB - 1)) : 0.0;
+            // predicted escapes of this lane, once (bit i = element i)
+            uint32_t emask = 0;
+            {
+                double xp = x_left;
+                for (int i = 0; i < cnt; ++i) {
+                    const double x = xl[i];
+                    emask |= (uint32_t)predict_escape(cp, x, xp) << i;
+                    xp = x;
+                }
+            }
+            __syncthreads();
+            long long f = LLONG_MAX;
+            long long aidx = -1;
+            double aval = 0.0;
+            for (int round = 0;; ++round) {
+                const int np = S.npin[pl];
+                // (a) last event of the lane: last predicted escape or pin
+                long long my_last = emask ? (long long)e0 + (31 - __clz(emask)) : -1;
+                double my_val = my_last >= 0 ? xl[my_last - (long long)e0] : 0.0;
+                for (int q = 0; q < np; ++q) {
+                    const long long k = S.pin_idx[pl][q];
+                    if (k >= (long long)e0 && k < (long long)e0 + cnt && k >= my_last) {
+                        my_last = k;
+                        my_val = S.pin_val[pl][q];
+                    }
+                }
+                if (cnt == 0) my_last = -1;
+                aidx = fscan_last<WPL>(my_last, my_val, S, pl, aval);
+                // (b) speculate and verify every element
+                long long fail = LLONG_MAX;
+                double fprev = 0.0;
+                if (cnt > 0) {
+                    double A = aidx >= 0 ? aval : C.P;
+                    const long long Aidx = aidx >= 0 ? aidx : (long long)base - 1;
+                    double Pprev = (Aidx == (long long)e0 - 1) ? A : lattice_point(cp, A, x_left);
+                    if (np == 0) {
+                        // Mprev: lattice index of Pprev relative to A when Pprev is
+                        // known to be exactly A + 2d*Mprev (else NaN => full check)
+                        double Mprev = (Aidx == (long long)e0 - 1) ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
+                        if (Aidx != (long long)e0 - 1) {
+                            double Atmp = A, Mt;
+                            bool sf;
+                            const double v = lattice_step_m(cp, Atmp, x_left, Mt, sf);
+                            if (same_bits(Atmp, A) && same_bits(v, Pprev)) Mprev = Mt;
+                        }
+#pragma unroll 4
+                        for (int i = 0; i < cnt; ++i) {
+                            const double x = xl[i];
+                            double Ph, M = 0.0;
+                            bool safe = false;
+                            if ((emask >> i) & 1u) {
+                                Ph = x;
+                                A = x;
+                            } else {
+                                const double A0 = A;
+                                Ph = lattice_step_m(cp, A, x, M, safe);
+                                const double q = __dsub_rn(M, Mprev);  // NaN if Mprev unknown
+                                safe = safe && fabs(q) <= 32766.0;
+                                if (safe) cl[i] = (int16_t)q;
+                                if (!same_bits(A, A0)) M = 0.0;  // re-anchored at Ph
+                            }
+                            if (!safe) {
+                                double P2 = Pprev;
+                                const int32_t c = ref_step(cp, P2, x);
+                                cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
+                                if (!same_bits(P2, Ph) && fail == LLONG_MAX) {
+                                    fail = (long long)e0 + i;
+                                    fprev = Pprev;
+                                }
+                            }
+                            Mprev = ((emask >> i) & 1u) ? 0.0 : M;
+                            Pprev = Ph;
+                        }
+                    } else {
+                        int pp = 0;
+                        while (pp < np && S.pin_idx[pl][pp] < (long long)e0) ++pp;
+                        for (int i = 0; i < cnt; ++i) {
+                            const double x = xl[i];
+                            double Ph;
+                            int16_t c16;
+                            if (pp < np && S.pin_idx[pl][pp] == (long long)e0 + i) {
+                                Ph = S.pin_val[pl][pp];
+                                c16 = S.pin_code[pl][pp];
+                                A = Ph;
+                                ++pp;
+                            } else {
+                                if ((emask >> i) & 1u) {
+                                    Ph = x;
+                                    A = x;
+                                } else {
+                                    Ph = lattice_step(cp, A, x);
+                                }
+                                double P2 = Pprev;
+                                const int32_t c = ref_step(cp, P2, x);
+                                c16 = c == WCODE ? WCODE16 : (int16_t)c;
+                                if (!same_bits(P2, Ph) && fail == LLONG_MAX) {
+                                    fail = (long long)e0 + i;
+                                    fprev = Pprev;
+                                }
+                            }
+                            cl[i] = c16;
+                            Pprev = Ph;
+                        }
+                    }
+                }
+                long long mm = fail;
+                for (int o = 16; o; o >>= 1) mm = min(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+                if ((tid & 31) == 0) S.wfail[tid >> 5] = mm;
+                __syncthreads();
+                f = LLONG_MAX;
+                for (int w = pl * WPL; w < pl * WPL + WPL; ++w) f = min(f, S.wfail[w]);
+                if (fail != LLONG_MAX && fail == f) S.fail_prev[pl] = fprev;
+                const bool more = f != LLONG_MAX && S.npin[pl] < MAXPIN;
+                if (!__syncthreads_or(more)) break;
+                if (lane == 0 && more) {
+                    double P = S.fail_prev[pl];
+                    const int32_t c = ref_step(cp, P, xrow<LPL>(xs, pl, (int)(f - (long long)base)));
+                    const int q = S.npin[pl];
+                    S.pin_idx[pl][q] = f;
+                    S.pin_val[pl][q] = P;
+                    S.pin_code[pl][q] = c == WCODE ? WCODE16 : (int16_t)c;
+                    S.npin[pl] = q + 1;
+                    if (a.counters) atomicAdd(&a.counters[0], 1ull);
+                }
+                __syncthreads();
+            }
+            const long long fser = f;
+            QCS_PHASE(1);
+            // final predictors into xs (events of the last round still hold)
+            {
+                const int np = S.npin[pl];
+                if (cnt > 0) {
+                    double A = aidx >= 0 ? aval : C.P;
+                    const long long Aidx = aidx >= 0 ? aidx : (long long)base - 1;
+                    double Pprev = (Aidx == (long long)e0 - 1) ? A : lattice_point(cp, A, x_left);
+                    S.entryP[tid] = Pprev;
+                    int pp = 0;
+                    while (pp < np && S.pin_idx[pl][pp] < (long long)e0) ++pp;
+                    for (int i = 0; i < cnt; ++i) {
+                        const long long k = (long long)e0 + i;
+                        if (k >= fser) break;
+                        const double x = xl[i];
+                        double Ph;
+                        if (pp < np && S.pin_idx[pl][pp] == k) {
+                            Ph = S.pin_val[pl][pp];
+                            A = Ph;
+                            ++pp;
+                        } else if ((emask >> i) & 1u) {
+                            Ph = x;
+                            A = x;
+                        } else {
+                            Ph = lattice_step(cp, A, x);
+                        }
+                        xl[i] = Ph;
+                        Pprev = Ph;
+                    }
+                    S.exitP[tid] = Pprev;
+                }
+                __syncthreads();
+                if (lane == 0 && fser != LLONG_MAX) {
+                    if (a.counters) atomicAdd(&a.counters[3], 1ull);
+                    const int k0 = (int)(fser - (long long)base);
+                    double P = S.fail_prev[pl];
+                    for (int k = k0; k < n_it; ++k) {
+                        if ((k & (SUB - 1)) == 0) S.entryP[pl * LPL + k / SUB] = P;
+                        const int32_t c = ref_step(cp, P, xrow<LPL>(xs, pl, k));
+                        code[pl * ITP + k] = c == WCODE ? WCODE16 : (int16_t)c;
+                        xrow<LPL>(xs, pl, k) = P;
+                    }
+                    S.exitP[pl * LPL + active - 1] = P;
+                }
+                if (lane == 0 && active > 0) C.Pnext = S.exitP[pl * LPL + active - 1];
+                __syncthreads();
+            }
+        } else if (LOSSY) {
+            // other bounds: lane-serial reference chains from guessed entries,
+            // verified against the left neighbour's exit and repaired
+            double entry = 0.0;
+            if (cnt > 0) {
+                if (lane + 1 == active) C.xprev_next = xl[cnt - 1];
+                entry = lane == 0 ? C.P
+                                  : anchored_guess(cp, C.P, xrow<LPL>(xs, pl, lane * SUB - 2),
+                                                   xrow<LPL>(xs, pl, lane * SUB - 1));
+                S.entryP[tid] = entry;
+            }
+            __syncthreads();
+            if (cnt > 0) {
+                double P = entry;
+                for (int i = 0; i < cnt; ++i) {
+                    const int32_t c = ref_step(cp, P, xl[i]);
+                    cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
+                }
+                S.exitP[tid] = P;
+            }
+            __syncthreads();
+            for (int pass = 0; pass < 4; ++pass) {
+                const bool bad = cnt > 0 && lane > 0 && !same_bits(S.entryP[tid], S.exitP[tid - 1]);
+                const double want = bad ? S.exitP[tid - 1] : 0.0;
+                if (!__syncthreads_or(bad)) break;
+                if (bad) {
+                    if (a.counters) atomicAdd(&a.counters[0], 1ull);
+                    double Pn = want, Po = S.entryP[tid];
+                    bool resync = false;
+                    for (int i = 0; i < cnt; ++i) {
+                        const double x = xl[i];
+                        const int16_t co = cl[i];
+                        if (co == WCODE16) Po = x;
+                        else if (co != 0) Po = __dadd_rn(Po, __dmul_rn(cp.td, (double)co));
+                        const int32_t c = ref_step(cp, Pn, x);
+                        cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
+                        if (same_bits(Pn, Po)) {
+                            resync = true;
+                            break;
+                        }
+                    }
+                    S.entryP[tid] = want;
+                    if (!resync) S.exitP[tid] = Pn;
+                }
+                __syncthreads();
+            }
+            if (lane == 0 && active > 0) {
+                for (int l = 1; l < active; ++l) {
+                    const int id = pl * LPL + l;
+                    const double want = S.exitP[id - 1];
+                    if (same_bits(want, S.entryP[id])) continue;
+                    if (a.counters) atomicAdd(&a.counters[0], 1ull);
+                    double Pn = want, Po = S.entryP[id];
+                    S.entryP[id] = want;
+                    const int c2 = (int)umin64(SUB, n - (base + (uint64_t)l * SUB));
+                    const double* xl2 = xs + id * XS_STRIDE;
+                    int16_t* cl2 = code + pl * ITP + l * SUB;
+                    bool resync = false;
+                    for (int i = 0; i < c2; ++i) {
+                        const double x = xl2[i];
+                        const int16_t co = cl2[i];
+                        if (co == WCODE16) Po = x;
+                        else if (co != 0) Po = __dadd_rn(Po, __dmul_rn(cp.td, (double)co));
+                        const int32_t c = ref_step(cp, Pn, x);
+                        cl2[i] = c == WCODE ? WCODE16 : (int16_t)c;
+                        if (same_bits(Pn, Po)) {
+                            resync = true;
+                            break;
+                        }
+                    }
+                    if (!resync) S.exitP[id] = Pn;
+                }
+                C.Pnext = S.exitP[pl * LPL + active - 1];
+            }
+            __syncthreads();
+            if (cnt > 0) {
+                double P = S.entryP[tid];
+                for (int i = 0; i < cnt; ++i) {
+                    const int16_t co = cl[i];
+                    if (co == WCODE16) P = xl[i];
+                    else if (co != 0) P = __dadd_rn(P, __dmul_rn(cp.td, (double)co));
+                    xl[i] = P;
+                }
+            }
+            __syncthreads();
+        } else {
+            if (cnt > 0)
+                for (int i = 0; i < cnt; ++i) cl[i] = __double_as_longlong(xl[i]) == 0 ? (int16_t)0 : WCODE16;
+            __syncthreads();
+        }
+
+        QCS_PHASE(2);
+        // 5. stored sum of squares per stride
+        if (a.sumsq) fused_sumsq<LPL, NPL / 2>(xs, n_it, S, a.counters);
+
+        QCS_PHASE(3);
+        // 6. run summary of each lane (bitmasks) and the run entering it
+        const LaneMasks lm = cnt > 0 ? lane_masks(cl, cnt) : LaneMasks{0u, 0u, 0u};
+        const int t0 = cnt > 0 ? mask_type(lm, 0) : TY_NONE;
+        const bool full = cnt > 0 && (lm.z == lm.valid || lm.w == lm.valid);
+        S.ftype[pl * (LPL + 1) + lane] = (int8_t)t0;
+        if (lane == 0) S.ftype[pl * (LPL + 1) + LPL] = TY_NONE;
+        // tail run of the lane (lane-local start)
+        int tail_ty = TY_NONE, tail_j = 0;
+        if (cnt > 0) {
+            const int last = cnt - 1;
+            tail_ty = mask_type(lm, last);
+            if (tail_ty != TY_C) {
+                const uint32_t mm = tail_ty == TY_Z ? lm.z : lm.w;
+                const uint32_t below = (~mm) & ((1u << last) - 1u);
+                tail_j = below ? (32 - __clz(below)) : 0;
+            } else {
+                tail_ty = TY_NONE;
+            }
+        }
+        RunFn F{0, 0};
+        if (cnt > 0) {
+            if (full) F = RunFn{(2 << 2) | t0, e0};
+            else if (tail_ty != TY_NONE) F = RunFn{(1 << 2) | tail_ty, e0 + tail_j};
+            else F = RunFn{(1 << 2) | TY_NONE, 0};
+        }
+        const RunFn inc = fscan_fn<WPL>(F, S, pl);
+        S.fincl[tid] = inc;
+        __syncthreads();
+        int in_ty = C.open_ty;
+        uint64_t in_st = C.open_start;
+        if (lane > 0) fn_apply(S.fincl[tid - 1], in_ty, in_st);
+        const int next_ft = (lane + 1 < active) ? S.ftype[pl * (LPL + 1) + lane + 1] : TY_NONE;
+        uint64_t tail_st = e0 + tail_j;
+        if (tail_ty != TY_NONE && tail_j == 0 && in_ty == tail_ty) tail_st = in_st;
+        const bool tail_closes = lane + 1 < active ? (tail_ty != TY_NONE && next_ft != tail_ty) : final_iter;
+
+        // 7. byte count of the tokens this lane closes
+        uint32_t nbytes = 0;
+        int closes_open = 0;
+        uint64_t close_vlen = 0;
+        lane_tokens(
+            lm, cl, cnt, e0, in_ty, in_st, tail_closes, lane == 0,
+            [&](int t, uint64_t st, uint64_t end) {
+                const uint64_t len = end - st;
+                const int vl = varint_len(run_token(LOSSY, t, len));
+                nbytes += vl + (t == TY_W ? 8u * (uint32_t)len : 0u);
+                if (st < base) {
+                    closes_open = 1;
+                    close_vlen = vl;
+                }
+            },
+            [&](int16_t q) { nbytes += varint_len(code_token(q)); });
+        if (closes_open) {
+            C.closes_open = 1;
+            C.close_vlen = close_vlen;
+        }
+        uint64_t tot;
+        const uint64_t excl = fscan_sum<WPL>(nbytes, S, pl, tot);
+        const uint64_t bstart = C.out_pos + excl;
+        S.bstart[tid] = bstart;
+        if (lane == 0) {
+            C.iter_bytes = tot;
+            C.carry_tok = C.out_pos;
+            C.mv_bytes = 0;
+            C.mv_shift = 0;
+        }
+        __syncthreads();
+        if (lane == 0) {
+            if (C.open_ty != TY_NONE && C.closes_open) {
+                C.carry_w = C.out_pos + C.close_vlen;
+                if (C.open_ty == TY_W && C.open_vmax > C.close_vlen) {
+                    C.mv_bytes = 8 * (base - C.open_start);
+                    C.mv_shift = C.open_vmax - C.close_vlen;
+                }
+            } else {
+                C.carry_w = C.open_w;
+            }
+        }
+        __syncthreads();
+
+        QCS_PHASE(4);
+        // 8. slide words of a carried W run left if its varint came out shorter
+        if (tid == 0) {
+            uint64_t mx = 0;
+            for (int p = 0; p < NPL; ++p) mx = max(mx, S.carry[p].mv_bytes);
+            S.mvmax = mx;
+            if (a.counters && mx) atomicAdd(&a.counters[2], (unsigned long long)mx);
+        }
+        __syncthreads();
+        for (uint64_t o = 0; o < S.mvmax; o += LPL * 8) {
+            uint8_t tmp[8];
+            const uint64_t src0 = C.out_pos + C.open_vmax + o + lane * 8;
+            int m = 0;
+            if (o + lane * 8 < C.mv_bytes) {
+                m = (int)umin64(8, C.mv_bytes - o - lane * 8);
+                for (int i = 0; i < m; ++i) tmp[i] = out[src0 + i];
+            }
+            __syncthreads();
+            for (int i = 0; i < m; ++i) out[src0 - C.mv_shift + i] = tmp[i];
+            __syncthreads();
+        }
+
+        // 9. write tokens (see qcs_codec.cuh for the placement rules)
+        {
+            uint64_t pos = bstart;
+            lane_tokens(
+                lm, cl, cnt, e0, in_ty, in_st, tail_closes, lane == 0,
+                [&](int t, uint64_t st, uint64_t end) {
+                    const uint64_t len = end - st;
+                    const uint64_t v = run_token(LOSSY, t, len);
+                    const int vl = varint_len(v);
+                    put_varint(out + pos, v);
+                    if (t == TY_W) {
+                        for (uint64_t k = (st > e0 ? st : e0); k < end; ++k)
+                            put_word(out + pos + vl + 8 * (k - st), (uint64_t)__double_as_longlong(xl[k - e0]));
+                    }
+                    if (st < e0 && st >= base) {
+                        const int sl = pl * LPL + (int)((st - base) / SUB);
+                        S.runtok[sl] = pos;
+                        S.runw[sl] = pos + vl;
+                    }
+                    pos += vl + (t == TY_W ? 8 * len : 0);
+                },
+                [&](int16_t q) {
+                    const uint64_t v = code_token(q);
+                    put_varint(out + pos, v);
+                    pos += varint_len(v);
+                });
+            if (lane + 1 == active && !final_iter && tail_ty != TY_NONE && tail_st >= base) {
+                const uint64_t tokpos = C.out_pos + C.iter_bytes;
+                const uint64_t vmax = tail_ty == TY_W ? varint_len(run_token(LOSSY, TY_W, n - tail_st)) : 0;
+                const int sl = pl * LPL + (int)((tail_st - base) / SUB);
+                S.runtok[sl] = tokpos;
+                S.runw[sl] = tokpos + vmax;
+            }
+        }
+        __syncthreads();
+
+        // 10. words of a W run reaching past this lane
+        if (cnt > 0 && tail_ty == TY_W && !tail_closes) {
+            const uint64_t wb = tail_st < base ? C.carry_w : S.runw[pl * LPL + (tail_st - base) / SUB];
+            for (uint64_t k = (tail_st > e0 ? tail_st : e0); k < e0 + cnt; ++k)
+                put_word(out + wb + 8 * (k - tail_st), (uint64_t)__double_as_longlong(xl[k - e0]));
+        }
+
+        // 11. side index
+        if (cnt > 0) {
+            SideEntry se;
+            if (in_ty != TY_NONE && t0 == in_ty) {
+                se.off = (uint32_t)(in_st < base ? C.carry_tok : S.runtok[pl * LPL + (in_st - base) / SUB]);
+                se.skip = (uint32_t)(e0 - in_st);
+            } else {
+                const bool emitted_here = !full || tail_closes;
+                uint64_t cover = bstart;
+                if (lane == 0 && in_ty != TY_NONE) {
+                    const uint64_t len = e0 - in_st;
+                    cover += varint_len(run_token(LOSSY, in_ty, len)) + (in_ty == TY_W ? 8 * len : 0);
+                }
+                se.off = (uint32_t)(emitted_here ? cover : S.runtok[tid]);
+                se.skip = 0;
+            }
+            se.pred = LOSSY ? S.entryP[tid] : 0.0;
+            side[e0 / SUB] = se;
+        }
+
+        QCS_PHASE(5);
+        // 12. carry to the next iteration
+        __syncthreads();
+        if (lane == 0 && active > 0) {
+            const int last = pl * LPL + active - 1;
+            C.P = LOSSY ? C.Pnext : 0.0;
+            C.xprev = C.xprev_next;
+            const uint64_t new_pos = C.out_pos + C.iter_bytes;
+            int oty = C.open_ty;
+            uint64_t ost = C.open_start;
+            fn_apply(S.fincl[last], oty, ost);
+            if (final_iter || oty == TY_NONE) {
+                C.open_ty = TY_NONE;
+            } else if (ost < base) {
+                // the old carried run is still open: keep its reservation
+            } else {
+                C.open_ty = oty;
+                C.open_start = ost;
+                C.open_vmax = oty == TY_W ? varint_len(run_token(LOSSY, TY_W, n - ost)) : 0;
+                C.open_w = new_pos + C.open_vmax;
+            }
+            C.out_pos = new_pos;
+            C.closes_open = 0;
+        }
+        __syncthreads();
+    }
+
+    QCS_PHASE(6);
+    if (tid == 0 && a.counters)
+        for (int i = 0; i < 8; ++i) atomicAdd(&a.counters[8 + i], ph_acc[i]);
+    if (lane == 0) a.out_len[2 * slot + comp] = C.out_pos;
+    if (a.sumsq && (tid % (2 * LPL)) == 0) a.sumsq[MODE == MODE_PAIR ? 2ull * b + tid / (2 * LPL) : (uint64_t)b] =
+        S.s[tid / (2 * LPL)];
+}
+
+}  // namespace qcs

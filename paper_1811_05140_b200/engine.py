@@ -361,10 +361,12 @@ class CompressedState:
         return out
 
     def counters(self) -> dict:
-        buf = (C.c_uint64 * 4)()
-        _check(lib().qcs_state_counters(self._h, buf, 4))
+        buf = (C.c_uint64 * 16)()
+        _check(lib().qcs_state_counters(self._h, buf, 16))
         return {"repaired_lanes": buf[0], "sum_passes": buf[1], "slid_bytes": buf[2],
-                "serial_fallback_lanes": buf[3]}
+                "serial_fallback_lanes": buf[3],
+                "phase_cycles": {k: buf[8 + i] for i, k in enumerate(
+                    ("input", "rounds", "final", "sum", "tokcount", "write", "tail"))}}
 
     def launches(self) -> int:
         return lib().qcs_state_launches(self._h)
