@@ -85,7 +85,8 @@ const char* qcs_last_error(void);
 int qcs_version(void);
 
 /* CompressedState::basis_state (aalc.cpp:140-174) on `device`.
- * StateGeometry::make validation (core.cpp:9-23). */
+ * StateGeometry::make validation (core.cpp:9-23).  basis = UINT64_MAX creates
+ * an all-zero state (a shard that holds none of the amplitude). */
 int qcs_state_create(int n_qubits, int stride_bits, uint64_t basis, int device,
                      qcs_dev_state_t* out);
 void qcs_state_destroy(qcs_dev_state_t st);
@@ -99,6 +100,26 @@ void qcs_state_destroy(qcs_dev_state_t st);
 int qcs_apply_gate(qcs_dev_state_t st, const qcs_gate_desc* gate, const double* ladder,
                    int n_levels, double theta, qcs_stride_report* reports,
                    uint64_t* n_reports, double* norm_after);
+
+/* qcs_apply_gate with flags, for a state that is one shard of a larger one.
+ * QCS_NO_RENORM skips the lazy renormalisation (aalc.cpp:410-419) so the
+ * caller renormalises globally from qcs_stride_norms + qcs_scale_all in the
+ * reference's stride order.  QCS_GIVEN_MEAN makes reflect_mean use mean[2]
+ * (re, im) instead of this shard's own mean pass (aalc.cpp:270-295); the
+ * caller combines qcs_stride_sums of every shard in global stride order. */
+#define QCS_NO_RENORM 1
+#define QCS_GIVEN_MEAN 2
+int qcs_apply_gate_ex(qcs_dev_state_t st, const qcs_gate_desc* gate, const double* ladder,
+                      int n_levels, double theta, int flags, const double* mean,
+                      qcs_stride_report* reports, uint64_t* n_reports, double* norm_after);
+/* Per-stride amplitude sums (stride_amplitude_sum, gate.cpp:303-311) of the
+ * decompressed, scaled strides: partial[2j] = re, partial[2j+1] = im. */
+int qcs_stride_sums(qcs_dev_state_t st, double* partial);
+/* Per-stride pending scale and stored sum of squares (StrideStorage,
+ * aalc.hpp:162-167), 2^(n-s) doubles each; either pointer may be null. */
+int qcs_stride_norms(qcs_dev_state_t st, double* scales, double* sums);
+/* scale *= f for every stride (the renormalisation step, aalc.cpp:413). */
+int qcs_scale_all(qcs_dev_state_t st, double f);
 
 /* apply_program_range (aalc.cpp:588-634) over gates[0..n_gates): one
  * GateRecord per gate, gate_index = first_index + i.  Launches are queued

@@ -92,6 +92,15 @@ class Oracle:
                                          C.POINTER(C.c_uint64)]
         lib.qo_stored_stride.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_double),
                                          C.POINTER(C.c_double)]
+        lib.qo_apply_gate_ex.argtypes = [C.c_void_p, C.POINTER(Gate), C.POINTER(C.c_double),
+                                         C.c_int, C.c_double, C.c_int, C.POINTER(C.c_double),
+                                         C.POINTER(Report),
+                                         C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        lib.qo_stride_sums.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+        lib.qo_stride_norms.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        lib.qo_scale_all.argtypes = [C.c_void_p, C.c_double]
+        lib.qo_import_blocks.argtypes = [C.c_void_p, C.c_uint64, C.c_char_p, C.c_uint64,
+                                         C.c_double, C.c_double]
 
     def _check(self, rc: int):
         if rc:
@@ -178,6 +187,52 @@ class OracleState:
         buf = (C.c_uint8 * n.value)()
         self.o._check(self.o.lib.qo_export_blocks(self.h, C.c_uint64(j), buf, n.value, C.byref(n)))
         return bytes(buf)
+
+    # ---- sharded-run hooks (shard interface of paper_1811_05140_b200.distributed) ----
+    def apply(self, g, ladder: Sequence[float], theta: float, mean=None):
+        lad = (C.c_double * len(ladder))(*ladder)
+        reps = (Report * (1 << (self.n - self.s)))()
+        nr = C.c_uint64()
+        norm = C.c_double()
+        gs = gate_struct(g)
+        m = (C.c_double * 2)(*(mean or (0.0, 0.0)))
+        self.o._check(self.o.lib.qo_apply_gate_ex(self.h, C.byref(gs), lad, len(ladder),
+                                                  C.c_double(theta), 1 | (2 if mean else 0), m,
+                                                  reps, C.byref(nr), C.byref(norm)))
+        return [(r.stride_index, r.chosen_delta, r.ratio, r.bytes_in, r.bytes_out,
+                 bool(r.threshold_met)) for r in reps[: nr.value]]
+
+    def stride_sums(self) -> np.ndarray:
+        p = np.empty(2 << (self.n - self.s))
+        self.o._check(self.o.lib.qo_stride_sums(self.h, _dptr(p)))
+        return p
+
+    def stride_norms(self):
+        ns = 1 << (self.n - self.s)
+        sc, sm = np.empty(ns), np.empty(ns)
+        self.o._check(self.o.lib.qo_stride_norms(self.h, _dptr(sc), _dptr(sm)))
+        return sc, sm
+
+    def scale_all(self, f: float):
+        self.o._check(self.o.lib.qo_scale_all(self.h, C.c_double(f)))
+
+    def export(self, j: int):
+        sc, ss, _, _ = self.stride_info(j)
+        return self.export_blocks(j), sc, ss
+
+    def import_(self, j: int, blob: bytes, scale: float, ssq: float):
+        self.o._check(self.o.lib.qo_import_blocks(self.h, C.c_uint64(j), blob, len(blob),
+                                                  C.c_double(scale), C.c_double(ssq)))
+
+
+class OracleBackend:
+    """Local-shard factory for distributed.ShardedState on the CPU oracle."""
+
+    def __init__(self, oracle: Optional[Oracle] = None):
+        self.o = oracle or Oracle()
+
+    def create(self, n: int, s: int, basis: Optional[int]):
+        return OracleState(self.o, n, s, (1 << 64) - 1 if basis is None else basis)
 
 
 class Reference:

@@ -608,7 +608,8 @@ int qo_state_create(int n, int s, uint64_t basis, qo_state** out)
 {
     if (n < 1 || n > 59) return fail(QO_E_INVALID, "n_qubits must be in [1, 59], got %d", n);
     if (s < 0 || s > n) return fail(QO_E_INVALID, "stride_bits must be in [0, n_qubits], got %d", s);
-    if (basis >= ((uint64_t)1 << n)) return fail(QO_E_RANGE, "basis index out of range");
+    const int zero_state = basis == ~(uint64_t)0;  /* shard holding no amplitude */
+    if (!zero_state && basis >= ((uint64_t)1 << n)) return fail(QO_E_RANGE, "basis index out of range");
     qo_state* st = (qo_state*)calloc(1, sizeof *st);
     st->n = n;
     st->s = s;
@@ -618,7 +619,7 @@ int qo_state_create(int n, int s, uint64_t basis, qo_state** out)
     double* buf = (double*)calloc(st->L, sizeof(double));
     block_t zero;
     block_make(buf, st->L, 0.0, &zero);
-    const uint64_t hot = basis >> s;
+    const uint64_t hot = zero_state ? ~(uint64_t)0 : basis >> s;
     for (uint64_t j = 0; j < st->n_strides; ++j) {
         stride_t* t = &st->st[j];
         if (j == hot) {
@@ -636,7 +637,7 @@ int qo_state_create(int n, int s, uint64_t basis, qo_state** out)
     }
     block_free(&zero);
     free(buf);
-    st->norm_sq = 1.0;
+    st->norm_sq = zero_state ? 0.0 : 1.0;
     *out = st;
     return 0;
 }
@@ -712,10 +713,19 @@ static int check_ladder(const double* lad, int nl, double theta)
 
 /* CompressedState::apply_gate, aalc.cpp:261-420 (serial over units; the
  * reference result is independent of the worker count, aalc.hpp:127-129). */
+
 int qo_apply_gate(qo_state* st, const qo_gate* g, const double* lad, int nl,
                   double theta, qo_report* reports, uint64_t* n_reports,
                   double* norm_after)
 {
+    return qo_apply_gate_ex(st, g, lad, nl, theta, 0, NULL, reports, n_reports, norm_after);
+}
+
+int qo_apply_gate_ex(qo_state* st, const qo_gate* g, const double* lad, int nl,
+                     double theta, int flags, const double* given_mean, qo_report* reports,
+                     uint64_t* n_reports, double* norm_after)
+{
+    const int no_renorm = flags & 1;
     int rc = validate_gate(st->n, g);
     if (rc) return rc;
     rc = check_ladder(lad, nl, theta);
@@ -759,7 +769,10 @@ int qo_apply_gate(qo_state* st, const qo_gate* g, const double* lad, int nl,
 
     /* mean pass, aalc.cpp:270-295 */
     double mean_re = 0.0, mean_im = 0.0;
-    if (needs_mean) {
+    if (needs_mean && (flags & 2)) {
+        mean_re = given_mean[0];
+        mean_im = given_mean[1];
+    } else if (needs_mean) {
         double sr_tot = 0.0, si_tot = 0.0;
         for (uint64_t j = 0; j < NS && !rc; ++j) {
             rc = decompress_stride(st, j, a_re, a_im, 1);
@@ -891,7 +904,7 @@ int qo_apply_gate(qo_state* st, const qo_gate* g, const double* lad, int nl,
             t->scale = 1.0;
         }
         /* lazy renormalisation, aalc.cpp:410-418 */
-        const double total = norm_sq_tracked(st);
+        const double total = no_renorm ? 0.0 : norm_sq_tracked(st);
         if (total > 0.0) {
             const double f = 1.0 / sqrt(total);
             for (uint64_t j = 0; j < NS; ++j) st->st[j].scale *= f;
@@ -1059,4 +1072,80 @@ double qo_fidelity(const double* a, const double* b, uint64_t N)
         oi += a[2 * i] * b[2 * i + 1] - a[2 * i + 1] * b[2 * i];
     }
     return hypot(orr, oi) / (na * nb);
+}
+
+/* ---- hooks for sharded (multi-rank) runs ---------------------------------- */
+/* Per-stride stride_amplitude_sum (gate.cpp:303-311) of the scaled strides,
+ * the terms of the mean pass (aalc.cpp:270-295). */
+int qo_stride_sums(const qo_state* st, double* partial)
+{
+    const uint64_t L = st->L;
+    double* re = (double*)malloc(L * sizeof(double));
+    double* im = (double*)malloc(L * sizeof(double));
+    int rc = 0;
+    for (uint64_t j = 0; j < st->n_strides && !rc; ++j) {
+        rc = decompress_stride(st, j, re, im, 1);
+        double sr = 0.0, si = 0.0;
+        for (uint64_t i = 0; i < L && !rc; ++i) {
+            sr += re[i];
+            si += im[i];
+        }
+        partial[2 * j] = sr;
+        partial[2 * j + 1] = si;
+    }
+    free(re);
+    free(im);
+    return rc;
+}
+
+int qo_stride_norms(const qo_state* st, double* scales, double* sums)
+{
+    for (uint64_t j = 0; j < st->n_strides; ++j) {
+        if (scales) scales[j] = st->st[j].scale;
+        if (sums) sums[j] = st->st[j].sum_sq;
+    }
+    return 0;
+}
+
+int qo_scale_all(qo_state* st, double f)
+{
+    for (uint64_t j = 0; j < st->n_strides; ++j) st->st[j].scale *= f;
+    return 0;
+}
+
+/* Inverse of qo_export_blocks: two serialized QCS1 blocks installed verbatim. */
+int qo_import_blocks(qo_state* st, uint64_t j, const uint8_t* buf, uint64_t len, double scale,
+                     double sum_sq)
+{
+    if (j >= st->n_strides) return fail(QO_E_RANGE, "stride index out of range");
+    uint64_t off = 0;
+    block_t b[2];
+    for (int k = 0; k < 2; ++k) {
+        uint64_t count, plen;
+        int codec;
+        double delta;
+        const uint8_t* payload;
+        int rc = parse_block(buf, len, &off, &codec, &delta, &count, &payload, &plen);
+        if (rc) {
+            if (k) block_free(&b[0]);
+            return rc;
+        }
+        if (count != st->L) {
+            if (k) block_free(&b[0]);
+            return fail(QO_E_INVALID, "block length disagrees with geometry");
+        }
+        b[k].codec = codec;
+        b[k].delta = delta;
+        b[k].count = count;
+        b[k].len = plen;
+        b[k].payload = plen ? (uint8_t*)malloc(plen) : NULL;
+        if (plen) memcpy(b[k].payload, payload, plen);
+    }
+    block_free(&st->st[j].re);
+    block_free(&st->st[j].im);
+    st->st[j].re = b[0];
+    st->st[j].im = b[1];
+    st->st[j].scale = scale;
+    st->st[j].sum_sq = sum_sq;
+    return 0;
 }

@@ -98,6 +98,16 @@ int qo_stride_info(const qo_state* st, uint64_t j, double* scale, double* sum_sq
 int qo_export_blocks(const qo_state* st, uint64_t j, uint8_t* buf, uint64_t cap,
                      uint64_t* len);
 
+/* ---- sharded-run hooks (same contract as the C-ABI's) ---- */
+int qo_apply_gate_ex(qo_state* st, const qo_gate* g, const double* ladder, int n_levels,
+                     double theta, int flags, const double* mean, qo_report* reports,
+                     uint64_t* n_reports, double* norm_after);
+int qo_stride_sums(const qo_state* st, double* partial);
+int qo_stride_norms(const qo_state* st, double* scales, double* sums);
+int qo_scale_all(qo_state* st, double f);
+int qo_import_blocks(qo_state* st, uint64_t j, const uint8_t* buf, uint64_t len, double scale,
+                     double sum_sq);
+
 /* ---- dense oracle (dense.cpp) ---- */
 int qo_dense_run(int n_qubits, const qo_gate* gates, uint64_t n_gates,
                  uint64_t basis, double* amps);

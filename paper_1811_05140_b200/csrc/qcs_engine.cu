@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(128) k_commit_copy(Dev d, LevelTag lt, uint64_
 
 // Lazy renormalisation (aalc.cpp:410-419) and the GateRecord fold
 // (aalc.cpp:612-631), serial in stride / report order like the reference.
-__global__ void k_norm(Dev d, uint64_t n_slots, uint64_t rec_index, uint64_t gate_index)
+__global__ void k_norm(Dev d, uint64_t n_slots, uint64_t rec_index, uint64_t gate_index, int renorm)
 {
     if (threadIdx.x != 0) return;
     if (d.sc->err) {
@@ -436,9 +436,9 @@ __global__ void k_norm(Dev d, uint64_t n_slots, uint64_t rec_index, uint64_t gat
     }
     if (d.sc->mode == 1) d.sc->cur = 1 - d.sc->cur;
     double total = 0.0;
-    for (uint64_t j = 0; j < d.NS; ++j)
+    for (uint64_t j = 0; j < d.NS && renorm; ++j)
         total = __dadd_rn(total, __dmul_rn(__dmul_rn(d.scale[j], d.scale[j]), d.sum_sq[j]));
-    if (total > 0.0) {
+    if (renorm && total > 0.0) {
         const double f = __ddiv_rn(1.0, __dsqrt_rn(total));
         for (uint64_t j = 0; j < d.NS; ++j) d.scale[j] = __dmul_rn(d.scale[j], f);
     }
@@ -742,10 +742,16 @@ uint64_t grid_for(uint64_t work, uint64_t block = 256)
 {
     return umin64((work + block - 1) / block, 148ull * 32);
 }
+__global__ void k_set_mean(Dev d, double mr, double mi)
+{
+    d.sc->mean[0] = mr;
+    d.sc->mean[1] = mi;
+}
 
 // One gate, fully stream-ordered.  rec_index < 0: no record.
 int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, int nl,
-                 double theta, int64_t rec_index, uint64_t gate_index, uint64_t* n_slots_out)
+                 double theta, int64_t rec_index, uint64_t gate_index, uint64_t* n_slots_out,
+                 int renorm = 1, const double* given_mean = nullptr)
 {
     Dev& d = st->d;
     cudaStream_t s = st->stream;
@@ -758,7 +764,10 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen);
     prof_stop(st);
     ++st->launches;
-    if (p.reflect) {  // mean pass (aalc.cpp:270-295) needs every stride first
+    if (p.reflect && given_mean) {  // sharded run: mean combined across ranks
+        k_set_mean<<<1, 1, 0, s>>>(d, given_mean[0], given_mean[1]);
+        ++st->launches;
+    } else if (p.reflect) {  // mean pass (aalc.cpp:270-295) needs every stride first
         prof_start(st, 4);
         k_decode<<<(unsigned)d.NS, 256, 0, s>>>(d, DecodeJob{nullptr, 1});
         k_stride_sums<<<(unsigned)((d.NS + 127) / 128), 128, 0, s>>>(d);
@@ -819,7 +828,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     prof_start(st, 3);
     k_commit_plan<<<1, 1024, 0, s>>>(d, n_slots, gen);
     k_commit_copy<<<(unsigned)(2 * d.NS), 128, 0, s>>>(d, st->lt, gen);
-    k_norm<<<1, 32, 0, s>>>(d, n_slots, rec_index < 0 ? 0 : (uint64_t)rec_index, gate_index);
+    k_norm<<<1, 32, 0, s>>>(d, n_slots, rec_index < 0 ? 0 : (uint64_t)rec_index, gate_index, renorm);
     prof_stop(st);
     st->launches += 3;
     CU(cudaGetLastError());
@@ -859,7 +868,8 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
 {
     if (n < 1 || n > 59) return set_err(QCS_E_INVALID, "n_qubits must be in [1, 59], got %d", n);
     if (s < 0 || s > n) return set_err(QCS_E_INVALID, "stride_bits must be in [0, n_qubits], got %d", s);
-    if (basis >= (1ull << n)) return set_err(QCS_E_RANGE, "basis index out of range");
+    const bool zero_state = basis == ~0ull;  // shard that holds no amplitude
+    if (!zero_state && basis >= (1ull << n)) return set_err(QCS_E_RANGE, "basis index out of range");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
         cudaGetLastError();
@@ -949,10 +959,12 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     std::vector<uint64_t> h_off(2 * d.NS, 0), h_len(2 * d.NS, zero.size());
     std::vector<int8_t> h_codec(2 * d.NS, 0);
     std::vector<double> h_delta(2 * d.NS, 0.0), h_scale(d.NS, 1.0), h_sum(d.NS, 0.0);
-    const uint64_t hj = basis >> s;
-    h_off[2 * hj] = 16;
-    h_len[2 * hj] = hot.size();
-    h_sum[hj] = 1.0;
+    if (!zero_state) {
+        const uint64_t hj = basis >> s;
+        h_off[2 * hj] = 16;
+        h_len[2 * hj] = hot.size();
+        h_sum[hj] = 1.0;
+    }
     CU(cudaMemcpy(d.p_off, h_off.data(), 8 * h_off.size(), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(d.p_len, h_len.data(), 8 * h_len.size(), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(d.p_codec, h_codec.data(), h_codec.size(), cudaMemcpyHostToDevice));
@@ -963,7 +975,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     sc.bump = 32;
     sc.cur = 0;
     sc.err_gate = -1;
-    sc.norm_sq = 1.0;
+    sc.norm_sq = zero_state ? 0.0 : 1.0;
     CU(cudaMemcpy(d.sc, &sc, sizeof sc, cudaMemcpyHostToDevice));
     CU(cudaMemset(d.slot_of, 0xff, 8 * d.NS));
     k_index_planes<<<(unsigned)((2 * d.NS + 127) / 128), 128, 0, st->stream>>>(d, 0, 2 * d.NS);
@@ -1005,7 +1017,15 @@ int qcs_apply_gate(qcs_dev_state_t st, const qcs_gate_desc* g, const double* lad
                    double theta, qcs_stride_report* reports, uint64_t* n_reports,
                    double* norm_after)
 {
+    return qcs_apply_gate_ex(st, g, lad, nl, theta, 0, nullptr, reports, n_reports, norm_after);
+}
+
+int qcs_apply_gate_ex(qcs_dev_state_t st, const qcs_gate_desc* g, const double* lad, int nl,
+                      double theta, int flags, const double* mean, qcs_stride_report* reports,
+                      uint64_t* n_reports, double* norm_after)
+{
     if (!st || !g) return set_err(QCS_E_INVALID, "null argument");
+    if ((flags & QCS_GIVEN_MEAN) && !mean) return set_err(QCS_E_INVALID, "null mean");
     int rc = validate_gate(st, g);
     if (rc) return rc;
     rc = validate_ladder(lad, nl, theta);
@@ -1013,7 +1033,8 @@ int qcs_apply_gate(qcs_dev_state_t st, const qcs_gate_desc* g, const double* lad
     cudaSetDevice(st->device);
     uint64_t ns = 0;
     st->d.rec = nullptr;
-    rc = enqueue_gate(st, g, lad, nl, theta, -1, 0, &ns);
+    rc = enqueue_gate(st, g, lad, nl, theta, -1, 0, &ns, (flags & QCS_NO_RENORM) ? 0 : 1,
+                      (flags & QCS_GIVEN_MEAN) ? mean : nullptr);
     if (rc) return rc;
     rc = sync_and_check(st);
     if (rc) return rc;
@@ -1292,6 +1313,51 @@ int qcs_import_blocks(qcs_dev_state_t st, uint64_t j, const uint8_t* buf, uint64
     CU(cudaMemcpy(d.sc, &sc, sizeof sc, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(d.scale + j, &scale, 8, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(d.sum_sq + j, &ssq, 8, cudaMemcpyHostToDevice));
+    return 0;
+}
+
+__global__ void k_scale_all(double* scale, uint64_t ns, double f)
+{
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j < ns) scale[j] = __dmul_rn(scale[j], f);
+}
+
+int qcs_stride_norms(qcs_dev_state_t st, double* scales, double* sums)
+{
+    if (!st) return set_err(QCS_E_INVALID, "null state");
+    cudaSetDevice(st->device);
+    CU(cudaStreamSynchronize(st->stream));
+    if (scales) CU(cudaMemcpy(scales, st->d.scale, 8 * st->d.NS, cudaMemcpyDeviceToHost));
+    if (sums) CU(cudaMemcpy(sums, st->d.sum_sq, 8 * st->d.NS, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int qcs_stride_sums(qcs_dev_state_t st, double* partial)
+{
+    if (!st || !partial) return set_err(QCS_E_INVALID, "null argument");
+    cudaSetDevice(st->device);
+    int rc = sync_and_check(st);
+    if (rc) return rc;
+    Dev& d = st->d;
+    k_decode<<<(unsigned)d.NS, 256, 0, st->stream>>>(d, DecodeJob{nullptr, 1});
+    k_stride_sums<<<(unsigned)((d.NS + 127) / 128), 128, 0, st->stream>>>(d);
+    st->launches += 2;
+    CU(cudaGetLastError());
+    rc = sync_and_check(st);
+    if (rc) return rc;
+    if (st->h_sc->err) return report_device_error(st);
+    CU(cudaMemcpy(partial, d.partial, 16 * d.NS, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int qcs_scale_all(qcs_dev_state_t st, double f)
+{
+    if (!st) return set_err(QCS_E_INVALID, "null state");
+    cudaSetDevice(st->device);
+    k_scale_all<<<(unsigned)((st->d.NS + 255) / 256), 256, 0, st->stream>>>(st->d.scale, st->d.NS, f);
+    ++st->launches;
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(st->stream));
     return 0;
 }
 

@@ -1,0 +1,359 @@
+"""Sharded state across ranks.
+
+Rank = the top g = log2(world) qubits of the amplitude index, i.e. the top g
+bits of the stride index: rank r holds global strides [r*NSL, (r+1)*NSL) as an
+ordinary local engine state of n-g qubits with the same stride bits.  The
+reference has no distribution; this layer reproduces its
+single-process semantics exactly:
+
+* gates on local qubits run unchanged on every rank; a control on a rank
+  qubit turns into "this rank applies the uncontrolled gate or nothing",
+  which is what make_stride_plan's control-bit skip does (gate.cpp:351-379);
+* a target on a rank qubit b: partner ranks r and r^(1<<b) swap rank bit b
+  with a local stride bit (half of each rank's strides change hands, blocks
+  moved verbatim with their scale and sum), run the ordinary cross-stride
+  pair unit locally (aalc.cpp:333-382), and swap back;
+* the lazy renormalisation (aalc.cpp:410-419) is global: per-stride
+  (scale, sum_sq) are all-gathered and summed serially in global stride
+  order, so every world size reproduces the single-GPU bits;
+* GateRecords fold the stride reports in the reference's global unit order
+  (aalc.cpp:612-631).
+
+Exchanges go through host memory in this version (export/import of QCS1
+block images); a device-side NCCL exchange is the next step.
+The local engine is pluggable: GpuBackend (this package) or the oracle's
+backend in oracle/oracle.py (CPU tests with gloo).
+"""
+from __future__ import annotations
+
+import math
+import pickle
+import struct
+import threading
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from .circuit import KIND_CONTROLLED, KIND_FLIP, KIND_REFLECT, KIND_SINGLE, GateOp
+from .metrics import GateRecord
+
+
+# ---------------------------------------------------------------------------
+# communicators
+# ---------------------------------------------------------------------------
+class ThreadGroup:
+    """Shared state for ranks running as threads of one process."""
+
+    def __init__(self, size: int):
+        self.size = size
+        self.barrier = threading.Barrier(size)
+        self.slots: List[object] = [None] * size
+        self.p2p = {}
+
+
+class ThreadComm:
+    def __init__(self, group: ThreadGroup, rank: int):
+        self.group, self.rank, self.size = group, rank, group.size
+
+    def allgather(self, obj):
+        g = self.group
+        g.slots[self.rank] = obj
+        g.barrier.wait()
+        out = list(g.slots)
+        g.barrier.wait()
+        return out
+
+    def exchange(self, peer: Optional[int], obj):
+        """Collective: every rank calls it; peer None = no partner."""
+        g = self.group
+        if peer is not None:
+            g.p2p[(self.rank, peer)] = obj
+        g.barrier.wait()
+        got = g.p2p.pop((peer, self.rank)) if peer is not None else None
+        g.barrier.wait()
+        return got
+
+
+class TorchComm:
+    """torch.distributed (gloo) communicator for host-staged exchanges."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def allgather(self, obj):
+        out = [None] * self.size
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def exchange(self, peer: Optional[int], obj):
+        # pairwise exchange through an all-gather keeps the pattern collective
+        got = self.allgather((peer, obj))
+        if peer is None:
+            return None
+        p_peer, p_obj = got[peer]
+        assert p_peer == self.rank, "asymmetric exchange"
+        return p_obj
+
+
+# ---------------------------------------------------------------------------
+# local engine backends
+# ---------------------------------------------------------------------------
+class GpuBackend:
+    """Local shard on a GPU through the C-ABI."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+
+    def create(self, n: int, s: int, basis: Optional[int]):
+        import ctypes as C
+        from .engine import _check, lib
+        h = C.c_void_p()
+        b = (1 << 64) - 1 if basis is None else basis
+        _check(lib().qcs_state_create(n, s, C.c_uint64(b), self.device, C.byref(h)))
+        return _GpuShard(h, n, s)
+
+
+class _GpuShard:
+    def __init__(self, h, n, s):
+        self.h, self.n, self.s = h, n, s
+
+    def __del__(self):
+        from .engine import _lib_handle
+        if getattr(self, "h", None) and _lib_handle is not None:
+            _lib_handle.qcs_state_destroy(self.h)
+            self.h = None
+
+    def apply(self, gate: GateOp, ladder, theta, mean=None):
+        import ctypes as C
+        from .circuit import pack_gates
+        from .engine import Report, _check, lib
+        reps = (Report * (1 << (self.n - self.s)))()
+        nr = C.c_uint64()
+        norm = C.c_double()
+        lad = (C.c_double * len(ladder))(*ladder)
+        m = (C.c_double * 2)(*(mean or (0.0, 0.0)))
+        flags = 1 | (2 if mean else 0)   # QCS_NO_RENORM | QCS_GIVEN_MEAN
+        _check(lib().qcs_apply_gate_ex(self.h, pack_gates([gate]), lad, len(ladder), theta, flags,
+                                       m, reps, C.byref(nr), C.byref(norm)))
+        return [(r.stride_index, r.chosen_delta, r.ratio, r.bytes_in, r.bytes_out,
+                 bool(r.threshold_met)) for r in reps[: nr.value]]
+
+    def stride_sums(self):
+        from .engine import _check, lib
+        p = np.empty(2 << (self.n - self.s))
+        _check(lib().qcs_stride_sums(self.h, p.ctypes.data))
+        return p
+
+    def stride_norms(self):
+        from .engine import _check, lib
+        L = lib()
+        ns = 1 << (self.n - self.s)
+        sc = np.empty(ns)
+        sm = np.empty(ns)
+        _check(L.qcs_stride_norms(self.h, sc.ctypes.data, sm.ctypes.data))
+        return sc, sm
+
+    def scale_all(self, f: float):
+        from .engine import _check, lib
+        _check(lib().qcs_scale_all(self.h, f))
+
+    def export(self, j: int):
+        import ctypes as C
+        from .engine import _check, lib
+        n, sc, ss = C.c_uint64(), C.c_double(), C.c_double()
+        _check(lib().qcs_export_blocks(self.h, j, None, 0, C.byref(n), C.byref(sc), C.byref(ss)))
+        buf = C.create_string_buffer(n.value)
+        _check(lib().qcs_export_blocks(self.h, j, buf, n.value, C.byref(n), C.byref(sc),
+                                       C.byref(ss)))
+        return buf.raw[: n.value], sc.value, ss.value
+
+    def import_(self, j: int, blob: bytes, scale: float, ssq: float):
+        from .engine import _check, lib
+        _check(lib().qcs_import_blocks(self.h, j, blob, len(blob), scale, ssq))
+
+    def amplitudes(self):
+        from .engine import _check, lib
+        a = np.empty(2 << self.n, dtype=np.float64)
+        _check(lib().qcs_to_amplitudes(self.h, a.ctypes.data))
+        return a.view(np.complex128)
+
+
+# ---------------------------------------------------------------------------
+# the sharded state
+# ---------------------------------------------------------------------------
+@dataclass
+class ShardGeometry:
+    n_qubits: int
+    stride_bits: int
+    rank_bits: int
+
+    @property
+    def local_qubits(self) -> int:
+        return self.n_qubits - self.rank_bits
+
+    @property
+    def local_strides(self) -> int:
+        return 1 << (self.local_qubits - self.stride_bits)
+
+
+class ShardedState:
+    def __init__(self, geom: ShardGeometry, comm, backend, basis: int):
+        if (1 << geom.rank_bits) != comm.size:
+            raise ValueError("world size must be 2^rank_bits")
+        if geom.local_qubits < geom.stride_bits + 1:
+            raise ValueError("each rank needs at least two strides")
+        self.geom, self.comm, self.r = geom, comm, comm.rank
+        Q = geom.local_qubits
+        mine = (basis >> Q) == self.r
+        self.local = backend.create(Q, geom.stride_bits, basis & ((1 << Q) - 1) if mine else None)
+        self.norm_sq = 1.0
+
+    # -- data movement: swap rank bit b with local stride bit qb ------------
+    def _swap(self, active: bool, b: int, qb: int):
+        r = self.r
+        nsl = self.geom.local_strides
+        peer = r ^ (1 << b) if active else None
+        payload = None
+        if active:
+            send_bit = 0 if (r >> b) & 1 else 1   # lo rank sends local-bit-1 strides
+            payload = [(j, *self.local.export(j)) for j in range(nsl) if ((j >> qb) & 1) == send_bit]
+        got = self.comm.exchange(peer, payload)
+        if active:
+            for (j, blob, sc, ss) in got:
+                self.local.import_(j ^ (1 << qb), blob, sc, ss)
+
+    def _global_stride(self, jl: int, swapped: Optional[tuple]) -> int:
+        nsl = self.geom.local_strides
+        r = self.r
+        if swapped is None:
+            return r * nsl + jl
+        b, qb = swapped
+        rb = (r & ~(1 << b)) | (((jl >> qb) & 1) << b)
+        jb = (jl & ~(1 << qb)) | (((r >> b) & 1) << qb)
+        return rb * nsl + jb
+
+    def apply_gate(self, gate: GateOp, ladder: Sequence[float], theta: float, index: int = 0):
+        g = self.geom
+        Q, s = g.local_qubits, g.stride_bits
+        gate.validate(g.n_qubits)
+        pair_bit_global = None
+        swapped = None
+        reports: List[tuple] = []
+        if gate.kind in (KIND_SINGLE, KIND_CONTROLLED):
+            t, c = gate.target, gate.control
+            participate = True
+            local = GateOp(gate.kind, gate.unitary, t, c, 0, gate.phase_theta, gate.label)
+            if gate.kind == KIND_CONTROLLED and c >= Q:
+                participate = bool((self.r >> (c - Q)) & 1)
+                local = GateOp.single(gate.unitary, t, gate.label)
+            if t >= s:
+                pair_bit_global = 1 << (t - s)
+            if t >= Q:
+                qs = Q - 1
+                if local.kind == KIND_CONTROLLED and local.control == qs:
+                    qs = Q - 2
+                if qs < s:
+                    raise NotImplementedError("needs two local stride bits besides the control")
+                swapped = (t - Q, qs - s)
+                local.target = qs
+                self._swap(participate, *swapped)
+            if participate:
+                reports = self.local.apply(local, ladder, theta)
+            if swapped is not None:
+                self._swap(participate, *swapped)
+        elif gate.kind == KIND_FLIP:
+            if (gate.flip_index >> Q) == self.r:
+                reports = self.local.apply(GateOp.phase_flip(gate.flip_index & ((1 << Q) - 1)),
+                                           ladder, theta)
+        else:
+            # mean pass (aalc.cpp:270-295): per-stride sums, combined serially
+            # in global stride order, divided by the global amplitude count
+            parts = self.comm.allgather(self.local.stride_sums().tobytes())
+            sr = si = 0.0
+            for p in parts:
+                v = np.frombuffer(p).tolist()
+                for j in range(0, len(v), 2):
+                    sr += v[j]
+                    si += v[j + 1]
+            na = float(1 << g.n_qubits)
+            reports = self.local.apply(gate, ladder, theta, mean=(sr / na, si / na))
+        # global unit order of this rank's reports (reference: ascending lo
+        # stride; a pair unit reports lo then hi)
+        keyed = []
+        for rep in reports:
+            gj = self._global_stride(rep[0], swapped)
+            if pair_bit_global is not None:
+                key = (gj & ~pair_bit_global, 1 if gj & pair_bit_global else 0)
+            else:
+                key = (gj, 0)
+            keyed.append((key, (gj,) + tuple(rep[1:])))
+        # global renormalisation, serial in global stride order (aalc.cpp:410-419)
+        sc, sm = self.local.stride_norms()
+        parts = self.comm.allgather((sc.tobytes(), sm.tobytes(), keyed))
+        scales = np.concatenate([np.frombuffer(p[0]) for p in parts])
+        sums = np.concatenate([np.frombuffer(p[1]) for p in parts])
+        total = 0.0
+        for a, m in zip(scales.tolist(), sums.tolist()):
+            total += a * a * m
+        f = None
+        if total > 0.0:
+            f = 1.0 / math.sqrt(total)
+            self.local.scale_all(f)
+        nsq = 0.0
+        for a, m in zip(scales.tolist(), sums.tolist()):
+            a2 = a * f if f is not None else a
+            nsq += a2 * a2 * m
+        self.norm_sq = nsq
+        all_reps = sorted((kr for p in parts for kr in p[2]), key=lambda kr: kr[0])
+        from .metrics import gate_record
+        rec, viol = gate_record(index, gate.label, [r for _, r in all_reps], math.sqrt(nsq))
+        return rec, viol
+
+    def amplitudes(self) -> np.ndarray:
+        """Whole state on every rank (small states only; for tests)."""
+        parts = self.comm.allgather(self.local.amplitudes().tobytes())
+        return np.concatenate([np.frombuffer(p, dtype=np.complex128) for p in parts])
+
+
+def run_sharded(program, geom: ShardGeometry, comm, backend, basis: int, ladder, theta):
+    """run_program over a sharded state; returns (state, records, violations)."""
+    st = ShardedState(geom, comm, backend, basis)
+    recs = []
+    viol = 0
+    for i, g in enumerate(program.gates):
+        rec, v = st.apply_gate(g, ladder, theta, i)
+        recs.append(rec)
+        viol += v
+    return st, recs, viol
+
+
+def run_thread_cluster(program, geom: ShardGeometry, backend_factory, basis: int, ladder, theta):
+    """All ranks as threads of this process (ThreadComm); returns
+    (amplitudes, records of rank 0)."""
+    size = 1 << geom.rank_bits
+    grp = ThreadGroup(size)
+    out = [None] * size
+    errs = []
+
+    def worker(r):
+        try:
+            st, recs, _ = run_sharded(program, geom, ThreadComm(grp, r), backend_factory(r), basis,
+                                      ladder, theta)
+            out[r] = (st.amplitudes(), recs)
+        except BaseException as e:  # surface worker failures
+            errs.append(e)
+            grp.barrier.abort()
+
+    ts = [threading.Thread(target=worker, args=(r,)) for r in range(size)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out[0]

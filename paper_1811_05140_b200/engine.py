@@ -63,6 +63,12 @@ def lib() -> C.CDLL:
         L.qcs_state_launches.restype = C.c_uint64
         L.qcs_state_create.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int, C.POINTER(C.c_void_p)]
         L.qcs_state_destroy.argtypes = [C.c_void_p]
+        L.qcs_apply_gate_ex.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_double), C.c_int,
+                                        C.c_double, C.c_int, C.POINTER(C.c_double), C.c_void_p,
+                                        C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        L.qcs_stride_norms.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.qcs_stride_sums.argtypes = [C.c_void_p, C.c_void_p]
+        L.qcs_scale_all.argtypes = [C.c_void_p, C.c_double]
         L.qcs_apply_gate.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_double), C.c_int,
                                      C.c_double, C.c_void_p, C.POINTER(C.c_uint64),
                                      C.POINTER(C.c_double)]

@@ -1,0 +1,131 @@
+"""Sharded state: every world size reproduces the single-process
+bits — per-gate CSV (minus wall time) and the final amplitudes.
+
+CPU: ranks as threads (ThreadComm) and as gloo processes (TorchComm,
+world_size 2) over the oracle backend.  GPU: two ranks on one GPU through the
+C-ABI, host-staged exchange (no rank waits on another's kernel).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_1811_05140_b200 as q
+from paper_1811_05140_b200 import metrics as mm
+from paper_1811_05140_b200.distributed import (GpuBackend, ShardGeometry, run_thread_cluster)
+
+from helpers import golden_program, golden_runs, oracle_run, sha
+
+
+def _cases():
+    lad = [q.pow2_bound(1e-3, 10)]
+    return [
+        ("qft10", q.build_qft(10), 4, 397, lad, 1.0),
+        ("grover_gates10", q.build_grover_gate_form(10, 0x2d3, 3), 4, 0, lad, 1.0),
+        ("grover10_reflect", q.build_grover(10, 0x155, 2), 4, 0, lad, 1.0),
+        ("grid3x3", q.build_grid(3, 3, 8, 11), 3, 5, [2.0 ** -16, 2.0 ** -12], 2.0),
+        ("qft10_lossless", q.build_qft(10), 3, 17, [0.0], 1.0),
+    ]
+
+
+def _single(oracle, prog, s, basis, lad, theta):
+    st, csv = oracle_run(oracle, prog, s, basis, lad, theta)
+    return st.amplitudes(), csv
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+@pytest.mark.parametrize("case", _cases(), ids=lambda c: c[0])
+def test_thread_cluster_oracle(oracle, case, ranks):
+    from oracle import OracleBackend
+    name, prog, s, basis, lad, theta = case
+    rb = ranks.bit_length() - 1
+    if prog.n_qubits - rb < s + 2:
+        pytest.skip("too few local strides")
+    want_amp, want_csv = _single(oracle, prog, s, basis, lad, theta)
+    geom = ShardGeometry(prog.n_qubits, s, rb)
+    amp, recs = run_thread_cluster(prog, geom, lambda r: OracleBackend(oracle), basis, lad, theta)
+    got_csv = mm.emit_csv(recs, with_elapsed=False)
+    assert got_csv == want_csv
+    assert amp.tobytes() == want_amp.tobytes()
+
+
+def _golden_sharded():
+    out = []
+    for name, e in sorted(golden_runs().items()):
+        n = golden_program(e).n_qubits
+        for ranks in (2, 4):
+            if n - (ranks.bit_length() - 1) >= e["stride_bits"] + 2:
+                out.append((name, ranks))
+    return out
+
+
+@pytest.mark.parametrize("name,ranks", _golden_sharded())
+def test_thread_cluster_matches_reference_golden(oracle, name, ranks):
+    """Sharded run vs the reference's own outputs (tests/golden/runs.json)."""
+    from oracle import OracleBackend
+    e = golden_runs()[name]
+    prog = golden_program(e)
+    geom = ShardGeometry(prog.n_qubits, e["stride_bits"], ranks.bit_length() - 1)
+    amp, recs = run_thread_cluster(prog, geom, lambda r: OracleBackend(oracle), e["basis"],
+                                   e["ladder"], e["theta"])
+    assert mm.emit_csv(recs, with_elapsed=False) == e["csv"]
+    assert sha(amp) == e["amps_sha256"]
+
+
+def _free_port():
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, outdir):
+    import torch.distributed as dist
+    from oracle import OracleBackend
+    from paper_1811_05140_b200.distributed import TorchComm, run_sharded
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for name, prog, s, basis, lad, theta in _cases():
+            st, recs, _ = run_sharded(prog, ShardGeometry(prog.n_qubits, s, 1), TorchComm(),
+                                      OracleBackend(), basis, lad, theta)
+            amp = st.amplitudes()
+            if rank == 0:
+                with open(os.path.join(outdir, name + ".csv"), "w") as f:
+                    f.write(mm.emit_csv(recs, with_elapsed=False))
+                np.save(os.path.join(outdir, name + ".npy"), amp)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_oracle(oracle, tmp_path):
+    import torch.multiprocessing as tmp
+    tmp.spawn(_gloo_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    for name, prog, s, basis, lad, theta in _cases():
+        want_amp, want_csv = _single(oracle, prog, s, basis, lad, theta)
+        assert (tmp_path / (name + ".csv")).read_text() == want_csv, name
+        assert np.load(tmp_path / (name + ".npy")).tobytes() == want_amp.tobytes(), name
+
+
+def test_rank_geometry_errors(oracle):
+    from oracle import OracleBackend
+    from paper_1811_05140_b200.distributed import ShardedState, ThreadComm, ThreadGroup
+    with pytest.raises(ValueError):
+        ShardedState(ShardGeometry(8, 7, 1), ThreadComm(ThreadGroup(2), 0), OracleBackend(oracle), 0)
+    with pytest.raises(ValueError):
+        ShardedState(ShardGeometry(8, 4, 2), ThreadComm(ThreadGroup(2), 0), OracleBackend(oracle), 0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ranks", [2, 4])
+@pytest.mark.parametrize("case", _cases(), ids=lambda c: c[0])
+def test_thread_cluster_gpu(oracle, case, ranks):
+    name, prog, s, basis, lad, theta = case
+    rb = ranks.bit_length() - 1
+    if prog.n_qubits - rb < s + 2:
+        pytest.skip("too few local strides")
+    want_amp, want_csv = _single(oracle, prog, s, basis, lad, theta)
+    amp, recs = run_thread_cluster(prog, ShardGeometry(prog.n_qubits, s, rb),
+                                   lambda r: GpuBackend(0), basis, lad, theta)
+    assert mm.emit_csv(recs, with_elapsed=False) == want_csv
+    assert amp.tobytes() == want_amp.tobytes()
