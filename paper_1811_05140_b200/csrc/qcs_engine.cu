@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -220,6 +221,109 @@ __global__ void __launch_bounds__(256) k_gate(Dev d, Plan p, GateParams gp)
             double* b = d.X + (lo | (1ull << p.pb)) * 2 * L;
             pair_update(m, a[i], a[L + i], b[i], b[L + i]);
         }
+    }
+}
+
+// Decode + gate + snap for the encoder's RAW input (split path).  Fully
+// parallel over (unit, chunk): each CTA decodes 256 sub-chunks (one per
+// thread, via the side index), applies run_plan_unit's apply_pair
+// (gate.cpp:405-454) and snap_zeros (core.cpp:39-47), and writes the planes
+// uncompressed into the slot-ordered scratch X[slot][re|im][L].
+//   DG_IN    partner inside the 4096-element chunk (t < 12), 2 planes x 4096
+//   DG_FAR   partner 2^t >= 2048 away in the same stride, 2 x 2 planes x 2048
+//   DG_PAIR  lo / hi stride of a cross-stride unit, 2 x 2 planes x 2048
+enum { DG_IN = 0, DG_FAR = 1, DG_PAIR = 2 };
+constexpr int DG_ROWS = 256;
+constexpr size_t DG_SMEM = sizeof(double) * DG_ROWS * XS_STRIDE;
+
+__global__ void __launch_bounds__(256) k_decode_gate(Dev d, Plan p, GateParams gp, int mode,
+                                                   uint64_t chunks)
+{
+    if (d.sc->err) return;
+    extern __shared__ __align__(16) unsigned char dg_smem[];
+    double* xs = reinterpret_cast<double*>(dg_smem);
+    const uint64_t u = blockIdx.x / chunks, c = blockIdx.x % chunks;
+    const int tid = threadIdx.x;
+    const uint64_t L = d.L;
+    const uint64_t hb = 1ull << (p.pair ? 0 : p.t);
+    // this thread's row: (stride, component, element base)
+    uint64_t slot, e0;
+    int comp;
+    if (mode == DG_IN) {
+        slot = u;
+        comp = tid >> 7;
+        e0 = c * 4096 + (uint64_t)(tid & 127) * SUB;
+    } else {
+        const int q = tid >> 6;            // 0 A.re, 1 A.im, 2 B.re, 3 B.im
+        const uint64_t sub = (uint64_t)(tid & 63) * SUB;
+        comp = q & 1;
+        if (mode == DG_PAIR) {
+            slot = 2 * u + (q >> 1);
+            e0 = c * 2048 + sub;
+        } else {
+            slot = u;
+            const uint64_t e = c * 2048;
+            const uint64_t elo = ((e >> p.t) << (p.t + 1)) | (e & (hb - 1));
+            e0 = elo + ((q >> 1) ? hb : 0) + sub;
+        }
+    }
+    const uint64_t j = d.job_stride[slot];
+    const uint64_t g = 2 * j + comp;
+    const int cnt = (int)umin64(SUB, L - umin64(e0, L));
+    if (cnt > 0)
+        decode_sub(d.arena[d.sc->cur] + d.p_off[g], d.p_codec[g], 2.0 * d.p_delta[g],
+                   d.side[g * d.nsub + e0 / SUB], cnt, xs + tid * XS_STRIDE, d.scale[j]);
+    __syncthreads();
+    double m[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = gp.u[i];
+    auto at = [&](int row_base, int k) -> double& { return xs[(row_base + (k >> 5)) * XS_STRIDE + (k & 31)]; };
+    if (mode == DG_IN) {
+        const uint64_t lo_mask = hb - 1;
+        for (int q = tid; q < 2048; q += 256) {
+            const int i0 = (int)((((uint64_t)q & ~lo_mask) << 1) | ((uint64_t)q & lo_mask));
+            const int i1 = i0 | (int)hb;
+            if (p.local_ctl >= 0 && !(((c * 4096 + i0) >> p.local_ctl) & 1)) continue;
+            pair_update(m, at(0, i0), at(128, i0), at(0, i1), at(128, i1));
+        }
+    } else {
+        for (int i = tid; i < 2048; i += 256) {
+            uint64_t gi;
+            if (mode == DG_PAIR) {
+                gi = c * 2048 + i;
+            } else {
+                const uint64_t e = c * 2048;
+                gi = (((e >> p.t) << (p.t + 1)) | (e & (hb - 1))) + i;
+            }
+            if (p.local_ctl >= 0 && !((gi >> p.local_ctl) & 1)) continue;
+            pair_update(m, at(0, i), at(64, i), at(128, i), at(192, i));
+        }
+    }
+    __syncthreads();
+    // snap and write out, coalesced along elements
+    for (int k = tid; k < DG_ROWS * SUB; k += 256) {
+        const int row = k >> 5;
+        const double v = snap(xs[row * XS_STRIDE + (k & 31)]);
+        uint64_t oslot, oe;
+        int ocomp;
+        if (mode == DG_IN) {
+            oslot = u;
+            ocomp = row >> 7;
+            oe = c * 4096 + (uint64_t)(k & 4095);
+        } else {
+            const int q = row >> 6;
+            ocomp = q & 1;
+            const uint64_t off = (uint64_t)(k & 2047);
+            if (mode == DG_PAIR) {
+                oslot = 2 * u + (q >> 1);
+                oe = c * 2048 + off;
+            } else {
+                oslot = u;
+                const uint64_t e = c * 2048;
+                oe = (((e >> p.t) << (p.t + 1)) | (e & (hb - 1))) + ((q >> 1) ? hb : 0) + off;
+            }
+        }
+        if (oe < L) d.X[(2 * oslot + ocomp) * L + oe] = v;
     }
 }
 
@@ -427,50 +531,118 @@ __global__ void __launch_bounds__(128) k_commit_copy(Dev d, LevelTag lt, uint64_
 
 // Lazy renormalisation (aalc.cpp:410-419) and the GateRecord fold
 // (aalc.cpp:612-631), serial in stride / report order like the reference.
-__global__ void k_norm(Dev d, uint64_t n_slots, uint64_t rec_index, uint64_t gate_index, int renorm)
+// The tables are staged through shared memory by all threads; thread 0 folds
+// serially (the FP order is the reference's), so the chain never waits on HBM.
+constexpr int NORM_THREADS = 256;
+constexpr int NORM_CHUNK = 2048;
+
+__device__ double norm_fold(const Dev& d, double f, bool scale_by_f, double* sh_a, double* sh_b)
 {
-    if (threadIdx.x != 0) return;
+    double total = 0.0;
+    for (uint64_t c0 = 0; c0 < d.NS; c0 += NORM_CHUNK) {
+        const int m = (int)umin64(NORM_CHUNK, d.NS - c0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            const double sc = d.scale[c0 + i];
+            sh_a[i] = scale_by_f ? __dmul_rn(sc, f) : sc;
+            sh_b[i] = d.sum_sq[c0 + i];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int i = 0; i < m; ++i) total = __dadd_rn(total, __dmul_rn(__dmul_rn(sh_a[i], sh_a[i]), sh_b[i]));
+    }
+    return total;
+}
+
+__global__ void __launch_bounds__(NORM_THREADS) k_norm(Dev d, uint64_t n_slots, uint64_t rec_index,
+                                                      uint64_t gate_index, int renorm)
+{
+    __shared__ double sh_a[NORM_CHUNK], sh_b[NORM_CHUNK];
+    __shared__ double sh_f;
+    __shared__ int sh_do;
     if (d.sc->err) {
-        if (d.sc->err_gate < 0) d.sc->err_gate = (int)gate_index;
+        if (threadIdx.x == 0 && d.sc->err_gate < 0) d.sc->err_gate = (int)gate_index;
         return;
     }
-    if (d.sc->mode == 1) d.sc->cur = 1 - d.sc->cur;
-    double total = 0.0;
-    for (uint64_t j = 0; j < d.NS && renorm; ++j)
-        total = __dadd_rn(total, __dmul_rn(__dmul_rn(d.scale[j], d.scale[j]), d.sum_sq[j]));
-    if (renorm && total > 0.0) {
-        const double f = __ddiv_rn(1.0, __dsqrt_rn(total));
-        for (uint64_t j = 0; j < d.NS; ++j) d.scale[j] = __dmul_rn(d.scale[j], f);
+    __syncthreads();
+    if (threadIdx.x == 0 && d.sc->mode == 1) d.sc->cur = 1 - d.sc->cur;
+    const double total = renorm ? norm_fold(d, 1.0, false, sh_a, sh_b) : 0.0;
+    if (threadIdx.x == 0) {
+        sh_do = renorm && total > 0.0;
+        sh_f = sh_do ? __ddiv_rn(1.0, __dsqrt_rn(total)) : 1.0;
     }
-    double nsq = 0.0;
-    for (uint64_t j = 0; j < d.NS; ++j)
-        nsq = __dadd_rn(nsq, __dmul_rn(__dmul_rn(d.scale[j], d.scale[j]), d.sum_sq[j]));
-    d.sc->norm_sq = nsq;
-    if (d.rec) {
-        qcs_gate_record r;
-        r.gate_index = gate_index;
-        r.stride_count = n_slots;
-        r.min_ratio = INFINITY;
-        r.max_chosen_delta = 0.0;
-        r.bytes_before = 0;
-        r.bytes_after = 0;
-        r.threshold_violations = 0;
-        double rs = 0.0;
-        for (uint64_t s = 0; s < n_slots; ++s) {
-            const qcs_stride_report& rep = d.reports[s];
+    __syncthreads();
+    const bool do_scale = sh_do;
+    const double f = sh_f;
+    // norm_sq_tracked after scaling: same products as the reference's
+    // scale *= f followed by the serial re-measure
+    const double nsq = norm_fold(d, f, do_scale, sh_a, sh_b);
+    __syncthreads();
+    if (do_scale)
+        for (uint64_t j = threadIdx.x; j < d.NS; j += blockDim.x) d.scale[j] = __dmul_rn(d.scale[j], f);
+    if (threadIdx.x == 0) d.sc->norm_sq = nsq;
+    if (!d.rec) return;
+    // GateRecord fold in report order: min / max / sums are order-free, the
+    // ratio sum is serial
+    double* rr = sh_a;
+    qcs_gate_record r;
+    r.min_ratio = INFINITY;
+    r.max_chosen_delta = 0.0;
+    double rs = 0.0;
+    uint64_t b_in = 0, b_out = 0, viol = 0;
+    for (uint64_t c0 = 0; c0 < n_slots; c0 += NORM_CHUNK) {
+        const int m = (int)umin64(NORM_CHUNK, n_slots - c0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            const qcs_stride_report& rep = d.reports[c0 + i];
+            rr[i] = rep.ratio;
             r.min_ratio = fmin(r.min_ratio, rep.ratio);
-            rs = __dadd_rn(rs, rep.ratio);
             r.max_chosen_delta = fmax(r.max_chosen_delta, rep.chosen_delta);
-            r.bytes_before += rep.bytes_in;
-            r.bytes_after += rep.bytes_out;
-            if (!rep.threshold_met) ++r.threshold_violations;
+            b_in += rep.bytes_in;
+            b_out += rep.bytes_out;
+            viol += rep.threshold_met ? 0 : 1;
         }
-        r.mean_ratio = n_slots ? __ddiv_rn(rs, (double)n_slots) : 0.0;
-        r.elapsed_ns = 0;
-        r.norm_after = __dsqrt_rn(nsq);
-        r.compressed_in = d.sc->gate_cin;
-        d.rec[rec_index] = r;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int i = 0; i < m; ++i) rs = __dadd_rn(rs, rr[i]);
     }
+    // block reductions of the order-free parts
+    __shared__ double red_min[NORM_THREADS / 32], red_max[NORM_THREADS / 32];
+    __shared__ uint64_t red_in[NORM_THREADS / 32], red_out[NORM_THREADS / 32], red_v[NORM_THREADS / 32];
+    for (int o = 16; o; o >>= 1) {
+        r.min_ratio = fmin(r.min_ratio, __shfl_xor_sync(0xffffffffu, r.min_ratio, o));
+        r.max_chosen_delta = fmax(r.max_chosen_delta, __shfl_xor_sync(0xffffffffu, r.max_chosen_delta, o));
+        b_in += __shfl_xor_sync(0xffffffffu, b_in, o);
+        b_out += __shfl_xor_sync(0xffffffffu, b_out, o);
+        viol += __shfl_xor_sync(0xffffffffu, viol, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red_min[w] = r.min_ratio;
+        red_max[w] = r.max_chosen_delta;
+        red_in[w] = b_in;
+        red_out[w] = b_out;
+        red_v[w] = viol;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    r.min_ratio = INFINITY;
+    r.max_chosen_delta = 0.0;
+    r.bytes_before = r.bytes_after = r.threshold_violations = 0;
+    for (int i = 0; i < NORM_THREADS / 32; ++i) {
+        r.min_ratio = fmin(r.min_ratio, red_min[i]);
+        r.max_chosen_delta = fmax(r.max_chosen_delta, red_max[i]);
+        r.bytes_before += red_in[i];
+        r.bytes_after += red_out[i];
+        r.threshold_violations += red_v[i];
+    }
+    r.gate_index = gate_index;
+    r.stride_count = n_slots;
+    r.mean_ratio = n_slots ? __ddiv_rn(rs, (double)n_slots) : 0.0;
+    r.elapsed_ns = 0;
+    r.norm_after = __dsqrt_rn(nsq);
+    r.compressed_in = d.sc->gate_cin;
+    d.rec[rec_index] = r;
 }
 
 __global__ void k_index_planes(Dev d, uint64_t g0, uint64_t count)
@@ -585,6 +757,7 @@ struct qcs_dev_state {
     LevelTag lt{};
     uint64_t gen = 0;
     uint64_t launches = 0;
+    int split_local = 0;  // QCS_SPLIT_LOCAL=1: in-chunk gates also take the split path
     Dev::Scal* h_sc = nullptr;   // pinned mirror
     qcs_stride_report* h_rep = nullptr;
     std::vector<void*> allocs;
@@ -777,11 +950,28 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     }
     int fm = FM_LOCAL;
     uint64_t grid = n_slots;
-    if (p.pair) {
-        fm = FM_PAIR;
-        grid = p.n_units;
-    } else if (p.kind <= 1 && (1ull << p.t) >= 4096) {
-        fm = FM_FAR;
+    // cross-chunk partners (pair units, in-stride targets >= 2^12): decode +
+    // gate fully parallel into X, then the encoder reads X (split path)
+    int dg = -1;
+    if (p.pair) dg = DG_PAIR;
+    else if (p.kind <= 1 && (1ull << p.t) >= 4096) dg = DG_FAR;
+    else if (p.kind <= 1 && st->split_local && d.L >= 4096) dg = DG_IN;
+    if (dg >= 0) {
+        static bool dg_attr = false;
+        if (!dg_attr) {
+            CU(cudaFuncSetAttribute(k_decode_gate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DG_SMEM));
+            dg_attr = true;
+        }
+        GateParams gp;
+        for (int i = 0; i < 8; ++i) gp.u[i] = g->u[i];
+        const uint64_t chunks = dg == DG_IN ? d.L / 4096 : (dg == DG_PAIR ? (d.L + 2047) / 2048 : d.L / 4096);
+        const uint64_t units = dg == DG_PAIR ? p.n_units : n_slots;
+        prof_start(st, 0);
+        k_decode_gate<<<(unsigned)(units * chunks), 256, DG_SMEM, s>>>(d, p, gp, dg, chunks);
+        prof_stop(st);
+        ++st->launches;
+        fm = FM_RAW2;
+        grid = n_slots;
     }
     for (int k = 0; k < nl; ++k) {
         FusedArgs a{};
@@ -803,6 +993,11 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         a.n = d.L;
         a.pending = d.pending;
         a.snap = 1;
+        if (fm == FM_RAW2) {  // split path: gated, snapped planes in X
+            a.X = d.X;
+            a.x_plane_stride = d.L;
+            a.snap = 0;
+        }
         a.out = d.slot_out;
         a.cap = d.slot_cap;
         a.side = d.slot_side;
@@ -828,7 +1023,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     prof_start(st, 3);
     k_commit_plan<<<1, 1024, 0, s>>>(d, n_slots, gen);
     k_commit_copy<<<(unsigned)(2 * d.NS), 128, 0, s>>>(d, st->lt, gen);
-    k_norm<<<1, 32, 0, s>>>(d, n_slots, rec_index < 0 ? 0 : (uint64_t)rec_index, gate_index, renorm);
+    k_norm<<<1, NORM_THREADS, 0, s>>>(d, n_slots, rec_index < 0 ? 0 : (uint64_t)rec_index, gate_index, renorm);
     prof_stop(st);
     st->launches += 3;
     CU(cudaGetLastError());
@@ -878,6 +1073,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     if (device < 0 || device >= ndev) return set_err(QCS_E_INVALID, "bad device %d", device);
     qcs_dev_state* st = new qcs_dev_state();
     st->device = device;
+    if (const char* e = getenv("QCS_SPLIT_LOCAL")) st->split_local = atoi(e);
     cudaSetDevice(device);
     int rc = 0;
 #define TRY(x)                    \
