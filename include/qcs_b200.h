@@ -165,8 +165,10 @@ int qcs_state_kernel_time(qcs_dev_state_t st, int kernel_class, double* total_ns
 /* Cumulative device diagnostics of the codec kernel: [0] lanes whose entry
  * predictor guess was wrong and were re-run serially, [1] passes of the exact
  * sum-of-squares emulation, [2] bytes slid to close carried word runs,
- * [3] lanes finished by the serial chain, [8..14] cycles per kernel phase
- * (input, rounds, final, sum, token count, token write, tail). */
+ * [3] lanes finished by the serial chain, [4] in-place arena compactions
+ * and [5] slots per wave (wave layout for large states, 0 otherwise),
+ * [8..14] cycles per kernel phase (input, rounds, final, sum, token count,
+ * token write, tail). */
 int qcs_state_counters(qcs_dev_state_t st, uint64_t* out, int n);
 
 /* Codec plugin (codec.hpp:80-105): compress(x, ErrorBound(delta)) then

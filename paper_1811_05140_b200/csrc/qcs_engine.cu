@@ -4,7 +4,7 @@
 // Per gate (CompressedState::apply_gate, aalc.cpp:261-420):
 //   k_make_jobs   unit list of make_stride_plan (gate.cpp:313-403), on device
 //   k_decode      decompress_into + scale (aalc.cpp:176-189), lane per sub-chunk
-//   [k_stride_sums, k_mean]  reflect_mean's mean pass (aalc.cpp:270-295)
+//   [k_stride_partial, k_mean]  reflect_mean's mean pass (aalc.cpp:270-295)
 //   k_gate        run_plan_unit (gate.cpp:405-454), FMA-free apply_pair order
 //   per ladder level: k_encode (snap + compress + stored sum_sq) and
 //                     k_ladder (compress_stride_adaptive / joint pair ladder,
@@ -157,14 +157,15 @@ __global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen)
 }
 
 struct DecodeJob {
-    const uint64_t* job_stride;  // null: stride = blockIdx
+    uint64_t j0;       // first stride (stride = j0 + blockIdx)
     int apply_scale;
+    double* out;       // [blocks][re|im][L]
 };
 
 __global__ void __launch_bounds__(256) k_decode(Dev d, DecodeJob dj)
 {
     if (d.sc->err) return;
-    const uint64_t j = dj.job_stride ? dj.job_stride[blockIdx.x] : blockIdx.x;
+    const uint64_t j = dj.j0 + blockIdx.x;
     const int pl = threadIdx.x >> 7;
     const int lane = threadIdx.x & 127;
     const uint64_t g = 2 * j + pl;
@@ -172,55 +173,12 @@ __global__ void __launch_bounds__(256) k_decode(Dev d, DecodeJob dj)
     const int codec = d.p_codec[g];
     const double td = 2.0 * d.p_delta[g];
     const double scale = dj.apply_scale ? d.scale[j] : 1.0;
-    double* o = d.X + j * 2 * d.L + (uint64_t)pl * d.L;
+    double* o = dj.out + (uint64_t)blockIdx.x * 2 * d.L + (uint64_t)pl * d.L;
     const SideEntry* side = d.side + g * d.nsub;
     for (uint64_t sc = lane; sc < d.nsub; sc += PLANE_LANES) {
         const uint64_t e0 = sc * SUB;
         const int cnt = (int)umin64(SUB, d.L - e0);
         decode_sub(in, codec, td, side[sc], cnt, o + e0, scale);
-    }
-}
-
-// run_plan_unit over all units: one thread per amplitude pair / amplitude.
-__global__ void __launch_bounds__(256) k_gate(Dev d, Plan p, GateParams gp)
-{
-    if (d.sc->err) return;
-    const uint64_t L = d.L;
-    const uint64_t per = (p.kind <= 1 && !p.pair) ? L / 2 : L;
-    const uint64_t total = p.n_units * per;
-    double m[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) m[i] = gp.u[i];
-    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < total;
-         w += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t u = w / per, i = w % per;
-        if (p.kind == 2) {  // apply_phase_flip_in_stride (gate.cpp:279-286)
-            if (i != 0) continue;
-            double* x = d.X + unit_lo(p, u) * 2 * L;
-            x[p.flip_off] = -x[p.flip_off];
-            x[L + p.flip_off] = -x[L + p.flip_off];
-            continue;
-        }
-        if (p.kind == 3) {  // apply_reflect_mean_in_stride (gate.cpp:288-301)
-            double* x = d.X + unit_lo(p, u) * 2 * L;
-            const double mr2 = 2.0 * d.sc->mean[0], mi2 = 2.0 * d.sc->mean[1];
-            x[i] = __dsub_rn(mr2, x[i]);
-            x[L + i] = __dsub_rn(mi2, x[L + i]);
-            continue;
-        }
-        if (!p.pair) {  // in-stride: apply_single_in_stride / apply_controlled_in_stride
-            const uint64_t half = 1ull << p.t, lo_mask = half - 1;
-            const uint64_t i0 = ((i & ~lo_mask) << 1) | (i & lo_mask);
-            if (p.local_ctl >= 0 && !(i0 & (1ull << p.local_ctl))) continue;
-            double* x = d.X + unit_lo(p, u) * 2 * L;
-            pair_update(m, x[i0], x[L + i0], x[i0 | half], x[L + (i0 | half)]);
-        } else {  // cross-stride
-            if (p.local_ctl >= 0 && !(i & (1ull << p.local_ctl))) continue;
-            const uint64_t lo = unit_lo(p, u);
-            double* a = d.X + lo * 2 * L;
-            double* b = d.X + (lo | (1ull << p.pb)) * 2 * L;
-            pair_update(m, a[i], a[L + i], b[i], b[L + i]);
-        }
     }
 }
 
@@ -237,7 +195,7 @@ constexpr int DG_ROWS = 256;
 constexpr size_t DG_SMEM = sizeof(double) * DG_ROWS * XS_STRIDE;
 
 __global__ void __launch_bounds__(256) k_decode_gate(Dev d, Plan p, GateParams gp, int mode,
-                                                   uint64_t chunks)
+                                                   uint64_t chunks, uint64_t slot_base)
 {
     if (d.sc->err) return;
     extern __shared__ __align__(16) unsigned char dg_smem[];
@@ -267,7 +225,7 @@ __global__ void __launch_bounds__(256) k_decode_gate(Dev d, Plan p, GateParams g
             e0 = elo + ((q >> 1) ? hb : 0) + sub;
         }
     }
-    const uint64_t j = d.job_stride[slot];
+    const uint64_t j = d.job_stride[slot_base + slot];
     const uint64_t g = 2 * j + comp;
     const int cnt = (int)umin64(SUB, L - umin64(e0, L));
     if (cnt > 0)
@@ -327,20 +285,34 @@ __global__ void __launch_bounds__(256) k_decode_gate(Dev d, Plan p, GateParams g
     }
 }
 
-// stride_amplitude_sum (gate.cpp:303-311): serial per stride, index order.
-__global__ void k_stride_sums(Dev d)
+// stride_amplitude_sum (gate.cpp:303-311) of every scaled stride, straight
+// from the block store: one CTA per stride decodes 4096-element chunks of both
+// planes into shared memory; one thread per plane folds them serially in
+// index order (the reference's FP order).
+__global__ void __launch_bounds__(128) k_stride_partial(Dev d)
 {
     if (d.sc->err) return;
-    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (j >= d.NS) return;
-    const double* x = d.X + j * 2 * d.L;
-    double sr = 0.0, si = 0.0;
-    for (uint64_t i = 0; i < d.L; ++i) {
-        sr = __dadd_rn(sr, x[i]);
-        si = __dadd_rn(si, x[d.L + i]);
+    __shared__ double xs[128 * XS_STRIDE];
+    const uint64_t j = blockIdx.x;
+    const int tid = threadIdx.x, pl = tid >> 6, lane = tid & 63;
+    const uint64_t g = 2 * j + pl;
+    const uint8_t* in = d.arena[d.sc->cur] + d.p_off[g];
+    const int codec = d.p_codec[g];
+    const double td = 2.0 * d.p_delta[g];
+    const double scale = d.scale[j];
+    const SideEntry* side = d.side + g * d.nsub;
+    double acc = 0.0;
+    for (uint64_t base = 0; base < d.L; base += 2048) {
+        const uint64_t e0 = base + (uint64_t)lane * SUB;
+        __syncthreads();
+        if (e0 < d.L) decode_sub(in, codec, td, side[e0 / SUB], (int)umin64(SUB, d.L - e0), xs + tid * XS_STRIDE, scale);
+        __syncthreads();
+        if (lane == 0) {
+            const int m = (int)umin64(2048, d.L - base);
+            for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, xs[(pl * 64 + (k >> 5)) * XS_STRIDE + (k & 31)]);
+        }
     }
-    d.partial[2 * j] = sr;
-    d.partial[2 * j + 1] = si;
+    if (lane == 0) d.partial[2 * j + pl] = acc;
 }
 
 __global__ void k_mean(Dev d)
@@ -359,11 +331,11 @@ __global__ void k_mean(Dev d)
 // Ladder step for every unit: block_pair_ratio (aalc.cpp:37-42); stop at the
 // first level whose ratio (pairs: min of both) reaches theta, else keep the
 // last level (aalc.cpp:125-137, 346-356).
-__global__ void k_ladder(Dev d, Plan p, double delta, double theta, int last_level)
+__global__ void k_ladder(Dev d, Plan p, uint64_t u0, uint64_t u1, double delta, double theta, int last_level)
 {
     if (d.sc->err) return;
-    const uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (u >= p.n_units) return;
+    const uint64_t u = u0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (u >= u1) return;
     const uint64_t s0 = p.pair ? 2 * u : u;
     if (!d.pending[s0]) return;
     const uint64_t bytes_in = d.L * 16;
@@ -398,10 +370,10 @@ struct LevelTag {
     double* slot_delta;   // [NS]
 };
 
-__global__ void k_tag_level(Dev d, LevelTag lt, uint64_t n_slots, int codec, double delta)
+__global__ void k_tag_level(Dev d, LevelTag lt, uint64_t s0, uint64_t s1, int codec, double delta)
 {
-    const uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (s >= n_slots || !d.pending[s]) return;
+    const uint64_t s = s0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (s >= s1 || !d.pending[s]) return;
     lt.slot_codec[s] = (int8_t)codec;
     lt.slot_delta[s] = delta;
 }
@@ -758,6 +730,16 @@ struct qcs_dev_state {
     uint64_t gen = 0;
     uint64_t launches = 0;
     int split_local = 0;  // QCS_SPLIT_LOCAL=1: in-chunk gates also take the split path
+    // Large states ("wave mode"): one arena, per-wave staging
+    // buffers (slots, side, X) for `wave` slots, per-wave commit placed by the
+    // host, in-place compaction through the X buffer.
+    int big = 0;
+    uint64_t wave = 0;           // slots per wave (== NS in the small layout)
+    uint64_t bump = 0;           // wave mode: arena fill (host-authoritative)
+    uint64_t compactions = 0;
+    uint64_t* mv_src = nullptr;  // [2NS] compaction work lists
+    uint64_t* mv_dst = nullptr;
+    uint64_t* mv_len = nullptr;
     Dev::Scal* h_sc = nullptr;   // pinned mirror
     qcs_stride_report* h_rep = nullptr;
     std::vector<void*> allocs;
@@ -921,6 +903,161 @@ __global__ void k_set_mean(Dev d, double mr, double mi)
     d.sc->mean[1] = mi;
 }
 
+// Wave mode: install the wave's new blocks at host-chosen arena offsets
+// (new_off), replace the side index, tables, scale and sum (the staged commit
+// of aalc.cpp:395-408, one wave at a time).
+__global__ void __launch_bounds__(128) k_wave_commit(Dev d, LevelTag lt, uint64_t s0)
+{
+    const uint64_t loc = blockIdx.x >> 1;
+    const int c = (int)(blockIdx.x & 1);
+    const uint64_t slot = s0 + loc;
+    const uint64_t j = d.job_stride[slot];
+    const uint64_t g = 2 * j + c;
+    const uint64_t len = d.slot_len[2 * slot + c];
+    const uint64_t dst_off = d.new_off[2 * slot + c];
+    const uint4* s4 = reinterpret_cast<const uint4*>(d.slot_out + (2 * loc + c) * d.slot_cap);
+    uint4* d4 = reinterpret_cast<uint4*>(d.arena[0] + dst_off);
+    for (uint64_t i = threadIdx.x; i < (len + 15) / 16; i += blockDim.x) d4[i] = s4[i];
+    const SideEntry* ss = d.slot_side + (2 * loc + c) * d.nsub;
+    SideEntry* ds = d.side + g * d.nsub;
+    for (uint64_t i = threadIdx.x; i < d.nsub; i += blockDim.x) ds[i] = ss[i];
+    if (threadIdx.x == 0) {
+        d.p_off[g] = dst_off;
+        d.p_len[g] = len;
+        d.p_codec[g] = lt.slot_codec[slot];
+        d.p_delta[g] = lt.slot_delta[slot];
+        if (c == 0) {
+            d.sum_sq[j] = d.slot_sum[slot];
+            d.scale[j] = 1.0;
+        }
+    }
+}
+
+// Byte moves for compaction: item i copies len[i] bytes from src+so[i] to
+// dst+do[i] (16-byte aligned; one CTA per item).
+__global__ void __launch_bounds__(128) k_move(const uint8_t* src, uint8_t* dst, const uint64_t* so,
+                                              const uint64_t* dof, const uint64_t* len)
+{
+    const uint64_t i = blockIdx.x;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + so[i]);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + dof[i]);
+    for (uint64_t k = threadIdx.x; k < (len[i] + 15) / 16; k += blockDim.x) d4[k] = s4[k];
+}
+
+inline uint64_t round16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
+
+// In-place compaction of the single arena: live blocks slide down in offset
+// order.  Batches go arena -> X -> arena; a block's destination never reaches
+// past its own source end, so it can only overlap sources of blocks already
+// moved (earlier batches) or of its own batch (bounced).  Blocks shared by
+// several planes (basis-state zero block) move once.
+int compact_arena(qcs_dev_state* st)
+{
+    Dev& d = st->d;
+    cudaStream_t s = st->stream;
+    const uint64_t np = 2 * d.NS;
+    CU(cudaStreamSynchronize(s));
+    std::vector<uint64_t> off(np), len(np), nof(np);
+    CU(cudaMemcpy(off.data(), d.p_off, 8 * np, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(len.data(), d.p_len, 8 * np, cudaMemcpyDeviceToHost));
+    std::vector<uint64_t> ord(np);
+    for (uint64_t i = 0; i < np; ++i) ord[i] = i;
+    std::sort(ord.begin(), ord.end(), [&](uint64_t a, uint64_t b) { return off[a] < off[b]; });
+    const uint64_t bounce = 16 * st->wave * d.L;
+    uint8_t* X = reinterpret_cast<uint8_t*>(d.X);
+    std::vector<uint64_t> bs, bt, bd, bl;  // batch: src, bounce offset, dst, len
+    uint64_t at = 0, bfill = 0;
+    auto flush = [&]() -> int {
+        if (bs.empty()) return 0;
+        const uint64_t m = bs.size();
+        CU(cudaMemcpyAsync(st->mv_src, bs.data(), 8 * m, cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(st->mv_dst, bt.data(), 8 * m, cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(st->mv_len, bl.data(), 8 * m, cudaMemcpyHostToDevice, s));
+        k_move<<<(unsigned)m, 128, 0, s>>>(d.arena[0], X, st->mv_src, st->mv_dst, st->mv_len);
+        CU(cudaMemcpyAsync(st->mv_src, bd.data(), 8 * m, cudaMemcpyHostToDevice, s));
+        k_move<<<(unsigned)m, 128, 0, s>>>(X, d.arena[0], st->mv_dst, st->mv_src, st->mv_len);
+        st->launches += 2;
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(s));  // the host vectors are reused
+        bs.clear(), bt.clear(), bd.clear(), bl.clear();
+        bfill = 0;
+        return 0;
+    };
+    for (uint64_t k = 0; k < np;) {
+        const uint64_t g0 = ord[k];
+        uint64_t k2 = k + 1;
+        while (k2 < np && off[ord[k2]] == off[g0]) ++k2;
+        const uint64_t l16 = round16(len[g0]);
+        if (bfill + l16 > bounce) {
+            const int rc = flush();
+            if (rc) return rc;
+        }
+        if (at != off[g0] && l16) {
+            bs.push_back(off[g0]);
+            bt.push_back(bfill);
+            bd.push_back(at);
+            bl.push_back(len[g0]);
+            bfill += l16;
+        }
+        for (uint64_t q = k; q < k2; ++q) nof[ord[q]] = at;
+        at += l16;
+        k = k2;
+    }
+    int rc = flush();
+    if (rc) return rc;
+    CU(cudaMemcpy(d.p_off, nof.data(), 8 * np, cudaMemcpyHostToDevice));
+    st->bump = at;
+    CU(cudaMemcpy(&d.sc->bump, &st->bump, 8, cudaMemcpyHostToDevice));
+    ++st->compactions;
+    return 0;
+}
+
+// Reserve `need` arena bytes in wave mode (compacting when full).
+int big_reserve(qcs_dev_state* st, uint64_t need, uint64_t* at)
+{
+    if (st->bump + need > st->d.arena_cap) {
+        const int rc = compact_arena(st);
+        if (rc) return rc;
+    }
+    if (st->bump + need > st->d.arena_cap) return QCS_E_NOMEM;
+    *at = st->bump;
+    st->bump += need;
+    return 0;
+}
+
+// Wave mode: place and install the wave [s0, s1) after its encode.
+int big_commit_wave(qcs_dev_state* st, uint64_t s0, uint64_t s1, uint64_t gate_index, uint64_t units_done)
+{
+    Dev& d = st->d;
+    cudaStream_t s = st->stream;
+    const uint64_t m = 2 * (s1 - s0);
+    std::vector<uint64_t> len(m), nof(m);
+    CU(cudaMemcpyAsync(len.data(), d.slot_len + 2 * s0, 8 * m, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(st->h_sc, d.sc, sizeof(Dev::Scal), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (st->h_sc->err) return -1;  // device error: the caller reports it
+    uint64_t need = 0;
+    for (uint64_t i = 0; i < m; ++i) need += round16(len[i]);
+    uint64_t at = 0;
+    const int rc = big_reserve(st, need, &at);
+    if (rc == QCS_E_NOMEM)
+        return set_err(QCS_E_NOMEM, units_done == 0 ? "gate %llu failed: block arena exhausted"
+                                                    : "gate %llu failed: block arena exhausted after %llu of its units were committed",
+                       (unsigned long long)gate_index, (unsigned long long)units_done);
+    if (rc) return rc;
+    for (uint64_t i = 0; i < m; ++i) {
+        nof[i] = at;
+        at += round16(len[i]);
+    }
+    CU(cudaMemcpyAsync(d.new_off + 2 * s0, nof.data(), 8 * m, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(&d.sc->bump, &st->bump, 8, cudaMemcpyHostToDevice, s));
+    k_wave_commit<<<(unsigned)m, 128, 0, s>>>(d, st->lt, s0);
+    ++st->launches;
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(s));  // nof / bump are host locals
+    return 0;
+}
+
 // One gate, fully stream-ordered.  rec_index < 0: no record.
 int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, int nl,
                  double theta, int64_t rec_index, uint64_t gate_index, uint64_t* n_slots_out,
@@ -942,90 +1079,105 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         ++st->launches;
     } else if (p.reflect) {  // mean pass (aalc.cpp:270-295) needs every stride first
         prof_start(st, 4);
-        k_decode<<<(unsigned)d.NS, 256, 0, s>>>(d, DecodeJob{nullptr, 1});
-        k_stride_sums<<<(unsigned)((d.NS + 127) / 128), 128, 0, s>>>(d);
+        k_stride_partial<<<(unsigned)d.NS, 128, 0, s>>>(d);
         k_mean<<<1, 1, 0, s>>>(d);
         prof_stop(st);
-        st->launches += 3;
+        st->launches += 2;
     }
-    int fm = FM_LOCAL;
-    uint64_t grid = n_slots;
     // cross-chunk partners (pair units, in-stride targets >= 2^12): decode +
     // gate fully parallel into X, then the encoder reads X (split path)
     int dg = -1;
     if (p.pair) dg = DG_PAIR;
     else if (p.kind <= 1 && (1ull << p.t) >= 4096) dg = DG_FAR;
     else if (p.kind <= 1 && st->split_local && d.L >= 4096) dg = DG_IN;
+    const int fm = dg >= 0 ? FM_RAW2 : (p.pair ? FM_PAIR : FM_LOCAL);
     if (dg >= 0) {
         static bool dg_attr = false;
         if (!dg_attr) {
             CU(cudaFuncSetAttribute(k_decode_gate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DG_SMEM));
             dg_attr = true;
         }
-        GateParams gp;
-        for (int i = 0; i < 8; ++i) gp.u[i] = g->u[i];
-        const uint64_t chunks = dg == DG_IN ? d.L / 4096 : (dg == DG_PAIR ? (d.L + 2047) / 2048 : d.L / 4096);
-        const uint64_t units = dg == DG_PAIR ? p.n_units : n_slots;
-        prof_start(st, 0);
-        k_decode_gate<<<(unsigned)(units * chunks), 256, DG_SMEM, s>>>(d, p, gp, dg, chunks);
-        prof_stop(st);
-        ++st->launches;
-        fm = FM_RAW2;
-        grid = n_slots;
     }
-    for (int k = 0; k < nl; ++k) {
-        FusedArgs a{};
-        a.arena0 = d.arena[0];
-        a.arena1 = d.arena[1];
-        a.arena_cur = &d.sc->cur;
-        a.p_off = d.p_off;
-        a.p_codec = d.p_codec;
-        a.p_delta = d.p_delta;
-        a.side_in = d.side;
-        a.scale = d.scale;
-        a.job_stride = d.job_stride;
-        for (int i = 0; i < 8; ++i) a.u[i] = g->u[i];
-        a.kind = p.kind;
-        a.t = p.t;
-        a.local_ctl = p.local_ctl;
-        a.flip_off = p.flip_off;
-        a.mean = d.sc->mean;
-        a.n = d.L;
-        a.pending = d.pending;
-        a.snap = 1;
-        if (fm == FM_RAW2) {  // split path: gated, snapped planes in X
-            a.X = d.X;
-            a.x_plane_stride = d.L;
-            a.snap = 0;
+    GateParams gp;
+    for (int i = 0; i < 8; ++i) gp.u[i] = g->u[i];
+    const uint64_t spu = p.pair ? 2 : 1;                        // slots per unit
+    const uint64_t wave_units = std::max<uint64_t>(1, st->wave / spu);
+    for (uint64_t u0 = 0; u0 < p.n_units; u0 += wave_units) {
+        const uint64_t u1 = std::min<uint64_t>(p.n_units, u0 + wave_units);
+        const uint64_t s0 = u0 * spu, s1 = u1 * spu, nw = s1 - s0;
+        if (dg >= 0) {
+            const uint64_t chunks = dg == DG_PAIR ? (d.L + 2047) / 2048 : d.L / 4096;
+            const uint64_t units = dg == DG_PAIR ? (u1 - u0) : nw;
+            prof_start(st, 0);
+            k_decode_gate<<<(unsigned)(units * chunks), 256, DG_SMEM, s>>>(d, p, gp, dg, chunks, s0);
+            prof_stop(st);
+            ++st->launches;
         }
-        a.out = d.slot_out;
-        a.cap = d.slot_cap;
-        a.side = d.slot_side;
-        a.nsub = d.nsub;
-        a.out_len = d.slot_len;
-        a.sumsq = d.slot_sum;
-        a.cp = make_params(lad[k]);
-        a.counters = d.counters;
-        prof_start(st, 5);
-        k_tag_level<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, st->lt, n_slots, a.cp.lossy ? 1 : 0, lad[k]);
-        prof_stop(st);
-        ++st->launches;
-        prof_start(st, 2);
-        int rc = launch_fused(a, fm, grid, s);
-        prof_stop(st);
-        if (rc) return rc;
-        ++st->launches;
-        prof_start(st, 5);
-        k_ladder<<<(unsigned)((p.n_units + 127) / 128), 128, 0, s>>>(d, p, lad[k], theta, k == nl - 1);
-        prof_stop(st);
-        ++st->launches;
+        for (int k = 0; k < nl; ++k) {
+            FusedArgs a{};
+            a.arena0 = d.arena[0];
+            a.arena1 = d.arena[1];
+            a.arena_cur = &d.sc->cur;
+            a.p_off = d.p_off;
+            a.p_codec = d.p_codec;
+            a.p_delta = d.p_delta;
+            a.side_in = d.side;
+            a.scale = d.scale;
+            a.job_stride = d.job_stride;
+            for (int i = 0; i < 8; ++i) a.u[i] = g->u[i];
+            a.kind = p.kind;
+            a.t = p.t;
+            a.local_ctl = p.local_ctl;
+            a.flip_off = p.flip_off;
+            a.mean = d.sc->mean;
+            a.n = d.L;
+            a.pending = d.pending;
+            a.slot_base = s0;
+            a.snap = 1;
+            if (fm == FM_RAW2) {  // split path: gated, snapped planes in X
+                a.X = d.X;
+                a.x_plane_stride = d.L;
+                a.snap = 0;
+            }
+            a.out = d.slot_out;
+            a.cap = d.slot_cap;
+            a.side = d.slot_side;
+            a.nsub = d.nsub;
+            a.out_len = d.slot_len;
+            a.sumsq = d.slot_sum;
+            a.cp = make_params(lad[k]);
+            a.counters = d.counters;
+            prof_start(st, 5);
+            k_tag_level<<<(unsigned)grid_for(nw), 256, 0, s>>>(d, st->lt, s0, s1, a.cp.lossy ? 1 : 0, lad[k]);
+            prof_stop(st);
+            ++st->launches;
+            prof_start(st, 2);
+            int rc = launch_fused(a, fm, fm == FM_PAIR ? (u1 - u0) : nw, s);
+            prof_stop(st);
+            if (rc) return rc;
+            ++st->launches;
+            prof_start(st, 5);
+            k_ladder<<<(unsigned)((u1 - u0 + 127) / 128), 128, 0, s>>>(d, p, u0, u1, lad[k], theta, k == nl - 1);
+            prof_stop(st);
+            ++st->launches;
+        }
+        if (st->big) {
+            prof_start(st, 3);
+            const int rc = big_commit_wave(st, s0, s1, gate_index, u0);
+            prof_stop(st);
+            if (rc < 0) break;  // device error word set: k_norm records the gate
+            if (rc) return rc;
+        }
     }
     prof_start(st, 3);
-    k_commit_plan<<<1, 1024, 0, s>>>(d, n_slots, gen);
-    k_commit_copy<<<(unsigned)(2 * d.NS), 128, 0, s>>>(d, st->lt, gen);
+    if (!st->big) {
+        k_commit_plan<<<1, 1024, 0, s>>>(d, n_slots, gen);
+        k_commit_copy<<<(unsigned)(2 * d.NS), 128, 0, s>>>(d, st->lt, gen);
+        st->launches += 2;
+    }
     k_norm<<<1, NORM_THREADS, 0, s>>>(d, n_slots, rec_index < 0 ? 0 : (uint64_t)rec_index, gate_index, renorm);
     prof_stop(st);
-    st->launches += 3;
+    ++st->launches;
     CU(cudaGetLastError());
     return 0;
 }
@@ -1095,10 +1247,46 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
         qcs_state_destroy(st);
         return set_err(QCS_E_CUDA, "stream creation failed");
     }
-    d.arena_cap = std::max<uint64_t>(raw + raw / 8 + 4096 * d.NS, 1ull << 24);
     d.slot_cap = payload_cap(d.L);
-    TRY(dalloc(st, &d.arena[0], d.arena_cap));
-    TRY(dalloc(st, &d.arena[1], d.arena_cap));
+    // layout: small (two arenas, whole-gate staging, device-side commit) when
+    // it fits comfortably, else wave mode
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const uint64_t side_b = 2 * d.NS * d.nsub * sizeof(SideEntry);
+    const uint64_t small_arena = std::max<uint64_t>(raw + raw / 8 + 4096 * d.NS, 1ull << 24);
+    const uint64_t small_need = 2 * small_arena + raw + 2 * d.NS * d.slot_cap + 2 * side_b;
+    const char* fb = getenv("QCS_FORCE_BIG");
+    st->big = (fb && atoi(fb)) || (double)small_need > 0.7 * (double)free_b;
+    if (!st->big) {
+        st->wave = d.NS;
+        d.arena_cap = small_arena;
+        TRY(dalloc(st, &d.arena[0], d.arena_cap));
+        TRY(dalloc(st, &d.arena[1], d.arena_cap));
+    } else {
+        const uint64_t per_slot = 16 * d.L + 2 * d.slot_cap + 2 * d.nsub * sizeof(SideEntry);
+        uint64_t w = d.NS < 2 ? 1 : std::min<uint64_t>(d.NS, 296);
+        if (const char* e = getenv("QCS_WAVE_SLOTS")) w = std::max<uint64_t>(1, std::min<uint64_t>(d.NS, strtoull(e, nullptr, 10)));
+        while (w > 2 && w * per_slot > (8ull << 30)) w /= 2;
+        w = std::max<uint64_t>(w, std::min<uint64_t>(d.NS, 2));  // a pair unit needs 2 slots
+        if (w > 1 && (w & 1)) --w;  // whole pair units per wave
+        st->wave = w;
+        const uint64_t tables = 2 * d.NS * 64 + d.NS * 64;
+        const uint64_t reserve = 1ull << 30;
+        uint64_t cap = 0, min_cap = 1ull << 20;
+        if (const char* e = getenv("QCS_ARENA_BYTES")) cap = strtoull(e, nullptr, 10), min_cap = 64;
+        else if (free_b > side_b + w * per_slot + tables + reserve) cap = free_b - side_b - w * per_slot - tables - reserve;
+        cap &= ~uint64_t(15);
+        if (cap < min_cap) {
+            qcs_state_destroy(st);
+            return set_err(QCS_E_NOMEM, "not enough device memory for a %d-qubit state with %d stride bits", n, s);
+        }
+        d.arena_cap = cap;
+        TRY(dalloc(st, &d.arena[0], d.arena_cap));
+        d.arena[1] = nullptr;
+        TRY(dalloc(st, &st->mv_src, 2 * d.NS));
+        TRY(dalloc(st, &st->mv_dst, 2 * d.NS));
+        TRY(dalloc(st, &st->mv_len, 2 * d.NS));
+    }
     TRY(dalloc(st, &d.p_off, 2 * d.NS));
     TRY(dalloc(st, &d.p_len, 2 * d.NS));
     TRY(dalloc(st, &d.p_codec, 2 * d.NS));
@@ -1106,9 +1294,9 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     TRY(dalloc(st, &d.side, 2 * d.NS * d.nsub));
     TRY(dalloc(st, &d.scale, d.NS));
     TRY(dalloc(st, &d.sum_sq, d.NS));
-    TRY(dalloc(st, &d.X, 2 * d.NS * d.L));
-    TRY(dalloc(st, &d.slot_out, 2 * d.NS * d.slot_cap));
-    TRY(dalloc(st, &d.slot_side, 2 * d.NS * d.nsub));
+    TRY(dalloc(st, &d.X, 2 * st->wave * d.L));
+    TRY(dalloc(st, &d.slot_out, 2 * st->wave * d.slot_cap));
+    TRY(dalloc(st, &d.slot_side, 2 * st->wave * d.nsub));
     TRY(dalloc(st, &d.slot_len, 2 * d.NS));
     TRY(dalloc(st, &d.slot_sum, d.NS));
     TRY(dalloc(st, &d.job_stride, d.NS));
@@ -1169,6 +1357,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     CU(cudaMemcpy(d.sum_sq, h_sum.data(), 8 * h_sum.size(), cudaMemcpyHostToDevice));
     Dev::Scal sc{};
     sc.bump = 32;
+    st->bump = 32;
     sc.cur = 0;
     sc.err_gate = -1;
     sc.norm_sq = zero_state ? 0.0 : 1.0;
@@ -1305,29 +1494,18 @@ int qcs_run_program(qcs_dev_state_t st, const qcs_gate_desc* gates, uint64_t n_g
     return 0;
 }
 
-static int decode_all(qcs_dev_state* st, int apply_scale)
-{
-    k_decode<<<(unsigned)st->d.NS, 256, 0, st->stream>>>(st->d, DecodeJob{nullptr, apply_scale});
-    ++st->launches;
-    CU(cudaGetLastError());
-    return 0;
-}
-
 int qcs_read_stride(qcs_dev_state_t st, uint64_t j, int apply_scale, double* re, double* im)
 {
     if (!st) return set_err(QCS_E_INVALID, "null state");
     if (j >= st->d.NS) return set_err(QCS_E_RANGE, "stride index out of range");
     cudaSetDevice(st->device);
-    std::vector<uint64_t> one(1, j);
-    uint64_t* dj = st->d.job_stride;
-    CU(cudaMemcpyAsync(dj, &j, 8, cudaMemcpyHostToDevice, st->stream));
-    k_decode<<<1, 256, 0, st->stream>>>(st->d, DecodeJob{dj, apply_scale});
+    k_decode<<<1, 256, 0, st->stream>>>(st->d, DecodeJob{j, apply_scale, st->d.X});
     ++st->launches;
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(st->stream));
     const uint64_t L = st->d.L;
-    CU(cudaMemcpy(re, st->d.X + j * 2 * L, L * 8, cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(im, st->d.X + j * 2 * L + L, L * 8, cudaMemcpyDeviceToHost));
+    if (re) CU(cudaMemcpy(re, st->d.X, L * 8, cudaMemcpyDeviceToHost));
+    if (im) CU(cudaMemcpy(im, st->d.X + L, L * 8, cudaMemcpyDeviceToHost));
     return 0;
 }
 
@@ -1335,16 +1513,21 @@ int qcs_to_amplitudes(qcs_dev_state_t st, double* amps)
 {
     if (!st || !amps) return set_err(QCS_E_INVALID, "null argument");
     cudaSetDevice(st->device);
-    int rc = decode_all(st, 1);
-    if (rc) return rc;
-    CU(cudaStreamSynchronize(st->stream));
-    const uint64_t L = st->d.L;
-    std::vector<double> buf(2 * L);
-    for (uint64_t j = 0; j < st->d.NS; ++j) {
-        CU(cudaMemcpy(buf.data(), st->d.X + j * 2 * L, 16 * L, cudaMemcpyDeviceToHost));
-        for (uint64_t i = 0; i < L; ++i) {
-            amps[2 * (j * L + i)] = buf[i];
-            amps[2 * (j * L + i) + 1] = buf[L + i];
+    const uint64_t L = st->d.L, NS = st->d.NS;
+    std::vector<double> buf(2 * L * st->wave);
+    for (uint64_t j0 = 0; j0 < NS; j0 += st->wave) {
+        const uint64_t m = std::min<uint64_t>(st->wave, NS - j0);
+        k_decode<<<(unsigned)m, 256, 0, st->stream>>>(st->d, DecodeJob{j0, 1, st->d.X});
+        ++st->launches;
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(buf.data(), st->d.X, 16 * L * m, cudaMemcpyDeviceToHost, st->stream));
+        CU(cudaStreamSynchronize(st->stream));
+        for (uint64_t q = 0; q < m; ++q) {
+            const uint64_t j = j0 + q;
+            for (uint64_t i = 0; i < L; ++i) {
+                amps[2 * (j * L + i)] = buf[2 * L * q + i];
+                amps[2 * (j * L + i) + 1] = buf[2 * L * q + L + i];
+            }
         }
     }
     return 0;
@@ -1465,9 +1648,15 @@ int qcs_import_blocks(qcs_dev_state_t st, uint64_t j, const uint8_t* buf, uint64
     CU(cudaStreamSynchronize(st->stream));
     CU(cudaMemcpy(st->h_sc, d.sc, sizeof(Dev::Scal), cudaMemcpyDeviceToHost));
     const uint64_t need = ((plen[0] + 15) & ~15ull) + ((plen[1] + 15) & ~15ull);
-    if (st->h_sc->bump + need > d.arena_cap) return set_err(QCS_E_NOMEM, "block arena exhausted");
-    const int cur = st->h_sc->cur;
     uint64_t at = st->h_sc->bump;
+    if (st->big) {
+        const int r = big_reserve(st, need, &at);
+        if (r == QCS_E_NOMEM) return set_err(QCS_E_NOMEM, "block arena exhausted");
+        if (r) return r;
+    } else if (st->h_sc->bump + need > d.arena_cap) {
+        return set_err(QCS_E_NOMEM, "block arena exhausted");
+    }
+    const int cur = st->h_sc->cur;
     uint64_t new_off[2];
     for (int c = 0; c < 2; ++c) {
         new_off[c] = at;
@@ -1505,7 +1694,7 @@ int qcs_import_blocks(qcs_dev_state_t st, uint64_t j, const uint8_t* buf, uint64
         return set_err(e, "corrupt block for stride %llu", (unsigned long long)j);
     }
     Dev::Scal sc = *st->h_sc;
-    sc.bump = at;
+    sc.bump = st->big ? st->bump : at;
     CU(cudaMemcpy(d.sc, &sc, sizeof sc, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(d.scale + j, &scale, 8, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(d.sum_sq + j, &ssq, 8, cudaMemcpyHostToDevice));
@@ -1535,9 +1724,8 @@ int qcs_stride_sums(qcs_dev_state_t st, double* partial)
     int rc = sync_and_check(st);
     if (rc) return rc;
     Dev& d = st->d;
-    k_decode<<<(unsigned)d.NS, 256, 0, st->stream>>>(d, DecodeJob{nullptr, 1});
-    k_stride_sums<<<(unsigned)((d.NS + 127) / 128), 128, 0, st->stream>>>(d);
-    st->launches += 2;
+    k_stride_partial<<<(unsigned)d.NS, 128, 0, st->stream>>>(d);
+    st->launches += 1;
     CU(cudaGetLastError());
     rc = sync_and_check(st);
     if (rc) return rc;
@@ -1565,7 +1753,7 @@ int qcs_state_memory(qcs_dev_state_t st, uint64_t* arena, uint64_t* side, uint64
     const Dev& d = st->d;
     if (arena) *arena = st->h_sc->bump;
     if (side) *side = 2 * d.NS * d.nsub * sizeof(SideEntry);
-    if (scratch) *scratch = 16 * d.NS * d.L + 2 * d.NS * d.slot_cap + 2 * d.NS * d.nsub * sizeof(SideEntry);
+    if (scratch) *scratch = 16 * st->wave * d.L + 2 * st->wave * d.slot_cap + 2 * st->wave * d.nsub * sizeof(SideEntry);
     return 0;
 }
 
@@ -1590,6 +1778,8 @@ int qcs_state_counters(qcs_dev_state_t st, uint64_t* out, int n)
     int rc = sync_and_check(st);
     if (rc) return rc;
     CU(cudaMemcpy(out, st->d.counters, 8 * n, cudaMemcpyDeviceToHost));
+    if (n > 4) out[4] = st->compactions;  // host-side: in-place arena compactions
+    if (n > 5) out[5] = st->big ? st->wave : 0;
     return 0;
 }
 

@@ -81,6 +81,8 @@ struct FusedArgs {
     // ---- encoder ----
     uint64_t n;                   // elements per plane (stride length)
     const uint8_t* pending;       // per slot (null = all)
+    uint64_t slot_base;           // first slot of this launch (tables are global,
+                                  // out / side / X buffers are launch-local)
     int snap;
     uint8_t* out;
     uint64_t cap;
@@ -331,7 +333,8 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
     // output slot of this plane
     const uint64_t slot = MODE == MODE_PAIR ? 2ull * b + (pl >> 1) : (uint64_t)b;
     const int comp = MODE == MODE_PAIR ? (pl & 1) : pl;
-    if (a.pending && !a.pending[MODE == MODE_PAIR ? 2ull * b : (uint64_t)b]) return;
+    const uint64_t gslot = a.slot_base + slot;  // global slot (tables)
+    if (a.pending && !a.pending[a.slot_base + (MODE == MODE_PAIR ? 2ull * b : (uint64_t)b)]) return;
 
     extern __shared__ __align__(16) unsigned char smem[];
     double* xs = reinterpret_cast<double*>(smem);
@@ -356,7 +359,7 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
     if (MODE == MODE_RAW) {
         xg = a.X + (uint64_t)b * NPL * a.x_plane_stride + (uint64_t)pl * a.x_plane_stride;
     } else {
-        in_stride = a.job_stride[MODE == MODE_PAIR ? 2ull * b + (pl >> 1) : (uint64_t)b];
+        in_stride = a.job_stride[gslot];
         const uint64_t gpl = 2 * in_stride + comp;
         in_bytes = (*a.arena_cur ? a.arena1 : a.arena0) + a.p_off[gpl];
         in_codec = a.p_codec[gpl];
@@ -935,8 +938,9 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
     QCS_PHASE(6);
     if (tid == 0 && a.counters)
         for (int i = 0; i < 8; ++i) atomicAdd(&a.counters[8 + i], ph_acc[i]);
-    if (lane == 0) a.out_len[2 * slot + comp] = C.out_pos;
-    if (a.sumsq && (tid % (2 * LPL)) == 0) a.sumsq[MODE == MODE_PAIR ? 2ull * b + tid / (2 * LPL) : (uint64_t)b] =
+    if (lane == 0) a.out_len[2 * gslot + comp] = C.out_pos;
+    if (a.sumsq && (tid % (2 * LPL)) == 0)
+        a.sumsq[a.slot_base + (MODE == MODE_PAIR ? 2ull * b + tid / (2 * LPL) : (uint64_t)b)] =
         S.s[tid / (2 * LPL)];
 }
 

@@ -370,7 +370,7 @@ class CompressedState:
         buf = (C.c_uint64 * 16)()
         _check(lib().qcs_state_counters(self._h, buf, 16))
         return {"repaired_lanes": buf[0], "sum_passes": buf[1], "slid_bytes": buf[2],
-                "serial_fallback_lanes": buf[3],
+                "serial_fallback_lanes": buf[3], "compactions": buf[4], "wave_slots": buf[5],
                 "phase_cycles": {k: buf[8 + i] for i, k in enumerate(
                     ("input", "rounds", "final", "sum", "tokcount", "write", "tail"))}}
 
