@@ -24,8 +24,9 @@ cpu_baseline  the unmodified reference (oracle/_ref/libqcsref.so) on this
           host's cores, bounded sample of the same circuit.
 
 --impl reference runs the reference CPU path on the same workload instead.
-N > 1 (torchrun): independent replicas, one per GPU (the C2 state fits one
-GPU; the sharded multi-GPU path is DESIGN.md §7), max device time over ranks.
+N > 1 (torchrun): the C2 workload weak-scaled to 24 + log2(N) qubits and
+sharded over the ranks (rank = top qubits; gates on rank qubits exchange
+stride images with NCCL send/recv), device time max over ranks.
 """
 from __future__ import annotations
 
@@ -232,6 +233,97 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
+def run_sharded(args, rank, world, local_rank):
+    """N > 1: one state of 24 + log2(N) qubits sharded over the ranks (rank =
+    top qubits), so per-GPU work equals the N = 1 workload
+    (weak scaling).  Gates on rank qubits exchange stride images with NCCL
+    send/recv (paper_1811_05140_b200/distributed.py); renormalisation and
+    GateRecords are global.  Device time: CUDA events around the timed
+    steps on every rank, max over ranks."""
+    import torch
+    import paper_1811_05140_b200 as q
+    from paper_1811_05140_b200.distributed import GpuBackend, ShardedState, ShardGeometry, TorchComm
+
+    g = world.bit_length() - 1
+    if (1 << g) != world:
+        raise SystemExit("--gpus must be a power of two")
+    n = N_QUBITS + g
+    marked = next(cc.splitmix64(SEED)) & ((1 << n) - 1)
+    prog = cc.build_grover_gate_form(n, marked, ITERS)
+    delta = cc.pow2_bound(EPS, n)
+    gps = 2 * n + 2
+    dev = 0 if os.environ.get("QCS_SAME_DEVICE") else local_rank
+    torch.cuda.set_device(dev)
+    comm = TorchComm()
+    st = ShardedState(ShardGeometry(n, STRIDE_BITS, g), comm, GpuBackend(dev), 0)
+    lad, th = [delta], 1.0
+    for i in range(n):                                          # untimed prologue
+        st.apply_gate(prog.gates[i], lad, th, i)
+
+    def run_steps(first, count):
+        upd = 0
+        mr = math.inf
+        for k in range(count):
+            a = n + ((first + k) % ITERS) * gps
+            for i in range(a, a + gps):
+                rec, _ = st.apply_gate(prog.gates[i], lad, th, i)
+                upd += rec.bytes_before // 16
+                mr = min(mr, rec.min_ratio)
+        return upd, mr
+
+    run_steps(0, args.warmup)
+    l0 = q.engine.lib().qcs_state_launches(st.local.h)
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out"))
+                                 else ".", f"clocks_rank{rank}.csv"))
+    if rank == 0:
+        clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record()
+    upd, min_ratio = run_steps(args.warmup, args.steps)
+    torch.cuda.synchronize()
+    e1.record()
+    e1.synchronize()
+    wall = time.perf_counter() - w0
+    torch.distributed.barrier()
+    clk = clocks.stop() if rank == 0 else None
+    launches = q.engine.lib().qcs_state_launches(st.local.h) - l0
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3, wall], dtype=torch.float64, device=torch.device("cuda", dev))
+    if torch.distributed.get_backend() == "nccl":
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    else:
+        tc = t.cpu()
+        torch.distributed.all_reduce(tc, op=torch.distributed.ReduceOp.MAX)
+        t = tc
+    dev_s, wall_s = float(t[0]), float(t[1])
+    if rank != 0:
+        return 0
+    peak, peak_src = measured_peaks()
+    line = {"metric": METRIC, "value": upd / dev_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_s * 1e3 / max(1, args.steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generated circuit, seeded marked index)",
+            "config": {"workload": f"C2 weak-scaled: grover-{n} gate form sharded over {world} GPUs "
+                                   f"(2^{N_QUBITS} amplitudes per GPU, as at N=1)",
+                       "n_qubits": n, "stride_bits": STRIDE_BITS, "eps": EPS, "delta": delta,
+                       "delta_mapping": "largest power of two <= eps*2^-ceil(n/2)", "ladder": [delta],
+                       "theta": 1.0, "marked": marked, "iterations": ITERS,
+                       "step": f"one Grover iteration ({gps} gates)",
+                       "l2": "per-GPU state 2^24 amplitudes; no explicit flush (exchange traffic between gates)",
+                       "parallelism": f"{world} shards, rank = top {g} qubits, NCCL stride-image exchange"},
+            "roofline": {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
+                         "traffic": None, "peak_source": peak_src,
+                         "note": "see the N=1 line for the kernel roofline"},
+            "cpu_baseline": None,
+            "e2e": {"value": upd / wall_s, "unit": UNIT, "h2d_bytes_per_step": DESC_BYTES * gps,
+                    "d2h_bytes_per_step": 48 * (1 << (N_QUBITS - STRIDE_BITS)) * gps},
+            "gpu_launches": launches, "clocks": clk, "min_stride_ratio": min_ratio}
+    print(json.dumps(line))
+    return 0
+
+
 def run_b200(args, rank, world, local_rank):
     import torch
     import paper_1811_05140_b200 as q
@@ -357,6 +449,103 @@ def run_b200(args, rank, world, local_rank):
     return 0
 
 
+# ---------------------------------------------------------------------------
+# QFT configurations: the whole circuit once, fidelity
+# against the closed-form DFT row a_y = exp(2 pi i (x*y mod 2^n)/2^n)/2^(n/2)
+# (circuit.hpp:137-138), streamed from the device stride by stride.
+# ---------------------------------------------------------------------------
+QFT_CONFIGS = {
+    "C1": dict(n=20, s=14, eps=1e-3, basis=552808, note="BASELINE configs[0]; basis = mt19937_64(1)() & (2^20-1)"),
+    "C3": dict(n=34, s=20, eps=1e-3, basis=None, note="BASELINE configs[2]; 256 GiB uncompressed > one GPU"),
+}
+
+
+def qft_basis(name, n):
+    c = QFT_CONFIGS[name]
+    return c["basis"] if c["basis"] is not None else next(cc.splitmix64(n)) & ((1 << n) - 1)
+
+
+def dft_fidelity(state, n, s, x, device):
+    import torch
+    L, NS = 1 << s, 1 << (n - s)
+    batch = max(1, min(NS, (1 << 28) // (16 * L)))
+    buf = torch.empty(batch * 2 * L, dtype=torch.float64, device=device)
+    ov = torch.zeros((), dtype=torch.complex128, device=device)
+    nrm = torch.zeros((), dtype=torch.float64, device=device)
+    maxerr = torch.zeros((), dtype=torch.float64, device=device)
+    mask = (1 << n) - 1
+    xs = torch.tensor(x, dtype=torch.int64, device=device)
+    inv = 1.0 / math.sqrt(float(1 << n))
+    for j0 in range(0, NS, batch):
+        m = min(batch, NS - j0)
+        state.read_strides_device(j0, m, buf.data_ptr())
+        v = buf[: m * 2 * L].view(m, 2, L)
+        a = torch.complex(v[:, 0, :], v[:, 1, :])
+        y = torch.arange(j0 * L, (j0 + m) * L, dtype=torch.int64, device=device).view(m, L)
+        r = (xs * y) & mask                      # uint64 wrap-around product mod 2^n
+        ph = r.to(torch.float64) * (2.0 * math.pi / float(1 << n))
+        e = torch.complex(torch.cos(ph), torch.sin(ph)) * inv
+        ov += torch.sum(torch.conj(e) * a)
+        nrm += torch.sum(a.real * a.real + a.imag * a.imag)
+        maxerr = torch.maximum(maxerr, torch.max(torch.abs(a - e)))
+    return float(torch.abs(ov) ** 2 / nrm), float(maxerr)
+
+
+def run_qft_config(args, name):
+    import torch
+    import paper_1811_05140_b200 as q
+    c = QFT_CONFIGS[name]
+    n, s = c["n"], c["s"]
+    x = qft_basis(name, n)
+    delta = cc.pow2_bound(c["eps"], n)
+    prog = cc.build_qft(n)
+    torch.cuda.set_device(0)
+    lad = q.ErrorBoundLadder.make([delta])
+    th = q.RatioThreshold(1.0)
+    os.environ.setdefault("QCS_RESERVE_BYTES", str(8 << 30))  # room for the fidelity pass
+    state = q.CompressedState.basis_state(q.StateGeometry.make(n, s), x)
+    clocks = Clocks(os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out"))
+                                 else ".", f"clocks_{name}.csv"))
+    clocks.start()
+    dev_ns = upd = cin = cout = 0
+    min_ratio = math.inf
+    t0 = time.perf_counter()
+    chunk = 16
+    for a in range(0, len(prog.gates), chunk):
+        m = q.apply_program_range(state, prog, a, min(len(prog.gates), a + chunk), lad, th)
+        for r in m.records:
+            dev_ns += r.elapsed_ns
+            upd += r.bytes_before // 16
+            cin += r.compressed_in
+            cout += r.bytes_after
+            min_ratio = min(min_ratio, r.min_ratio)
+        if a % 128 == 0:
+            log(f"{name}: {a + len(m.records)}/{len(prog.gates)} gates, {dev_ns * 1e-9:.1f} s device")
+    wall = time.perf_counter() - t0
+    clk = clocks.stop()
+    cbytes, min_stride, nsq = state._stats()
+    fid, maxerr = dft_fidelity(state, n, s, x, torch.device("cuda", 0))
+    ctr = state.counters()
+    line = {"metric": METRIC, "value": upd / (dev_ns * 1e-9), "unit": UNIT, "n_gpus": 1,
+            "steps": 1, "warmup": 0, "ms_per_step": dev_ns * 1e-6, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generated QFT circuit, seeded basis state)",
+            "config": {"workload": f"{name}: qft-{n} ({len(prog.gates)} gates), 2^{s}-amp strides",
+                       "n_qubits": n, "stride_bits": s, "eps": c["eps"], "delta": delta,
+                       "delta_mapping": "largest power of two <= eps*2^-ceil(n/2)", "basis": x,
+                       "note": c["note"], "step": "the whole circuit once"},
+            "e2e": {"value": upd / wall, "unit": UNIT, "h2d_bytes_per_step": DESC_BYTES * len(prog.gates),
+                    "d2h_bytes_per_step": RECORD_BYTES * len(prog.gates)},
+            "fidelity_vs_dft_row": fid, "max_abs_amp_error": maxerr, "pointwise_bound": delta,
+            "norm_sq_tracked": nsq, "min_stride_ratio": min_ratio,
+            "final_state_ratio": (16 << n) / cbytes, "final_compressed_bytes": cbytes,
+            "bytes_per_amp_update": (cin + cout) / max(1, upd),
+            "layout": {"wave_slots": ctr["wave_slots"], "compactions": ctr["compactions"]},
+            "gpu_launches": state.launches(), "clocks": clk}
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -365,7 +554,11 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-fidelity", action="store_true")
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3"],
+                    help="C2 (default) is the headline workload; C1/C3 run a whole QFT once")
     args = ap.parse_args()
+    if args.config != "C2":
+        return run_qft_config(args, args.config)
     if args.warmup < 3 and args.impl == "b200":
         log("warning: timing rules ask for >= 3 warm-up steps")
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -374,13 +567,15 @@ def main():
     if world > 1:
         import torch
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        backend = "nccl" if args.impl == "b200" else "gloo"
+        backend = os.environ.get("QCS_DIST_BACKEND", "nccl" if args.impl == "b200" else "gloo")
         if backend == "nccl":
             torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group(backend)
     try:
         if args.impl == "reference":
             return run_reference(args, rank, world)
+        if world > 1:
+            return run_sharded(args, rank, world, local_rank)
         return run_b200(args, rank, world, local_rank)
     finally:
         if world > 1:

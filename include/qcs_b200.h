@@ -112,6 +112,17 @@ int qcs_apply_gate(qcs_dev_state_t st, const qcs_gate_desc* gate, const double* 
 int qcs_apply_gate_ex(qcs_dev_state_t st, const qcs_gate_desc* gate, const double* ladder,
                       int n_levels, double theta, int flags, const double* mean,
                       qcs_stride_report* reports, uint64_t* n_reports, double* norm_after);
+/* Stride images for sharded runs: the reference has no
+ * distribution; these move whole strides between shards as
+ * device-resident images (both blocks + side index + scale + sum), e.g. with
+ * NCCL send/recv over NVLink.  qcs_pack_strides packs every stride j with bit
+ * `bit` of j equal to `value`, ascending, into dev_buf (device memory, cap
+ * bytes); with dev_buf null it only reports *len.  qcs_unpack_strides installs
+ * an image: stride j of the image becomes stride j ^ xor_mask, blocks verbatim,
+ * through the ordinary commit path. */
+int qcs_pack_strides(qcs_dev_state_t st, int bit, int value, void* dev_buf, uint64_t cap,
+                     uint64_t* len);
+int qcs_unpack_strides(qcs_dev_state_t st, const void* dev_buf, uint64_t len, uint64_t xor_mask);
 /* Per-stride amplitude sums (stride_amplitude_sum, gate.cpp:303-311) of the
  * decompressed, scaled strides: partial[2j] = re, partial[2j+1] = im. */
 int qcs_stride_sums(qcs_dev_state_t st, double* partial);
@@ -132,6 +143,11 @@ int qcs_run_program(qcs_dev_state_t st, const qcs_gate_desc* gates, uint64_t n_g
 /* stored_stride / decompress_stride (aalc.cpp:191-209). */
 int qcs_read_stride(qcs_dev_state_t st, uint64_t stride, int apply_scale, double* re,
                     double* im);
+/* Device-resident variant for large states: strides [first, first+count)
+ * decoded (and scaled if apply_scale) into dev_out, a device buffer of
+ * count * 2 * 2^s doubles laid out [stride][re|im][element]. */
+int qcs_read_strides_device(qcs_dev_state_t st, uint64_t first, uint64_t count, int apply_scale,
+                            double* dev_out);
 /* to_amplitudes (aalc.cpp:211-223): interleaved re/im, 2^(n+1) doubles. */
 int qcs_to_amplitudes(qcs_dev_state_t st, double* amps);
 /* compressed_bytes / min_stride_ratio / norm_sq_tracked (aalc.cpp:233-259). */

@@ -220,6 +220,13 @@ class OracleState:
         sc, ss, _, _ = self.stride_info(j)
         return self.export_blocks(j), sc, ss
 
+    def pack(self, bit: int, value: int):
+        return [(j, *self.export(j)) for j in range(1 << (self.n - self.s)) if ((j >> bit) & 1) == value]
+
+    def unpack(self, payload, xor_mask: int):
+        for (j, blob, sc, ss) in payload:
+            self.import_(j ^ xor_mask, blob, sc, ss)
+
     def import_(self, j: int, blob: bytes, scale: float, ssq: float):
         self.o._check(self.o.lib.qo_import_blocks(self.h, C.c_uint64(j), blob, len(blob),
                                                   C.c_double(scale), C.c_double(ssq)))

@@ -147,6 +147,7 @@ struct Dev {
 
 __global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen)
 {
+    if (blockIdx.x == 0 && threadIdx.x == 0) d.sc->gate_cin = 0;  // wave layout accumulates it
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t j = slot_stride(p, s);
@@ -922,6 +923,7 @@ __global__ void __launch_bounds__(128) k_wave_commit(Dev d, LevelTag lt, uint64_
     SideEntry* ds = d.side + g * d.nsub;
     for (uint64_t i = threadIdx.x; i < d.nsub; i += blockDim.x) ds[i] = ss[i];
     if (threadIdx.x == 0) {
+        atomicAdd((unsigned long long*)&d.sc->gate_cin, (unsigned long long)(HEADER_BYTES + d.p_len[g]));
         d.p_off[g] = dst_off;
         d.p_len[g] = len;
         d.p_codec[g] = lt.slot_codec[slot];
@@ -1271,10 +1273,13 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
         if (w > 1 && (w & 1)) --w;  // whole pair units per wave
         st->wave = w;
         const uint64_t tables = 2 * d.NS * 64 + d.NS * 64;
-        const uint64_t reserve = 1ull << 30;
+        uint64_t reserve = 1ull << 30;  // left to the caller (QCS_RESERVE_BYTES)
+        if (const char* e = getenv("QCS_RESERVE_BYTES")) reserve = strtoull(e, nullptr, 10);
         uint64_t cap = 0, min_cap = 1ull << 20;
         if (const char* e = getenv("QCS_ARENA_BYTES")) cap = strtoull(e, nullptr, 10), min_cap = 64;
-        else if (free_b > side_b + w * per_slot + tables + reserve) cap = free_b - side_b - w * per_slot - tables - reserve;
+        else if (free_b > side_b + w * per_slot + tables + reserve)
+            // never more than a live state plus a full rewrite can use
+            cap = std::min<uint64_t>(free_b - side_b - w * per_slot - tables - reserve, 2 * small_arena + (64ull << 20));
         cap &= ~uint64_t(15);
         if (cap < min_cap) {
             qcs_state_destroy(st);
@@ -1509,6 +1514,22 @@ int qcs_read_stride(qcs_dev_state_t st, uint64_t j, int apply_scale, double* re,
     return 0;
 }
 
+int qcs_read_strides_device(qcs_dev_state_t st, uint64_t first, uint64_t count, int apply_scale,
+                            double* dev_out)
+{
+    if (!st || !dev_out) return set_err(QCS_E_INVALID, "null argument");
+    if (first > st->d.NS || count > st->d.NS - first) return set_err(QCS_E_RANGE, "stride range out of range");
+    cudaSetDevice(st->device);
+    for (uint64_t j0 = first; j0 < first + count; j0 += 65535) {
+        const uint64_t m = std::min<uint64_t>(65535, first + count - j0);
+        k_decode<<<(unsigned)m, 256, 0, st->stream>>>(st->d, DecodeJob{j0, apply_scale, dev_out + (j0 - first) * 2 * st->d.L});
+        ++st->launches;
+    }
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(st->stream));
+    return 0;
+}
+
 int qcs_to_amplitudes(qcs_dev_state_t st, double* amps)
 {
     if (!st || !amps) return set_err(QCS_E_INVALID, "null argument");
@@ -1698,6 +1719,185 @@ int qcs_import_blocks(qcs_dev_state_t st, uint64_t j, const uint8_t* buf, uint64
     CU(cudaMemcpy(d.sc, &sc, sizeof sc, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(d.scale + j, &scale, 8, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(d.sum_sq + j, &ssq, 8, cudaMemcpyHostToDevice));
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// stride images for sharded runs
+// ---------------------------------------------------------------------------
+struct PackEntry {
+    uint64_t j;
+    double scale, sum_sq;
+    uint64_t len[2];
+    uint64_t codec[2];
+    double delta[2];
+    uint64_t off[2];   // payload offsets in the image
+    uint64_t soff;     // side index offset in the image (plane 0, then plane 1)
+};
+constexpr uint64_t PACK_MAGIC = 0x31504b5053434351ull;  // "QCSPKP1"
+constexpr uint64_t PACK_HDR = 32;                      // magic, count, L, total
+
+__global__ void __launch_bounds__(128) k_pack_copy(Dev d, uint8_t* img, const PackEntry* ent)
+{
+    const PackEntry& e = ent[blockIdx.x >> 1];
+    const int c = (int)(blockIdx.x & 1);
+    const uint64_t g = 2 * e.j + c;
+    const uint4* s4 = reinterpret_cast<const uint4*>(d.arena[d.sc->cur] + d.p_off[g]);
+    uint4* d4 = reinterpret_cast<uint4*>(img + e.off[c]);
+    for (uint64_t i = threadIdx.x; i < (e.len[c] + 15) / 16; i += blockDim.x) d4[i] = s4[i];
+    const SideEntry* ss = d.side + g * d.nsub;
+    SideEntry* ds = reinterpret_cast<SideEntry*>(img + e.soff) + (uint64_t)c * d.nsub;
+    for (uint64_t i = threadIdx.x; i < d.nsub; i += blockDim.x) ds[i] = ss[i];
+}
+
+// Stage image entries [i0, i0 + gridDim/2) into slots 0.. as if a gate had
+// produced them, so the ordinary commit path installs them.
+__global__ void __launch_bounds__(128) k_unpack_stage(Dev d, LevelTag lt, const uint8_t* img, const PackEntry* ent,
+                                                      uint64_t i0, uint64_t xr, uint64_t gen)
+{
+    const uint64_t loc = blockIdx.x >> 1;
+    const int c = (int)(blockIdx.x & 1);
+    const PackEntry& e = ent[i0 + loc];
+    const uint4* s4 = reinterpret_cast<const uint4*>(img + e.off[c]);
+    uint4* d4 = reinterpret_cast<uint4*>(d.slot_out + (2 * loc + c) * d.slot_cap);
+    for (uint64_t i = threadIdx.x; i < (e.len[c] + 15) / 16; i += blockDim.x) d4[i] = s4[i];
+    const SideEntry* ss = reinterpret_cast<const SideEntry*>(img + e.soff) + (uint64_t)c * d.nsub;
+    SideEntry* ds = d.slot_side + (2 * loc + c) * d.nsub;
+    for (uint64_t i = threadIdx.x; i < d.nsub; i += blockDim.x) ds[i] = ss[i];
+    if (threadIdx.x == 0) {
+        const uint64_t j = e.j ^ xr;
+        d.slot_len[2 * loc + c] = e.len[c];
+        if (c == 0) {
+            d.job_stride[loc] = j;
+            d.slot_sum[loc] = e.sum_sq;
+            lt.slot_codec[loc] = (int8_t)e.codec[0];
+            lt.slot_delta[loc] = e.delta[0];
+            d.slot_of[j] = (int64_t)((gen << 32) | loc);
+        }
+    }
+}
+
+__global__ void k_unpack_finish(Dev d, const PackEntry* ent, uint64_t i0, uint64_t m, uint64_t xr)
+{
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i == 0 && d.sc->mode == 1) {  // the small layout compacted into the other arena
+        d.sc->cur = 1 - d.sc->cur;
+        d.sc->mode = 0;
+    }
+    if (i >= m) return;
+    const PackEntry& e = ent[i0 + i];
+    const uint64_t j = e.j ^ xr;
+    d.scale[j] = e.scale;
+    // the im plane may use another codec than re (k_unpack_stage tagged re's)
+    d.p_codec[2 * j + 1] = (int8_t)e.codec[1];
+    d.p_delta[2 * j + 1] = e.delta[1];
+}
+
+int qcs_pack_strides(qcs_dev_state_t st, int bit, int value, void* dev_buf, uint64_t cap, uint64_t* len)
+{
+    if (!st || !len) return set_err(QCS_E_INVALID, "null argument");
+    Dev& d = st->d;
+    if (bit < 0 || (bit < 63 && (1ull << bit) >= d.NS)) return set_err(QCS_E_RANGE, "stride bit out of range");
+    cudaSetDevice(st->device);
+    int rc = sync_and_check(st);
+    if (rc) return rc;
+    const uint64_t np = 2 * d.NS;
+    std::vector<uint64_t> plen(np);
+    std::vector<int8_t> pc(np);
+    std::vector<double> pd(np), sc(d.NS), ss(d.NS);
+    CU(cudaMemcpy(plen.data(), d.p_len, 8 * np, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(pc.data(), d.p_codec, np, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(pd.data(), d.p_delta, 8 * np, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(sc.data(), d.scale, 8 * d.NS, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(ss.data(), d.sum_sq, 8 * d.NS, cudaMemcpyDeviceToHost));
+    std::vector<PackEntry> ent;
+    for (uint64_t j = 0; j < d.NS; ++j)
+        if ((int)((j >> bit) & 1) == (value ? 1 : 0)) {
+            PackEntry e{};
+            e.j = j;
+            e.scale = sc[j];
+            e.sum_sq = ss[j];
+            for (int c = 0; c < 2; ++c) {
+                e.len[c] = plen[2 * j + c];
+                e.codec[c] = (uint64_t)pc[2 * j + c];
+                e.delta[c] = pd[2 * j + c];
+            }
+            ent.push_back(e);
+        }
+    uint64_t at = round16(PACK_HDR + sizeof(PackEntry) * ent.size());
+    const uint64_t side_b = 2 * d.nsub * sizeof(SideEntry);
+    for (auto& e : ent) {
+        e.off[0] = at;
+        at += round16(e.len[0]);
+        e.off[1] = at;
+        at += round16(e.len[1]);
+        e.soff = at;
+        at += side_b;
+    }
+    *len = at;
+    if (!dev_buf) return 0;
+    if (at > cap) return set_err(QCS_E_CAPACITY, "image buffer too small");
+    std::vector<uint8_t> hdr(PACK_HDR + sizeof(PackEntry) * ent.size());
+    const uint64_t h4[4] = {PACK_MAGIC, (uint64_t)ent.size(), d.L, at};
+    memcpy(hdr.data(), h4, PACK_HDR);
+    if (!ent.empty()) memcpy(hdr.data() + PACK_HDR, ent.data(), sizeof(PackEntry) * ent.size());
+    uint8_t* img = static_cast<uint8_t*>(dev_buf);
+    CU(cudaMemcpyAsync(img, hdr.data(), hdr.size(), cudaMemcpyHostToDevice, st->stream));
+    if (!ent.empty()) {
+        k_pack_copy<<<(unsigned)(2 * ent.size()), 128, 0, st->stream>>>(d, img, reinterpret_cast<const PackEntry*>(img + PACK_HDR));
+        ++st->launches;
+    }
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(st->stream));
+    return 0;
+}
+
+int qcs_unpack_strides(qcs_dev_state_t st, const void* dev_buf, uint64_t len, uint64_t xor_mask)
+{
+    if (!st || !dev_buf) return set_err(QCS_E_INVALID, "null argument");
+    Dev& d = st->d;
+    cudaSetDevice(st->device);
+    int rc = sync_and_check(st);
+    if (rc) return rc;
+    if (len < PACK_HDR) return set_err(QCS_E_TRUNCATED, "stride image truncated");
+    const uint8_t* img = static_cast<const uint8_t*>(dev_buf);
+    uint64_t h4[4];
+    CU(cudaMemcpy(h4, img, PACK_HDR, cudaMemcpyDeviceToHost));
+    if (h4[0] != PACK_MAGIC) return set_err(QCS_E_BAD_MAGIC, "bad stride image magic");
+    if (h4[2] != d.L) return set_err(QCS_E_INVALID, "stride image length disagrees with geometry");
+    const uint64_t count = h4[1];
+    if (count > d.NS || h4[3] > len || PACK_HDR + sizeof(PackEntry) * count > len)
+        return set_err(QCS_E_TRUNCATED, "stride image truncated");
+    std::vector<PackEntry> ent(count);
+    if (count) CU(cudaMemcpy(ent.data(), img + PACK_HDR, sizeof(PackEntry) * count, cudaMemcpyDeviceToHost));
+    for (const auto& e : ent) {
+        if ((e.j ^ xor_mask) >= d.NS) return set_err(QCS_E_RANGE, "stride index out of range");
+        for (int c = 0; c < 2; ++c)
+            if (e.len[c] > d.slot_cap || e.off[c] + e.len[c] > len || e.codec[c] > 1)
+                return set_err(QCS_E_BAD_VALUE, "corrupt stride image entry");
+    }
+    const PackEntry* dent = reinterpret_cast<const PackEntry*>(img + PACK_HDR);
+    for (uint64_t i0 = 0; i0 < count; i0 += st->wave) {
+        const uint64_t m = std::min<uint64_t>(st->wave, count - i0);
+        const uint64_t gen = ++st->gen;
+        k_unpack_stage<<<(unsigned)(2 * m), 128, 0, st->stream>>>(d, st->lt, img, dent, i0, xor_mask, gen);
+        ++st->launches;
+        if (st->big) {
+            rc = big_commit_wave(st, 0, m, 0, i0);
+            if (rc < 0) return report_device_error(st);
+            if (rc) return rc;
+        } else {
+            k_commit_plan<<<1, 1024, 0, st->stream>>>(d, m, gen);
+            k_commit_copy<<<(unsigned)(2 * d.NS), 128, 0, st->stream>>>(d, st->lt, gen);
+            st->launches += 2;
+        }
+        k_unpack_finish<<<(unsigned)((m + 127) / 128), 128, 0, st->stream>>>(d, dent, i0, m, xor_mask);
+        ++st->launches;
+        CU(cudaGetLastError());
+        rc = sync_and_check(st);
+        if (rc) return rc;
+        if (st->h_sc->err) return report_device_error(st);
+    }
     return 0;
 }
 

@@ -64,6 +64,9 @@ class ThreadComm:
         g.barrier.wait()
         return out
 
+    def allgather_array(self, arr: np.ndarray) -> List[np.ndarray]:
+        return self.allgather(np.array(arr, copy=True))
+
     def exchange(self, peer: Optional[int], obj):
         """Collective: every rank calls it; peer None = no partner."""
         g = self.group
@@ -90,14 +93,45 @@ class TorchComm:
         self.dist.all_gather_object(out, obj, group=self.group)
         return out
 
+    def allgather_array(self, arr: np.ndarray) -> List[np.ndarray]:
+        """Equal-shape float64 arrays, through device tensors on NCCL."""
+        import torch
+        dev = (torch.device("cuda", torch.cuda.current_device())
+               if self.dist.get_backend(self.group) == "nccl" else torch.device("cpu"))
+        t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(dev)
+        out = [torch.empty_like(t) for _ in range(self.size)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [o.cpu().numpy() for o in out]
+
     def exchange(self, peer: Optional[int], obj):
-        # pairwise exchange through an all-gather keeps the pattern collective
-        got = self.allgather((peer, obj))
-        if peer is None:
-            return None
-        p_peer, p_obj = got[peer]
-        assert p_peer == self.rank, "asymmetric exchange"
-        return p_obj
+        """Pairwise exchange.  Device tensors (stride images) go point to point
+        (NCCL send/recv over NVLink; staged through host memory on gloo); other
+        objects through an all-gather, which keeps the pattern collective."""
+        import torch
+        if peer is None or not torch.is_tensor(obj):
+            got = self.allgather((peer, None if torch.is_tensor(obj) else obj))
+            if peer is None:
+                return None
+            p_peer, p_obj = got[peer]
+            assert p_peer == self.rank, "asymmetric exchange"
+            return p_obj
+        dist = self.dist
+        nccl = dist.get_backend(self.group) == "nccl"
+        dev = obj.device if nccl else torch.device("cpu")
+        send = obj if nccl else obj.cpu()
+        n_send = torch.tensor([send.numel()], dtype=torch.int64, device=dev)
+        n_recv = torch.empty_like(n_send)
+        self._p2p(send=n_send, recv=n_recv, peer=peer)
+        recv = torch.empty(int(n_recv.item()), dtype=torch.uint8, device=dev)
+        self._p2p(send=send, recv=recv, peer=peer)
+        return recv if nccl else recv.to(obj.device)
+
+    def _p2p(self, send, recv, peer):
+        dist = self.dist
+        gp = peer if self.group is None else dist.get_global_rank(self.group, peer)
+        ops = [dist.P2POp(dist.isend, send, gp, self.group), dist.P2POp(dist.irecv, recv, gp, self.group)]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
 
 
 # ---------------------------------------------------------------------------
@@ -115,12 +149,12 @@ class GpuBackend:
         h = C.c_void_p()
         b = (1 << 64) - 1 if basis is None else basis
         _check(lib().qcs_state_create(n, s, C.c_uint64(b), self.device, C.byref(h)))
-        return _GpuShard(h, n, s)
+        return _GpuShard(h, n, s, self.device)
 
 
 class _GpuShard:
-    def __init__(self, h, n, s):
-        self.h, self.n, self.s = h, n, s
+    def __init__(self, h, n, s, device=0):
+        self.h, self.n, self.s, self.device = h, n, s, device
 
     def __del__(self):
         from .engine import _lib_handle
@@ -176,6 +210,21 @@ class _GpuShard:
         from .engine import _check, lib
         _check(lib().qcs_import_blocks(self.h, j, blob, len(blob), scale, ssq))
 
+    def pack(self, bit: int, value: int):
+        """Device image of the strides with stride bit `bit` == value."""
+        import ctypes as C
+        import torch
+        from .engine import _check, lib
+        n = C.c_uint64()
+        _check(lib().qcs_pack_strides(self.h, bit, value, None, 0, C.byref(n)))
+        t = torch.empty(n.value, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        _check(lib().qcs_pack_strides(self.h, bit, value, t.data_ptr(), n.value, C.byref(n)))
+        return t
+
+    def unpack(self, img, xor_mask: int):
+        from .engine import _check, lib
+        _check(lib().qcs_unpack_strides(self.h, img.data_ptr(), img.numel(), xor_mask))
+
     def amplitudes(self):
         from .engine import _check, lib
         a = np.empty(2 << self.n, dtype=np.float64)
@@ -215,17 +264,17 @@ class ShardedState:
 
     # -- data movement: swap rank bit b with local stride bit qb ------------
     def _swap(self, active: bool, b: int, qb: int):
+        """The lo rank of the pair sends its strides with local bit qb = 1, the
+        hi rank those with qb = 0; each lands at j ^ 2^qb on the other side."""
         r = self.r
-        nsl = self.geom.local_strides
         peer = r ^ (1 << b) if active else None
         payload = None
         if active:
-            send_bit = 0 if (r >> b) & 1 else 1   # lo rank sends local-bit-1 strides
-            payload = [(j, *self.local.export(j)) for j in range(nsl) if ((j >> qb) & 1) == send_bit]
+            send_bit = 0 if (r >> b) & 1 else 1
+            payload = self.local.pack(qb, send_bit)
         got = self.comm.exchange(peer, payload)
         if active:
-            for (j, blob, sc, ss) in got:
-                self.local.import_(j ^ (1 << qb), blob, sc, ss)
+            self.local.unpack(got, 1 << qb)
 
     def _global_stride(self, jl: int, swapped: Optional[tuple]) -> int:
         nsl = self.geom.local_strides
@@ -282,36 +331,45 @@ class ShardedState:
                     si += v[j + 1]
             na = float(1 << g.n_qubits)
             reports = self.local.apply(gate, ladder, theta, mean=(sr / na, si / na))
-        # global unit order of this rank's reports (reference: ascending lo
-        # stride; a pair unit reports lo then hi)
-        keyed = []
-        for rep in reports:
+        # one gather per gate: this rank's reports keyed by global unit order
+        # (reference: ascending lo stride; a pair unit reports lo then hi) and
+        # its per-stride (scale, sum_sq)
+        nsl = g.local_strides
+        buf = np.zeros((nsl + 1, 10))
+        buf[0, 0] = len(reports)
+        for i, rep in enumerate(reports):
             gj = self._global_stride(rep[0], swapped)
             if pair_bit_global is not None:
-                key = (gj & ~pair_bit_global, 1 if gj & pair_bit_global else 0)
+                k0, k1 = gj & ~pair_bit_global, (1 if gj & pair_bit_global else 0)
             else:
-                key = (gj, 0)
-            keyed.append((key, (gj,) + tuple(rep[1:])))
-        # global renormalisation, serial in global stride order (aalc.cpp:410-419)
+                k0, k1 = gj, 0
+            buf[i + 1, :8] = (k0, k1, gj, rep[1], rep[2], rep[3], rep[4], 1.0 if rep[5] else 0.0)
         sc, sm = self.local.stride_norms()
-        parts = self.comm.allgather((sc.tobytes(), sm.tobytes(), keyed))
-        scales = np.concatenate([np.frombuffer(p[0]) for p in parts])
-        sums = np.concatenate([np.frombuffer(p[1]) for p in parts])
-        total = 0.0
-        for a, m in zip(scales.tolist(), sums.tolist()):
-            total += a * a * m
-        f = None
+        buf[1:, 8] = sc
+        buf[1:, 9] = sm
+        parts = self.comm.allgather_array(buf)
+        # global renormalisation, serial in global stride order (aalc.cpp:410-419);
+        # np.cumsum is a sequential left-to-right fold, the reference's order
+        scales = np.concatenate([p_[1:, 8] for p_ in parts])
+        sums = np.concatenate([p_[1:, 9] for p_ in parts])
+        total = float(np.cumsum(scales * scales * sums)[-1])
         if total > 0.0:
             f = 1.0 / math.sqrt(total)
             self.local.scale_all(f)
-        nsq = 0.0
-        for a, m in zip(scales.tolist(), sums.tolist()):
-            a2 = a * f if f is not None else a
-            nsq += a2 * a2 * m
+            scales = scales * f
+        nsq = float(np.cumsum(scales * scales * sums)[-1])
         self.norm_sq = nsq
-        all_reps = sorted((kr for p in parts for kr in p[2]), key=lambda kr: kr[0])
-        from .metrics import gate_record
-        rec, viol = gate_record(index, gate.label, [r for _, r in all_reps], math.sqrt(nsq))
+        # GateRecord fold in global unit order (aalc.cpp:612-631)
+        rows = np.concatenate([p_[1:1 + int(p_[0, 0]), :8] for p_ in parts])
+        rows = rows[np.lexsort((rows[:, 1], rows[:, 0]))]
+        rec = GateRecord(gate_index=index, gate_label=gate.label, stride_count=len(rows))
+        rec.min_ratio = float(rows[:, 4].min()) if len(rows) else math.inf
+        rec.mean_ratio = float(np.cumsum(rows[:, 4])[-1]) / len(rows) if len(rows) else 0.0
+        rec.max_chosen_delta = max(0.0, float(rows[:, 3].max())) if len(rows) else 0.0
+        rec.bytes_before = int(rows[:, 5].sum())
+        rec.bytes_after = int(rows[:, 6].sum())
+        rec.norm_after = math.sqrt(nsq)
+        viol = int((rows[:, 7] == 0.0).sum())
         return rec, viol
 
     def amplitudes(self) -> np.ndarray:

@@ -69,6 +69,9 @@ def lib() -> C.CDLL:
         L.qcs_stride_norms.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.qcs_stride_sums.argtypes = [C.c_void_p, C.c_void_p]
         L.qcs_scale_all.argtypes = [C.c_void_p, C.c_double]
+        L.qcs_pack_strides.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_uint64,
+                                       C.POINTER(C.c_uint64)]
+        L.qcs_unpack_strides.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64]
         L.qcs_apply_gate.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_double), C.c_int,
                                      C.c_double, C.c_void_p, C.POINTER(C.c_uint64),
                                      C.POINTER(C.c_double)]
@@ -76,6 +79,7 @@ def lib() -> C.CDLL:
                                       C.POINTER(C.c_double), C.c_int, C.c_double, C.c_void_p,
                                       C.POINTER(C.c_uint64)]
         L.qcs_read_stride.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]
+        L.qcs_read_strides_device.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p]
         L.qcs_to_amplitudes.argtypes = [C.c_void_p, C.c_void_p]
         L.qcs_state_stats.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_double),
                                       C.POINTER(C.c_double)]
@@ -315,6 +319,11 @@ class CompressedState:
 
     def decompress_stride(self, j: int):
         return self._stride(j, True)
+
+    def read_strides_device(self, first: int, count: int, out_ptr: int, apply_scale: bool = True):
+        """Decode strides [first, first+count) into a device buffer (e.g. a
+        torch.float64 CUDA tensor's data_ptr()) laid out [stride][re|im][L]."""
+        _check(lib().qcs_read_strides_device(self._h, first, count, int(apply_scale), out_ptr))
 
     def to_amplitudes(self) -> np.ndarray:
         a = np.empty(2 * self._geom.n_amplitudes(), dtype=np.float64)

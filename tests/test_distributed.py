@@ -129,3 +129,54 @@ def test_thread_cluster_gpu(oracle, case, ranks):
                                    lambda r: GpuBackend(0), basis, lad, theta)
     assert mm.emit_csv(recs, with_elapsed=False) == want_csv
     assert amp.tobytes() == want_amp.tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("force_big", [0, 1])
+def test_stride_images_round_trip_gpu(oracle, monkeypatch, force_big):
+    """qcs_pack_strides / qcs_unpack_strides move strides verbatim (blocks,
+    side index, scale, sum) through the commit path of either layout."""
+    import torch
+    from oracle import OracleBackend
+    if force_big:
+        monkeypatch.setenv("QCS_FORCE_BIG", "1")
+        monkeypatch.setenv("QCS_WAVE_SLOTS", "2")
+    prog = q.build_qft(11)
+    lad = [q.pow2_bound(1e-3, 11)]
+    a = GpuBackend(0).create(11, 6, 5)
+    o = OracleBackend(oracle).create(11, 6, 5)
+    for g in prog.gates[:40]:
+        a.apply(g, lad, 1.0)
+        o.apply(g, lad, 1.0)
+    # swap stride bit 3 = 1 half into a fresh zero state's bit 3 = 0 half
+    b = GpuBackend(0).create(11, 6, None)
+    img = a.pack(3, 1)
+    assert img.is_cuda and img.dtype == torch.uint8
+    b.unpack(img, 1 << 3)
+    ob = OracleBackend(oracle).create(11, 6, None)
+    ob.unpack(o.pack(3, 1), 1 << 3)
+    for j in range(32):
+        assert b.export(j) == ob.export(j), j
+    # and back onto the source: a no-op on its content
+    a.unpack(b.pack(3, 0), 1 << 3)
+    for j in range(32):
+        assert a.export(j) == o.export(j), j
+
+
+@pytest.mark.gpu
+def test_sharded_bench_functional(tmp_path):
+    """bench.py's N > 1 path (sharded C2 weak scaling) end to end with two
+    ranks.  One GPU here: both ranks share it and exchange through gloo, so no
+    rank waits on another's kernel; the numbers are not a measurement."""
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ, QCS_DIST_BACKEND="gloo", QCS_SAME_DEVICE="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+                        os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=900, env=env, cwd=str(tmp_path))
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["n_qubits"] == 25
