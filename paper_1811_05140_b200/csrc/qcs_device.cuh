@@ -180,14 +180,23 @@ __device__ __forceinline__ double lattice_point(const CodecParams& cp, double a,
 // lattice_point with rounding emulation: if a + 2*delta*M is not exact the
 // reference chain rounds right here, and the rounded value anchors what
 // follows (a heuristic for the speculation; verification decides).
+// v = fl(a + y) is exact iff fl(v - a) == y and fl(v - y) == a: if the add
+// rounded, its error e is a non-zero multiple of u = min(ulp a, ulp y) (the
+// result then has ulp >= u), so |e| >= u and e cannot vanish in both
+// re-subtractions, each of which would need |e| <= ulp/2.  Branch-free, and
+// the two subtractions are independent.
+__device__ __forceinline__ bool add_exact(double a, double y, double v)
+{
+    return (__dsub_rn(v, a) == y) & (__dsub_rn(v, y) == a);
+}
+
 __device__ __forceinline__ double lattice_step(const CodecParams& cp, double& a, double x)
 {
     const double M = rint(__dmul_rn(__dsub_rn(x, a), cp.inv_td));
     const double y = __dmul_rn(cp.td, M);
     const double v = __dadd_rn(a, y);
-    // Fast2Sum error of a + y: non-zero exactly when the chain rounds here
-    const double err = fabs(a) >= fabs(y) ? __dsub_rn(y, __dsub_rn(v, a)) : __dsub_rn(a, __dsub_rn(v, y));
-    if (err != 0.0) a = v;
+    // the chain rounds here exactly when a + y is inexact
+    if (!add_exact(a, y, v)) a = v;
     return v;
 }
 
@@ -215,8 +224,22 @@ __device__ __forceinline__ double lattice_step_m(const CodecParams& cp, double& 
     safe = fabs(y) < 1073741824.0 && fr < 0.5 - 1.9073486328125e-06;  // 2^30, 0.5 - 2^-19
     const double yv = __dmul_rn(cp.td, M);
     const double v = __dadd_rn(a, yv);
-    const double err = fabs(a) >= fabs(yv) ? __dsub_rn(yv, __dsub_rn(v, a)) : __dsub_rn(a, __dsub_rn(v, yv));
-    if (err != 0.0) a = v;  // the chain rounds here: re-anchor (M relative to v is 0)
+    if (!add_exact(a, yv, v)) a = v;  // the chain rounds here: re-anchor (M relative to v is 0)
+    return v;
+}
+
+// lattice_step_m without moving the anchor: sets rnd when the chain would
+// round (re-anchor) here, so a group of steps can run independently.
+__device__ __forceinline__ double lattice_try(const CodecParams& cp, double a, double x, double& M,
+                                              bool& safe, bool& rnd)
+{
+    const double y = __dmul_rn(__dsub_rn(x, a), cp.inv_td);
+    M = rint(y);
+    const double fr = fabs(__dsub_rn(y, M));
+    safe = fabs(y) < 1073741824.0 && fr < 0.5 - 1.9073486328125e-06;
+    const double yv = __dmul_rn(cp.td, M);
+    const double v = __dadd_rn(a, yv);
+    rnd |= !add_exact(a, yv, v);
     return v;
 }
 

@@ -1268,7 +1268,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
         const uint64_t per_slot = 16 * d.L + 2 * d.slot_cap + 2 * d.nsub * sizeof(SideEntry);
         uint64_t w = d.NS < 2 ? 1 : std::min<uint64_t>(d.NS, 296);
         if (const char* e = getenv("QCS_WAVE_SLOTS")) w = std::max<uint64_t>(1, std::min<uint64_t>(d.NS, strtoull(e, nullptr, 10)));
-        while (w > 2 && w * per_slot > (8ull << 30)) w /= 2;
+        while (w > 2 && w * per_slot > (12ull << 30)) w /= 2;
         w = std::max<uint64_t>(w, std::min<uint64_t>(d.NS, 2));  // a pair unit needs 2 slots
         if (w > 1 && (w & 1)) --w;  // whole pair units per wave
         st->wave = w;

@@ -26,6 +26,8 @@
 
 namespace qcs {
 
+constexpr int GRP = 4;  // elements per independent group in the chain loops
+
 enum : int { MODE_RAW = 0, MODE_LOCAL = 1, MODE_FAR = 2, MODE_PAIR = 3 };
 
 struct FusedShared {
@@ -518,8 +520,9 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
                             const double v = lattice_step_m(cp, Atmp, x_left, Mt, sf);
                             if (same_bits(Atmp, A) && same_bits(v, Pprev)) Mprev = Mt;
                         }
-#pragma unroll 4
-                        for (int i = 0; i < cnt; ++i) {
+                        // one element of the chain, in order (the reference's step
+                        // verifies every element the cheap test cannot prove)
+                        auto elem = [&](int i) {
                             const double x = xl[i];
                             double Ph, M = 0.0;
                             bool safe = false;
@@ -545,6 +548,57 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
                             }
                             Mprev = ((emask >> i) & 1u) ? 0.0 : M;
                             Pprev = Ph;
+                        };
+                        // groups of GRP elements: anchors move only at escapes unless
+                        // the chain rounds, so the lattice steps of a group are
+                        // independent (ILP); a rounding event replays the group in order
+                        for (int i0 = 0; i0 < cnt; i0 += GRP) {
+                            double Mv[GRP], Pv[GRP];
+                            uint32_t sf = 0;
+                            bool rnd = false;
+                            double a = A;
+#pragma unroll
+                            for (int k = 0; k < GRP; ++k) {
+                                const int i = i0 + k;
+                                const double x = xl[i];  // rows are padded: i < 32 always
+                                const bool esc = (emask >> i) & 1u;
+                                a = esc ? x : a;
+                                bool sk, rk = false;
+                                const double v = lattice_try(cp, a, x, Mv[k], sk, rk);
+                                Pv[k] = esc ? x : v;
+                                rnd |= rk & !esc & (i < cnt);
+                                sf |= (uint32_t)(sk & !esc) << k;
+                            }
+                            if (rnd) {
+                                for (int k = 0; k < GRP && i0 + k < cnt; ++k) elem(i0 + k);
+                                continue;
+                            }
+#pragma unroll
+                            for (int k = 0; k < GRP; ++k) {
+                                const int i = i0 + k;
+                                if (i < cnt) {
+                                    const bool esc = (emask >> i) & 1u;
+                                    bool safe = false;
+                                    if (!esc) {
+                                        const double q = __dsub_rn(Mv[k], Mprev);
+                                        safe = ((sf >> k) & 1u) && fabs(q) <= 32766.0;
+                                        if (safe) cl[i] = (int16_t)q;
+                                    }
+                                    if (!safe) {
+                                        const double x = xl[i];
+                                        double P2 = Pprev;
+                                        const int32_t c = ref_step(cp, P2, x);
+                                        cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
+                                        if (!same_bits(P2, Pv[k]) && fail == LLONG_MAX) {
+                                            fail = (long long)e0 + i;
+                                            fprev = Pprev;
+                                        }
+                                    }
+                                    Mprev = esc ? 0.0 : Mv[k];
+                                    Pprev = Pv[k];
+                                }
+                            }
+                            A = a;
                         }
                     } else {
                         int pp = 0;
@@ -611,9 +665,8 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
                     S.entryP[tid] = Pprev;
                     int pp = 0;
                     while (pp < np && S.pin_idx[pl][pp] < (long long)e0) ++pp;
-                    for (int i = 0; i < cnt; ++i) {
+                    auto fin = [&](int i) {
                         const long long k = (long long)e0 + i;
-                        if (k >= fser) break;
                         const double x = xl[i];
                         double Ph;
                         if (pp < np && S.pin_idx[pl][pp] == k) {
@@ -628,6 +681,36 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
                         }
                         xl[i] = Ph;
                         Pprev = Ph;
+                    };
+                    const int lim = fser <= (long long)e0 ? 0 : (int)min((long long)cnt, fser - (long long)e0);
+                    for (int i0 = 0; i0 < lim; i0 += GRP) {
+                        const bool pin_here = pp < np && S.pin_idx[pl][pp] < (long long)e0 + i0 + GRP;
+                        if (pin_here || i0 + GRP > lim) {
+                            for (int k = 0; k < GRP && i0 + k < lim; ++k) fin(i0 + k);
+                            continue;
+                        }
+                        double Pv[GRP], Mv[GRP];
+                        bool rnd = false;
+                        double a = A;
+#pragma unroll
+                        for (int k = 0; k < GRP; ++k) {
+                            const int i = i0 + k;
+                            const double x = xl[i];
+                            const bool esc = (emask >> i) & 1u;
+                            a = esc ? x : a;
+                            bool sk, rk = false;
+                            const double v = lattice_try(cp, a, x, Mv[k], sk, rk);
+                            Pv[k] = esc ? x : v;
+                            rnd |= rk & !esc;
+                        }
+                        if (rnd) {
+                            for (int k = 0; k < GRP; ++k) fin(i0 + k);
+                            continue;
+                        }
+#pragma unroll
+                        for (int k = 0; k < GRP; ++k) xl[i0 + k] = Pv[k];
+                        A = a;
+                        Pprev = Pv[GRP - 1];
                     }
                     S.exitP[tid] = Pprev;
                 }
