@@ -204,6 +204,21 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FusedShared& S
     const int kb = gt * PER;
     int k0 = 0;
     bool done = false;
+    // While s is still 0 the next elements double it again and again (a binade
+    // crossing, i.e. a parallel pass, per doubling): sum the first SERIAL_SUM
+    // elements of a stride in the reference's order on one thread instead.
+    constexpr int SERIAL_SUM = 512;
+    __syncthreads();
+    if (S.s[g] == 0.0) {
+        const int m = min(n_it, SERIAL_SUM);
+        if (gt == 0) {
+            double acc = 0.0;
+#pragma unroll 4
+            for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, tsq_g<LPL>(xs, g, k));
+            S.s[g] = acc;
+        }
+        k0 = m;
+    }
     for (;;) {
         __syncthreads();
         const double s = S.s[g];
