@@ -396,11 +396,21 @@ __device__ __forceinline__ void lane_walk(const int16_t* cl, int cnt, uint64_t e
 // ---- bitmask view of a lane's codes (zero codes / raw words / nonzero codes)
 struct LaneMasks {
     uint32_t z, w, valid;
+    uint32_t cbytes;  // bytes of the lane's code tokens (varint of zigzag(q)<<2|1)
 };
+
+// varint length of code_token(q) for a 16-bit code: zigzag(q) < 2^16, so the
+// token is below 2^18 and takes 1..3 bytes
+__device__ __forceinline__ uint32_t code_token_len16(uint32_t c16)
+{
+    const int32_t q = (int32_t)(int16_t)c16;
+    const uint32_t v = ((((uint32_t)q << 1) ^ (uint32_t)(q >> 31)) << 2) | 1u;
+    return 1u + (v >= 128u) + (v >= 16384u);
+}
 
 __device__ __forceinline__ LaneMasks lane_masks(const int16_t* cl, int cnt)
 {
-    LaneMasks m{0u, 0u, cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u)};
+    LaneMasks m{0u, 0u, cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u), 0u};
     const uint32_t* c2 = reinterpret_cast<const uint32_t*>(cl);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -408,10 +418,35 @@ __device__ __forceinline__ LaneMasks lane_masks(const int16_t* cl, int cnt)
         const uint32_t lo = v & 0xffffu, hi = v >> 16;
         m.z |= ((uint32_t)(lo == 0u) << (2 * j)) | ((uint32_t)(hi == 0u) << (2 * j + 1));
         m.w |= ((uint32_t)(lo == 0x8000u) << (2 * j)) | ((uint32_t)(hi == 0x8000u) << (2 * j + 1));
+        const bool clo = lo != 0u && lo != 0x8000u && 2 * j < cnt;
+        const bool chi = hi != 0u && hi != 0x8000u && 2 * j + 1 < cnt;
+        m.cbytes += (clo ? code_token_len16(lo) : 0u) + (chi ? code_token_len16(hi) : 0u);
     }
     m.z &= m.valid;
     m.w &= m.valid;
     return m;
+}
+
+// The run tokens of lane_tokens only (same emission contract for runs):
+// iterates over run starts instead of every token.
+template <typename FR>
+__device__ __forceinline__ void lane_runs(const LaneMasks& m, int cnt, uint64_t e0, int in_ty, uint64_t in_st,
+                                          bool tail_closes, bool close_carried, FR on_run)
+{
+    if (cnt <= 0) return;
+    const int t0 = ((m.z & 1u) ? TY_Z : ((m.w & 1u) ? TY_W : TY_C));
+    const bool cont = in_ty != TY_NONE && t0 == in_ty;
+    if (!cont && close_carried && in_ty != TY_NONE) on_run(in_ty, in_st, e0);
+    uint32_t starts = (m.z & ~(m.z << 1)) | (m.w & ~(m.w << 1));
+    while (starts) {
+        const int p = __ffs(starts) - 1;
+        starts &= starts - 1u;
+        const bool isz = (m.z >> p) & 1u;
+        const uint32_t run = (isz ? m.z : m.w) >> p;
+        const int end = p + (run == 0xffffffffu ? 32 : __ffs(~run) - 1);
+        const uint64_t rst = (p == 0 && cont) ? in_st : e0 + (uint64_t)p;
+        if (end < cnt || tail_closes) on_run(isz ? TY_Z : TY_W, rst, e0 + (uint64_t)end);
+    }
 }
 
 __device__ __forceinline__ int mask_type(const LaneMasks& m, int p)

@@ -92,6 +92,10 @@ __device__ __forceinline__ void put_varint(uint8_t* p, uint64_t v)
 
 __device__ __forceinline__ void put_word(uint8_t* p, uint64_t w)
 {
+    if ((reinterpret_cast<uintptr_t>(p) & 7u) == 0) {  // aligned: one 8-byte store
+        *reinterpret_cast<uint64_t*>(p) = w;
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) p[i] = static_cast<uint8_t>(w >> (8 * i));
 }

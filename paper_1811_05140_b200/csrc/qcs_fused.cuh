@@ -881,18 +881,16 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
         uint32_t nbytes = 0;
         int closes_open = 0;
         uint64_t close_vlen = 0;
-        lane_tokens(
-            lm, cl, cnt, e0, in_ty, in_st, tail_closes, lane == 0,
-            [&](int t, uint64_t st, uint64_t end) {
-                const uint64_t len = end - st;
-                const int vl = varint_len(run_token(LOSSY, t, len));
-                nbytes += vl + (t == TY_W ? 8u * (uint32_t)len : 0u);
-                if (st < base) {
-                    closes_open = 1;
-                    close_vlen = vl;
-                }
-            },
-            [&](int16_t q) { nbytes += varint_len(code_token(q)); });
+        nbytes = lm.cbytes;
+        lane_runs(lm, cnt, e0, in_ty, in_st, tail_closes, lane == 0, [&](int t, uint64_t st, uint64_t end) {
+            const uint64_t len = end - st;
+            const int vl = varint_len(run_token(LOSSY, t, len));
+            nbytes += vl + (t == TY_W ? 8u * (uint32_t)len : 0u);
+            if (st < base) {
+                closes_open = 1;
+                close_vlen = vl;
+            }
+        });
         if (closes_open) {
             C.closes_open = 1;
             C.close_vlen = close_vlen;
@@ -965,9 +963,15 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
                     pos += vl + (t == TY_W ? 8 * len : 0);
                 },
                 [&](int16_t q) {
-                    const uint64_t v = code_token(q);
-                    put_varint(out + pos, v);
-                    pos += varint_len(v);
+                    // code token: < 2^18, 1..3 varint bytes, stored without a loop
+                    const int32_t qq = q;
+                    const uint32_t v = ((((uint32_t)qq << 1) ^ (uint32_t)(qq >> 31)) << 2) | 1u;
+                    const uint32_t len = 1u + (v >= 128u) + (v >= 16384u);
+                    uint8_t* o = out + pos;
+                    o[0] = (uint8_t)((v & 0x7fu) | (len > 1u ? 0x80u : 0u));
+                    if (len > 1u) o[1] = (uint8_t)(((v >> 7) & 0x7fu) | (len > 2u ? 0x80u : 0u));
+                    if (len > 2u) o[2] = (uint8_t)(v >> 14);
+                    pos += len;
                 });
             if (lane + 1 == active && !final_iter && tail_ty != TY_NONE && tail_st >= base) {
                 const uint64_t tokpos = C.out_pos + C.iter_bytes;
