@@ -411,6 +411,14 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
 
         // 1. input: decode (+ gate) or raw load, then snap_zeros
         if (MODE == MODE_RAW) {
+            // pull the NEXT chunk of this plane towards L2 while this one is
+            // processed (one bulk prefetch per plane; no shared memory needed)
+            if (lane == 0 && base + ITP < n) {
+                const uint64_t nb = umin64((uint64_t)ITP, n - base - ITP) * 8;
+                if ((nb & 15) == 0)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(xg + base + ITP), "r"((unsigned)nb)
+                                 : "memory");
+            }
 #pragma unroll 8
             for (int i = lane; i < ITP; i += LPL) {
                 double* dst = &xrow<LPL>(xs, pl, i);
