@@ -706,6 +706,12 @@ int launch_fused_t(const FusedArgs& a, uint64_t grid, cudaStream_t s)
 
 enum { FM_LOCAL = 0, FM_FAR = 1, FM_PAIR = 2, FM_RAW1 = 3, FM_RAW2 = 4 };
 
+int codec_max_pins()
+{
+    const char* e = getenv("QCS_MAX_PINS");
+    return e ? std::max(0, std::min(MAXPIN, atoi(e))) : MAXPIN;
+}
+
 int launch_fused(const FusedArgs& a, int fm, uint64_t grid, cudaStream_t s)
 {
     const bool L = a.cp.lossy != 0;
@@ -731,6 +737,7 @@ struct qcs_dev_state {
     uint64_t gen = 0;
     uint64_t launches = 0;
     int split_local = 0;  // QCS_SPLIT_LOCAL=1: in-chunk gates also take the split path
+    int max_pins = MAXPIN;  // QCS_MAX_PINS (tests force the lane-serial fallback)
     // Large states ("wave mode"): one arena, per-wave staging
     // buffers (slots, side, X) for `wave` slots, per-wave commit placed by the
     // host, in-place compaction through the X buffer.
@@ -1135,6 +1142,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             a.n = d.L;
             a.pending = d.pending;
             a.slot_base = s0;
+            a.max_pins = st->max_pins;
             a.snap = 1;
             if (fm == FM_RAW2) {  // split path: gated, snapped planes in X
                 a.X = d.X;
@@ -1228,6 +1236,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     qcs_dev_state* st = new qcs_dev_state();
     st->device = device;
     if (const char* e = getenv("QCS_SPLIT_LOCAL")) st->split_local = atoi(e);
+    if (const char* e = getenv("QCS_MAX_PINS")) st->max_pins = std::max(0, std::min(MAXPIN, atoi(e)));
     cudaSetDevice(device);
     int rc = 0;
 #define TRY(x)                    \
@@ -2031,6 +2040,7 @@ int qcs_codec_compress(const double* x, uint64_t n, double delta, uint8_t* out, 
     cudaMemcpyAsync(dx, x, 8 * n, cudaMemcpyHostToDevice, s);
     cudaMemsetAsync(dlen, 0, 16, s);
     FusedArgs a{};
+    a.max_pins = codec_max_pins();
     a.X = dx;
     a.x_plane_stride = n;
     a.n = n;
@@ -2133,6 +2143,7 @@ int qcs_debug_stride_sumsq(const double* re, const double* im, uint64_t n, doubl
         cudaMemcpy(dx, re, 8 * n, cudaMemcpyHostToDevice);
         cudaMemcpy(dx + n, im, 8 * n, cudaMemcpyHostToDevice);
         FusedArgs a{};
+        a.max_pins = codec_max_pins();
         a.X = dx; a.x_plane_stride = n; a.n = n; a.snap = 0; a.out = dout; a.cap = pcap;
         a.side = dside; a.nsub = nsub; a.out_len = dlen; a.sumsq = dsum; a.cp = make_params(0.0);
         rc = launch_fused(a, FM_RAW2, 1, 0);

@@ -83,6 +83,8 @@ struct FusedArgs {
     // ---- encoder ----
     uint64_t n;                   // elements per plane (stride length)
     const uint8_t* pending;       // per slot (null = all)
+    int max_pins;                 // pinned steps per plane-iteration before the
+                                  // lane-serial fallback (<= MAXPIN)
     uint64_t slot_base;           // first slot of this launch (tables are global,
                                   // out / side / X buffers are launch-local)
     int snap;
@@ -662,7 +664,7 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
                 f = LLONG_MAX;
                 for (int w = pl * WPL; w < pl * WPL + WPL; ++w) f = min(f, S.wfail[w]);
                 if (fail != LLONG_MAX && fail == f) S.fail_prev[pl] = fprev;
-                const bool more = f != LLONG_MAX && S.npin[pl] < MAXPIN;
+                const bool more = f != LLONG_MAX && S.npin[pl] < a.max_pins;
                 if (!__syncthreads_or(more)) break;
                 if (lane == 0 && more) {
                     double P = S.fail_prev[pl];
@@ -737,18 +739,93 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
                     }
                     S.exitP[tid] = Pprev;
                 }
-                __syncthreads();
-                if (lane == 0 && fser != LLONG_MAX) {
-                    if (a.counters) atomicAdd(&a.counters[3], 1ull);
-                    const int k0 = (int)(fser - (long long)base);
-                    double P = S.fail_prev[pl];
-                    for (int k = k0; k < n_it; ++k) {
-                        if ((k & (SUB - 1)) == 0) S.entryP[pl * LPL + k / SUB] = P;
-                        const int32_t c = ref_step(cp, P, xrow<LPL>(xs, pl, k));
-                        code[pl * ITP + k] = c == WCODE ? WCODE16 : (int16_t)c;
-                        xrow<LPL>(xs, pl, k) = P;
+                // Pins exhausted at fser (a plane-iteration the speculation keeps
+                // missing): finish it from the exact predictor at fser with
+                // lane-serial reference chains from guessed lane entries,
+                // verified against the left neighbour's exit and repaired.
+                if (__syncthreads_or(fser != LLONG_MAX)) {
+                    const bool fb = fser != LLONG_MAX;
+                    const double P0 = fb ? S.fail_prev[pl] : 0.0;
+                    const bool act = fb && cnt > 0 && (long long)e0 + cnt > fser;
+                    const bool head = act && (long long)e0 <= fser;
+                    const int is = head ? (int)(fser - (long long)e0) : 0;
+                    if (fb && lane == 0 && a.counters) atomicAdd(&a.counters[3], 1ull);
+                    double entry = P0;
+                    if (act && !head)
+                        entry = anchored_guess(cp, P0, xrow<LPL>(xs, pl, lane * SUB - 2), xrow<LPL>(xs, pl, lane * SUB - 1));
+                    if (act && !head) S.entryP[tid] = entry;
+                    if (act) {
+                        double P = entry;
+                        for (int i = is; i < cnt; ++i) {
+                            const int32_t c = ref_step(cp, P, xl[i]);
+                            cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
+                        }
+                        S.exitP[tid] = P;
                     }
-                    S.exitP[pl * LPL + active - 1] = P;
+                    __syncthreads();
+                    for (int pass = 0; pass < 4; ++pass) {
+                        const bool bad = act && !head && !same_bits(S.entryP[tid], S.exitP[tid - 1]);
+                        const double want = bad ? S.exitP[tid - 1] : 0.0;
+                        if (!__syncthreads_or(bad)) break;
+                        if (bad) {
+                            if (a.counters) atomicAdd(&a.counters[0], 1ull);
+                            double Pn = want, Po = S.entryP[tid];
+                            bool resync = false;
+                            for (int i = 0; i < cnt; ++i) {
+                                const double x = xl[i];
+                                const int16_t co = cl[i];
+                                if (co == WCODE16) Po = x;
+                                else if (co != 0) Po = __dadd_rn(Po, __dmul_rn(cp.td, (double)co));
+                                const int32_t c = ref_step(cp, Pn, x);
+                                cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
+                                if (same_bits(Pn, Po)) {
+                                    resync = true;
+                                    break;
+                                }
+                            }
+                            S.entryP[tid] = want;
+                            if (!resync) S.exitP[tid] = Pn;
+                        }
+                        __syncthreads();
+                    }
+                    if (fb && lane == 0 && active > 0) {
+                        const int hl = (int)((fser - (long long)base) / SUB);  // head lane
+                        for (int l = hl + 1; l < active; ++l) {
+                            const int id = pl * LPL + l;
+                            const double want = S.exitP[id - 1];
+                            if (same_bits(want, S.entryP[id])) continue;
+                            if (a.counters) atomicAdd(&a.counters[0], 1ull);
+                            double Pn = want, Po = S.entryP[id];
+                            S.entryP[id] = want;
+                            const int c2 = (int)umin64(SUB, n - (base + (uint64_t)l * SUB));
+                            const double* xl2 = xs + id * XS_STRIDE;
+                            int16_t* cl2 = code + pl * ITP + l * SUB;
+                            bool resync = false;
+                            for (int i = 0; i < c2; ++i) {
+                                const double x = xl2[i];
+                                const int16_t co = cl2[i];
+                                if (co == WCODE16) Po = x;
+                                else if (co != 0) Po = __dadd_rn(Po, __dmul_rn(cp.td, (double)co));
+                                const int32_t c = ref_step(cp, Pn, x);
+                                cl2[i] = c == WCODE ? WCODE16 : (int16_t)c;
+                                if (same_bits(Pn, Po)) {
+                                    resync = true;
+                                    break;
+                                }
+                            }
+                            if (!resync) S.exitP[id] = Pn;
+                        }
+                    }
+                    __syncthreads();
+                    if (act) {  // reconstructed predictors from the codes
+                        double P = head ? P0 : S.entryP[tid];
+                        for (int i = is; i < cnt; ++i) {
+                            const int16_t co = cl[i];
+                            if (co == WCODE16) P = xl[i];
+                            else if (co != 0) P = __dadd_rn(P, __dmul_rn(cp.td, (double)co));
+                            xl[i] = P;
+                        }
+                    }
                 }
                 if (lane == 0 && active > 0) C.Pnext = S.exitP[pl * LPL + active - 1];
                 __syncthreads();

@@ -85,3 +85,15 @@ def test_codec_errors(q):
     with pytest.raises(q.CodecError) as e:
         q.decompress(bytes(bad), 100)
     assert e.value.kind == "bad_value"
+
+
+@pytest.mark.parametrize("max_pins", [0, 2])
+def test_codec_fuzz_lane_serial_fallback(q, oracle, monkeypatch, max_pins):
+    """The codec with the pin budget capped (QCS_MAX_PINS): misses go to the
+    lane-serial fallback right away; bytes must not change."""
+    monkeypatch.setenv("QCS_MAX_PINS", str(max_pins))
+    for n in (33, 4097, 50000):
+        rng = np.random.default_rng(1000 + n)
+        for x in _planes(rng, n):
+            for d in (2.0 ** -20, 2.0 ** -12):
+                assert q.compress(x, d) == oracle.compress(x, d), (n, d)

@@ -122,3 +122,17 @@ def test_degenerate_wipe_stays_finite(q):
     a = r.state.to_amplitudes()
     assert np.all(np.isfinite(a))
     assert float(np.sum(np.abs(a) ** 2)) == 0.0
+
+
+@pytest.mark.parametrize("max_pins", [0, 1, 3])
+@pytest.mark.parametrize("kind,n,s,basis,ladder,theta", [c for c in CASES if c[0] != "grid"][:5])
+def test_engine_lane_serial_fallback(q, oracle, monkeypatch, max_pins, kind, n, s, basis, ladder, theta):
+    """QCS_MAX_PINS caps the pinned steps per plane-iteration, so the
+    lane-serial fallback (guessed lane entries, verified and repaired)
+    finishes every iteration the speculation misses — still bit-exact."""
+    monkeypatch.setenv("QCS_MAX_PINS", str(max_pins))
+    prog = _prog(kind, n)
+    st, want = oracle_run(oracle, prog, s, basis, ladder, theta)
+    res, got = gpu_run(prog, s, basis, ladder, theta)
+    assert got == want, first_diff(want, got)
+    assert res.state.to_amplitudes().tobytes() == st.amplitudes().tobytes()
