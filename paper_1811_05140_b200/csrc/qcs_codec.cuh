@@ -87,7 +87,7 @@ struct PlaneCarry {
     uint64_t mv_shift;
 };
 
-constexpr int MAXPIN = 8;  // pinned exact steps per plane and iteration (then lane-serial chains)
+constexpr int MAXPIN = 12;  // pinned exact steps per plane and iteration (then lane-serial chains)
 
 struct EncShared {
     double entryP[2][PLANE_LANES];
