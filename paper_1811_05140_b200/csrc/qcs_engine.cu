@@ -706,10 +706,10 @@ int launch_fused_t(const FusedArgs& a, uint64_t grid, cudaStream_t s)
 
 enum { FM_LOCAL = 0, FM_FAR = 1, FM_PAIR = 2, FM_RAW1 = 3, FM_RAW2 = 4 };
 
-int codec_max_pins()
+int codec_max_rounds()
 {
-    const char* e = getenv("QCS_MAX_PINS");
-    return e ? std::max(0, std::min(MAXPIN, atoi(e))) : MAXPIN;
+    const char* e = getenv("QCS_MAX_ROUNDS");
+    return e ? std::max(1, atoi(e)) : 6;
 }
 
 int launch_fused(const FusedArgs& a, int fm, uint64_t grid, cudaStream_t s)
@@ -737,7 +737,8 @@ struct qcs_dev_state {
     uint64_t gen = 0;
     uint64_t launches = 0;
     int split_local = 0;  // QCS_SPLIT_LOCAL=1: in-chunk gates also take the split path
-    int max_pins = MAXPIN;  // QCS_MAX_PINS (tests force the lane-serial fallback)
+    int max_rounds = 6;  // QCS_MAX_ROUNDS (tests force the neighbour-exit repair)
+    unsigned long long* cta_trace = nullptr;  // QCS_CTA_TRACE=1: per-slot phase cycles
     // Large states ("wave mode"): one arena, per-wave staging
     // buffers (slots, side, X) for `wave` slots, per-wave commit placed by the
     // host, in-place compaction through the X buffer.
@@ -1142,7 +1143,8 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             a.n = d.L;
             a.pending = d.pending;
             a.slot_base = s0;
-            a.max_pins = st->max_pins;
+            a.max_rounds = st->max_rounds;
+            a.cta_trace = st->cta_trace;
             a.snap = 1;
             if (fm == FM_RAW2) {  // split path: gated, snapped planes in X
                 a.X = d.X;
@@ -1236,7 +1238,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     qcs_dev_state* st = new qcs_dev_state();
     st->device = device;
     if (const char* e = getenv("QCS_SPLIT_LOCAL")) st->split_local = atoi(e);
-    if (const char* e = getenv("QCS_MAX_PINS")) st->max_pins = std::max(0, std::min(MAXPIN, atoi(e)));
+    if (const char* e = getenv("QCS_MAX_ROUNDS")) st->max_rounds = std::max(1, atoi(e));
     cudaSetDevice(device);
     int rc = 0;
 #define TRY(x)                    \
@@ -1321,6 +1323,8 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     TRY(dalloc(st, &d.partial, 2 * d.NS));
     TRY(dalloc(st, &d.sc, 1));
     TRY(dalloc(st, &d.counters, 16));
+    if (const char* e = getenv("QCS_CTA_TRACE"))
+        if (atoi(e)) TRY(dalloc(st, &st->cta_trace, 8 * d.NS));
     CU(cudaMemset(d.counters, 0, 128));
     TRY(dalloc(st, &st->lt.slot_codec, d.NS));
     TRY(dalloc(st, &st->lt.slot_delta, d.NS));
@@ -2040,7 +2044,7 @@ int qcs_codec_compress(const double* x, uint64_t n, double delta, uint8_t* out, 
     cudaMemcpyAsync(dx, x, 8 * n, cudaMemcpyHostToDevice, s);
     cudaMemsetAsync(dlen, 0, 16, s);
     FusedArgs a{};
-    a.max_pins = codec_max_pins();
+    a.max_rounds = codec_max_rounds();
     a.X = dx;
     a.x_plane_stride = n;
     a.n = n;
@@ -2127,6 +2131,25 @@ int qcs_codec_decompress(const uint8_t* blk, uint64_t len, double* out, uint64_t
 
 // Test hook: lossless-encode a (re, im) stride pair and return the stored
 // sum of squares the engine would record (StrideBuffer::sum_sq, core.cpp:30-37).
+// Test/diagnostic hook (not in the public header): per-slot phase cycles of
+// the last encoder launch when QCS_CTA_TRACE=1.
+int qcs_debug_cta_trace(qcs_dev_state_t st, uint64_t* out, uint64_t n_slots)
+{
+    if (!st || !st->cta_trace) return set_err(QCS_E_INVALID, "trace off");
+    CU(cudaStreamSynchronize(st->stream));
+    CU(cudaMemcpy(out, st->cta_trace, 8 * 8 * std::min<uint64_t>(n_slots, st->d.NS), cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+// Diagnostic hook: the split path's uncompressed encoder input of a slot.
+int qcs_debug_read_x(qcs_dev_state_t st, uint64_t slot, double* out)
+{
+    if (!st || slot >= st->wave) return set_err(QCS_E_INVALID, "bad slot");
+    CU(cudaStreamSynchronize(st->stream));
+    CU(cudaMemcpy(out, st->d.X + 2 * slot * st->d.L, 16 * st->d.L, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
 int qcs_debug_stride_sumsq(const double* re, const double* im, uint64_t n, double* out)
 {
     const uint64_t nsub = (n + SUB - 1) / SUB, pcap = payload_cap(n);
@@ -2143,7 +2166,7 @@ int qcs_debug_stride_sumsq(const double* re, const double* im, uint64_t n, doubl
         cudaMemcpy(dx, re, 8 * n, cudaMemcpyHostToDevice);
         cudaMemcpy(dx + n, im, 8 * n, cudaMemcpyHostToDevice);
         FusedArgs a{};
-        a.max_pins = codec_max_pins();
+        a.max_rounds = codec_max_rounds();
         a.X = dx; a.x_plane_stride = n; a.n = n; a.snap = 0; a.out = dout; a.cap = pcap;
         a.side = dside; a.nsub = nsub; a.out_len = dlen; a.sumsq = dsum; a.cp = make_params(0.0);
         rc = launch_fused(a, FM_RAW2, 1, 0);

@@ -83,8 +83,7 @@ struct FusedArgs {
     // ---- encoder ----
     uint64_t n;                   // elements per plane (stride length)
     const uint8_t* pending;       // per slot (null = all)
-    int max_pins;                 // pinned steps per plane-iteration before the
-                                  // lane-serial fallback (<= MAXPIN)
+    int max_rounds;               // event rounds before the neighbour-exit repair (>= 1)
     uint64_t slot_base;           // first slot of this launch (tables are global,
                                   // out / side / X buffers are launch-local)
     int snap;
@@ -96,6 +95,7 @@ struct FusedArgs {
     double* sumsq;
     CodecParams cp;
     unsigned long long* counters;
+    unsigned long long* cta_trace;  // debug: [global slot][8] phase cycles (null = off)
 };
 
 template <int LPL>
@@ -328,6 +328,101 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FusedShared& S
     }
 }
 
+// The reference chain (LossyEmitter, codec.cpp:153-250) over one lane's c
+// elements from predictor Pin: writes the codes, returns the exit predictor
+// and the lane's last event (ev_i lane-relative, -1 none; ev_v the predictor
+// it set).  For a power-of-two bound a step is PROVEN equal to the reference
+// step when, with P = A + 2d*Mprev exactly on the anchor's lattice,
+// y = (x-A)/2d has |y| < 2^30, its fractional part is >= 2^-19 away from a
+// half and |rint(y) - Mprev| <= 32766 (see lattice_step_m); GRP such steps run
+// as a group with independent arithmetic.  Any other step is the reference
+// step itself and an event (the anchor moves to its predictor).
+// resync: a repair run from the left neighbour's exit; the old codes (from
+// entry Pold) give the old chain, and once the new predictor equals the old
+// one the rest of the lane is unchanged (synced).
+__device__ __forceinline__ double lane_chain(const CodecParams& cp, const double* xr, int16_t* cr, int c, double Pin,
+                                             bool resync, double Pold, bool& synced, long long& ev_i, double& ev_v)
+{
+    double P = Pin, A = Pin, Mprev = 0.0, Po = Pold;
+    synced = false;
+    ev_i = -1;
+    ev_v = 0.0;
+    for (int i0 = 0; i0 < c; i0 += GRP) {
+        if (cp.pow2 && !resync) {
+            double Mv[GRP], Pv[GRP];
+            bool ok = true;
+#pragma unroll
+            for (int k = 0; k < GRP; ++k) {
+                const double x = xr[i0 + k];  // rows are padded: i0 + k < 32
+                const double y = __dmul_rn(__dsub_rn(x, A), cp.inv_td);
+                const double M = rint(y);
+                const double fr = fabs(__dsub_rn(y, M));
+                const double yv = __dmul_rn(cp.td, M);
+                const double v = __dadd_rn(A, yv);
+                const double q = __dsub_rn(M, k == 0 ? Mprev : Mv[k - 1]);
+                const bool good = fabs(y) < 1073741824.0 && fr < 0.5 - 1.9073486328125e-06 && fabs(q) <= 32766.0 &&
+                                  add_exact(A, yv, v);
+                ok &= good | (i0 + k >= c);
+                Mv[k] = M;
+                Pv[k] = v;
+            }
+            if (ok) {
+#pragma unroll
+                for (int k = 0; k < GRP; ++k)
+                    if (i0 + k < c) {
+                        cr[i0 + k] = (int16_t)__dsub_rn(Mv[k], k == 0 ? Mprev : Mv[k - 1]);
+                        P = Pv[k];
+                        Mprev = Mv[k];
+                    }
+                continue;
+            }
+        }
+        for (int i = i0; i < i0 + GRP && i < c; ++i) {
+            const double x = xr[i];
+            if (resync) {  // the old chain's predictor after this element
+                const int16_t co = cr[i];
+                if (co == WCODE16) Po = x;
+                else if (co != 0) Po = __dadd_rn(Po, __dmul_rn(cp.td, (double)co));
+            }
+            bool done = false;
+            if (cp.pow2) {
+                const double y = __dmul_rn(__dsub_rn(x, A), cp.inv_td);
+                const double M = rint(y);
+                const double fr = fabs(__dsub_rn(y, M));
+                const double q = __dsub_rn(M, Mprev);
+                if (fabs(y) < 1073741824.0 && fr < 0.5 - 1.9073486328125e-06 && fabs(q) <= 32766.0) {
+                    const double yv = __dmul_rn(cp.td, M);
+                    const double v = __dadd_rn(A, yv);
+                    cr[i] = (int16_t)q;
+                    P = v;
+                    if (add_exact(A, yv, v)) {
+                        Mprev = M;
+                    } else {  // the chain rounds here: re-anchor
+                        A = v;
+                        Mprev = 0.0;
+                        ev_i = i;
+                        ev_v = v;
+                    }
+                    done = true;
+                }
+            }
+            if (!done) {
+                const int32_t k = ref_step(cp, P, x);
+                cr[i] = k == WCODE ? WCODE16 : (int16_t)k;
+                A = P;  // re-anchor at the reference predictor
+                Mprev = 0.0;
+                ev_i = i;
+                ev_v = P;
+            }
+            if (resync && same_bits(P, Po)) {
+                synced = true;
+                return P;
+            }
+        }
+    }
+    return P;
+}
+
 // Per-phase cycle accounting (thread 0 of each CTA) into counters[8..15].
 #define QCS_PHASE(id)                                                        \
     do {                                                                     \
@@ -495,417 +590,98 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
 
         QCS_PHASE(0);
         // 2-4. codes and exact predictors
-        if (LOSSY && cp.pow2) {
-            // event rounds (see qcs_codec.cuh k_encode for the argument)
-            if (lane == 0) S.npin[pl] = 0;
+        if (LOSSY) {
+            // Self-correcting event rounds.  Every lane runs the
+            // reference chain from an entry predictor derived from the last
+            // EVENT before it (an escape, a rounding re-anchor or any step the
+            // lattice test could not prove — the anchors the chain's predictor
+            // is exactly defined by).  Round 0 uses predicted escapes as events;
+            // later rounds the events the lanes' chains actually produced, and
+            // only lanes whose entry changes re-run.  The chain is exact when
+            // its entry is, so when every lane's entry equals its left
+            // neighbour's exit the iteration is the reference's.  By induction
+            // each round fixes at least the first wrong lane; after max_rounds
+            // the remaining lanes are repaired from their neighbours' exits.
             if (cnt > 0 && lane + 1 == active) C.xprev_next = xl[cnt - 1];
             const double x_left = cnt > 0 ? (lane == 0 ? C.xprev : xrow<LPL>(xs, pl, lane * SUB - 1)) : 0.0;
-            // predicted escapes of this lane, once (bit i = element i)
-            uint32_t emask = 0;
+            long long ev_idx = -1;  // this lane's last event (absolute index)
+            double ev_val = 0.0;
             {
                 double xp = x_left;
                 for (int i = 0; i < cnt; ++i) {
                     const double x = xl[i];
-                    emask |= (uint32_t)predict_escape(cp, x, xp) << i;
+                    if (predict_escape(cp, x, xp)) {
+                        ev_idx = (long long)e0 + i;
+                        ev_val = x;
+                    }
                     xp = x;
                 }
             }
-            __syncthreads();
-            long long f = LLONG_MAX;
-            long long aidx = -1;
-            double aval = 0.0;
+            double used = __longlong_as_double(0x7ff8000000000000ll);  // entry of the last run
             for (int round = 0;; ++round) {
-                const int np = S.npin[pl];
-                // (a) last event of the lane: last predicted escape or pin
-                long long my_last = emask ? (long long)e0 + (31 - __clz(emask)) : -1;
-                double my_val = my_last >= 0 ? xl[my_last - (long long)e0] : 0.0;
-                for (int q = 0; q < np; ++q) {
-                    const long long k = S.pin_idx[pl][q];
-                    if (k >= (long long)e0 && k < (long long)e0 + cnt && k >= my_last) {
-                        my_last = k;
-                        my_val = S.pin_val[pl][q];
-                    }
-                }
-                if (cnt == 0) my_last = -1;
-                aidx = fscan_last<WPL>(my_last, my_val, S, pl, aval);
-                // (b) speculate and verify every element
-                long long fail = LLONG_MAX;
-                double fprev = 0.0;
+                double aval = 0.0;
+                const long long aidx = fscan_last<WPL>(cnt > 0 ? ev_idx : -1, ev_val, S, pl, aval);
                 if (cnt > 0) {
-                    double A = aidx >= 0 ? aval : C.P;
+                    const double A = aidx >= 0 ? aval : C.P;
                     const long long Aidx = aidx >= 0 ? aidx : (long long)base - 1;
-                    double Pprev = (Aidx == (long long)e0 - 1) ? A : lattice_point(cp, A, x_left);
-                    if (np == 0) {
-                        // Mprev: lattice index of Pprev relative to A when Pprev is
-                        // known to be exactly A + 2d*Mprev (else NaN => full check)
-                        double Mprev = (Aidx == (long long)e0 - 1) ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
-                        if (Aidx != (long long)e0 - 1) {
-                            double Atmp = A, Mt;
-                            bool sf;
-                            const double v = lattice_step_m(cp, Atmp, x_left, Mt, sf);
-                            if (same_bits(Atmp, A) && same_bits(v, Pprev)) Mprev = Mt;
-                        }
-                        // one element of the chain, in order (the reference's step
-                        // verifies every element the cheap test cannot prove)
-                        auto elem = [&](int i) {
-                            const double x = xl[i];
-                            double Ph, M = 0.0;
-                            bool safe = false;
-                            if ((emask >> i) & 1u) {
-                                Ph = x;
-                                A = x;
-                            } else {
-                                const double A0 = A;
-                                Ph = lattice_step_m(cp, A, x, M, safe);
-                                const double q = __dsub_rn(M, Mprev);  // NaN if Mprev unknown
-                                safe = safe && fabs(q) <= 32766.0;
-                                if (safe) cl[i] = (int16_t)q;
-                                if (!same_bits(A, A0)) M = 0.0;  // re-anchored at Ph
-                            }
-                            if (!safe) {
-                                double P2 = Pprev;
-                                const int32_t c = ref_step(cp, P2, x);
-                                cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
-                                if (!same_bits(P2, Ph) && fail == LLONG_MAX) {
-                                    fail = (long long)e0 + i;
-                                    fprev = Pprev;
-                                }
-                            }
-                            Mprev = ((emask >> i) & 1u) ? 0.0 : M;
-                            Pprev = Ph;
-                        };
-                        // groups of GRP elements: anchors move only at escapes unless
-                        // the chain rounds, so the lattice steps of a group are
-                        // independent (ILP); a rounding event replays the group in order
-                        for (int i0 = 0; i0 < cnt; i0 += GRP) {
-                            double Mv[GRP], Pv[GRP];
-                            uint32_t sf = 0;
-                            bool rnd = false;
-                            double a = A;
-#pragma unroll
-                            for (int k = 0; k < GRP; ++k) {
-                                const int i = i0 + k;
-                                const double x = xl[i];  // rows are padded: i < 32 always
-                                const bool esc = (emask >> i) & 1u;
-                                a = esc ? x : a;
-                                bool sk, rk = false;
-                                const double v = lattice_try(cp, a, x, Mv[k], sk, rk);
-                                Pv[k] = esc ? x : v;
-                                rnd |= rk & !esc & (i < cnt);
-                                sf |= (uint32_t)(sk & !esc) << k;
-                            }
-                            if (rnd) {
-                                for (int k = 0; k < GRP && i0 + k < cnt; ++k) elem(i0 + k);
-                                continue;
-                            }
-#pragma unroll
-                            for (int k = 0; k < GRP; ++k) {
-                                const int i = i0 + k;
-                                if (i < cnt) {
-                                    const bool esc = (emask >> i) & 1u;
-                                    bool safe = false;
-                                    if (!esc) {
-                                        const double q = __dsub_rn(Mv[k], Mprev);
-                                        safe = ((sf >> k) & 1u) && fabs(q) <= 32766.0;
-                                        if (safe) cl[i] = (int16_t)q;
-                                    }
-                                    if (!safe) {
-                                        const double x = xl[i];
-                                        double P2 = Pprev;
-                                        const int32_t c = ref_step(cp, P2, x);
-                                        cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
-                                        if (!same_bits(P2, Pv[k]) && fail == LLONG_MAX) {
-                                            fail = (long long)e0 + i;
-                                            fprev = Pprev;
-                                        }
-                                    }
-                                    Mprev = esc ? 0.0 : Mv[k];
-                                    Pprev = Pv[k];
-                                }
-                            }
-                            A = a;
-                        }
-                    } else {
-                        int pp = 0;
-                        while (pp < np && S.pin_idx[pl][pp] < (long long)e0) ++pp;
-                        for (int i = 0; i < cnt; ++i) {
-                            const double x = xl[i];
-                            double Ph;
-                            int16_t c16;
-                            if (pp < np && S.pin_idx[pl][pp] == (long long)e0 + i) {
-                                Ph = S.pin_val[pl][pp];
-                                c16 = S.pin_code[pl][pp];
-                                A = Ph;
-                                ++pp;
-                            } else {
-                                if ((emask >> i) & 1u) {
-                                    Ph = x;
-                                    A = x;
-                                } else {
-                                    Ph = lattice_step(cp, A, x);
-                                }
-                                double P2 = Pprev;
-                                const int32_t c = ref_step(cp, P2, x);
-                                c16 = c == WCODE ? WCODE16 : (int16_t)c;
-                                if (!same_bits(P2, Ph) && fail == LLONG_MAX) {
-                                    fail = (long long)e0 + i;
-                                    fprev = Pprev;
-                                }
-                            }
-                            cl[i] = c16;
-                            Pprev = Ph;
-                        }
-                    }
-                }
-                long long mm = fail;
-                for (int o = 16; o; o >>= 1) mm = min(mm, __shfl_xor_sync(0xffffffffu, mm, o));
-                if ((tid & 31) == 0) S.wfail[tid >> 5] = mm;
-                __syncthreads();
-                f = LLONG_MAX;
-                for (int w = pl * WPL; w < pl * WPL + WPL; ++w) f = min(f, S.wfail[w]);
-                if (fail != LLONG_MAX && fail == f) S.fail_prev[pl] = fprev;
-                const bool more = f != LLONG_MAX && S.npin[pl] < a.max_pins;
-                if (!__syncthreads_or(more)) break;
-                if (lane == 0 && more) {
-                    double P = S.fail_prev[pl];
-                    const int32_t c = ref_step(cp, P, xrow<LPL>(xs, pl, (int)(f - (long long)base)));
-                    const int q = S.npin[pl];
-                    S.pin_idx[pl][q] = f;
-                    S.pin_val[pl][q] = P;
-                    S.pin_code[pl][q] = c == WCODE ? WCODE16 : (int16_t)c;
-                    S.npin[pl] = q + 1;
-                    if (a.counters) atomicAdd(&a.counters[0], 1ull);
-                }
-                __syncthreads();
-            }
-            const long long fser = f;
-            QCS_PHASE(1);
-            // final predictors into xs (events of the last round still hold)
-            {
-                const int np = S.npin[pl];
-                if (cnt > 0) {
-                    double A = aidx >= 0 ? aval : C.P;
-                    const long long Aidx = aidx >= 0 ? aidx : (long long)base - 1;
-                    double Pprev = (Aidx == (long long)e0 - 1) ? A : lattice_point(cp, A, x_left);
-                    S.entryP[tid] = Pprev;
-                    int pp = 0;
-                    while (pp < np && S.pin_idx[pl][pp] < (long long)e0) ++pp;
-                    auto fin = [&](int i) {
-                        const long long k = (long long)e0 + i;
-                        const double x = xl[i];
-                        double Ph;
-                        if (pp < np && S.pin_idx[pl][pp] == k) {
-                            Ph = S.pin_val[pl][pp];
-                            A = Ph;
-                            ++pp;
-                        } else if ((emask >> i) & 1u) {
-                            Ph = x;
-                            A = x;
+                    const double entry = (Aidx == (long long)e0 - 1) ? A : lattice_point(cp, A, x_left);
+                    if (!same_bits(entry, used)) {
+                        used = entry;
+                        bool sy;
+                        long long li = -1;
+                        double lv = 0.0;
+                        S.exitP[tid] = lane_chain(cp, xl, cl, cnt, entry, false, 0.0, sy, li, lv);
+                        if (li >= 0) {
+                            ev_idx = (long long)e0 + li;
+                            ev_val = lv;
                         } else {
-                            Ph = lattice_step(cp, A, x);
+                            ev_idx = -1;
                         }
-                        xl[i] = Ph;
-                        Pprev = Ph;
-                    };
-                    const int lim = fser <= (long long)e0 ? 0 : (int)min((long long)cnt, fser - (long long)e0);
-                    for (int i0 = 0; i0 < lim; i0 += GRP) {
-                        const bool pin_here = pp < np && S.pin_idx[pl][pp] < (long long)e0 + i0 + GRP;
-                        if (pin_here || i0 + GRP > lim) {
-                            for (int k = 0; k < GRP && i0 + k < lim; ++k) fin(i0 + k);
-                            continue;
-                        }
-                        double Pv[GRP], Mv[GRP];
-                        bool rnd = false;
-                        double a = A;
-#pragma unroll
-                        for (int k = 0; k < GRP; ++k) {
-                            const int i = i0 + k;
-                            const double x = xl[i];
-                            const bool esc = (emask >> i) & 1u;
-                            a = esc ? x : a;
-                            bool sk, rk = false;
-                            const double v = lattice_try(cp, a, x, Mv[k], sk, rk);
-                            Pv[k] = esc ? x : v;
-                            rnd |= rk & !esc;
-                        }
-                        if (rnd) {
-                            for (int k = 0; k < GRP; ++k) fin(i0 + k);
-                            continue;
-                        }
-#pragma unroll
-                        for (int k = 0; k < GRP; ++k) xl[i0 + k] = Pv[k];
-                        A = a;
-                        Pprev = Pv[GRP - 1];
                     }
-                    S.exitP[tid] = Pprev;
+                    S.entryP[tid] = used;
                 }
-                // Pins exhausted at fser (a plane-iteration the speculation keeps
-                // missing): finish it from the exact predictor at fser with
-                // lane-serial reference chains from guessed lane entries,
-                // verified against the left neighbour's exit and repaired.
-                if (__syncthreads_or(fser != LLONG_MAX)) {
-                    const bool fb = fser != LLONG_MAX;
-                    const double P0 = fb ? S.fail_prev[pl] : 0.0;
-                    const bool act = fb && cnt > 0 && (long long)e0 + cnt > fser;
-                    const bool head = act && (long long)e0 <= fser;
-                    const int is = head ? (int)(fser - (long long)e0) : 0;
-                    if (fb && lane == 0 && a.counters) atomicAdd(&a.counters[3], 1ull);
-                    double entry = P0;
-                    if (act && !head)
-                        entry = anchored_guess(cp, P0, xrow<LPL>(xs, pl, lane * SUB - 2), xrow<LPL>(xs, pl, lane * SUB - 1));
-                    if (act && !head) S.entryP[tid] = entry;
-                    if (act) {
-                        double P = entry;
-                        for (int i = is; i < cnt; ++i) {
-                            const int32_t c = ref_step(cp, P, xl[i]);
-                            cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
-                        }
-                        S.exitP[tid] = P;
-                    }
-                    __syncthreads();
-                    for (int pass = 0; pass < 4; ++pass) {
-                        const bool bad = act && !head && !same_bits(S.entryP[tid], S.exitP[tid - 1]);
-                        const double want = bad ? S.exitP[tid - 1] : 0.0;
-                        if (!__syncthreads_or(bad)) break;
-                        if (bad) {
-                            if (a.counters) atomicAdd(&a.counters[0], 1ull);
-                            double Pn = want, Po = S.entryP[tid];
-                            bool resync = false;
-                            for (int i = 0; i < cnt; ++i) {
-                                const double x = xl[i];
-                                const int16_t co = cl[i];
-                                if (co == WCODE16) Po = x;
-                                else if (co != 0) Po = __dadd_rn(Po, __dmul_rn(cp.td, (double)co));
-                                const int32_t c = ref_step(cp, Pn, x);
-                                cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
-                                if (same_bits(Pn, Po)) {
-                                    resync = true;
-                                    break;
-                                }
-                            }
-                            S.entryP[tid] = want;
-                            if (!resync) S.exitP[tid] = Pn;
-                        }
-                        __syncthreads();
-                    }
-                    if (fb && lane == 0 && active > 0) {
-                        const int hl = (int)((fser - (long long)base) / SUB);  // head lane
-                        for (int l = hl + 1; l < active; ++l) {
-                            const int id = pl * LPL + l;
-                            const double want = S.exitP[id - 1];
-                            if (same_bits(want, S.entryP[id])) continue;
-                            if (a.counters) atomicAdd(&a.counters[0], 1ull);
-                            double Pn = want, Po = S.entryP[id];
-                            S.entryP[id] = want;
-                            const int c2 = (int)umin64(SUB, n - (base + (uint64_t)l * SUB));
-                            const double* xl2 = xs + id * XS_STRIDE;
-                            int16_t* cl2 = code + pl * ITP + l * SUB;
-                            bool resync = false;
-                            for (int i = 0; i < c2; ++i) {
-                                const double x = xl2[i];
-                                const int16_t co = cl2[i];
-                                if (co == WCODE16) Po = x;
-                                else if (co != 0) Po = __dadd_rn(Po, __dmul_rn(cp.td, (double)co));
-                                const int32_t c = ref_step(cp, Pn, x);
-                                cl2[i] = c == WCODE ? WCODE16 : (int16_t)c;
-                                if (same_bits(Pn, Po)) {
-                                    resync = true;
-                                    break;
-                                }
-                            }
-                            if (!resync) S.exitP[id] = Pn;
-                        }
-                    }
-                    __syncthreads();
-                    if (act) {  // reconstructed predictors from the codes
-                        double P = head ? P0 : S.entryP[tid];
-                        for (int i = is; i < cnt; ++i) {
-                            const int16_t co = cl[i];
-                            if (co == WCODE16) P = xl[i];
-                            else if (co != 0) P = __dadd_rn(P, __dmul_rn(cp.td, (double)co));
-                            xl[i] = P;
-                        }
-                    }
-                }
-                if (lane == 0 && active > 0) C.Pnext = S.exitP[pl * LPL + active - 1];
                 __syncthreads();
-            }
-        } else if (LOSSY) {
-            // other bounds: lane-serial reference chains from guessed entries,
-            // verified against the left neighbour's exit and repaired
-            double entry = 0.0;
-            if (cnt > 0) {
-                if (lane + 1 == active) C.xprev_next = xl[cnt - 1];
-                entry = lane == 0 ? C.P
-                                  : anchored_guess(cp, C.P, xrow<LPL>(xs, pl, lane * SUB - 2),
-                                                   xrow<LPL>(xs, pl, lane * SUB - 1));
-                S.entryP[tid] = entry;
-            }
-            __syncthreads();
-            if (cnt > 0) {
-                double P = entry;
-                for (int i = 0; i < cnt; ++i) {
-                    const int32_t c = ref_step(cp, P, xl[i]);
-                    cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
-                }
-                S.exitP[tid] = P;
-            }
-            __syncthreads();
-            for (int pass = 0; pass < 4; ++pass) {
                 const bool bad = cnt > 0 && lane > 0 && !same_bits(S.entryP[tid], S.exitP[tid - 1]);
-                const double want = bad ? S.exitP[tid - 1] : 0.0;
                 if (!__syncthreads_or(bad)) break;
-                if (bad) {
-                    if (a.counters) atomicAdd(&a.counters[0], 1ull);
-                    double Pn = want, Po = S.entryP[tid];
-                    bool resync = false;
-                    for (int i = 0; i < cnt; ++i) {
-                        const double x = xl[i];
-                        const int16_t co = cl[i];
-                        if (co == WCODE16) Po = x;
-                        else if (co != 0) Po = __dadd_rn(Po, __dmul_rn(cp.td, (double)co));
-                        const int32_t c = ref_step(cp, Pn, x);
-                        cl[i] = c == WCODE ? WCODE16 : (int16_t)c;
-                        if (same_bits(Pn, Po)) {
-                            resync = true;
-                            break;
-                        }
+                if (bad && a.counters) atomicAdd(&a.counters[0], 1ull);
+                if (round + 1 < a.max_rounds) continue;
+                // repair from the neighbours' exits (parallel passes, then in order)
+                for (int pass = 0; pass < 4; ++pass) {
+                    const bool bad2 = cnt > 0 && lane > 0 && !same_bits(S.entryP[tid], S.exitP[tid - 1]);
+                    const double want = bad2 ? S.exitP[tid - 1] : 0.0;
+                    if (!__syncthreads_or(bad2)) break;
+                    if (bad2) {
+                        bool sy;
+                        long long li;
+                        double lv;
+                        const double Pn = lane_chain(cp, xl, cl, cnt, want, true, S.entryP[tid], sy, li, lv);
+                        S.entryP[tid] = want;
+                        if (!sy) S.exitP[tid] = Pn;
                     }
-                    S.entryP[tid] = want;
-                    if (!resync) S.exitP[tid] = Pn;
+                    __syncthreads();
+                }
+                if (lane == 0 && active > 0) {
+                    for (int l = 1; l < active; ++l) {
+                        const int id = pl * LPL + l;
+                        const double want = S.exitP[id - 1];
+                        if (same_bits(want, S.entryP[id])) continue;
+                        if (a.counters) atomicAdd(&a.counters[3], 1ull);
+                        const int c2 = (int)umin64(SUB, n - (base + (uint64_t)l * SUB));
+                        bool sy;
+                        long long li;
+                        double lv;
+                        const double Pn = lane_chain(cp, xs + id * XS_STRIDE, code + pl * ITP + l * SUB, c2, want, true,
+                                                     S.entryP[id], sy, li, lv);
+                        S.entryP[id] = want;
+                        if (!sy) S.exitP[id] = Pn;
+                    }
                 }
                 __syncthreads();
+                break;
             }
-            if (lane == 0 && active > 0) {
-                for (int l = 1; l < active; ++l) {
-                    const int id = pl * LPL + l;
-                    const double want = S.exitP[id - 1];
-                    if (same_bits(want, S.entryP[id])) continue;
-                    if (a.counters) atomicAdd(&a.counters[0], 1ull);
-                    double Pn = want, Po = S.entryP[id];
-                    S.entryP[id] = want;
-                    const int c2 = (int)umin64(SUB, n - (base + (uint64_t)l * SUB));
-                    const double* xl2 = xs + id * XS_STRIDE;
-                    int16_t* cl2 = code + pl * ITP + l * SUB;
-                    bool resync = false;
-                    for (int i = 0; i < c2; ++i) {
-                        const double x = xl2[i];
-                        const int16_t co = cl2[i];
-                        if (co == WCODE16) Po = x;
-                        else if (co != 0) Po = __dadd_rn(Po, __dmul_rn(cp.td, (double)co));
-                        const int32_t c = ref_step(cp, Pn, x);
-                        cl2[i] = c == WCODE ? WCODE16 : (int16_t)c;
-                        if (same_bits(Pn, Po)) {
-                            resync = true;
-                            break;
-                        }
-                    }
-                    if (!resync) S.exitP[id] = Pn;
-                }
-                C.Pnext = S.exitP[pl * LPL + active - 1];
-            }
-            __syncthreads();
-            if (cnt > 0) {
+            QCS_PHASE(1);
+            if (lane == 0 && active > 0) C.Pnext = S.exitP[pl * LPL + active - 1];
+            if (cnt > 0) {  // the reference's reconstructed predictors from the codes
                 double P = S.entryP[tid];
                 for (int i = 0; i < cnt; ++i) {
                     const int16_t co = cl[i];
@@ -1125,6 +901,8 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
     QCS_PHASE(6);
     if (tid == 0 && a.counters)
         for (int i = 0; i < 8; ++i) atomicAdd(&a.counters[8 + i], ph_acc[i]);
+    if (tid == 0 && a.cta_trace)
+        for (int i = 0; i < 8; ++i) a.cta_trace[8 * (a.slot_base + (uint64_t)b) + i] = ph_acc[i];
     if (lane == 0) a.out_len[2 * gslot + comp] = C.out_pos;
     if (a.sumsq && (tid % (2 * LPL)) == 0)
         a.sumsq[a.slot_base + (MODE == MODE_PAIR ? 2ull * b + tid / (2 * LPL) : (uint64_t)b)] =

@@ -87,11 +87,11 @@ def test_codec_errors(q):
     assert e.value.kind == "bad_value"
 
 
-@pytest.mark.parametrize("max_pins", [0, 2])
-def test_codec_fuzz_lane_serial_fallback(q, oracle, monkeypatch, max_pins):
-    """The codec with the pin budget capped (QCS_MAX_PINS): misses go to the
-    lane-serial fallback right away; bytes must not change."""
-    monkeypatch.setenv("QCS_MAX_PINS", str(max_pins))
+@pytest.mark.parametrize("max_rounds", [1, 2])
+def test_codec_fuzz_neighbour_repair(q, oracle, monkeypatch, max_rounds):
+    """The codec with the event rounds capped (QCS_MAX_ROUNDS): misses go to
+    the neighbour-exit repair right away; bytes must not change."""
+    monkeypatch.setenv("QCS_MAX_ROUNDS", str(max_rounds))
     for n in (33, 4097, 50000):
         rng = np.random.default_rng(1000 + n)
         for x in _planes(rng, n):

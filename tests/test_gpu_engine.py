@@ -124,13 +124,13 @@ def test_degenerate_wipe_stays_finite(q):
     assert float(np.sum(np.abs(a) ** 2)) == 0.0
 
 
-@pytest.mark.parametrize("max_pins", [0, 1, 3])
+@pytest.mark.parametrize("max_rounds", [1, 2])
 @pytest.mark.parametrize("kind,n,s,basis,ladder,theta", [c for c in CASES if c[0] != "grid"][:5])
-def test_engine_lane_serial_fallback(q, oracle, monkeypatch, max_pins, kind, n, s, basis, ladder, theta):
-    """QCS_MAX_PINS caps the pinned steps per plane-iteration, so the
-    lane-serial fallback (guessed lane entries, verified and repaired)
-    finishes every iteration the speculation misses — still bit-exact."""
-    monkeypatch.setenv("QCS_MAX_PINS", str(max_pins))
+def test_engine_neighbour_repair(q, oracle, monkeypatch, max_rounds, kind, n, s, basis, ladder, theta):
+    """QCS_MAX_ROUNDS caps the event rounds, so every lane still inconsistent
+    after them is repaired from its left neighbour's exit (parallel passes,
+    then in order) — still bit-exact."""
+    monkeypatch.setenv("QCS_MAX_ROUNDS", str(max_rounds))
     prog = _prog(kind, n)
     st, want = oracle_run(oracle, prog, s, basis, ladder, theta)
     res, got = gpu_run(prog, s, basis, ladder, theta)
