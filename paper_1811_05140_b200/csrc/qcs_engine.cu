@@ -2,18 +2,21 @@
 // + the C-ABI declared in include/qcs_b200.h.
 //
 // Per gate (CompressedState::apply_gate, aalc.cpp:261-420):
-//   k_make_jobs   unit list of make_stride_plan (gate.cpp:313-403), on device
-//   k_decode      decompress_into + scale (aalc.cpp:176-189), lane per sub-chunk
+//   k_make_jobs     unit list of make_stride_plan (gate.cpp:313-403), on device
 //   [k_stride_partial, k_mean]  reflect_mean's mean pass (aalc.cpp:270-295)
-//   k_gate        run_plan_unit (gate.cpp:405-454), FMA-free apply_pair order
-//   per ladder level: k_encode (snap + compress + stored sum_sq) and
-//                     k_ladder (compress_stride_adaptive / joint pair ladder,
-//                     aalc.cpp:117-138, 337-356)
-//   k_commit_plan / k_commit_copy  staged commit into the block arena
-//   k_norm        lazy renormalisation + GateRecord (aalc.cpp:410-419, 612-631)
-// All launches are stream-ordered; the host only synchronises at API
-// boundaries.  A device error word makes every later kernel a no-op and
-// keeps the state as it was before the failing gate.
+//   per wave of units:
+//     [k_decode_gate]  split path: decompress_into + scale + run_plan_unit +
+//                      snap_zeros for cross-chunk partners, into scratch X
+//     per ladder level: k_fused (decode + gate + snap + compress + stored
+//                       sum_sq + side index, or the same from X) and
+//                       k_ladder (compress_stride_adaptive / joint pair
+//                       ladder, aalc.cpp:117-138, 337-356)
+//     [k_wave_commit]  wave layout: install the wave's blocks
+//   k_commit_plan / k_commit_copy  staged commit into the block arena (small layout)
+//   k_norm          lazy renormalisation + GateRecord (aalc.cpp:410-419, 612-631)
+// All launches are stream-ordered; in the small layout the host only
+// synchronises at API boundaries.  A device error word makes every later
+// kernel a no-op and keeps the state as it was before the failing gate.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -672,22 +675,6 @@ CodecParams make_params(double delta)
     cp.inv_td = cp.pow2 ? 1.0 / cp.td : 0.0;
     return cp;
 }
-
-int launch_encode(const EncodeArgs& a, uint64_t n_jobs, cudaStream_t st)
-{
-    if (n_jobs == 0) return 0;
-    static bool attr_set = false;
-    if (!attr_set) {
-        CU(cudaFuncSetAttribute(k_encode<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ENC_SMEM));
-        CU(cudaFuncSetAttribute(k_encode<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ENC_SMEM));
-        attr_set = true;
-    }
-    if (a.cp.lossy) k_encode<true><<<(unsigned)n_jobs, CODEC_THREADS, ENC_SMEM, st>>>(a);
-    else k_encode<false><<<(unsigned)n_jobs, CODEC_THREADS, ENC_SMEM, st>>>(a);
-    CU(cudaGetLastError());
-    return 0;
-}
-
 
 template <bool L, int NPL, int LPL, int MODE>
 int launch_fused_t(const FusedArgs& a, uint64_t grid, cudaStream_t s)

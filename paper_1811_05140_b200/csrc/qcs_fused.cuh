@@ -43,13 +43,7 @@ struct FusedShared {
     double wesc_v[8];
     uint64_t wsum[8];
     long long wmin[8];
-    long long wfail[8];
     PlaneCarry carry[4];
-    long long pin_idx[4][MAXPIN];
-    double pin_val[4][MAXPIN];
-    int16_t pin_code[4][MAXPIN];
-    int npin[4];
-    double fail_prev[4];
     double s[2];  // exact running sum of squares per stride
     uint64_t mvmax;
 };
@@ -185,7 +179,7 @@ __device__ __forceinline__ long long fscan_last(long long idx, double val, Fused
 // ---- exact stored sum of squares over a stride group ------------------------
 // group g = planes (2g, 2g+1), threads [g*GT, (g+1)*GT), GT = 2*LPL; each thread
 // owns 16 consecutive elements of the chunk.  Same algorithm as
-// sumsq_iteration (qcs_codec.cuh), restricted to the group's warps.
+// the integer-sum argument of DESIGN.md §4, restricted to the group's warps.
 template <int LPL>
 __device__ __forceinline__ double tsq_g(double* xs, int g, int k)
 {
