@@ -1116,6 +1116,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             a.arena1 = d.arena[1];
             a.arena_cur = &d.sc->cur;
             a.p_off = d.p_off;
+            a.p_len = d.p_len;
             a.p_codec = d.p_codec;
             a.p_delta = d.p_delta;
             a.side_in = d.side;

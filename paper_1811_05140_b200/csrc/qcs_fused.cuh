@@ -59,6 +59,7 @@ struct FusedArgs {
     const uint8_t* arena1;
     const int* arena_cur;         // device scalar: which one is live
     const uint64_t* p_off;
+    const uint64_t* p_len;
     const int8_t* p_codec;
     const double* p_delta;
     const SideEntry* side_in;     // [plane][nsub]
@@ -524,7 +525,36 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
             asm volatile("cp.async.wait_all;\n" ::: "memory");
             __syncthreads();
         } else {
-            if (cnt > 0) decode_sub(in_bytes, in_codec, in_td, in_side[e0 / SUB], cnt, xl, in_scale);
+            // Stage this iteration's payload bytes of the plane in shared memory
+            // (the code buffer is free until the chain runs) with coalesced
+            // 16-byte loads, so the lanes' serial token walks read shared
+            // memory instead of waiting on L2 per byte.  The range runs from
+            // the token covering the iteration's first element to the token
+            // covering the next iteration's first one, plus that token's
+            // varint and the words it owns for this iteration's elements.
+            const uint8_t* src = in_bytes;
+            if (MODE == MODE_LOCAL) {
+                constexpr uint64_t STAGE = sizeof(int16_t) * ITP;  // bytes per plane
+                uint8_t* stage = reinterpret_cast<uint8_t*>(code + pl * ITP);
+                const uint64_t sc0 = base / SUB;
+                const uint64_t lo = in_side[sc0].off & ~uint64_t(15);
+                uint64_t hi;
+                if (final_iter) {
+                    hi = a.p_len[2 * in_stride + comp];
+                } else {
+                    const SideEntry nx = in_side[sc0 + LPL];
+                    hi = (uint64_t)nx.off + 10 + 8 * (uint64_t)nx.skip;
+                }
+                const uint64_t nb = hi > lo ? ((hi - lo + 15) & ~uint64_t(15)) : 0;
+                if (nb <= STAGE) {
+                    const uint4* s4 = reinterpret_cast<const uint4*>(in_bytes + lo);
+                    uint4* d4 = reinterpret_cast<uint4*>(stage);
+                    for (uint64_t k = lane; k < nb / 16; k += LPL) d4[k] = s4[k];
+                    src = stage - lo;  // token offsets stay plane-relative
+                }
+                __syncthreads();
+            }
+            if (cnt > 0) decode_sub(src, in_codec, in_td, in_side[e0 / SUB], cnt, xl, in_scale);
             if (MODE == MODE_FAR && cnt > 0) {
                 const uint64_t pe0 = e0 ^ hb;
                 decode_sub(in_bytes, in_codec, in_td, in_side[pe0 / SUB], cnt,
