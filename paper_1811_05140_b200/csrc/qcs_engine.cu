@@ -195,11 +195,16 @@ __global__ void __launch_bounds__(256) k_decode(Dev d, DecodeJob dj)
 //   DG_FAR   partner 2^t >= 2048 away in the same stride, 2 x 2 planes x 2048
 //   DG_PAIR  lo / hi stride of a cross-stride unit, 2 x 2 planes x 2048
 enum { DG_IN = 0, DG_FAR = 1, DG_PAIR = 2 };
-constexpr int DG_ROWS = 256;
-constexpr size_t DG_SMEM = sizeof(double) * DG_ROWS * XS_STRIDE;
+// R sub-chunk rows per CTA (R threads): DG_IN covers 2 planes x R/2 rows
+// (IN_CH = 16 R elements, partners inside it), DG_FAR / DG_PAIR 4 planes x R/4
+// rows (HALF = 8 R elements per side).
+constexpr int DG_R = 128;
+constexpr int DG_IN_CH = 16 * DG_R;
+constexpr int DG_HALF = 8 * DG_R;
+constexpr size_t DG_SMEM = sizeof(double) * DG_R * XS_STRIDE;
 
-__global__ void __launch_bounds__(256) k_decode_gate(Dev d, Plan p, GateParams gp, int mode,
-                                                   uint64_t chunks, uint64_t slot_base)
+__global__ void __launch_bounds__(DG_R) k_decode_gate(Dev d, Plan p, GateParams gp, int mode,
+                                                    uint64_t chunks, uint64_t slot_base)
 {
     if (d.sc->err) return;
     extern __shared__ __align__(16) unsigned char dg_smem[];
@@ -208,25 +213,25 @@ __global__ void __launch_bounds__(256) k_decode_gate(Dev d, Plan p, GateParams g
     const int tid = threadIdx.x;
     const uint64_t L = d.L;
     const uint64_t hb = 1ull << (p.pair ? 0 : p.t);
+    constexpr int RQ = DG_R / 4, RH = DG_R / 2;
     // this thread's row: (stride, component, element base)
     uint64_t slot, e0;
     int comp;
+    auto far_lo = [&](uint64_t e) { return ((e >> p.t) << (p.t + 1)) | (e & (hb - 1)); };
     if (mode == DG_IN) {
         slot = u;
-        comp = tid >> 7;
-        e0 = c * 4096 + (uint64_t)(tid & 127) * SUB;
+        comp = tid / RH;
+        e0 = c * DG_IN_CH + (uint64_t)(tid % RH) * SUB;
     } else {
-        const int q = tid >> 6;            // 0 A.re, 1 A.im, 2 B.re, 3 B.im
-        const uint64_t sub = (uint64_t)(tid & 63) * SUB;
+        const int q = tid / RQ;            // 0 A.re, 1 A.im, 2 B.re, 3 B.im
+        const uint64_t sub = (uint64_t)(tid % RQ) * SUB;
         comp = q & 1;
         if (mode == DG_PAIR) {
             slot = 2 * u + (q >> 1);
-            e0 = c * 2048 + sub;
+            e0 = c * DG_HALF + sub;
         } else {
             slot = u;
-            const uint64_t e = c * 2048;
-            const uint64_t elo = ((e >> p.t) << (p.t + 1)) | (e & (hb - 1));
-            e0 = elo + ((q >> 1) ? hb : 0) + sub;
+            e0 = far_lo(c * DG_HALF) + ((q >> 1) ? hb : 0) + sub;
         }
     }
     const uint64_t j = d.job_stride[slot_base + slot];
@@ -242,47 +247,40 @@ __global__ void __launch_bounds__(256) k_decode_gate(Dev d, Plan p, GateParams g
     auto at = [&](int row_base, int k) -> double& { return xs[(row_base + (k >> 5)) * XS_STRIDE + (k & 31)]; };
     if (mode == DG_IN) {
         const uint64_t lo_mask = hb - 1;
-        for (int q = tid; q < 2048; q += 256) {
+        for (int q = tid; q < DG_IN_CH / 2; q += DG_R) {
             const int i0 = (int)((((uint64_t)q & ~lo_mask) << 1) | ((uint64_t)q & lo_mask));
             const int i1 = i0 | (int)hb;
-            if (p.local_ctl >= 0 && !(((c * 4096 + i0) >> p.local_ctl) & 1)) continue;
-            pair_update(m, at(0, i0), at(128, i0), at(0, i1), at(128, i1));
+            if (p.local_ctl >= 0 && !(((c * DG_IN_CH + i0) >> p.local_ctl) & 1)) continue;
+            pair_update(m, at(0, i0), at(RH, i0), at(0, i1), at(RH, i1));
         }
     } else {
-        for (int i = tid; i < 2048; i += 256) {
-            uint64_t gi;
-            if (mode == DG_PAIR) {
-                gi = c * 2048 + i;
-            } else {
-                const uint64_t e = c * 2048;
-                gi = (((e >> p.t) << (p.t + 1)) | (e & (hb - 1))) + i;
-            }
+        for (int i = tid; i < DG_HALF; i += DG_R) {
+            const uint64_t gi = (mode == DG_PAIR ? c * DG_HALF : far_lo(c * DG_HALF)) + i;
             if (p.local_ctl >= 0 && !((gi >> p.local_ctl) & 1)) continue;
-            pair_update(m, at(0, i), at(64, i), at(128, i), at(192, i));
+            pair_update(m, at(0, i), at(RQ, i), at(2 * RQ, i), at(3 * RQ, i));
         }
     }
     __syncthreads();
     // snap and write out, coalesced along elements
-    for (int k = tid; k < DG_ROWS * SUB; k += 256) {
+    for (int k = tid; k < DG_R * SUB; k += DG_R) {
         const int row = k >> 5;
         const double v = snap(xs[row * XS_STRIDE + (k & 31)]);
         uint64_t oslot, oe;
         int ocomp;
         if (mode == DG_IN) {
             oslot = u;
-            ocomp = row >> 7;
-            oe = c * 4096 + (uint64_t)(k & 4095);
+            ocomp = row / RH;
+            oe = c * DG_IN_CH + (uint64_t)(k % DG_IN_CH);
         } else {
-            const int q = row >> 6;
+            const int q = row / RQ;
             ocomp = q & 1;
-            const uint64_t off = (uint64_t)(k & 2047);
+            const uint64_t off = (uint64_t)(k % DG_HALF);
             if (mode == DG_PAIR) {
                 oslot = 2 * u + (q >> 1);
-                oe = c * 2048 + off;
+                oe = c * DG_HALF + off;
             } else {
                 oslot = u;
-                const uint64_t e = c * 2048;
-                oe = (((e >> p.t) << (p.t + 1)) | (e & (hb - 1))) + ((q >> 1) ? hb : 0) + off;
+                oe = far_lo(c * DG_HALF) + ((q >> 1) ? hb : 0) + off;
             }
         }
         if (oe < L) d.X[(2 * oslot + ocomp) * L + oe] = v;
@@ -1086,7 +1084,8 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     int dg = -1;
     if (p.pair) dg = DG_PAIR;
     else if (p.kind <= 1 && (1ull << p.t) >= 4096) dg = DG_FAR;
-    else if (p.kind <= 1 && st->split_local && d.L >= 4096) dg = DG_IN;
+    else if (p.kind <= 1 && st->split_local && (1ull << p.t) >= DG_HALF) dg = DG_FAR;
+    else if (p.kind <= 1 && st->split_local && d.L >= DG_IN_CH) dg = DG_IN;
     const int fm = dg >= 0 ? FM_RAW2 : (p.pair ? FM_PAIR : FM_LOCAL);
     if (dg >= 0) {
         static bool dg_attr = false;
@@ -1103,10 +1102,11 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         const uint64_t u1 = std::min<uint64_t>(p.n_units, u0 + wave_units);
         const uint64_t s0 = u0 * spu, s1 = u1 * spu, nw = s1 - s0;
         if (dg >= 0) {
-            const uint64_t chunks = dg == DG_PAIR ? (d.L + 2047) / 2048 : d.L / 4096;
+            const uint64_t chunks = dg == DG_PAIR ? (d.L + DG_HALF - 1) / DG_HALF
+                                                  : (dg == DG_FAR ? d.L / (2 * DG_HALF) : d.L / DG_IN_CH);
             const uint64_t units = dg == DG_PAIR ? (u1 - u0) : nw;
             prof_start(st, 0);
-            k_decode_gate<<<(unsigned)(units * chunks), 256, DG_SMEM, s>>>(d, p, gp, dg, chunks, s0);
+            k_decode_gate<<<(unsigned)(units * chunks), DG_R, DG_SMEM, s>>>(d, p, gp, dg, chunks, s0);
             prof_stop(st);
             ++st->launches;
         }
