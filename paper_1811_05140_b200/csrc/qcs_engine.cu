@@ -457,7 +457,22 @@ __global__ void __launch_bounds__(1024) k_commit_plan(Dev d, uint64_t n_slots, u
     }
 }
 
-__global__ void __launch_bounds__(128) k_commit_copy(Dev d, LevelTag lt, uint64_t gen)
+// Block-wide copy of n 16-byte words, four independent loads in flight per thread.
+__device__ __forceinline__ void copy16(uint4* dst, const uint4* src, uint64_t n)
+{
+    const uint64_t step = blockDim.x;
+    uint64_t i = threadIdx.x;
+    for (; i + 3 * step < n; i += 4 * step) {
+        const uint4 a = src[i], b = src[i + step], c = src[i + 2 * step], e = src[i + 3 * step];
+        dst[i] = a;
+        dst[i + step] = b;
+        dst[i + 2 * step] = c;
+        dst[i + 3 * step] = e;
+    }
+    for (; i < n; i += step) dst[i] = src[i];
+}
+
+__global__ void __launch_bounds__(256) k_commit_copy(Dev d, LevelTag lt, uint64_t gen)
 {
     if (d.sc->err) return;
     const uint64_t g = blockIdx.x;
@@ -479,15 +494,10 @@ __global__ void __launch_bounds__(128) k_commit_copy(Dev d, LevelTag lt, uint64_
         len = d.p_len[g];
     }
     uint8_t* dst = d.arena[mode == 0 ? cur : 1 - cur] + d.new_off[g];
-    const uint64_t n16 = (len + 15) / 16;
-    const uint4* s4 = reinterpret_cast<const uint4*>(src);
-    uint4* d4 = reinterpret_cast<uint4*>(dst);
-    for (uint64_t i = threadIdx.x; i < n16; i += blockDim.x) d4[i] = s4[i];
-    if (rew) {
-        const SideEntry* ss = d.slot_side + (2 * slot + c) * d.nsub;
-        SideEntry* ds = d.side + g * d.nsub;
-        for (uint64_t i = threadIdx.x; i < d.nsub; i += blockDim.x) ds[i] = ss[i];
-    }
+    copy16(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), (len + 15) / 16);
+    if (rew)
+        copy16(reinterpret_cast<uint4*>(d.side + g * d.nsub),
+               reinterpret_cast<const uint4*>(d.slot_side + (2 * slot + c) * d.nsub), d.nsub);
     __syncthreads();
     if (threadIdx.x == 0) {
         d.p_off[g] = d.new_off[g];
@@ -1172,7 +1182,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     prof_start(st, 3);
     if (!st->big) {
         k_commit_plan<<<1, 1024, 0, s>>>(d, n_slots, gen);
-        k_commit_copy<<<(unsigned)(2 * d.NS), 128, 0, s>>>(d, st->lt, gen);
+        k_commit_copy<<<(unsigned)(2 * d.NS), 256, 0, s>>>(d, st->lt, gen);
         st->launches += 2;
     }
     k_norm<<<1, NORM_THREADS, 0, s>>>(d, n_slots, rec_index < 0 ? 0 : (uint64_t)rec_index, gate_index, renorm);
@@ -1889,7 +1899,7 @@ int qcs_unpack_strides(qcs_dev_state_t st, const void* dev_buf, uint64_t len, ui
             if (rc) return rc;
         } else {
             k_commit_plan<<<1, 1024, 0, st->stream>>>(d, m, gen);
-            k_commit_copy<<<(unsigned)(2 * d.NS), 128, 0, st->stream>>>(d, st->lt, gen);
+            k_commit_copy<<<(unsigned)(2 * d.NS), 256, 0, st->stream>>>(d, st->lt, gen);
             st->launches += 2;
         }
         k_unpack_finish<<<(unsigned)((m + 127) / 128), 128, 0, st->stream>>>(d, dent, i0, m, xor_mask);
