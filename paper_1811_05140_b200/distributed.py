@@ -67,7 +67,7 @@ class ThreadComm:
     def allgather_array(self, arr: np.ndarray) -> List[np.ndarray]:
         return self.allgather(np.array(arr, copy=True))
 
-    def exchange(self, peer: Optional[int], obj):
+    def exchange(self, peer: Optional[int], obj, device: bool = False):
         """Collective: every rank calls it; peer None = no partner."""
         g = self.group
         if peer is not None:
@@ -103,13 +103,17 @@ class TorchComm:
         self.dist.all_gather(out, t, group=self.group)
         return [o.cpu().numpy() for o in out]
 
-    def exchange(self, peer: Optional[int], obj):
-        """Pairwise exchange.  Device tensors (stride images) go point to point
-        (NCCL send/recv over NVLink; staged through host memory on gloo); other
-        objects through an all-gather, which keeps the pattern collective."""
+    def exchange(self, peer: Optional[int], obj, device: bool = False):
+        """Pairwise exchange.  device=True: device tensors (stride images) go
+        point to point between the pair only (NCCL send/recv over NVLink;
+        staged through host memory on gloo) and ranks without a partner do
+        nothing.  Otherwise objects go through an all-gather every rank joins."""
         import torch
-        if peer is None or not torch.is_tensor(obj):
-            got = self.allgather((peer, None if torch.is_tensor(obj) else obj))
+        if device:
+            if peer is None:
+                return None
+        else:
+            got = self.allgather((peer, obj))
             if peer is None:
                 return None
             p_peer, p_obj = got[peer]
@@ -153,6 +157,8 @@ class GpuBackend:
 
 
 class _GpuShard:
+    device_images = True  # stride images are device tensors (point-to-point exchange)
+
     def __init__(self, h, n, s, device=0):
         self.h, self.n, self.s, self.device = h, n, s, device
 
@@ -272,7 +278,7 @@ class ShardedState:
         if active:
             send_bit = 0 if (r >> b) & 1 else 1
             payload = self.local.pack(qb, send_bit)
-        got = self.comm.exchange(peer, payload)
+        got = self.comm.exchange(peer, payload, device=getattr(self.local, "device_images", False))
         if active:
             self.local.unpack(got, 1 << qb)
 

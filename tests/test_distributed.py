@@ -180,3 +180,36 @@ def test_sharded_bench_functional(tmp_path):
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["config"]["n_qubits"] == 25
+
+
+def _gloo_gpu_worker(rank, world, port, outdir):
+    import torch
+    import torch.distributed as dist
+    from paper_1811_05140_b200.distributed import TorchComm, run_sharded
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    try:
+        for name, prog, s, basis, lad, theta in _cases()[:3]:
+            st, recs, _ = run_sharded(prog, ShardGeometry(prog.n_qubits, s, 1), TorchComm(),
+                                      GpuBackend(0), basis, lad, theta)
+            amp = st.amplitudes()
+            if rank == 0:
+                with open(os.path.join(outdir, name + ".csv"), "w") as f:
+                    f.write(mm.emit_csv(recs, with_elapsed=False))
+                np.save(os.path.join(outdir, name + ".npy"), amp)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gloo_world2_gpu_shards(oracle, tmp_path):
+    """Two processes (one GPU shared; images staged through gloo) running QFT
+    (controlled phases with rank-qubit controls and targets), Grover gate form
+    and reflect_mean: equal to the single-process oracle."""
+    import torch.multiprocessing as tmp
+    tmp.spawn(_gloo_gpu_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    for name, prog, s, basis, lad, theta in _cases()[:3]:
+        want_amp, want_csv = _single(oracle, prog, s, basis, lad, theta)
+        assert (tmp_path / (name + ".csv")).read_text() == want_csv, name
+        assert np.load(tmp_path / (name + ".npy")).tobytes() == want_amp.tobytes(), name
