@@ -156,6 +156,11 @@ class GpuBackend:
         return _GpuShard(h, n, s, self.device)
 
 
+# qcs_stride_report (include/qcs_b200.h) as a numpy record
+_REPORT_DTYPE = np.dtype([("stride", "<u8"), ("b_in", "<u8"), ("b_out", "<u8"), ("delta", "<f8"),
+                          ("ratio", "<f8"), ("met", "<i4"), ("pad", "<i4")])
+
+
 class _GpuShard:
     device_images = True  # stride images are device tensors (point-to-point exchange)
 
@@ -163,7 +168,10 @@ class _GpuShard:
         self.h, self.n, self.s, self.device = h, n, s, device
 
     def __del__(self):
-        from .engine import _lib_handle
+        try:
+            from .engine import _lib_handle
+        except ImportError:  # interpreter shutdown
+            return
         if getattr(self, "h", None) and _lib_handle is not None:
             _lib_handle.qcs_state_destroy(self.h)
             self.h = None
@@ -180,8 +188,9 @@ class _GpuShard:
         flags = 1 | (2 if mean else 0)   # QCS_NO_RENORM | QCS_GIVEN_MEAN
         _check(lib().qcs_apply_gate_ex(self.h, pack_gates([gate]), lad, len(ladder), theta, flags,
                                        m, reps, C.byref(nr), C.byref(norm)))
-        return [(r.stride_index, r.chosen_delta, r.ratio, r.bytes_in, r.bytes_out,
-                 bool(r.threshold_met)) for r in reps[: nr.value]]
+        a = np.frombuffer(reps, dtype=_REPORT_DTYPE, count=nr.value)
+        return np.stack([a["stride"].astype(np.float64), a["delta"], a["ratio"], a["b_in"].astype(np.float64),
+                         a["b_out"].astype(np.float64), (a["met"] != 0).astype(np.float64)], axis=1)
 
     def stride_sums(self):
         from .engine import _check, lib
@@ -342,14 +351,25 @@ class ShardedState:
         # its per-stride (scale, sum_sq)
         nsl = g.local_strides
         buf = np.zeros((nsl + 1, 10))
-        buf[0, 0] = len(reports)
-        for i, rep in enumerate(reports):
-            gj = self._global_stride(rep[0], swapped)
-            if pair_bit_global is not None:
-                k0, k1 = gj & ~pair_bit_global, (1 if gj & pair_bit_global else 0)
+        rep = np.asarray(reports, dtype=np.float64).reshape(-1, 6)
+        buf[0, 0] = len(rep)
+        if len(rep):
+            jl = rep[:, 0].astype(np.int64)
+            if swapped is None:
+                gj = self.r * nsl + jl
             else:
-                k0, k1 = gj, 0
-            buf[i + 1, :8] = (k0, k1, gj, rep[1], rep[2], rep[3], rep[4], 1.0 if rep[5] else 0.0)
+                b, qb = swapped
+                rb = (self.r & ~(1 << b)) | (((jl >> qb) & 1) << b)
+                jb = (jl & ~(1 << qb)) | (((self.r >> b) & 1) << qb)
+                gj = rb * nsl + jb
+            if pair_bit_global is not None:
+                k0, k1 = gj & ~pair_bit_global, (gj & pair_bit_global) != 0
+            else:
+                k0, k1 = gj, np.zeros(len(gj))
+            buf[1:1 + len(rep), 0] = k0
+            buf[1:1 + len(rep), 1] = k1
+            buf[1:1 + len(rep), 2] = gj
+            buf[1:1 + len(rep), 3:8] = rep[:, 1:6]
         sc, sm = self.local.stride_norms()
         buf[1:, 8] = sc
         buf[1:, 9] = sm
