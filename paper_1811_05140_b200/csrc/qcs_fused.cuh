@@ -49,7 +49,10 @@ struct FusedShared {
 };
 
 constexpr size_t FUSED_XS_BYTES = sizeof(double) * 256 * XS_STRIDE;
-constexpr size_t FUSED_CODE_BYTES = sizeof(int16_t) * 256 * SUB;
+// code rows padded to 34 int16 (17 words) so the lanes' row accesses (32-bit
+// pairs in lane_masks, 16-bit in the chain) hit distinct banks
+constexpr int CODE_STRIDE = SUB + 2;
+constexpr size_t FUSED_CODE_BYTES = sizeof(int16_t) * 256 * CODE_STRIDE;
 constexpr size_t FUSED_S_OFF = (FUSED_XS_BYTES + FUSED_CODE_BYTES + 15) & ~size_t(15);
 constexpr size_t FUSED_SMEM = FUSED_S_OFF + sizeof(FusedShared);
 
@@ -455,7 +458,7 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
     uint8_t* out = a.out + (2 * slot + comp) * a.cap;
     SideEntry* side = a.side + (2 * slot + comp) * a.nsub;
     double* xl = xs + (pl * LPL + lane) * XS_STRIDE;
-    int16_t* cl = code + pl * ITP + lane * SUB;
+    int16_t* cl = code + (pl * LPL + lane) * CODE_STRIDE;
     PlaneCarry& C = S.carry[pl];
 
     // input plane of this thread (block store modes)
@@ -535,7 +538,7 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
             const uint8_t* src = in_bytes;
             if (MODE == MODE_LOCAL) {
                 constexpr uint64_t STAGE = sizeof(int16_t) * ITP;  // bytes per plane
-                uint8_t* stage = reinterpret_cast<uint8_t*>(code + pl * ITP);
+                uint8_t* stage = reinterpret_cast<uint8_t*>(code + pl * LPL * CODE_STRIDE);
                 const uint64_t sc0 = base / SUB;
                 const uint64_t lo = in_side[sc0].off & ~uint64_t(15);
                 uint64_t hi;
@@ -694,7 +697,7 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
                         bool sy;
                         long long li;
                         double lv;
-                        const double Pn = lane_chain(cp, xs + id * XS_STRIDE, code + pl * ITP + l * SUB, c2, want, true,
+                        const double Pn = lane_chain(cp, xs + id * XS_STRIDE, code + id * CODE_STRIDE, c2, want, true,
                                                      S.entryP[id], sy, li, lv);
                         S.entryP[id] = want;
                         if (!sy) S.exitP[id] = Pn;
