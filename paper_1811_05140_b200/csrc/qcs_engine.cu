@@ -261,29 +261,39 @@ __global__ void __launch_bounds__(DG_R) k_decode_gate(Dev d, Plan p, GateParams 
         }
     }
     __syncthreads();
-    // snap and write out, coalesced along elements
-    for (int k = tid; k < DG_R * SUB; k += DG_R) {
-        const int row = k >> 5;
-        const double v = snap(xs[row * XS_STRIDE + (k & 31)]);
-        uint64_t oslot, oe;
+    // snap and write out: every (plane, side) segment is contiguous in X, so
+    // each is one coalesced copy (pairs of doubles per thread)
+    const int nseg = mode == DG_IN ? 2 : 4;
+    const int seg = mode == DG_IN ? DG_IN_CH : DG_HALF;
+    for (int q = 0; q < nseg; ++q) {
+        uint64_t oslot, e_base;
         int ocomp;
         if (mode == DG_IN) {
             oslot = u;
-            ocomp = row / RH;
-            oe = c * DG_IN_CH + (uint64_t)(k % DG_IN_CH);
+            ocomp = q;
+            e_base = c * DG_IN_CH;
         } else {
-            const int q = row / RQ;
             ocomp = q & 1;
-            const uint64_t off = (uint64_t)(k % DG_HALF);
             if (mode == DG_PAIR) {
                 oslot = 2 * u + (q >> 1);
-                oe = c * DG_HALF + off;
+                e_base = c * DG_HALF;
             } else {
                 oslot = u;
-                oe = far_lo(c * DG_HALF) + ((q >> 1) ? hb : 0) + off;
+                e_base = far_lo(c * DG_HALF) + ((q >> 1) ? hb : 0);
             }
         }
-        if (oe < L) d.X[(2 * oslot + ocomp) * L + oe] = v;
+        double* dst = d.X + (2 * oslot + ocomp) * L + e_base;
+        const double* rows = xs + (uint64_t)q * (seg / SUB) * XS_STRIDE;
+        const int m = (int)umin64((uint64_t)seg, L - umin64(e_base, L));
+        if (m == seg) {
+            for (int k = 2 * tid; k < seg; k += 2 * DG_R) {
+                const double v0 = snap(rows[(k >> 5) * XS_STRIDE + (k & 31)]);
+                const double v1 = snap(rows[((k + 1) >> 5) * XS_STRIDE + ((k + 1) & 31)]);
+                *reinterpret_cast<double2*>(dst + k) = make_double2(v0, v1);
+            }
+        } else {
+            for (int k = tid; k < m; k += DG_R) dst[k] = snap(rows[(k >> 5) * XS_STRIDE + (k & 31)]);
+        }
     }
 }
 
