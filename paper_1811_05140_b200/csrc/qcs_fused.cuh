@@ -102,6 +102,32 @@ __device__ __forceinline__ double& xrow(double* xs, int row_plane, int k)
     return xs[(row_plane * LPL + (k >> 5)) * XS_STRIDE + (k & 31)];
 }
 
+// n consecutive little-endian words (the doubles' bits) at an arbitrary byte
+// address: byte stores for the unaligned head and tail, 8-byte aligned
+// stores for the body (each built from two neighbouring words).
+__device__ __forceinline__ void put_words(uint8_t* p, const double* v, int n)
+{
+    if (n <= 0) return;
+    const int r = (int)(reinterpret_cast<uintptr_t>(p) & 7u);
+    auto w = [&](int j) { return (uint64_t)__double_as_longlong(v[j]); };
+    if (r == 0) {
+        uint64_t* q = reinterpret_cast<uint64_t*>(p);
+        for (int j = 0; j < n; ++j) q[j] = w(j);
+        return;
+    }
+    const int d = 8 - r;  // bytes of word 0 before the first 8-byte boundary
+    uint64_t cur = w(0);
+    for (int i = 0; i < d; ++i) p[i] = (uint8_t)(cur >> (8 * i));
+    uint64_t* q = reinterpret_cast<uint64_t*>(p + d);
+    for (int j = 0; j + 1 < n; ++j) {
+        const uint64_t nxt = w(j + 1);
+        q[j] = (cur >> (8 * d)) | (nxt << (8 * r));
+        cur = nxt;
+    }
+    uint8_t* t = p + d + 8 * (n - 1);
+    for (int i = 0; i < r; ++i) t[i] = (uint8_t)(cur >> (8 * (d + i)));
+}
+
 // ---- scans over the WPL warps of one plane --------------------------------
 template <int WPL>
 __device__ __forceinline__ RunFn fscan_fn(RunFn F, FusedShared& S, int pl)
@@ -840,8 +866,8 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
                     const int vl = varint_len(v);
                     put_varint(out + pos, v);
                     if (t == TY_W) {
-                        for (uint64_t k = (st > e0 ? st : e0); k < end; ++k)
-                            put_word(out + pos + vl + 8 * (k - st), (uint64_t)__double_as_longlong(xl[k - e0]));
+                        const uint64_t k0 = st > e0 ? st : e0;
+                        put_words(out + pos + vl + 8 * (k0 - st), xl + (k0 - e0), (int)(end - k0));
                     }
                     if (st < e0 && st >= base) {
                         const int sl = pl * LPL + (int)((st - base) / SUB);
@@ -874,8 +900,8 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
         // 10. words of a W run reaching past this lane
         if (cnt > 0 && tail_ty == TY_W && !tail_closes) {
             const uint64_t wb = tail_st < base ? C.carry_w : S.runw[pl * LPL + (tail_st - base) / SUB];
-            for (uint64_t k = (tail_st > e0 ? tail_st : e0); k < e0 + cnt; ++k)
-                put_word(out + wb + 8 * (k - tail_st), (uint64_t)__double_as_longlong(xl[k - e0]));
+            const uint64_t k0 = tail_st > e0 ? tail_st : e0;
+            put_words(out + wb + 8 * (k0 - tail_st), xl + (k0 - e0), (int)(e0 + cnt - k0));
         }
 
         // 11. side index
