@@ -217,139 +217,122 @@ __device__ __forceinline__ double tsq_g(double* xs, int g, int k)
     return __dadd_rn(__dmul_rn(r, r), __dmul_rn(i, i));
 }
 
-template <int LPL, int NG>
+template <int LPL>
 __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FusedShared& S, unsigned long long* counters)
 {
-    constexpr int GT = 2 * LPL;          // threads per group
-    constexpr int GW = GT / 32;          // warps per group
-    constexpr int PER = (LPL * SUB) / GT;  // 16
+    constexpr int GT = 2 * LPL;            // threads (the CTA: one stride)
+    constexpr int GW = GT / 32;            // warps
+    constexpr int PER = (LPL * SUB) / GT;  // 16 elements per thread
+    constexpr uint64_t SAT = 1ull << 62;
     const int tid = threadIdx.x;
-    const int g = tid / GT;
-    const int gt = tid % GT;
     const int wl = tid & 31, w = tid >> 5;
-    const int kb = gt * PER;
+    const int kb = tid * PER;
+    __syncthreads();
+    double s = S.s[0];  // uniform across the CTA from here on
     int k0 = 0;
-    bool done = false;
     // While s is still 0 the next elements double it again and again (a binade
     // crossing, i.e. a parallel pass, per doubling): sum the first SERIAL_SUM
     // elements of a stride in the reference's order on one thread instead.
     constexpr int SERIAL_SUM = 512;
-    __syncthreads();
-    if (S.s[g] == 0.0) {
+    if (s == 0.0) {
         const int m = min(n_it, SERIAL_SUM);
-        if (gt == 0) {
+        if (tid == 0) {
             double acc = 0.0;
 #pragma unroll 4
-            for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, tsq_g<LPL>(xs, g, k));
-            S.s[g] = acc;
+            for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, tsq_g<LPL>(xs, 0, k));
+            S.s[0] = acc;
         }
+        __syncthreads();
+        s = S.s[0];
         k0 = m;
     }
-    for (;;) {
-        __syncthreads();
-        const double s = S.s[g];
-        if (k0 >= n_it) done = true;
-        const bool all_done = !__syncthreads_or(!done);
-        if (all_done) break;
-        if (counters && gt == 0 && !done) atomicAdd(&counters[1], 1ull);
-        // --- phase A: decide per group what to do (uniform within the group)
-        long long mine = LLONG_MAX;   // min-reduction candidate
-        uint64_t loc = 0;
-        int e = 0;
-        double to_units = 0.0;
-        uint64_t ms = 0;
-        const int state = done ? 0 : (s == 0.0 ? 1 : (ilogb(s) < -960 ? 2 : 3));
-        if (state == 1) {
-            for (int i = 0; i < PER; ++i) {
-                const int k = kb + i;
-                if (k >= k0 && k < n_it && tsq_g<LPL>(xs, g, k) != 0.0) {
-                    mine = k;
-                    break;
-                }
-            }
-        } else if (state == 3) {
-            e = ilogb(s);
-            to_units = ldexp(1.0, 52 - e);
-            ms = (uint64_t)(s * to_units);
+    while (k0 < n_it) {
+        if (counters && tid == 0) atomicAdd(&counters[1], 1ull);
+        long long mine = LLONG_MAX;  // this thread's event candidate
+        const int state = s == 0.0 ? 1 : (ilogb(s) < -960 ? 2 : 3);
+        if (state == 3) {
+            const int e = ilogb(s);
+            const double to_units = ldexp(1.0, 52 - e);
+            const uint64_t ms = (uint64_t)(s * to_units);
+            uint64_t loc = 0;
             for (int i = 0; i < PER; ++i) {
                 const int k = kb + i;
                 if (k < k0 || k >= n_it) continue;
-                const double y = tsq_g<LPL>(xs, g, k) * to_units;
-                // a tie (or an element beyond the binade) saturates the total, which
-                // forces the exact second pass below
-                loc = sat_add(loc, (y >= 9007199254740992.0 || y - floor(y) == 0.5) ? (1ull << 62)
-                                                                                   : (uint64_t)rint(y));
+                const double y = tsq_g<LPL>(xs, 0, k) * to_units;
+                // a tie (or an element beyond the binade) saturates the total
+                loc = sat_add(loc, (y >= 9007199254740992.0 || y - floor(y) == 0.5) ? SAT : (uint64_t)rint(y));
             }
-        }
-        // group exclusive scan of loc (saturating)
-        uint64_t inc = loc;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t u = __shfl_up_sync(0xffffffffu, inc, o);
-            if (wl >= o) inc = sat_add(inc, u);
-        }
-        const uint64_t prev = __shfl_up_sync(0xffffffffu, inc, 1);
-        __syncthreads();
-        if (wl == 31) S.wsum[w] = inc;
-        __syncthreads();
-        uint64_t pre = 0, total = 0;
-        for (int i = g * GW; i < (g + 1) * GW; ++i) {
-            if (i < w) pre = sat_add(pre, S.wsum[i]);
-            total = sat_add(total, S.wsum[i]);
-        }
-        const uint64_t off = sat_add(pre, wl ? prev : 0);
-        // pass 2 only if the group total may cross the binade (or hit a tie)
-        if (state == 3 && ms + total >= (1ull << 53)) {
+            uint64_t inc = loc;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t u = __shfl_up_sync(0xffffffffu, inc, o);
+                if (wl >= o) inc = sat_add(inc, u);
+            }
+            const uint64_t prev = __shfl_up_sync(0xffffffffu, inc, 1);
+            __syncthreads();
+            if (wl == 31) S.wsum[w] = inc;
+            __syncthreads();
+            uint64_t pre = 0, total = 0;
+            for (int i = 0; i < GW; ++i) {
+                if (i < w) pre = sat_add(pre, S.wsum[i]);
+                total = sat_add(total, S.wsum[i]);
+            }
+            if (ms + total < (1ull << 53)) {  // no event: the rest of the iteration
+                s = (double)(ms + total) / to_units;  // < 2^53 units: exact
+                break;
+            }
+            // find the first event (binade crossing or tie) and add it exactly
+            const uint64_t off = sat_add(pre, wl ? prev : 0);
             uint64_t run = off;
             for (int i = 0; i < PER && mine == LLONG_MAX; ++i) {
                 const int k = kb + i;
                 if (k < k0 || k >= n_it) continue;
-                const double y = tsq_g<LPL>(xs, g, k) * to_units;
+                const double y = tsq_g<LPL>(xs, 0, k) * to_units;
                 if (y >= 9007199254740992.0 || y - floor(y) == 0.5) {
                     mine = k;
                     break;
                 }
-                run = sat_add(run, (uint64_t)rint(y));
-                if (ms + run >= (1ull << 53)) mine = k;
+                const uint64_t c = (uint64_t)rint(y);
+                if (ms + run + c >= (1ull << 53)) {
+                    mine = k;
+                    break;
+                }
+                run = sat_add(run, c);
             }
-        } else if (state == 2) {
-            if (gt == 0) mine = k0;
-        }
-        // group min
-        long long m = mine;
-        for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-        __syncthreads();
-        if (wl == 0) S.wmin[w] = m;
-        __syncthreads();
-        long long kstar = LLONG_MAX;
-        for (int i = g * GW; i < (g + 1) * GW; ++i) kstar = min(kstar, S.wmin[i]);
-        if (state == 0) continue;
-        if (state == 1) {
-            if (kstar == LLONG_MAX) {
-                k0 = n_it;
-            } else {
-                if (gt == 0) S.s[g] = tsq_g<LPL>(xs, g, (int)kstar);
-                k0 = (int)kstar + 1;
+            long long m = mine;
+            for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (wl == 0) S.wmin[w] = m;
+            __syncthreads();
+            long long kstar = LLONG_MAX;
+            for (int i = 0; i < GW; ++i) kstar = min(kstar, S.wmin[i]);
+            if (mine == kstar && kstar != LLONG_MAX) S.s[0] = __dadd_rn((double)(ms + run) / to_units, tsq_g<LPL>(xs, 0, (int)kstar));
+            __syncthreads();
+            s = S.s[0];
+            k0 = (int)kstar + 1;
+        } else if (state == 1) {  // 0 + t = t exactly: the first non-zero term starts the sum
+            for (int i = 0; i < PER; ++i) {
+                const int k = kb + i;
+                if (k >= k0 && k < n_it && tsq_g<LPL>(xs, 0, k) != 0.0) {
+                    mine = k;
+                    break;
+                }
             }
-            continue;
-        }
-        if (state == 2) {
-            if (gt == 0) S.s[g] = __dadd_rn(s, tsq_g<LPL>(xs, g, k0));
+            long long m = mine;
+            for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+            __syncthreads();
+            if (wl == 0) S.wmin[w] = m;
+            __syncthreads();
+            long long kstar = LLONG_MAX;
+            for (int i = 0; i < GW; ++i) kstar = min(kstar, S.wmin[i]);
+            if (kstar == LLONG_MAX) break;  // all zero: s stays 0
+            s = tsq_g<LPL>(xs, 0, (int)kstar);
+            k0 = (int)kstar + 1;
+        } else {  // far below any practical state: one term at a time, in order
+            s = __dadd_rn(s, tsq_g<LPL>(xs, 0, k0));
             ++k0;
-            continue;
         }
-        if (kstar == LLONG_MAX) {
-            if (gt == 0) S.s[g] = (double)(ms + total) / to_units;
-            k0 = n_it;
-            continue;
-        }
-        if (kstar >= kb && kstar < kb + PER) {
-            uint64_t r2 = off;
-            for (int k = max(kb, k0); k < (int)kstar; ++k) r2 += (uint64_t)rint(tsq_g<LPL>(xs, g, k) * to_units);
-            const double before = (double)(ms + r2) / to_units;
-            S.s[g] = __dadd_rn(before, tsq_g<LPL>(xs, g, (int)kstar));
-        }
-        k0 = (int)kstar + 1;
     }
+    __syncthreads();
+    if (tid == 0) S.s[0] = s;
 }
 
 // The reference chain (LossyEmitter, codec.cpp:153-250) over one lane's c
@@ -752,7 +735,7 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
 
         QCS_PHASE(2);
         // 5. stored sum of squares per stride
-        if (a.sumsq) fused_sumsq<LPL, NPL / 2>(xs, n_it, S, a.counters);
+        if (a.sumsq) fused_sumsq<LPL>(xs, n_it, S, a.counters);
 
         QCS_PHASE(3);
         // 6. run summary of each lane (bitmasks) and the run entering it
