@@ -105,6 +105,10 @@ struct GateParams {
 struct Dev {
     // geometry
     int n, s;
+    // small layout: every plane owns two fixed slots (slot_cap bytes, nsub side
+    // entries each) in arena[0] / side; the live one is p_off / slot_cap & 1,
+    // the encoder writes the other and the commit flips (no copy)
+    int pool;
     uint64_t L, NS, nsub;
     // block store
     uint8_t* arena[2];
@@ -148,6 +152,16 @@ struct Dev {
     unsigned long long* counters;  // [16] device diagnostics
 };
 
+__global__ void k_make_jobs_reset_cin(Dev d) { d.sc->gate_cin = 0; }
+
+__device__ __forceinline__ int pool_sel(const Dev& d, uint64_t g) { return (int)((d.p_off[g] / d.slot_cap) & 1); }
+
+// side index of plane g's live block
+__device__ __forceinline__ SideEntry* side_of(const Dev& d, uint64_t g)
+{
+    return d.pool ? d.side + (2 * g + pool_sel(d, g)) * d.nsub : d.side + g * d.nsub;
+}
+
 __global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen)
 {
     if (blockIdx.x == 0 && threadIdx.x == 0) d.sc->gate_cin = 0;  // wave layout accumulates it
@@ -178,7 +192,7 @@ __global__ void __launch_bounds__(256) k_decode(Dev d, DecodeJob dj)
     const double td = 2.0 * d.p_delta[g];
     const double scale = dj.apply_scale ? d.scale[j] : 1.0;
     double* o = dj.out + (uint64_t)blockIdx.x * 2 * d.L + (uint64_t)pl * d.L;
-    const SideEntry* side = d.side + g * d.nsub;
+    const SideEntry* side = side_of(d, g);
     for (uint64_t sc = lane; sc < d.nsub; sc += PLANE_LANES) {
         const uint64_t e0 = sc * SUB;
         const int cnt = (int)umin64(SUB, d.L - e0);
@@ -239,7 +253,7 @@ __global__ void __launch_bounds__(DG_R) k_decode_gate(Dev d, Plan p, GateParams 
     const int cnt = (int)umin64(SUB, L - umin64(e0, L));
     if (cnt > 0)
         decode_sub(d.arena[d.sc->cur] + d.p_off[g], d.p_codec[g], 2.0 * d.p_delta[g],
-                   d.side[g * d.nsub + e0 / SUB], cnt, xs + tid * XS_STRIDE, d.scale[j]);
+                   side_of(d, g)[e0 / SUB], cnt, xs + tid * XS_STRIDE, d.scale[j]);
     __syncthreads();
     double m[8];
 #pragma unroll
@@ -312,7 +326,7 @@ __global__ void __launch_bounds__(128) k_stride_partial(Dev d)
     const int codec = d.p_codec[g];
     const double td = 2.0 * d.p_delta[g];
     const double scale = d.scale[j];
-    const SideEntry* side = d.side + g * d.nsub;
+    const SideEntry* side = side_of(d, g);
     double acc = 0.0;
     for (uint64_t base = 0; base < d.L; base += 2048) {
         const uint64_t e0 = base + (uint64_t)lane * SUB;
@@ -390,137 +404,47 @@ __global__ void k_tag_level(Dev d, LevelTag lt, uint64_t s0, uint64_t s1, int co
     lt.slot_delta[s] = delta;
 }
 
-// Placement of the new blocks: append after the live data, or — when the
-// arena would overflow — compact every live block into the other arena.
-__global__ void __launch_bounds__(1024) k_commit_plan(Dev d, uint64_t n_slots, uint64_t gen)
+// Small layout commit (the staged commit of aalc.cpp:395-408): the encoder
+// wrote every rewritten plane into its other slot; flip them and install the
+// tables.  One thread per (slot, plane).
+__global__ void k_pool_commit(Dev d, LevelTag lt, uint64_t n_slots)
 {
     if (d.sc->err) return;
-    __shared__ uint64_t wsum[32];
-    __shared__ uint64_t carry;
-    __shared__ int mode;
-    const int tid = threadIdx.x, wl = tid & 31, w = tid >> 5;
-    auto rounded = [](uint64_t x) { return (x + 15) & ~uint64_t(15); };
-    // pass 1: total of new blocks
-    uint64_t acc = 0, cin = 0;
-    for (uint64_t i = tid; i < 2 * n_slots; i += blockDim.x) {
-        acc += rounded(d.slot_len[i]);
-        cin += HEADER_BYTES + d.p_len[2 * d.job_stride[i >> 1] + (i & 1)];
-    }
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    for (int o = 16; o; o >>= 1) cin += __shfl_xor_sync(0xffffffffu, cin, o);
-    __shared__ uint64_t csum[32];
-    if (wl == 0) {
-        wsum[w] = acc;
-        csum[w] = cin;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        uint64_t t = 0, c = 0;
-        for (int i = 0; i < 32; ++i) {
-            t += wsum[i];
-            c += csum[i];
-        }
-        d.sc->gate_cin = c;
-        mode = (d.sc->bump + t <= d.arena_cap) ? 0 : 1;
-        carry = mode == 0 ? d.sc->bump : 0;
-    }
-    __syncthreads();
-    // pass 2: exclusive scan over the planes being placed
-    const uint64_t n_items = mode == 0 ? 2 * n_slots : 2 * d.NS;
-    for (uint64_t base = 0; base < n_items; base += blockDim.x) {
-        const uint64_t i = base + tid;
-        uint64_t v = 0;
-        uint64_t g = 0;
-        if (i < n_items) {
-            if (mode == 0) {
-                g = 2 * d.job_stride[i >> 1] + (i & 1);
-                v = rounded(d.slot_len[i]);
-            } else {
-                g = i;
-                const int64_t so = d.slot_of[g >> 1];
-                const bool rew = (uint64_t)(so >> 32) == gen;
-                v = rounded(rew ? d.slot_len[2 * (so & 0xffffffff) + (g & 1)] : d.p_len[g]);
-            }
-        }
-        uint64_t inc = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t t = __shfl_up_sync(0xffffffffu, inc, o);
-            if (wl >= o) inc += t;
-        }
-        __syncthreads();
-        if (wl == 31) wsum[w] = inc;
-        __syncthreads();
-        uint64_t pre = carry;
-        for (int k = 0; k < w; ++k) pre += wsum[k];
-        if (i < n_items) d.new_off[g] = pre + inc - v;
-        __syncthreads();
-        if (tid == blockDim.x - 1) carry = pre + inc;
-        __syncthreads();
-    }
-    if (tid == 0) {
-        if (carry > d.arena_cap) {
-            d.sc->err = QCS_E_NOMEM;
-            return;
-        }
-        d.sc->mode = mode;
-        d.sc->bump = carry;
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= 2 * n_slots) return;
+    const uint64_t slot = i >> 1;
+    const int c = (int)(i & 1);
+    const uint64_t j = d.job_stride[slot];
+    const uint64_t g = 2 * j + c;
+    const int sel = pool_sel(d, g);
+    atomicAdd((unsigned long long*)&d.sc->gate_cin, (unsigned long long)(HEADER_BYTES + d.p_len[g]));
+    d.p_off[g] = (2 * g + 1 - sel) * d.slot_cap;
+    d.p_len[g] = d.slot_len[i];
+    d.p_codec[g] = lt.slot_codec[slot];
+    d.p_delta[g] = lt.slot_delta[slot];
+    if (c == 0) {
+        d.sum_sq[j] = d.slot_sum[slot];
+        d.scale[j] = 1.0;
     }
 }
 
-// Block-wide copy of n 16-byte words, four independent loads in flight per thread.
-__device__ __forceinline__ void copy16(uint4* dst, const uint4* src, uint64_t n)
+// Small layout basis state (aalc.cpp:140-174): every plane's slot 0 holds the
+// lossless all-zero block, the hot stride's re plane the hot block.
+__global__ void k_init_pool(Dev d, uint64_t hot_g, uint4 zero, uint32_t zero_len, uint4 hot0, uint4 hot1,
+                            uint32_t hot_len)
 {
-    const uint64_t step = blockDim.x;
-    uint64_t i = threadIdx.x;
-    for (; i + 3 * step < n; i += 4 * step) {
-        const uint4 a = src[i], b = src[i + step], c = src[i + 2 * step], e = src[i + 3 * step];
-        dst[i] = a;
-        dst[i + step] = b;
-        dst[i + 2 * step] = c;
-        dst[i + 3 * step] = e;
-    }
-    for (; i < n; i += step) dst[i] = src[i];
-}
-
-__global__ void __launch_bounds__(256) k_commit_copy(Dev d, LevelTag lt, uint64_t gen)
-{
-    if (d.sc->err) return;
-    const uint64_t g = blockIdx.x;
-    const uint64_t j = g >> 1;
-    const int c = (int)(g & 1);
-    const int64_t so = d.slot_of[j];
-    const bool rew = (uint64_t)(so >> 32) == gen;
-    const int mode = d.sc->mode;
-    if (!rew && mode == 0) return;
-    const int cur = d.sc->cur;
-    const uint8_t* src;
-    uint64_t len;
-    const uint64_t slot = rew ? (uint64_t)(so & 0xffffffff) : 0;
-    if (rew) {
-        src = d.slot_out + (2 * slot + c) * d.slot_cap;
-        len = d.slot_len[2 * slot + c];
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (g >= 2 * d.NS) return;
+    uint4* dst = reinterpret_cast<uint4*>(d.arena[0] + 2 * g * d.slot_cap);
+    if (g == hot_g) {
+        dst[0] = hot0;
+        dst[1] = hot1;
+        d.p_len[g] = hot_len;
     } else {
-        src = d.arena[cur] + d.p_off[g];
-        len = d.p_len[g];
+        dst[0] = zero;
+        d.p_len[g] = zero_len;
     }
-    uint8_t* dst = d.arena[mode == 0 ? cur : 1 - cur] + d.new_off[g];
-    copy16(reinterpret_cast<uint4*>(dst), reinterpret_cast<const uint4*>(src), (len + 15) / 16);
-    if (rew)
-        copy16(reinterpret_cast<uint4*>(d.side + g * d.nsub),
-               reinterpret_cast<const uint4*>(d.slot_side + (2 * slot + c) * d.nsub), d.nsub);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        d.p_off[g] = d.new_off[g];
-        if (rew) {
-            d.p_len[g] = len;
-            d.p_codec[g] = lt.slot_codec[slot];
-            d.p_delta[g] = lt.slot_delta[slot];
-            if (c == 0) {
-                d.sum_sq[j] = d.slot_sum[slot];
-                d.scale[j] = 1.0;
-            }
-        }
-    }
+    d.p_off[g] = 2 * g * d.slot_cap;
 }
 
 // Lazy renormalisation (aalc.cpp:410-419) and the GateRecord fold
@@ -645,7 +569,7 @@ __global__ void k_index_planes(Dev d, uint64_t g0, uint64_t count)
     if (i >= count) return;
     const uint64_t g = g0 + i;
     const int rc = index_plane(d.arena[d.sc->cur] + d.p_off[g], d.p_len[g], d.p_codec[g],
-                               d.p_delta[g], d.L, d.side + g * d.nsub, nullptr);
+                               d.p_delta[g], d.L, side_of(d, g), nullptr);
     if (rc) atomicCAS(&d.sc->err, 0, rc);
 }
 
@@ -1159,9 +1083,10 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
                 a.x_plane_stride = d.L;
                 a.snap = 0;
             }
-            a.out = d.slot_out;
+            a.pool = d.pool;
+            a.out = d.pool ? d.arena[0] : d.slot_out;
             a.cap = d.slot_cap;
-            a.side = d.slot_side;
+            a.side = d.pool ? d.side : d.slot_side;
             a.nsub = d.nsub;
             a.out_len = d.slot_len;
             a.sumsq = d.slot_sum;
@@ -1191,9 +1116,8 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     }
     prof_start(st, 3);
     if (!st->big) {
-        k_commit_plan<<<1, 1024, 0, s>>>(d, n_slots, gen);
-        k_commit_copy<<<(unsigned)(2 * d.NS), 256, 0, s>>>(d, st->lt, gen);
-        st->launches += 2;
+        k_pool_commit<<<(unsigned)((2 * n_slots + 255) / 256), 256, 0, s>>>(d, st->lt, n_slots);
+        ++st->launches;
     }
     k_norm<<<1, NORM_THREADS, 0, s>>>(d, n_slots, rec_index < 0 ? 0 : (uint64_t)rec_index, gate_index, renorm);
     prof_stop(st);
@@ -1275,14 +1199,16 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     cudaMemGetInfo(&free_b, &total_b);
     const uint64_t side_b = 2 * d.NS * d.nsub * sizeof(SideEntry);
     const uint64_t small_arena = std::max<uint64_t>(raw + raw / 8 + 4096 * d.NS, 1ull << 24);
-    const uint64_t small_need = 2 * small_arena + raw + 2 * d.NS * d.slot_cap + 2 * side_b;
+    const uint64_t pool_b = 4 * d.NS * d.slot_cap;  // two slots per plane
+    const uint64_t small_need = pool_b + 2 * side_b + raw;
     const char* fb = getenv("QCS_FORCE_BIG");
     st->big = (fb && atoi(fb)) || (double)small_need > 0.7 * (double)free_b;
     if (!st->big) {
+        d.pool = 1;
         st->wave = d.NS;
-        d.arena_cap = small_arena;
+        d.arena_cap = pool_b;
         TRY(dalloc(st, &d.arena[0], d.arena_cap));
-        TRY(dalloc(st, &d.arena[1], d.arena_cap));
+        d.arena[1] = d.arena[0];
     } else {
         const uint64_t per_slot = 16 * d.L + 2 * d.slot_cap + 2 * d.nsub * sizeof(SideEntry);
         uint64_t w = d.NS < 2 ? 1 : std::min<uint64_t>(d.NS, 296);
@@ -1315,12 +1241,12 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     TRY(dalloc(st, &d.p_len, 2 * d.NS));
     TRY(dalloc(st, &d.p_codec, 2 * d.NS));
     TRY(dalloc(st, &d.p_delta, 2 * d.NS));
-    TRY(dalloc(st, &d.side, 2 * d.NS * d.nsub));
+    TRY(dalloc(st, &d.side, (d.pool ? 4 : 2) * d.NS * d.nsub));
     TRY(dalloc(st, &d.scale, d.NS));
     TRY(dalloc(st, &d.sum_sq, d.NS));
     TRY(dalloc(st, &d.X, 2 * st->wave * d.L));
-    TRY(dalloc(st, &d.slot_out, 2 * st->wave * d.slot_cap));
-    TRY(dalloc(st, &d.slot_side, 2 * st->wave * d.nsub));
+    TRY(dalloc(st, &d.slot_out, d.pool ? 16 : 2 * st->wave * d.slot_cap));   // pool: unused
+    TRY(dalloc(st, &d.slot_side, d.pool ? 1 : 2 * st->wave * d.nsub));
     TRY(dalloc(st, &d.slot_len, 2 * d.NS));
     TRY(dalloc(st, &d.slot_sum, d.NS));
     TRY(dalloc(st, &d.job_stride, d.NS));
@@ -1362,10 +1288,10 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     memcpy(&w, &one, 8);
     for (int i = 0; i < 8; ++i) hot.push_back((uint8_t)(w >> (8 * i)));
     if (d.L - off - 1) varint(hot, (d.L - off - 1) << 1);
-    std::vector<uint8_t> img(32, 0);
+    std::vector<uint8_t> img(48, 0);
     memcpy(img.data(), zero.data(), zero.size());
     memcpy(img.data() + 16, hot.data(), hot.size());
-    CU(cudaMemcpy(d.arena[0], img.data(), img.size(), cudaMemcpyHostToDevice));
+    if (!d.pool) CU(cudaMemcpy(d.arena[0], img.data(), 32 + 16, cudaMemcpyHostToDevice));
     std::vector<uint64_t> h_off(2 * d.NS, 0), h_len(2 * d.NS, zero.size());
     std::vector<int8_t> h_codec(2 * d.NS, 0);
     std::vector<double> h_delta(2 * d.NS, 0.0), h_scale(d.NS, 1.0), h_sum(d.NS, 0.0);
@@ -1377,6 +1303,17 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     }
     CU(cudaMemcpy(d.p_off, h_off.data(), 8 * h_off.size(), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(d.p_len, h_len.data(), 8 * h_len.size(), cudaMemcpyHostToDevice));
+    if (d.pool) {  // every plane owns its blocks: zero block, or the hot block
+        uint4 z, h0, h1;
+        memcpy(&z, img.data(), 16);
+        memcpy(&h0, img.data() + 16, 16);
+        memcpy(&h1, img.data() + 32, 16);
+        const uint64_t hot_g = zero_state ? ~0ull : 2 * (basis >> s);
+        k_init_pool<<<(unsigned)((2 * d.NS + 255) / 256), 256, 0, st->stream>>>(d, hot_g, z, (uint32_t)zero.size(), h0, h1,
+                                                                               (uint32_t)hot.size());
+        ++st->launches;
+        CU(cudaGetLastError());
+    }
     CU(cudaMemcpy(d.p_codec, h_codec.data(), h_codec.size(), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(d.p_delta, h_delta.data(), 8 * h_delta.size(), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(d.scale, h_scale.data(), 8 * h_scale.size(), cudaMemcpyHostToDevice));
@@ -1691,7 +1628,10 @@ int qcs_import_blocks(qcs_dev_state_t st, uint64_t j, const uint8_t* buf, uint64
     CU(cudaMemcpy(st->h_sc, d.sc, sizeof(Dev::Scal), cudaMemcpyDeviceToHost));
     const uint64_t need = ((plen[0] + 15) & ~15ull) + ((plen[1] + 15) & ~15ull);
     uint64_t at = st->h_sc->bump;
-    if (st->big) {
+    uint64_t pool_old[2] = {0, 0};
+    if (d.pool) {
+        CU(cudaMemcpy(pool_old, d.p_off + 2 * j, 16, cudaMemcpyDeviceToHost));
+    } else if (st->big) {
         const int r = big_reserve(st, need, &at);
         if (r == QCS_E_NOMEM) return set_err(QCS_E_NOMEM, "block arena exhausted");
         if (r) return r;
@@ -1701,9 +1641,15 @@ int qcs_import_blocks(qcs_dev_state_t st, uint64_t j, const uint8_t* buf, uint64
     const int cur = st->h_sc->cur;
     uint64_t new_off[2];
     for (int c = 0; c < 2; ++c) {
-        new_off[c] = at;
-        if (plen[c]) CU(cudaMemcpy(d.arena[cur] + at, buf + poff[c], plen[c], cudaMemcpyHostToDevice));
-        at += (plen[c] + 15) & ~15ull;
+        if (d.pool) {
+            if (plen[c] > d.slot_cap) return set_err(QCS_E_BAD_VALUE, "block payload larger than any valid block");
+            const uint64_t g = 2 * j + c;
+            new_off[c] = (2 * g + 1 - ((pool_old[c] / d.slot_cap) & 1)) * d.slot_cap;
+        } else {
+            new_off[c] = at;
+            at += (plen[c] + 15) & ~15ull;
+        }
+        if (plen[c]) CU(cudaMemcpy(d.arena[cur] + new_off[c], buf + poff[c], plen[c], cudaMemcpyHostToDevice));
     }
     // validate into a scratch side table first so a bad block leaves the state intact
     uint64_t old_off[2], old_len[2];
@@ -1766,7 +1712,7 @@ __global__ void __launch_bounds__(128) k_pack_copy(Dev d, uint8_t* img, const Pa
     const uint4* s4 = reinterpret_cast<const uint4*>(d.arena[d.sc->cur] + d.p_off[g]);
     uint4* d4 = reinterpret_cast<uint4*>(img + e.off[c]);
     for (uint64_t i = threadIdx.x; i < (e.len[c] + 15) / 16; i += blockDim.x) d4[i] = s4[i];
-    const SideEntry* ss = d.side + g * d.nsub;
+    const SideEntry* ss = side_of(d, g);
     SideEntry* ds = reinterpret_cast<SideEntry*>(img + e.soff) + (uint64_t)c * d.nsub;
     for (uint64_t i = threadIdx.x; i < d.nsub; i += blockDim.x) ds[i] = ss[i];
 }
@@ -1780,10 +1726,20 @@ __global__ void __launch_bounds__(128) k_unpack_stage(Dev d, LevelTag lt, const 
     const int c = (int)(blockIdx.x & 1);
     const PackEntry& e = ent[i0 + loc];
     const uint4* s4 = reinterpret_cast<const uint4*>(img + e.off[c]);
-    uint4* d4 = reinterpret_cast<uint4*>(d.slot_out + (2 * loc + c) * d.slot_cap);
+    uint8_t* dpay;
+    SideEntry* ds;
+    if (d.pool) {  // straight into the plane's other slot; k_pool_commit flips
+        const uint64_t g = 2 * (e.j ^ xr) + c;
+        const int other = 1 - pool_sel(d, g);
+        dpay = d.arena[0] + (2 * g + other) * d.slot_cap;
+        ds = d.side + (2 * g + other) * d.nsub;
+    } else {
+        dpay = d.slot_out + (2 * loc + c) * d.slot_cap;
+        ds = d.slot_side + (2 * loc + c) * d.nsub;
+    }
+    uint4* d4 = reinterpret_cast<uint4*>(dpay);
     for (uint64_t i = threadIdx.x; i < (e.len[c] + 15) / 16; i += blockDim.x) d4[i] = s4[i];
     const SideEntry* ss = reinterpret_cast<const SideEntry*>(img + e.soff) + (uint64_t)c * d.nsub;
-    SideEntry* ds = d.slot_side + (2 * loc + c) * d.nsub;
     for (uint64_t i = threadIdx.x; i < d.nsub; i += blockDim.x) ds[i] = ss[i];
     if (threadIdx.x == 0) {
         const uint64_t j = e.j ^ xr;
@@ -1908,8 +1864,8 @@ int qcs_unpack_strides(qcs_dev_state_t st, const void* dev_buf, uint64_t len, ui
             if (rc < 0) return report_device_error(st);
             if (rc) return rc;
         } else {
-            k_commit_plan<<<1, 1024, 0, st->stream>>>(d, m, gen);
-            k_commit_copy<<<(unsigned)(2 * d.NS), 256, 0, st->stream>>>(d, st->lt, gen);
+            k_make_jobs_reset_cin<<<1, 1, 0, st->stream>>>(d);
+            k_pool_commit<<<(unsigned)((2 * m + 255) / 256), 256, 0, st->stream>>>(d, st->lt, m);
             st->launches += 2;
         }
         k_unpack_finish<<<(unsigned)((m + 127) / 128), 128, 0, st->stream>>>(d, dent, i0, m, xor_mask);

@@ -82,6 +82,8 @@ struct FusedArgs {
     uint64_t n;                   // elements per plane (stride length)
     const uint8_t* pending;       // per slot (null = all)
     int max_rounds;               // event rounds before the neighbour-exit repair (>= 1)
+    int pool;                     // small layout: out / side / side_in are the plane
+                                  // slot pools (two slots per plane, p_off selects)
     uint64_t slot_base;           // first slot of this launch (tables are global,
                                   // out / side / X buffers are launch-local)
     int snap;
@@ -464,8 +466,18 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
 
     const CodecParams cp = a.cp;
     const uint64_t n = a.n;
-    uint8_t* out = a.out + (2 * slot + comp) * a.cap;
-    SideEntry* side = a.side + (2 * slot + comp) * a.nsub;
+    uint8_t* out;
+    SideEntry* side;
+    int live_sel = 0;
+    if (a.pool) {  // write the plane's other slot; the commit flips
+        const uint64_t g = 2 * a.job_stride[gslot] + comp;
+        live_sel = (int)((a.p_off[g] / a.cap) & 1);
+        out = a.out + (2 * g + 1 - live_sel) * a.cap;
+        side = a.side + (2 * g + 1 - live_sel) * a.nsub;
+    } else {
+        out = a.out + (2 * slot + comp) * a.cap;
+        side = a.side + (2 * slot + comp) * a.nsub;
+    }
     double* xl = xs + (pl * LPL + lane) * XS_STRIDE;
     int16_t* cl = code + (pl * LPL + lane) * CODE_STRIDE;
     PlaneCarry& C = S.carry[pl];
@@ -486,7 +498,7 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
         in_codec = a.p_codec[gpl];
         in_td = 2.0 * a.p_delta[gpl];
         in_scale = a.scale[in_stride];
-        in_side = a.side_in + gpl * a.nsub;
+        in_side = a.pool ? a.side_in + (2 * gpl + live_sel) * a.nsub : a.side_in + gpl * a.nsub;
     }
     double m8[8];
 #pragma unroll
