@@ -12,7 +12,7 @@
 //                       k_ladder (compress_stride_adaptive / joint pair
 //                       ladder, aalc.cpp:117-138, 337-356)
 //     [k_wave_commit]  wave layout: install the wave's blocks
-//   k_commit_plan / k_commit_copy  staged commit into the block arena (small layout)
+//   k_pool_commit   staged commit (small layout: flip each plane to its other slot)
 //   k_norm          lazy renormalisation + GateRecord (aalc.cpp:410-419, 612-631)
 // All launches are stream-ordered; in the small layout the host only
 // synchronises at API boundaries.  A device error word makes every later
@@ -152,6 +152,12 @@ struct Dev {
     unsigned long long* counters;  // [16] device diagnostics
 };
 
+// per-plane codec/delta of the chosen level, kept with the slot
+struct LevelTag {
+    int8_t* slot_codec;   // [NS]
+    double* slot_delta;   // [NS]
+};
+
 __global__ void k_make_jobs_reset_cin(Dev d) { d.sc->gate_cin = 0; }
 
 __device__ __forceinline__ int pool_sel(const Dev& d, uint64_t g) { return (int)((d.p_off[g] / d.slot_cap) & 1); }
@@ -162,15 +168,17 @@ __device__ __forceinline__ SideEntry* side_of(const Dev& d, uint64_t g)
     return d.pool ? d.side + (2 * g + pool_sel(d, g)) * d.nsub : d.side + g * d.nsub;
 }
 
-__global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen)
+__global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen, LevelTag lt, int codec0, double delta0)
 {
-    if (blockIdx.x == 0 && threadIdx.x == 0) d.sc->gate_cin = 0;  // wave layout accumulates it
+    if (blockIdx.x == 0 && threadIdx.x == 0) d.sc->gate_cin = 0;  // the commits accumulate it
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t j = slot_stride(p, s);
         d.job_stride[s] = j;
         d.pending[s] = 1;
         d.slot_of[j] = (int64_t)((gen << 32) | s);
+        lt.slot_codec[s] = (int8_t)codec0;  // ladder level 0
+        lt.slot_delta[s] = delta0;
     }
 }
 
@@ -390,11 +398,6 @@ __global__ void k_ladder(Dev d, Plan p, uint64_t u0, uint64_t u1, double delta, 
     }
 }
 
-// per-plane codec/delta of the chosen level, kept with the slot
-struct LevelTag {
-    int8_t* slot_codec;   // [NS]
-    double* slot_delta;   // [NS]
-};
 
 __global__ void k_tag_level(Dev d, LevelTag lt, uint64_t s0, uint64_t s1, int codec, double delta)
 {
@@ -426,6 +429,56 @@ __global__ void k_pool_commit(Dev d, LevelTag lt, uint64_t n_slots)
         d.sum_sq[j] = d.slot_sum[slot];
         d.scale[j] = 1.0;
     }
+}
+
+// The last ladder level (as k_ladder with last_level) fused with the small
+// layout's commit (as k_pool_commit) for every slot of the unit.
+__global__ void k_ladder_commit(Dev d, LevelTag lt, Plan p, double delta, double theta)
+{
+    if (d.sc->err) return;
+    const uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (u >= p.n_units) return;
+    const uint64_t s0 = p.pair ? 2 * u : u;
+    const int ns = p.pair ? 2 : 1;
+    const uint64_t bytes_in = d.L * 16;
+    if (d.pending[s0]) {
+        double r[2];
+        uint64_t bo[2];
+        for (int k = 0; k < ns; ++k) {
+            const uint64_t s = s0 + k;
+            bo[k] = (HEADER_BYTES + d.slot_len[2 * s]) + (HEADER_BYTES + d.slot_len[2 * s + 1]);
+            r[k] = (double)bytes_in / (double)bo[k];
+        }
+        for (int k = 0; k < ns; ++k) {
+            const uint64_t s = s0 + k;
+            qcs_stride_report& rep = d.reports[s];
+            rep.stride_index = d.job_stride[s];
+            rep.bytes_in = bytes_in;
+            rep.bytes_out = bo[k];
+            rep.chosen_delta = delta;
+            rep.ratio = r[k];
+            rep.threshold_met = r[k] >= theta;
+            rep.pad_ = 0;
+            d.pending[s] = 0;
+        }
+    }
+    unsigned long long cin = 0;
+    for (int k = 0; k < ns; ++k) {
+        const uint64_t s = s0 + k;
+        const uint64_t j = d.job_stride[s];
+        for (int c = 0; c < 2; ++c) {
+            const uint64_t g = 2 * j + c;
+            const int sel = pool_sel(d, g);
+            cin += HEADER_BYTES + d.p_len[g];
+            d.p_off[g] = (2 * g + 1 - sel) * d.slot_cap;
+            d.p_len[g] = d.slot_len[2 * s + c];
+            d.p_codec[g] = lt.slot_codec[s];
+            d.p_delta[g] = lt.slot_delta[s];
+        }
+        d.sum_sq[j] = d.slot_sum[s];
+        d.scale[j] = 1.0;
+    }
+    atomicAdd((unsigned long long*)&d.sc->gate_cin, cin);
 }
 
 // Small layout basis state (aalc.cpp:140-174): every plane's slot 0 holds the
@@ -1010,7 +1063,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     const uint64_t gen = ++st->gen;
 
     prof_start(st, 5);
-    k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen);
+    k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen, st->lt, lad[0] > 0.0 ? 1 : 0, lad[0]);
     prof_stop(st);
     ++st->launches;
     if (p.reflect && given_mean) {  // sharded run: mean combined across ranks
@@ -1092,18 +1145,26 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             a.sumsq = d.slot_sum;
             a.cp = make_params(lad[k]);
             a.counters = d.counters;
-            prof_start(st, 5);
-            k_tag_level<<<(unsigned)grid_for(nw), 256, 0, s>>>(d, st->lt, s0, s1, a.cp.lossy ? 1 : 0, lad[k]);
-            prof_stop(st);
-            ++st->launches;
+            if (k > 0) {  // level 0 was tagged by k_make_jobs
+                prof_start(st, 5);
+                k_tag_level<<<(unsigned)grid_for(nw), 256, 0, s>>>(d, st->lt, s0, s1, a.cp.lossy ? 1 : 0, lad[k]);
+                prof_stop(st);
+                ++st->launches;
+            }
             prof_start(st, 2);
             int rc = launch_fused(a, fm, fm == FM_PAIR ? (u1 - u0) : nw, s);
             prof_stop(st);
             if (rc) return rc;
             ++st->launches;
-            prof_start(st, 5);
-            k_ladder<<<(unsigned)((u1 - u0 + 127) / 128), 128, 0, s>>>(d, p, u0, u1, lad[k], theta, k == nl - 1);
-            prof_stop(st);
+            if (!st->big && k == nl - 1) {  // last level + commit in one kernel
+                prof_start(st, 3);
+                k_ladder_commit<<<(unsigned)((p.n_units + 127) / 128), 128, 0, s>>>(d, st->lt, p, lad[k], theta);
+                prof_stop(st);
+            } else {
+                prof_start(st, 5);
+                k_ladder<<<(unsigned)((u1 - u0 + 127) / 128), 128, 0, s>>>(d, p, u0, u1, lad[k], theta, k == nl - 1);
+                prof_stop(st);
+            }
             ++st->launches;
         }
         if (st->big) {
@@ -1115,10 +1176,6 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         }
     }
     prof_start(st, 3);
-    if (!st->big) {
-        k_pool_commit<<<(unsigned)((2 * n_slots + 255) / 256), 256, 0, s>>>(d, st->lt, n_slots);
-        ++st->launches;
-    }
     k_norm<<<1, NORM_THREADS, 0, s>>>(d, n_slots, rec_index < 0 ? 0 : (uint64_t)rec_index, gate_index, renorm);
     prof_stop(st);
     ++st->launches;
