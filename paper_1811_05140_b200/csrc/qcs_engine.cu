@@ -677,16 +677,18 @@ int launch_fused_t(const FusedArgs& a, uint64_t grid, cudaStream_t s)
     static bool set = false;
     if (!set) {
         CU(cudaFuncSetAttribute(k_fused<L, NPL, LPL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)FUSED_SMEM));
+                                (int)FusedLayout<NPL * LPL>::SMEM));
         set = true;
     }
     if (grid == 0) return 0;
-    k_fused<L, NPL, LPL, MODE><<<(unsigned)grid, NPL * LPL, FUSED_SMEM, s>>>(a);
+    k_fused<L, NPL, LPL, MODE><<<(unsigned)grid, NPL * LPL, FusedLayout<NPL * LPL>::SMEM, s>>>(a);
     CU(cudaGetLastError());
     return 0;
 }
 
-enum { FM_LOCAL = 0, FM_FAR = 1, FM_PAIR = 2, FM_RAW1 = 3, FM_RAW2 = 4 };
+// FM_*_W: 2 planes x 256 lanes (one CTA per SM), for gates with fewer units
+// than SMs, where per-stride parallelism is all there is
+enum { FM_LOCAL = 0, FM_LOCAL_W = 1, FM_RAW2_W = 2, FM_RAW1 = 3, FM_RAW2 = 4 };
 
 int codec_max_rounds()
 {
@@ -699,8 +701,8 @@ int launch_fused(const FusedArgs& a, int fm, uint64_t grid, cudaStream_t s)
     const bool L = a.cp.lossy != 0;
     switch (fm) {
         case FM_LOCAL: return L ? launch_fused_t<true, 2, 128, MODE_LOCAL>(a, grid, s) : launch_fused_t<false, 2, 128, MODE_LOCAL>(a, grid, s);
-        case FM_FAR: return L ? launch_fused_t<true, 2, 64, MODE_FAR>(a, grid, s) : launch_fused_t<false, 2, 64, MODE_FAR>(a, grid, s);
-        case FM_PAIR: return L ? launch_fused_t<true, 4, 64, MODE_PAIR>(a, grid, s) : launch_fused_t<false, 4, 64, MODE_PAIR>(a, grid, s);
+        case FM_LOCAL_W: return L ? launch_fused_t<true, 2, 256, MODE_LOCAL>(a, grid, s) : launch_fused_t<false, 2, 256, MODE_LOCAL>(a, grid, s);
+        case FM_RAW2_W: return L ? launch_fused_t<true, 2, 256, MODE_RAW>(a, grid, s) : launch_fused_t<false, 2, 256, MODE_RAW>(a, grid, s);
         case FM_RAW1: return L ? launch_fused_t<true, 1, 256, MODE_RAW>(a, grid, s) : launch_fused_t<false, 1, 256, MODE_RAW>(a, grid, s);
         default: return L ? launch_fused_t<true, 2, 128, MODE_RAW>(a, grid, s) : launch_fused_t<false, 2, 128, MODE_RAW>(a, grid, s);
     }
@@ -1083,7 +1085,8 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     else if (p.kind <= 1 && (1ull << p.t) >= 4096) dg = DG_FAR;
     else if (p.kind <= 1 && st->split_local && (1ull << p.t) >= DG_HALF) dg = DG_FAR;
     else if (p.kind <= 1 && st->split_local && d.L >= DG_IN_CH) dg = DG_IN;
-    const int fm = dg >= 0 ? FM_RAW2 : (p.pair ? FM_PAIR : FM_LOCAL);
+    const bool wide = n_slots < 148 && d.L >= 2 * 4096;
+    const int fm = dg >= 0 ? (wide ? FM_RAW2_W : FM_RAW2) : (wide ? FM_LOCAL_W : FM_LOCAL);  // pairs always split
     if (dg >= 0) {
         static bool dg_attr = false;
         if (!dg_attr) {
@@ -1131,7 +1134,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             a.max_rounds = st->max_rounds;
             a.cta_trace = st->cta_trace;
             a.snap = 1;
-            if (fm == FM_RAW2) {  // split path: gated, snapped planes in X
+            if (fm == FM_RAW2 || fm == FM_RAW2_W) {  // split path: gated, snapped planes in X
                 a.X = d.X;
                 a.x_plane_stride = d.L;
                 a.snap = 0;
@@ -1152,7 +1155,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
                 ++st->launches;
             }
             prof_start(st, 2);
-            int rc = launch_fused(a, fm, fm == FM_PAIR ? (u1 - u0) : nw, s);
+            int rc = launch_fused(a, fm, nw, s);
             prof_stop(st);
             if (rc) return rc;
             ++st->launches;

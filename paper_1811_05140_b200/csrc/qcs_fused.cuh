@@ -14,9 +14,6 @@
 // CTA shapes (template NPL planes x LPL lanes, SUB=32 elements per lane):
 //   MODE_LOCAL  2 x 128  one stride, gate partner inside the 4096-element chunk
 //                        (or flip / reflect / plain_single)
-//   MODE_FAR    2 x 64   one stride, partner chunk 2^t away (t >= 11) decoded
-//                        into the spare half of the chunk buffer
-//   MODE_PAIR   4 x 64   lo + hi stride of a cross-stride pair unit
 //   MODE_RAW    1|2 x .  input already uncompressed in HBM (codec API)
 // The encoder half is the verified-speculation codec of qcs_codec.cuh
 // generalised to NPL planes.
@@ -28,33 +25,40 @@ namespace qcs {
 
 constexpr int GRP = 4;  // elements per independent group in the chain loops
 
-enum : int { MODE_RAW = 0, MODE_LOCAL = 1, MODE_FAR = 2, MODE_PAIR = 3 };
+enum : int { MODE_RAW = 0, MODE_LOCAL = 1 };
 
-struct FusedShared {
-    double entryP[256];
-    double exitP[256];
-    RunFn fincl[256];
-    uint64_t bstart[256];
-    uint64_t runtok[256];
-    uint64_t runw[256];
-    int8_t ftype[264];
-    RunFn wfn[8];
-    long long wesc_i[8];
-    double wesc_v[8];
-    uint64_t wsum[8];
-    long long wmin[8];
+// Shared state of one encoder CTA with NT = planes x lanes threads.
+template <int NT>
+struct FusedSharedT {
+    double entryP[NT];
+    double exitP[NT];
+    RunFn fincl[NT];
+    uint64_t bstart[NT];
+    uint64_t runtok[NT];
+    uint64_t runw[NT];
+    int8_t ftype[NT + 8];
+    RunFn wfn[NT / 32];
+    long long wesc_i[NT / 32];
+    double wesc_v[NT / 32];
+    uint64_t wsum[NT / 32];
+    long long wmin[NT / 32];
     PlaneCarry carry[4];
     double s[2];  // exact running sum of squares per stride
     uint64_t mvmax;
 };
 
-constexpr size_t FUSED_XS_BYTES = sizeof(double) * 256 * XS_STRIDE;
 // code rows padded to 34 int16 (17 words) so the lanes' row accesses (32-bit
 // pairs in lane_masks, 16-bit in the chain) hit distinct banks
 constexpr int CODE_STRIDE = SUB + 2;
-constexpr size_t FUSED_CODE_BYTES = sizeof(int16_t) * 256 * CODE_STRIDE;
-constexpr size_t FUSED_S_OFF = (FUSED_XS_BYTES + FUSED_CODE_BYTES + 15) & ~size_t(15);
-constexpr size_t FUSED_SMEM = FUSED_S_OFF + sizeof(FusedShared);
+template <int NT>
+struct FusedLayout {
+    static constexpr size_t XS_BYTES = sizeof(double) * NT * XS_STRIDE;
+    static constexpr size_t CODE_BYTES = sizeof(int16_t) * NT * CODE_STRIDE;
+    static constexpr size_t S_OFF = (XS_BYTES + CODE_BYTES + 15) & ~size_t(15);
+    static constexpr size_t SMEM = S_OFF + sizeof(FusedSharedT<NT>);
+};
+static_assert(FusedLayout<256>::SMEM <= 113 * 1024, "two 256-thread encoder CTAs per SM");
+static_assert(FusedLayout<512>::SMEM <= 227 * 1024, "one 512-thread encoder CTA per SM");
 
 struct FusedArgs {
     // ---- input: block store (MODE_LOCAL/FAR/PAIR) ----
@@ -131,8 +135,8 @@ __device__ __forceinline__ void put_words(uint8_t* p, const double* v, int n)
 }
 
 // ---- scans over the WPL warps of one plane --------------------------------
-template <int WPL>
-__device__ __forceinline__ RunFn fscan_fn(RunFn F, FusedShared& S, int pl)
+template <int WPL, typename FS>
+__device__ __forceinline__ RunFn fscan_fn(RunFn F, FS& S, int pl)
 {
     const int wl = threadIdx.x & 31, w = threadIdx.x >> 5;
     RunFn inc = F;
@@ -150,8 +154,8 @@ __device__ __forceinline__ RunFn fscan_fn(RunFn F, FusedShared& S, int pl)
     return fn_compose(pre, inc);
 }
 
-template <int WPL>
-__device__ __forceinline__ uint64_t fscan_sum(uint64_t v, FusedShared& S, int pl, uint64_t& total)
+template <int WPL, typename FS>
+__device__ __forceinline__ uint64_t fscan_sum(uint64_t v, FS& S, int pl, uint64_t& total)
 {
     const int wl = threadIdx.x & 31, w = threadIdx.x >> 5;
     uint64_t inc = v;
@@ -171,8 +175,8 @@ __device__ __forceinline__ uint64_t fscan_sum(uint64_t v, FusedShared& S, int pl
     return pre + inc - v;
 }
 
-template <int WPL>
-__device__ __forceinline__ long long fscan_last(long long idx, double val, FusedShared& S, int pl,
+template <int WPL, typename FS>
+__device__ __forceinline__ long long fscan_last(long long idx, double val, FS& S, int pl,
                                                 double& out_val)
 {
     const int wl = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -219,8 +223,8 @@ __device__ __forceinline__ double tsq_g(double* xs, int g, int k)
     return __dadd_rn(__dmul_rn(r, r), __dmul_rn(i, i));
 }
 
-template <int LPL>
-__device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FusedShared& S, unsigned long long* counters)
+template <int LPL, typename FS>
+__device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigned long long* counters)
 {
     constexpr int GT = 2 * LPL;            // threads (the CTA: one stride)
     constexpr int GW = GT / 32;            // warps
@@ -443,7 +447,7 @@ __device__ __forceinline__ double lane_chain(const CodecParams& cp, const double
     } while (0)
 
 template <bool LOSSY, int NPL, int LPL, int MODE>
-__global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
+__global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : 2)) k_fused(FusedArgs a)
 {
     unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long ph_t = clock64();
@@ -454,15 +458,17 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
     const int pl = tid / LPL;
     const int lane = tid % LPL;
     // output slot of this plane
-    const uint64_t slot = MODE == MODE_PAIR ? 2ull * b + (pl >> 1) : (uint64_t)b;
-    const int comp = MODE == MODE_PAIR ? (pl & 1) : pl;
+    const uint64_t slot = (uint64_t)b;
+    const int comp = pl;
     const uint64_t gslot = a.slot_base + slot;  // global slot (tables)
-    if (a.pending && !a.pending[a.slot_base + (MODE == MODE_PAIR ? 2ull * b : (uint64_t)b)]) return;
+    if (a.pending && !a.pending[a.slot_base + (uint64_t)b]) return;
 
     extern __shared__ __align__(16) unsigned char smem[];
     double* xs = reinterpret_cast<double*>(smem);
-    int16_t* code = reinterpret_cast<int16_t*>(smem + FUSED_XS_BYTES);
-    FusedShared& S = *reinterpret_cast<FusedShared*>(smem + FUSED_S_OFF);
+    using FS = FusedSharedT<NPL * LPL>;
+    using LY = FusedLayout<NPL * LPL>;
+    int16_t* code = reinterpret_cast<int16_t*>(smem + LY::XS_BYTES);
+    FS& S = *reinterpret_cast<FS*>(smem + LY::S_OFF);
 
     const CodecParams cp = a.cp;
     const uint64_t n = a.n;
@@ -503,7 +509,7 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
     double m8[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) m8[i] = a.u[i];
-    const uint64_t hb = (MODE == MODE_LOCAL || MODE == MODE_FAR) && a.kind <= 1 ? (1ull << a.t) : 0;
+    const uint64_t hb = MODE == MODE_LOCAL && a.kind <= 1 ? (1ull << a.t) : 0;
 
     if (lane == 0) {
         C.P = 0.0;
@@ -579,33 +585,9 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
                 __syncthreads();
             }
             if (cnt > 0) decode_sub(src, in_codec, in_td, in_side[e0 / SUB], cnt, xl, in_scale);
-            if (MODE == MODE_FAR && cnt > 0) {
-                const uint64_t pe0 = e0 ^ hb;
-                decode_sub(in_bytes, in_codec, in_td, in_side[pe0 / SUB], cnt,
-                           xs + ((pl + 2) * LPL + lane) * XS_STRIDE, in_scale);
-            }
             __syncthreads();
             // gate (run_plan_unit, gate.cpp:405-454)
-            if (MODE == MODE_PAIR) {
-                for (int i = tid; i < n_it; i += NPL * LPL) {
-                    if (a.local_ctl >= 0 && !(((base + i) >> a.local_ctl) & 1)) continue;
-                    pair_update(m8, xrow<LPL>(xs, 0, i), xrow<LPL>(xs, 1, i), xrow<LPL>(xs, 2, i),
-                                xrow<LPL>(xs, 3, i));
-                }
-            } else if (MODE == MODE_FAR) {
-                for (int i = tid; i < n_it; i += NPL * LPL) {
-                    const uint64_t gi = base + i;
-                    const uint64_t lo_idx = gi & ~hb;
-                    if (a.local_ctl >= 0 && !((lo_idx >> a.local_ctl) & 1)) continue;
-                    const double sr = xrow<LPL>(xs, 0, i), si = xrow<LPL>(xs, 1, i);
-                    const double pr = xrow<LPL>(xs, 2, i), pi = xrow<LPL>(xs, 3, i);
-                    double r, im;
-                    if (!(gi & hb)) pair_lo(m8, sr, si, pr, pi, r, im);
-                    else pair_hi(m8, pr, pi, sr, si, r, im);
-                    xrow<LPL>(xs, 0, i) = r;
-                    xrow<LPL>(xs, 1, i) = im;
-                }
-            } else {  // MODE_LOCAL
+            {  // MODE_LOCAL
                 if (a.kind <= 1) {
                     const uint64_t lo_mask = hb - 1;
                     for (int q = tid; q < n_it / 2; q += NPL * LPL) {
@@ -952,9 +934,7 @@ __global__ void __launch_bounds__(NPL * LPL, 2) k_fused(FusedArgs a)
     if (tid == 0 && a.cta_trace)
         for (int i = 0; i < 8; ++i) a.cta_trace[8 * (a.slot_base + (uint64_t)b) + i] = ph_acc[i];
     if (lane == 0) a.out_len[2 * gslot + comp] = C.out_pos;
-    if (a.sumsq && (tid % (2 * LPL)) == 0)
-        a.sumsq[a.slot_base + (MODE == MODE_PAIR ? 2ull * b + tid / (2 * LPL) : (uint64_t)b)] =
-        S.s[tid / (2 * LPL)];
+    if (a.sumsq && tid == 0) a.sumsq[gslot] = S.s[0];
 }
 
 }  // namespace qcs
