@@ -8,15 +8,18 @@
 //   snap_zeros                core.cpp:39-47
 //   compress (one ladder level) codec.cpp:118-250
 //   stored_sum_sq             aalc.cpp:46-52, core.cpp:30-37
-// Everything stays on chip between the compressed input and the compressed
-// output; nothing uncompressed goes back to HBM.
+// MODE_LOCAL keeps everything on chip between the compressed input and the
+// compressed output.  MODE_RAW encodes planes already decompressed and gated
+// into HBM (k_decode_gate, the split path for cross-chunk partners; or the
+// codec API's input).
 //
-// CTA shapes (template NPL planes x LPL lanes, SUB=32 elements per lane):
-//   MODE_LOCAL  2 x 128  one stride, gate partner inside the 4096-element chunk
-//                        (or flip / reflect / plain_single)
-//   MODE_RAW    1|2 x .  input already uncompressed in HBM (codec API)
-// The encoder half is the verified-speculation codec of qcs_codec.cuh
-// generalised to NPL planes.
+// CTA shapes (template NPL planes x LPL lanes, SUB = 32 elements per lane):
+//   2 x 128  one stride per CTA, two CTAs per SM (the usual case)
+//   2 x 256  one stride per CTA, one per SM: gates with fewer units than SMs
+//   1 x 256  codec API, one plane
+// The encoder: self-correcting event rounds over lane-serial reference
+// chains, an exact emulation of the stored sum of squares, and a bitmask
+// tokenizer.
 #pragma once
 
 #include "qcs_codec.cuh"
