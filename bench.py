@@ -56,10 +56,10 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def workload():
-    marked = next(cc.splitmix64(SEED)) & ((1 << N_QUBITS) - 1)
-    prog = cc.build_grover_gate_form(N_QUBITS, marked, ITERS)
-    delta = cc.pow2_bound(EPS, N_QUBITS)
+def workload(n=N_QUBITS):
+    marked = next(cc.splitmix64(SEED)) & ((1 << n) - 1)
+    prog = cc.build_grover_gate_form(n, marked, ITERS)
+    delta = cc.pow2_bound(EPS, n)
     return prog, marked, delta
 
 
@@ -186,9 +186,22 @@ def cpu_baseline(prog, delta):
                       "workers = all cores"}
 
 
+def g_shift(n):
+    """Fewer gates per step for larger states (each gate costs 2^n)."""
+    return max(0, n - N_QUBITS)
+
+
 def run_reference(args, rank, world):
-    prog, marked, delta = workload()
+    """The unmodified reference (oracle/_ref) on this host's cores, on the same
+    workload as the B200 arm: C2, or at N > 1 the weak-scaled 24 + log2 N
+    qubit state the sharded arm runs (rank 0 only)."""
+    g = max(0, world.bit_length() - 1)
+    n = N_QUBITS + g
+    prog, marked, delta = workload(n)
     cfg = config_dict(marked, delta, "reference CPU, rank 0 only")
+    if world > 1:
+        cfg.update({"workload": f"C2 weak-scaled: grover-{n} gate form (the {world}-GPU arm's state)",
+                    "n_qubits": n, "delta": delta, "ladder": [delta], "step": f"a window of the grover-{n} gates"})
     if rank != 0:
         return 0
     ref, why = reference_lib()
@@ -197,10 +210,12 @@ def run_reference(args, rank, world):
         return 0
     text = cc.print_circuit(prog)
     st = ref.state(text, STRIDE_BITS, 0)
-    st.apply(0, N_QUBITS, [delta], 1.0, 0)                     # untimed prologue
+    st.apply(0, n, [delta], 1.0, 0)                            # untimed prologue
     total = args.warmup + args.steps
-    g = GATES_PER_STEP if total <= 12 else max(10, (12 * GATES_PER_STEP) // total)
-    pos = N_QUBITS
+    gps = 2 * n + 2
+    g = gps if total <= 12 else max(10, (12 * gps) // total)
+    g = max(4, g >> g_shift(n))
+    pos = n
     for _ in range(args.warmup):
         st.apply(pos, pos + g, [delta], 1.0, 0)
         pos += g
@@ -208,7 +223,7 @@ def run_reference(args, rank, world):
     wall0 = time.perf_counter()
     for _ in range(args.steps):
         if pos + g > len(prog.gates):
-            pos = N_QUBITS  # wrap (state keeps evolving; rate is what is measured)
+            pos = n  # wrap (state keeps evolving; rate is what is measured)
         r = st.apply(pos, pos + g, [delta], 1.0, 0)
         pos += g
         ns += r["gate_ns"]
@@ -216,7 +231,7 @@ def run_reference(args, rank, world):
     wall = time.perf_counter() - wall0
     value = upd / (ns * 1e-9)
     cores = ref.max_threads()
-    sample = f"{args.steps} steps x {g} consecutive C2 gates after the H^24 prologue, workers = {cores}"
+    sample = f"{args.steps} steps x {g} consecutive gates of grover-{n} after the H^{n} prologue, workers = {cores}"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ns * 1e-6 / max(1, args.steps),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
