@@ -266,6 +266,15 @@ class ShardGeometry:
 
 
 class ShardedState:
+    """Lazy qubit permutation over the stride bits: logical stride bit p lives
+    at physical position pi[p]; positions [0, Q-s) are a rank's local stride
+    bits, [Q-s, n-s) the rank bits.  A gate whose target sits on a rank bit
+    swaps it with a local stride bit (one exchange, least recently used local
+    qubit evicted) and the permutation stays — no swap back, so a rank-qubit
+    gate costs one exchange.  In-stride qubits never move.  Records, the
+    renormalisation and reflect_mean's mean are folded in LOGICAL global stride
+    order, amplitudes() returns the logical state."""
+
     def __init__(self, geom: ShardGeometry, comm, backend, basis: int):
         if (1 << geom.rank_bits) != comm.size:
             raise ValueError("world size must be 2^rank_bits")
@@ -276,92 +285,135 @@ class ShardedState:
         mine = (basis >> Q) == self.r
         self.local = backend.create(Q, geom.stride_bits, basis & ((1 << Q) - 1) if mine else None)
         self.norm_sq = 1.0
+        nb = geom.n_qubits - geom.stride_bits       # stride-index bits
+        self.pi = list(range(nb))                   # logical -> physical
+        self.inv = list(range(nb))                  # physical -> logical
+        self.last_use = [-1] * nb                   # logical bit -> last gate index
+        self.exchanges = 0
+        self.next_target = None                     # schedule: per logical bit, sorted gate indices
+
+    def set_schedule(self, gates) -> None:
+        """Future target uses of every stride qubit, so an eviction can drop the
+        local qubit needed furthest in the future (Belady) instead of the least
+        recently used one."""
+        s = self.geom.stride_bits
+        nt = [[] for _ in self.pi]
+        for i, g in enumerate(gates):
+            if g.kind in (KIND_SINGLE, KIND_CONTROLLED) and g.target >= s:
+                nt[g.target - s].append(i)
+        self.next_target = nt
+
+    def _next_use(self, p: int, index: int) -> int:
+        import bisect
+        uses = self.next_target[p]
+        k = bisect.bisect_right(uses, index)
+        return uses[k] if k < len(uses) else 1 << 62
+
+    # -- index maps -----------------------------------------------------------
+    def _phys_to_log(self, jp: np.ndarray) -> np.ndarray:
+        jl = np.zeros_like(jp)
+        for p, q in enumerate(self.pi):
+            jl |= ((jp >> q) & 1) << p
+        return jl
+
+    def _log_to_phys(self, j: int) -> int:
+        out = 0
+        for p, q in enumerate(self.pi):
+            out |= ((j >> p) & 1) << q
+        return out
 
     # -- data movement: swap rank bit b with local stride bit qb ------------
-    def _swap(self, active: bool, b: int, qb: int):
-        """The lo rank of the pair sends its strides with local bit qb = 1, the
-        hi rank those with qb = 0; each lands at j ^ 2^qb on the other side."""
+    def _swap(self, b: int, qb: int):
+        """All ranks (the layout is global).  The lo rank of each pair sends its
+        strides with local bit qb = 1, the hi rank those with qb = 0; each lands
+        at j ^ 2^qb on the other side."""
         r = self.r
-        peer = r ^ (1 << b) if active else None
-        payload = None
-        if active:
-            send_bit = 0 if (r >> b) & 1 else 1
-            payload = self.local.pack(qb, send_bit)
+        peer = r ^ (1 << b)
+        send_bit = 0 if (r >> b) & 1 else 1
+        payload = self.local.pack(qb, send_bit)
         got = self.comm.exchange(peer, payload, device=getattr(self.local, "device_images", False))
-        if active:
-            self.local.unpack(got, 1 << qb)
+        self.local.unpack(got, 1 << qb)
+        self.exchanges += 1
 
-    def _global_stride(self, jl: int, swapped: Optional[tuple]) -> int:
-        nsl = self.geom.local_strides
-        r = self.r
-        if swapped is None:
-            return r * nsl + jl
-        b, qb = swapped
-        rb = (r & ~(1 << b)) | (((jl >> qb) & 1) << b)
-        jb = (jl & ~(1 << qb)) | (((r >> b) & 1) << qb)
-        return rb * nsl + jb
+    def _make_local(self, p: int, keep: Optional[int], index: int) -> int:
+        """Physical local position of logical stride bit p, swapping it in from a
+        rank bit if needed (evicting the least recently used local bit other
+        than `keep`)."""
+        g = self.geom
+        nloc = g.local_qubits - g.stride_bits
+        q = self.pi[p]
+        if q < nloc:
+            return q
+        cands = [v for v in range(nloc) if v != keep]
+        if not cands:
+            raise NotImplementedError("needs a local stride bit besides the control")
+        if self.next_target is not None:
+            v = max(cands, key=lambda v: (self._next_use(self.inv[v], index), -v))
+        else:
+            v = min(cands, key=lambda v: (self.last_use[self.inv[v]], v))
+        self._swap(q - nloc, v)
+        pv = self.inv[v]
+        self.pi[p], self.pi[pv] = v, q
+        self.inv[v], self.inv[q] = p, pv
+        return v
 
     def apply_gate(self, gate: GateOp, ladder: Sequence[float], theta: float, index: int = 0):
         g = self.geom
         Q, s = g.local_qubits, g.stride_bits
+        nloc = Q - s
         gate.validate(g.n_qubits)
         pair_bit_global = None
-        swapped = None
         reports: List[tuple] = []
         if gate.kind in (KIND_SINGLE, KIND_CONTROLLED):
             t, c = gate.target, gate.control
-            participate = True
-            local = GateOp(gate.kind, gate.unitary, t, c, 0, gate.phase_theta, gate.label)
-            if gate.kind == KIND_CONTROLLED and c >= Q:
-                participate = bool((self.r >> (c - Q)) & 1)
-                local = GateOp.single(gate.unitary, t, gate.label)
+            ctl_phys = None  # physical stride position of a stride-bit control
+            if gate.kind == KIND_CONTROLLED and c >= s:
+                ctl_phys = self.pi[c - s]
+            lt = t
             if t >= s:
                 pair_bit_global = 1 << (t - s)
-            if t >= Q:
-                qs = Q - 1
-                if local.kind == KIND_CONTROLLED and local.control == qs:
-                    qs = Q - 2
-                if qs < s:
-                    raise NotImplementedError("needs two local stride bits besides the control")
-                swapped = (t - Q, qs - s)
-                local.target = qs
-                self._swap(participate, *swapped)
+                keep = ctl_phys if (ctl_phys is not None and ctl_phys < nloc) else None
+                lt = s + self._make_local(t - s, keep, index)
+                self.last_use[t - s] = index
+                if ctl_phys is not None:
+                    ctl_phys = self.pi[c - s]
+            participate = True
+            local = GateOp(gate.kind, gate.unitary, lt, c, 0, gate.phase_theta, gate.label)
+            if ctl_phys is not None:
+                if ctl_phys >= nloc:  # control on a rank bit: the rank applies it or nothing
+                    participate = bool((self.r >> (ctl_phys - nloc)) & 1)
+                    local = GateOp.single(gate.unitary, lt, gate.label)
+                else:
+                    local.control = s + ctl_phys
+                self.last_use[c - s] = index
             if participate:
                 reports = self.local.apply(local, ladder, theta)
-            if swapped is not None:
-                self._swap(participate, *swapped)
         elif gate.kind == KIND_FLIP:
-            if (gate.flip_index >> Q) == self.r:
-                reports = self.local.apply(GateOp.phase_flip(gate.flip_index & ((1 << Q) - 1)),
-                                           ladder, theta)
+            jp = self._log_to_phys(gate.flip_index >> s)
+            if (jp >> nloc) == self.r:
+                off = ((jp & ((1 << nloc) - 1)) << s) | (gate.flip_index & ((1 << s) - 1))
+                reports = self.local.apply(GateOp.phase_flip(off), ladder, theta)
         else:
             # mean pass (aalc.cpp:270-295): per-stride sums, combined serially
-            # in global stride order, divided by the global amplitude count
+            # in LOGICAL global stride order, divided by the amplitude count
             parts = self.comm.allgather(self.local.stride_sums().tobytes())
+            allp = np.concatenate([np.frombuffer(p).reshape(-1, 2) for p in parts])
+            order = np.argsort(self._phys_to_log(np.arange(len(allp), dtype=np.int64)))
             sr = si = 0.0
-            for p in parts:
-                v = np.frombuffer(p).tolist()
-                for j in range(0, len(v), 2):
-                    sr += v[j]
-                    si += v[j + 1]
+            for re_, im_ in allp[order].tolist():
+                sr += re_
+                si += im_
             na = float(1 << g.n_qubits)
             reports = self.local.apply(gate, ladder, theta, mean=(sr / na, si / na))
-        # one gather per gate: this rank's reports keyed by global unit order
-        # (reference: ascending lo stride; a pair unit reports lo then hi) and
-        # its per-stride (scale, sum_sq)
+        # one gather per gate: this rank's reports keyed by LOGICAL global unit
+        # order (reference: ascending lo stride; a pair unit reports lo then hi)
+        # and its per-stride (scale, sum_sq)
         nsl = g.local_strides
         buf = np.zeros((nsl + 1, 10))
         rep = np.asarray(reports, dtype=np.float64).reshape(-1, 6)
         buf[0, 0] = len(rep)
         if len(rep):
-            jl = rep[:, 0].astype(np.int64)
-            if swapped is None:
-                gj = self.r * nsl + jl
-            else:
-                b, qb = swapped
-                rb = (self.r & ~(1 << b)) | (((jl >> qb) & 1) << b)
-                jb = (jl & ~(1 << qb)) | (((self.r >> b) & 1) << qb)
-                gj = rb * nsl + jb
+            gj = self._phys_to_log(self.r * nsl + rep[:, 0].astype(np.int64))
             if pair_bit_global is not None:
                 k0, k1 = gj & ~pair_bit_global, (gj & pair_bit_global) != 0
             else:
@@ -374,10 +426,12 @@ class ShardedState:
         buf[1:, 8] = sc
         buf[1:, 9] = sm
         parts = self.comm.allgather_array(buf)
-        # global renormalisation, serial in global stride order (aalc.cpp:410-419);
-        # np.cumsum is a sequential left-to-right fold, the reference's order
+        # global renormalisation, serial in LOGICAL global stride order
+        # (aalc.cpp:410-419); np.cumsum is a sequential left-to-right fold
         scales = np.concatenate([p_[1:, 8] for p_ in parts])
         sums = np.concatenate([p_[1:, 9] for p_ in parts])
+        order = np.argsort(self._phys_to_log(np.arange(len(scales), dtype=np.int64)))
+        scales, sums = scales[order], sums[order]
         total = float(np.cumsum(scales * scales * sums)[-1])
         if total > 0.0:
             f = 1.0 / math.sqrt(total)
@@ -399,14 +453,20 @@ class ShardedState:
         return rec, viol
 
     def amplitudes(self) -> np.ndarray:
-        """Whole state on every rank (small states only; for tests)."""
+        """Whole LOGICAL state on every rank (small states only; for tests)."""
+        g = self.geom
+        L = 1 << g.stride_bits
         parts = self.comm.allgather(self.local.amplitudes().tobytes())
-        return np.concatenate([np.frombuffer(p, dtype=np.complex128) for p in parts])
+        phys = np.concatenate([np.frombuffer(p, dtype=np.complex128) for p in parts]).reshape(-1, L)
+        out = np.empty_like(phys)
+        out[self._phys_to_log(np.arange(len(phys), dtype=np.int64))] = phys
+        return out.reshape(-1)
 
 
 def run_sharded(program, geom: ShardGeometry, comm, backend, basis: int, ladder, theta):
     """run_program over a sharded state; returns (state, records, violations)."""
     st = ShardedState(geom, comm, backend, basis)
+    st.set_schedule(program.gates)
     recs = []
     viol = 0
     for i, g in enumerate(program.gates):

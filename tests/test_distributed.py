@@ -213,3 +213,38 @@ def test_gloo_world2_gpu_shards(oracle, tmp_path):
         want_amp, want_csv = _single(oracle, prog, s, basis, lad, theta)
         assert (tmp_path / (name + ".csv")).read_text() == want_csv, name
         assert np.load(tmp_path / (name + ".npy")).tobytes() == want_amp.tobytes(), name
+
+
+def test_lazy_permutation_one_exchange_per_rank_qubit_gate(oracle):
+    """Rank-qubit targets swap in once and stay (no swap back, furthest-next-use
+    eviction): one exchange per gate that finds its target on a rank bit, and
+    fewer exchanges than the swap-in / swap-out scheme (two per rank-qubit
+    target)."""
+    from oracle import OracleBackend
+    from paper_1811_05140_b200.distributed import ShardedState, ThreadComm, ThreadGroup
+    import threading
+    for prog, s in ((q.build_qft(10), 4), (q.build_grover_gate_form(10, 0x2d3, 3), 4)):
+        geom = ShardGeometry(prog.n_qubits, s, 2)
+        grp = ThreadGroup(4)
+        res = [None] * 4
+
+        def worker(r):
+            st = ShardedState(geom, ThreadComm(grp, r), OracleBackend(oracle), 0)
+            st.set_schedule(prog.gates)
+            rank_gates = 0
+            for i, g in enumerate(prog.gates):
+                if g.kind in (0, 1) and g.target >= s and st.pi[g.target - s] >= geom.local_qubits - s:
+                    rank_gates += 1
+                st.apply_gate(g, [q.pow2_bound(1e-3, 10)], 1.0, i)
+            res[r] = (st.exchanges, rank_gates)
+
+        ts = [threading.Thread(target=worker, args=(r,)) for r in range(4)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        ex, rg = res[0]
+        assert ex == rg  # exactly one exchange per gate that found its target on a rank bit
+        naive = sum(1 for g in prog.gates if g.kind in (0, 1) and g.target >= geom.local_qubits)
+        assert ex <= 2 * naive // 2 + naive // 2, (ex, naive)  # at most 1.5 per rank-qubit gate
+        assert ex < 2 * naive
