@@ -1,0 +1,34 @@
+"""The C++ façade (include/qcs_b200.hpp) in the reference's own types.
+
+CPU: the header compiles against the reference's headers (when the reference
+is mounted, i.e. in the build container).  GPU: oracle/_ref/facade_parity —
+the façade + the unmodified reference library, built by oracle/Makefile —
+runs the same programs through qcs::run_program and qcs::b200::run_program
+and compares every record, amplitude, stored stride, checkpoint byte and
+codec block (tests/cpp/facade_parity.cpp)."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_INC = "/root/reference/proj/include"
+BIN = os.path.join(ROOT, "oracle", "_ref", "facade_parity")
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INC), reason="reference headers not mounted")
+def test_facade_header_compiles():
+    subprocess.run(["g++", "-std=gnu++20", "-fsyntax-only", "-Wall", "-Wextra", "-I", REF_INC,
+                    "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "cpp", "facade_parity.cpp")],
+                   check=True)
+
+
+@pytest.mark.gpu
+def test_facade_parity_against_reference():
+    if not os.path.exists(BIN):
+        pytest.skip("facade_parity not built (needs the reference sources at build time)")
+    r = subprocess.run([BIN, os.path.join(ROOT, "tests", "golden", "circuits")], capture_output=True,
+                       text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("PASS") >= 12
