@@ -48,6 +48,7 @@ struct FusedSharedT {
     PlaneCarry carry[4];
     double s[2];  // exact running sum of squares per stride
     uint64_t mvmax;
+    uint64_t bar[4];  // per-plane mbarrier of the payload bulk copy (MODE_LOCAL)
 };
 
 // code rows padded to 34 int16 (17 words) so the lanes' row accesses (32-bit
@@ -525,6 +526,8 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : 2)) k_fused(
         C.closes_open = 0;
     }
     if (tid < 2) S.s[tid] = 0.0;
+    if (MODE == MODE_LOCAL && tid < NPL) mbar_init(&S.bar[tid], 1);
+    unsigned stage_phase = 0;  // parity of this plane's next bulk copy
     __syncthreads();
 
     for (uint64_t base = 0; base < n; base += ITP) {
@@ -559,8 +562,8 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : 2)) k_fused(
             __syncthreads();
         } else {
             // Stage this iteration's payload bytes of the plane in shared memory
-            // (the code buffer is free until the chain runs) with coalesced
-            // 16-byte loads, so the lanes' serial token walks read shared
+            // (the code buffer is free until the chain runs) with one TMA bulk
+            // copy (cp.async.bulk + mbarrier), so the lanes' serial token walks read shared
             // memory instead of waiting on L2 per byte.  The range runs from
             // the token covering the iteration's first element to the token
             // covering the next iteration's first one, plus that token's
@@ -579,13 +582,15 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : 2)) k_fused(
                     hi = (uint64_t)nx.off + 10 + 8 * (uint64_t)nx.skip;
                 }
                 const uint64_t nb = hi > lo ? ((hi - lo + 15) & ~uint64_t(15)) : 0;
-                if (nb <= STAGE) {
-                    const uint4* s4 = reinterpret_cast<const uint4*>(in_bytes + lo);
-                    uint4* d4 = reinterpret_cast<uint4*>(stage);
-                    for (uint64_t k = lane; k < nb / 16; k += LPL) d4[k] = s4[k];
+                if (nb > 0 && nb <= STAGE) {  // uniform over the plane's lanes
+                    // one TMA bulk copy per plane (payloads start 16-byte
+                    // aligned; the code rows are free: the previous
+                    // iteration ended with a barrier)
+                    if (lane == 0) bulk_g2s(stage, in_bytes + lo, (unsigned)nb, &S.bar[pl]);
+                    mbar_wait(&S.bar[pl], stage_phase);
+                    stage_phase ^= 1u;
                     src = stage - lo;  // token offsets stay plane-relative
                 }
-                __syncthreads();
             }
             if (cnt > 0) decode_sub(src, in_codec, in_td, in_side[e0 / SUB], cnt, xl, in_scale);
             __syncthreads();
