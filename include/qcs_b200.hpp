@@ -38,7 +38,9 @@
 #include <utility>
 #include <vector>
 
+#ifndef QCS_B200_DROPIN_API  // drop-in builds declare the engine API themselves
 #include "qcs/aalc.hpp"
+#endif
 #include "qcs_b200.h"
 
 namespace qcs::b200 {
@@ -136,10 +138,15 @@ inline std::uint64_t now_ns()
 /// compress (codec.cpp:252-256) on the device: lossless when bound.delta == 0.
 inline CompressedBlock compress(std::span<const double> scalars, ErrorBound bound)
 {
+    // worst case of the token coder: 9 bytes per scalar + run tokens
     std::uint64_t len = 0;
-    check(qcs_codec_compress(scalars.data(), scalars.size(), bound.delta, nullptr, 0, &len));
-    std::vector<std::uint8_t> buf(len);
-    check(qcs_codec_compress(scalars.data(), scalars.size(), bound.delta, buf.data(), len, &len));
+    std::vector<std::uint8_t> buf(kBlockHeaderBytes + 9 * scalars.size() + 64);
+    int rc = qcs_codec_compress(scalars.data(), scalars.size(), bound.delta, buf.data(), buf.size(), &len);
+    if (rc == QCS_E_CAPACITY) {
+        buf.resize(len);
+        rc = qcs_codec_compress(scalars.data(), scalars.size(), bound.delta, buf.data(), buf.size(), &len);
+    }
+    check(rc);
     std::size_t off = 0;
     return detail::take_block(buf.data(), off);
 }

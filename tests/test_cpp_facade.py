@@ -32,3 +32,33 @@ def test_facade_parity_against_reference():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("PASS") >= 11 and "0 failure(s)" in r.stdout
+
+
+ACC = os.path.join(ROOT, "oracle", "_ref", "acceptance_b200")
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_suite_on_b200():
+    """The reference's UNMODIFIED acceptance suite (proj/tests/acceptance.cpp,
+    11 criteria) linked to the B200 engine through the
+    link-level drop-in (include/qcs_b200_dropin.hpp +
+    paper_1811_05140_b200/host/qcs_b200_dropin.cpp) instead of the reference's
+    aalc.cpp and codec.cpp."""
+    if not os.path.exists(ACC):
+        pytest.skip("acceptance_b200 not built (needs the reference sources at build time)")
+    r = subprocess.run([ACC], capture_output=True, text=True, timeout=900, cwd="/tmp")
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "11 of 11 criteria passed" in r.stdout
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INC), reason="reference headers not mounted")
+def test_dropin_objects_replace_engine_and_codec():
+    """acceptance_b200 defines the engine/codec symbols from the drop-in object
+    (not the reference's aalc.o / codec.o) and loads libqcs_b200.so."""
+    if not os.path.exists(ACC):
+        pytest.skip("acceptance_b200 not built")
+    nm = subprocess.run(["nm", "-C", ACC], capture_output=True, text=True).stdout
+    for sym in ("qcs::compress_lossy(", "qcs::CompressedState::apply_gate(", "qcs::run_program("):
+        assert any(sym in l and " T " in l for l in nm.splitlines()), sym
+    assert "libqcs_b200.so" in subprocess.run(["ldd", ACC], capture_output=True, text=True).stdout
