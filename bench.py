@@ -416,7 +416,7 @@ def run_b200(args, rank, world, local_rank):
     raw = upd * 16                                # uncompressed bytes of rewritten strides
     # k_fused reads the compressed input strides and writes the recompressed ones
     # (algorithmic bytes = C_in + C_out); commit copies C_out
-    alg = {"decode": cin + raw, "gate": 2 * raw, "fused": cin + cout, "commit": 2 * cout}
+    alg = {"decode": cin + raw, "serial_chain": raw + raw // 4, "fused": cin + cout, "commit": 2 * cout}
     alg_bytes = alg.get(cls, cin + cout)
     achieved = alg_bytes / (t_cls * 1e-9) / 1e9 if t_cls else 0.0
     path_gbs = (cin + cout) / (dev_ns * 1e-9) / 1e9

@@ -172,7 +172,8 @@ int qcs_state_memory(qcs_dev_state_t st, uint64_t* arena_bytes, uint64_t* side_b
 /* Number of kernel launches issued by this state so far (bench accounting). */
 uint64_t qcs_state_launches(qcs_dev_state_t st);
 /* Per-kernel-class device timing with CUDA events on the engine's stream
- * (bench roofline accounting).  Classes: 0 decode, 1 gate, 2 encode,
+ * (bench roofline accounting).  Classes: 0 decode (k_decode_gate, input
+ * passes), 1 serial chain (k_serial_chain), 2 encode (k_fused),
  * 3 commit+norm, 4 mean pass, 5 bookkeeping.  Enabling resets the totals;
  * totals cover every gate enqueued while enabled. */
 int qcs_state_profile(qcs_dev_state_t st, int enable);

@@ -146,6 +146,11 @@ struct Dev {
         uint64_t compressed_bytes;
         double min_ratio;
         uint64_t gate_cin;
+        // serial-chain policy (non-power-of-two bounds): on for a few gates
+        // once the event rounds needed many serial repairs
+        int chain_on;
+        int chain_left;
+        unsigned long long fb_prev;
     }* sc;
     qcs_gate_record* rec;  // record ring for run_program
     uint64_t rec_cap;
@@ -179,6 +184,27 @@ __global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen, Level
         d.slot_of[j] = (int64_t)((gen << 32) | s);
         lt.slot_codec[s] = (int8_t)codec0;  // ladder level 0
         lt.slot_delta[s] = delta0;
+    }
+}
+
+// Per-gate choice between the event rounds and the serial chain for
+// non-power-of-two levels: the rounds win while the lanes'
+// entry guesses hold (early, structured states); once a gate needed
+// `threshold` or more in-order serial repairs, the next CHAIN_SPAN gates
+// precompute every plane's chain for all levels at once, then one gate
+// re-measures with the rounds.
+constexpr int CHAIN_SPAN = 8;
+__global__ void k_chain_policy(Dev d, unsigned long long threshold)
+{
+    auto* sc = d.sc;
+    const unsigned long long fb = d.counters[3];
+    const unsigned long long delta = fb - sc->fb_prev;
+    sc->fb_prev = fb;
+    if (sc->chain_on) {
+        if (--sc->chain_left <= 0) sc->chain_on = 0;
+    } else if (delta >= threshold) {
+        sc->chain_on = 1;
+        sc->chain_left = CHAIN_SPAN;
     }
 }
 
@@ -722,6 +748,12 @@ struct qcs_dev_state {
     uint64_t launches = 0;
     int split_local = 0;  // QCS_SPLIT_LOCAL=1: in-chunk gates also take the split path
     int max_rounds = 6;  // QCS_MAX_ROUNDS (tests force the neighbour-exit repair)
+    // serial-chain mode for non-power-of-two bounds (QCS_SERIAL_CHAIN=0 turns
+    // it off): codes/predictor scratch for `chain_levels` ladder levels
+    int serial_chain = 1;
+    int chain_levels = 0;
+    int16_t* chain_codes = nullptr;
+    double* chain_preds = nullptr;
     unsigned long long* cta_trace = nullptr;  // QCS_CTA_TRACE=1: per-slot phase cycles
     // Large states ("wave mode"): one arena, per-wave staging
     // buffers (slots, side, X) for `wave` slots, per-wave commit placed by the
@@ -1052,6 +1084,36 @@ int big_commit_wave(qcs_dev_state* st, uint64_t s0, uint64_t s1, uint64_t gate_i
     return 0;
 }
 
+// Scratch for the serial-chain mode: codes and sub-chunk predictors of
+// `levels` ladder levels for one wave.  Grows once; false (and the event-
+// round path) when it would take more than a quarter of the free memory.
+bool ensure_chain_scratch(qcs_dev_state* st, int levels)
+{
+    if (st->chain_levels >= levels) return true;
+    const Dev& d = st->d;
+    const size_t rows = 2 * st->wave;
+    const size_t cb = (size_t)levels * rows * d.L * sizeof(int16_t);
+    const size_t pb = (size_t)levels * rows * d.nsub * sizeof(double);
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess || cb + pb > fr / 4) {
+        cudaGetLastError();
+        return false;
+    }
+    if (st->chain_codes) cudaFree(st->chain_codes), cudaFree(st->chain_preds);
+    auto drop = [&](void* q) { st->allocs.erase(std::remove(st->allocs.begin(), st->allocs.end(), q), st->allocs.end()); };
+    drop(st->chain_codes);
+    drop(st->chain_preds);
+    st->chain_codes = nullptr;
+    st->chain_preds = nullptr;
+    st->chain_levels = 0;
+    if (dalloc(st, &st->chain_codes, cb / sizeof(int16_t)) || dalloc(st, &st->chain_preds, pb / sizeof(double))) {
+        g_err.clear();
+        return false;
+    }
+    st->chain_levels = levels;
+    return true;
+}
+
 // One gate, fully stream-ordered.  rec_index < 0: no record.
 int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, int nl,
                  double theta, int64_t rec_index, uint64_t gate_index, uint64_t* n_slots_out,
@@ -1096,6 +1158,74 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     }
     GateParams gp;
     for (int i = 0; i < 8; ++i) gp.u[i] = g->u[i];
+    // Serial-chain mode: lossy levels whose 2*delta is not a
+    // power of two have no lattice to verify lanes against, so their
+    // reference chains are computed up front, serially per plane but for all
+    // planes and all such levels at once (k_serial_chain); the encoder then
+    // only tokenizes.  Needs the gated planes in X: the split path provides
+    // them, in-chunk gates get a decode+gate+snap pass that only writes X.
+    ChainLevels chl{};
+    int lev_of[64];
+    for (int k = 0; k < nl && k < 64; ++k) {
+        lev_of[k] = -1;
+        const CodecParams cpk = make_params(lad[k]);
+        if (cpk.lossy && !cpk.pow2 && chl.n < 8) {
+            lev_of[k] = chl.n;
+            chl.delta[chl.n] = lad[k];
+            chl.td[chl.n] = cpk.td;
+            chl.inv[chl.n] = 1.0 / cpk.td;
+            chl.lim[chl.n] = cpk.lim;
+            ++chl.n;
+        }
+    }
+    bool chain = chl.n > 0 && st->serial_chain && nl <= 64;
+    for (int k = 0; chain && k < nl; ++k)
+        if (make_params(lad[k]).lossy && !make_params(lad[k]).pow2 && lev_of[k] < 0) chain = false;
+    if (chain) chain = ensure_chain_scratch(st, chl.n);
+    // QCS_SERIAL_CHAIN=1: policy (default); 2: always the serial chain
+    const int* chain_flag = nullptr;
+    if (chain && st->serial_chain == 1) {
+        const unsigned long long thr = std::max<unsigned long long>(1, 2 * d.NS * d.nsub / 16);
+        k_chain_policy<<<1, 1, 0, s>>>(d, thr);
+        ++st->launches;
+        chain_flag = &d.sc->chain_on;
+    }
+    const int fm_lvl = chain ? (wide ? FM_RAW2_W : FM_RAW2) : fm;
+    auto fused_args = [&](double delta, uint64_t s0) {
+        FusedArgs a{};
+        a.arena0 = d.arena[0];
+        a.arena1 = d.arena[1];
+        a.arena_cur = &d.sc->cur;
+        a.p_off = d.p_off;
+        a.p_len = d.p_len;
+        a.p_codec = d.p_codec;
+        a.p_delta = d.p_delta;
+        a.side_in = d.side;
+        a.scale = d.scale;
+        a.job_stride = d.job_stride;
+        for (int i = 0; i < 8; ++i) a.u[i] = g->u[i];
+        a.kind = p.kind;
+        a.t = p.t;
+        a.local_ctl = p.local_ctl;
+        a.flip_off = p.flip_off;
+        a.mean = d.sc->mean;
+        a.n = d.L;
+        a.pending = d.pending;
+        a.slot_base = s0;
+        a.max_rounds = st->max_rounds;
+        a.cta_trace = st->cta_trace;
+        a.snap = 1;
+        a.pool = d.pool;
+        a.out = d.pool ? d.arena[0] : d.slot_out;
+        a.cap = d.slot_cap;
+        a.side = d.pool ? d.side : d.slot_side;
+        a.nsub = d.nsub;
+        a.out_len = d.slot_len;
+        a.sumsq = d.slot_sum;
+        a.cp = make_params(delta);
+        a.counters = d.counters;
+        return a;
+    };
     const uint64_t spu = p.pair ? 2 : 1;                        // slots per unit
     const uint64_t wave_units = std::max<uint64_t>(1, st->wave / spu);
     for (uint64_t u0 = 0; u0 < p.n_units; u0 += wave_units) {
@@ -1110,44 +1240,36 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             prof_stop(st);
             ++st->launches;
         }
+        if (chain) {
+            if (dg < 0) {  // in-chunk gate: decode + gate + snap into X only
+                FusedArgs a = fused_args(lad[0], s0);
+                a.dump_x = d.X;
+                prof_start(st, 0);
+                const int rc = launch_fused(a, fm, nw, s);
+                prof_stop(st);
+                if (rc) return rc;
+                ++st->launches;
+            }
+            const uint64_t chains = 2 * nw * (uint64_t)chl.n;
+            prof_start(st, 1);
+            k_serial_chain<<<(unsigned)((chains + 127) / 128), 128, 0, s>>>(d.X, 2 * nw, d.L, d.nsub, chl,
+                                                                           st->chain_codes, st->chain_preds,
+                                                                           d.pending, s0, chain_flag);
+            prof_stop(st);
+            ++st->launches;
+        }
         for (int k = 0; k < nl; ++k) {
-            FusedArgs a{};
-            a.arena0 = d.arena[0];
-            a.arena1 = d.arena[1];
-            a.arena_cur = &d.sc->cur;
-            a.p_off = d.p_off;
-            a.p_len = d.p_len;
-            a.p_codec = d.p_codec;
-            a.p_delta = d.p_delta;
-            a.side_in = d.side;
-            a.scale = d.scale;
-            a.job_stride = d.job_stride;
-            for (int i = 0; i < 8; ++i) a.u[i] = g->u[i];
-            a.kind = p.kind;
-            a.t = p.t;
-            a.local_ctl = p.local_ctl;
-            a.flip_off = p.flip_off;
-            a.mean = d.sc->mean;
-            a.n = d.L;
-            a.pending = d.pending;
-            a.slot_base = s0;
-            a.max_rounds = st->max_rounds;
-            a.cta_trace = st->cta_trace;
-            a.snap = 1;
-            if (fm == FM_RAW2 || fm == FM_RAW2_W) {  // split path: gated, snapped planes in X
+            FusedArgs a = fused_args(lad[k], s0);
+            if (fm_lvl == FM_RAW2 || fm_lvl == FM_RAW2_W) {  // split path: gated, snapped planes in X
                 a.X = d.X;
                 a.x_plane_stride = d.L;
                 a.snap = 0;
             }
-            a.pool = d.pool;
-            a.out = d.pool ? d.arena[0] : d.slot_out;
-            a.cap = d.slot_cap;
-            a.side = d.pool ? d.side : d.slot_side;
-            a.nsub = d.nsub;
-            a.out_len = d.slot_len;
-            a.sumsq = d.slot_sum;
-            a.cp = make_params(lad[k]);
-            a.counters = d.counters;
+            if (chain && lev_of[k] >= 0) {
+                a.pre_codes = st->chain_codes + (uint64_t)lev_of[k] * 2 * nw * d.L;
+                a.pre_pred = st->chain_preds + (uint64_t)lev_of[k] * 2 * nw * d.nsub;
+                a.chain_on = chain_flag;
+            }
             if (k > 0) {  // level 0 was tagged by k_make_jobs
                 prof_start(st, 5);
                 k_tag_level<<<(unsigned)grid_for(nw), 256, 0, s>>>(d, st->lt, s0, s1, a.cp.lossy ? 1 : 0, lad[k]);
@@ -1155,7 +1277,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
                 ++st->launches;
             }
             prof_start(st, 2);
-            int rc = launch_fused(a, fm, nw, s);
+            int rc = launch_fused(a, fm_lvl, nw, s);
             prof_stop(st);
             if (rc) return rc;
             ++st->launches;
@@ -1230,6 +1352,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     qcs_dev_state* st = new qcs_dev_state();
     st->device = device;
     if (const char* e = getenv("QCS_SPLIT_LOCAL")) st->split_local = atoi(e);
+    if (const char* e = getenv("QCS_SERIAL_CHAIN")) st->serial_chain = atoi(e);
     if (const char* e = getenv("QCS_MAX_ROUNDS")) st->max_rounds = std::max(1, atoi(e));
     cudaSetDevice(device);
     int rc = 0;
@@ -2031,6 +2154,14 @@ int qcs_state_kernel_time(qcs_dev_state_t st, int cls, double* total_ns, uint64_
     return 0;
 }
 
+namespace {
+int codec_serial_chain()
+{
+    const char* e = getenv("QCS_SERIAL_CHAIN");
+    return e ? atoi(e) : 1;
+}
+}  // namespace
+
 int qcs_codec_compress(const double* x, uint64_t n, double delta, uint8_t* out, uint64_t cap,
                        uint64_t* len)
 {
@@ -2081,7 +2212,26 @@ int qcs_codec_compress(const double* x, uint64_t n, double delta, uint8_t* out, 
     a.out_len = dlen;
     a.sumsq = nullptr;
     a.cp = make_params(delta);
-    int rc = n ? launch_fused(a, FM_RAW1, 1, s) : 0;
+    int16_t* dcodes = nullptr;
+    double* dpreds = nullptr;
+    int rc = 0;
+    if (n && a.cp.lossy && !a.cp.pow2 && codec_serial_chain()) {  // serial-chain mode
+        if (cudaMalloc(&dcodes, 2 * n + 16) != cudaSuccess || cudaMalloc(&dpreds, 8 * nsub + 16) != cudaSuccess) {
+            cudaGetLastError();
+            rc = set_err(QCS_E_NOMEM, "device allocation failed");
+        } else {
+            ChainLevels chl{};
+            chl.n = 1;
+            chl.delta[0] = delta;
+            chl.td[0] = a.cp.td;
+            chl.inv[0] = 1.0 / a.cp.td;
+            chl.lim[0] = a.cp.lim;
+            k_serial_chain<<<1, 128, 0, s>>>(dx, 1, n, nsub, chl, dcodes, dpreds, nullptr, 0, nullptr);
+            a.pre_codes = dcodes;
+            a.pre_pred = dpreds;
+        }
+    }
+    if (!rc && n) rc = launch_fused(a, FM_RAW1, 1, s);
     uint64_t plen = 0;
     if (!rc) {
         cudaMemcpyAsync(&plen, dlen, 8, cudaMemcpyDeviceToHost, s);
@@ -2099,6 +2249,8 @@ int qcs_codec_compress(const double* x, uint64_t n, double delta, uint8_t* out, 
             }
         }
     }
+    cudaFree(dcodes);
+    cudaFree(dpreds);
     cleanup();
     return rc;
 }

@@ -79,6 +79,14 @@ struct FusedArgs {
     // ---- input: raw planes (MODE_RAW) ----
     const double* X;
     uint64_t x_plane_stride;      // elements between a CTA's planes
+    // ---- serial-chain mode (non-power-of-two bounds) ----
+    double* dump_x;               // MODE_LOCAL: write the gated, snapped planes
+                                  // here ([slot][plane][n]) and stop
+    const int16_t* pre_codes;     // MODE_RAW: the reference chain's codes,
+    const double* pre_pred;       // [slot][plane][n] and its predictor entering
+                                  // every sub-chunk [slot][plane][nsub]
+                                  // (k_serial_chain); no event rounds
+    const int* chain_on;          // device flag gating pre_codes (null = always)
     // ---- gate ----
     double u[8];
     int kind;                     // GateKind
@@ -624,11 +632,35 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : 2)) k_fused(
         if (a.snap && cnt > 0) {
             for (int i = 0; i < cnt; ++i) xl[i] = snap(xl[i]);
         }
+        if (MODE == MODE_LOCAL && a.dump_x) {  // serial-chain mode: input only
+            double* dx = a.dump_x + ((uint64_t)b * NPL + pl) * n + e0;
+            for (int i = 0; i < cnt; ++i) dx[i] = xl[i];
+            __syncthreads();
+            continue;
+        }
         __syncthreads();
 
         QCS_PHASE(0);
         // 2-4. codes and exact predictors
-        if (LOSSY) {
+        if (LOSSY && MODE == MODE_RAW && a.pre_codes && (!a.chain_on || *a.chain_on)) {
+            // serial-chain mode: the codes and sub-chunk entry predictors of
+            // the reference chain were computed by k_serial_chain
+            if (cnt > 0) {
+                const uint64_t row = (uint64_t)b * NPL + pl;
+                const int16_t* pc = a.pre_codes + row * n + e0;
+                for (int i = 0; i < cnt; ++i) cl[i] = pc[i];
+                const double P0 = a.pre_pred[row * a.nsub + e0 / SUB];
+                S.entryP[tid] = P0;
+                double P = P0;
+                for (int i = 0; i < cnt; ++i) {  // reconstructed values
+                    const int16_t co = cl[i];
+                    if (co == WCODE16) P = xl[i];
+                    else if (co != 0) P = __dadd_rn(P, __dmul_rn(cp.td, (double)co));
+                    xl[i] = P;
+                }
+            }
+            __syncthreads();
+        } else if (LOSSY) {
             // Self-correcting event rounds.  Every lane runs the
             // reference chain from an entry predictor derived from the last
             // EVENT before it (an escape, a rounding re-anchor or any step the
@@ -936,6 +968,7 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : 2)) k_fused(
         __syncthreads();
     }
 
+    if (MODE == MODE_LOCAL && a.dump_x) return;
     QCS_PHASE(6);
     if (tid == 0 && a.counters)
         for (int i = 0; i < 8; ++i) atomicAdd(&a.counters[8 + i], ph_acc[i]);
@@ -943,6 +976,90 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : 2)) k_fused(
         for (int i = 0; i < 8; ++i) a.cta_trace[8 * (a.slot_base + (uint64_t)b) + i] = ph_acc[i];
     if (lane == 0) a.out_len[2 * gslot + comp] = C.out_pos;
     if (a.sumsq && tid == 0) a.sumsq[gslot] = S.s[0];
+}
+
+// The reference chain of compress_lossy (codec.cpp:206-250) for bounds whose
+// 2*delta is not a power of two: there the predictor `pred + 2d*q` leaves
+// any fixed lattice and every step depends on the rounding history, so the
+// chain is computed serially, one thread per (slot, plane, level) — all
+// ladder levels of a gate at once.  x: the gated, snapped planes
+// [slot][plane][n]; out: codes [level][slot][plane][n] (WCODE16 = escape)
+// and the predictor entering every SUB-element sub-chunk
+// [level][slot][plane][nsub].  The quotient fl(diff/2d) is formed as
+// diff * fl(1/2d) when that provably rounds to the same integer (it is at
+// least 2^-40 relative away from a half-integer; the two differ by < 2^-51
+// relative), else by the exact division — fewer cycles on the serial path.
+struct ChainLevels {
+    double delta[8];
+    double td[8];
+    double inv[8];
+    double lim[8];
+    int n;
+};
+
+// rare path of the quotient (kept out of line so the compiler does not
+// compute the division speculatively on every step)
+__device__ __noinline__ double chain_div(double diff, double td) { return __ddiv_rn(diff, td); }
+
+__global__ void __launch_bounds__(128) k_serial_chain(const double* __restrict__ x, uint64_t rows, uint64_t n,
+                                                      uint64_t nsub, ChainLevels lv, int16_t* __restrict__ codes,
+                                                      double* __restrict__ preds, const uint8_t* pending,
+                                                      uint64_t slot_base, const int* on)
+{
+    if (on && !*on) return;
+    const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= rows * (uint64_t)lv.n) return;
+    const int lev = (int)(c / rows);
+    const uint64_t row = c % rows;  // slot * 2 + plane
+    if (pending && !pending[slot_base + row / 2]) return;
+    const double delta = lv.delta[lev], td = lv.td[lev], inv = lv.inv[lev], lim = lv.lim[lev];
+    const double* xr = x + row * n;
+    int16_t* cr = codes + ((uint64_t)lev * rows + row) * n;
+    double* pr = preds + ((uint64_t)lev * rows + row) * nsub;
+    double P = 0.0;
+    constexpr int G = 8;
+    double nx[G];  // the next group's inputs, loaded one group ahead
+#pragma unroll
+    for (int k = 0; k < G; ++k) nx[k] = (uint64_t)k < n ? xr[k] : 0.0;
+    for (uint64_t e0 = 0; e0 < n; e0 += G) {
+        double xv[G];
+#pragma unroll
+        for (int k = 0; k < G; ++k) xv[k] = nx[k];
+#pragma unroll
+        for (int k = 0; k < G; ++k) nx[k] = e0 + G + k < n ? __ldcs(xr + e0 + G + k) : 0.0;
+        if ((e0 & (SUB - 1)) == 0) pr[e0 / SUB] = P;
+        uint32_t cw[G / 2];
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+            const double xx = xv[k];
+            const double diff = __dsub_rn(xx, P);
+            uint32_t code = 0x8000u;  // WCODE16
+            double Pn = xx;
+            if (fabs(diff) < lim) {
+                double qd = __dmul_rn(diff, inv);
+                const double fr = fabs(__dsub_rn(qd, trunc(qd)));
+                if (fabs(__dsub_rn(fr, 0.5)) <= fabs(qd) * 9.094947017729282e-13) qd = chain_div(diff, td);  // 2^-40
+                double t = trunc(qd);
+                if (fabs(__dsub_rn(qd, t)) >= 0.5) t = __dadd_rn(t, copysign(1.0, qd));
+                if (t > -32768.0 && t < 32768.0) {
+                    const double recon = __dadd_rn(P, __dmul_rn(td, t));
+                    if (fabs(__dsub_rn(xx, recon)) <= delta) {
+                        Pn = recon;
+                        code = (uint32_t)(uint16_t)(int16_t)t;
+                    }
+                }
+            }
+            P = Pn;
+            if (k & 1) cw[k / 2] |= code << 16;
+            else cw[k / 2] = code;
+        }
+        const uint64_t m = umin64(G, n - e0);
+        if (m == G && (reinterpret_cast<uintptr_t>(cr + e0) & 15) == 0) {
+            *reinterpret_cast<uint4*>(cr + e0) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+        } else {
+            for (uint64_t k = 0; k < m; ++k) cr[e0 + k] = (int16_t)(uint16_t)(cw[k / 2] >> (16 * (k & 1)));
+        }
+    }
 }
 
 }  // namespace qcs

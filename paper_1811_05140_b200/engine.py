@@ -362,7 +362,7 @@ class CompressedState:
                                        C.byref(ss)))
         return buf.raw[: n.value], sc.value, ss.value
 
-    KERNEL_CLASSES = ("decode", "gate", "fused", "commit", "mean", "bookkeeping")
+    KERNEL_CLASSES = ("decode", "serial_chain", "fused", "commit", "mean", "bookkeeping")
 
     def profile(self, enable: bool) -> None:
         _check(lib().qcs_state_profile(self._h, 1 if enable else 0))

@@ -97,3 +97,15 @@ def test_codec_fuzz_neighbour_repair(q, oracle, monkeypatch, max_rounds):
         for x in _planes(rng, n):
             for d in (2.0 ** -20, 2.0 ** -12):
                 assert q.compress(x, d) == oracle.compress(x, d), (n, d)
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_codec_serial_chain_vs_oracle(q, oracle, monkeypatch, mode):
+    """Codec plugin with decimal bounds: serial-chain precompute (1) and the
+    event rounds (0) both reproduce the oracle's blocks."""
+    monkeypatch.setenv("QCS_SERIAL_CHAIN", mode)
+    rng = np.random.default_rng(5)
+    for n in (1, 7, 33, 4096, 20000):
+        for x in _planes(rng, n):
+            for d in (1e-7, 1e-5, 3e-3):
+                assert q.compress(x, d) == oracle.compress(x, d), (n, d)

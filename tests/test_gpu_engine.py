@@ -136,3 +136,26 @@ def test_engine_neighbour_repair(q, oracle, monkeypatch, max_rounds, kind, n, s,
     res, got = gpu_run(prog, s, basis, ladder, theta)
     assert got == want, first_diff(want, got)
     assert res.state.to_amplitudes().tobytes() == st.amplitudes().tobytes()
+
+
+SERIAL_CASES = [
+    ("qft", 12, 8, 5, [0.0, 1e-7, 1e-6, 1e-5, 1e-4, 1e-3], 16.0),   # the reference's default ladder
+    ("qft", 13, 13, 777, [1e-3 * 2 ** -7], 1.0),
+    ("grover_ref", 10, 6, 0, [0.0, 1e-6, 1e-4], 32.0),                # reflect_mean + flips
+    ("grid", 9, 6, 0, [0.0, 3e-6, 2.0 ** -14, 1e-3], 8.0),           # mixed decimal / power-of-two levels
+]
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+@pytest.mark.parametrize("kind,n,s,basis,ladder,theta", SERIAL_CASES)
+def test_engine_serial_chain_modes(q, oracle, monkeypatch, mode, kind, n, s, basis, ladder, theta):
+    """Non-power-of-two bounds: event rounds only (QCS_SERIAL_CHAIN=0), the
+    per-gate policy (1, default) and the serial chain always (2, k_serial_chain
+    precomputes every plane's reference chain for all levels) are all
+    bit-identical to the oracle."""
+    monkeypatch.setenv("QCS_SERIAL_CHAIN", mode)
+    prog = _prog(kind, n)
+    st, want = oracle_run(oracle, prog, s, basis, ladder, theta)
+    res, got = gpu_run(prog, s, basis, ladder, theta)
+    assert got == want, first_diff(want, got)
+    assert res.state.to_amplitudes().tobytes() == st.amplitudes().tobytes()
