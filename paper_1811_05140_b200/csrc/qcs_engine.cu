@@ -193,7 +193,7 @@ __global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen, Level
 // `threshold` or more in-order serial repairs, the next CHAIN_SPAN gates
 // precompute every plane's chain for all levels at once, then one gate
 // re-measures with the rounds.
-constexpr int CHAIN_SPAN = 8;
+constexpr int CHAIN_SPAN = 16;
 __global__ void k_chain_policy(Dev d, unsigned long long threshold)
 {
     auto* sc = d.sc;
@@ -722,9 +722,24 @@ int codec_max_rounds()
     return e ? std::max(1, atoi(e)) : 6;
 }
 
+int fused_narrow()
+{
+    static const int narrow = [] {
+        const char* e = getenv("QCS_NARROW");
+        return e ? atoi(e) : 0;
+    }();
+    return narrow;
+}
+// elements per plane per iteration of the usual encoder CTA: in-stride
+// partners closer than this are gated inside it (MODE_LOCAL)
+int fused_span() { return fused_narrow() ? 2048 : 4096; }
+
 int launch_fused(const FusedArgs& a, int fm, uint64_t grid, cudaStream_t s)
 {
     const bool L = a.cp.lossy != 0;
+    const int narrow = fused_narrow();
+    if (narrow && L && fm == FM_LOCAL) return launch_fused_t<true, 2, 64, MODE_LOCAL>(a, grid, s);
+    if (narrow && L && fm == FM_RAW2) return launch_fused_t<true, 2, 64, MODE_RAW>(a, grid, s);
     switch (fm) {
         case FM_LOCAL: return L ? launch_fused_t<true, 2, 128, MODE_LOCAL>(a, grid, s) : launch_fused_t<false, 2, 128, MODE_LOCAL>(a, grid, s);
         case FM_LOCAL_W: return L ? launch_fused_t<true, 2, 256, MODE_LOCAL>(a, grid, s) : launch_fused_t<false, 2, 256, MODE_LOCAL>(a, grid, s);
@@ -1144,10 +1159,14 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     // gate fully parallel into X, then the encoder reads X (split path)
     int dg = -1;
     if (p.pair) dg = DG_PAIR;
-    else if (p.kind <= 1 && (1ull << p.t) >= 4096) dg = DG_FAR;
+    else if (p.kind <= 1 && (1ull << p.t) >= (uint64_t)fused_span()) dg = DG_FAR;
     else if (p.kind <= 1 && st->split_local && (1ull << p.t) >= DG_HALF) dg = DG_FAR;
     else if (p.kind <= 1 && st->split_local && d.L >= DG_IN_CH) dg = DG_IN;
-    const bool wide = n_slots < 148 && d.L >= 2 * 4096;
+    static const int force_wide = [] {
+        const char* e = getenv("QCS_WIDE");
+        return e ? atoi(e) : -1;
+    }();
+    const bool wide = force_wide >= 0 ? (force_wide && d.L >= 2 * 4096) : (n_slots < 148 && d.L >= 2 * 4096);
     const int fm = dg >= 0 ? (wide ? FM_RAW2_W : FM_RAW2) : (wide ? FM_LOCAL_W : FM_LOCAL);  // pairs always split
     if (dg >= 0) {
         static bool dg_attr = false;

@@ -459,7 +459,7 @@ __device__ __forceinline__ double lane_chain(const CodecParams& cp, const double
     } while (0)
 
 template <bool LOSSY, int NPL, int LPL, int MODE>
-__global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : 2)) k_fused(FusedArgs a)
+__global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL > 128 ? 2 : 4))) k_fused(FusedArgs a)
 {
     unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long ph_t = clock64();
@@ -1033,23 +1033,25 @@ __global__ void __launch_bounds__(128) k_serial_chain(const double* __restrict__
         for (int k = 0; k < G; ++k) {
             const double xx = xv[k];
             const double diff = __dsub_rn(xx, P);
-            uint32_t code = 0x8000u;  // WCODE16
-            double Pn = xx;
-            if (fabs(diff) < lim) {
-                double qd = __dmul_rn(diff, inv);
-                const double fr = fabs(__dsub_rn(qd, trunc(qd)));
-                if (fabs(__dsub_rn(fr, 0.5)) <= fabs(qd) * 9.094947017729282e-13) qd = chain_div(diff, td);  // 2^-40
-                double t = trunc(qd);
-                if (fabs(__dsub_rn(qd, t)) >= 0.5) t = __dadd_rn(t, copysign(1.0, qd));
-                if (t > -32768.0 && t < 32768.0) {
-                    const double recon = __dadd_rn(P, __dmul_rn(td, t));
-                    if (fabs(__dsub_rn(xx, recon)) <= delta) {
-                        Pn = recon;
-                        code = (uint32_t)(uint16_t)(int16_t)t;
-                    }
-                }
+            // fast quotient and llround (half away from zero) with the
+            // candidates formed in parallel; `slow` flags a quotient within
+            // 2^-40 (relative) of a half-integer: that step is redone with
+            // the exact division (off the critical path otherwise)
+            const double qd = __dmul_rn(diff, inv);
+            const double t0 = trunc(qd);
+            const double fr = fabs(__dsub_rn(qd, t0));
+            const double tu = __dadd_rn(t0, copysign(1.0, qd));
+            const bool slow = fabs(__dsub_rn(fr, 0.5)) <= fabs(qd) * 9.094947017729282e-13;  // 2^-40
+            double t = fr >= 0.5 ? tu : t0;
+            if (slow) {
+                const double qx = chain_div(diff, td);
+                t = trunc(qx);
+                if (fabs(__dsub_rn(qx, t)) >= 0.5) t = __dadd_rn(t, copysign(1.0, qx));
             }
-            P = Pn;
+            const double recon = __dadd_rn(P, __dmul_rn(td, t));
+            const bool ok = fabs(diff) < lim && t > -32768.0 && t < 32768.0 && fabs(__dsub_rn(xx, recon)) <= delta;
+            P = ok ? recon : xx;
+            const uint32_t code = ok ? (uint32_t)(uint16_t)(int16_t)t : 0x8000u;  // 0x8000 = WCODE16
             if (k & 1) cw[k / 2] |= code << 16;
             else cw[k / 2] = code;
         }
