@@ -127,6 +127,14 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def measured_clock_mhz():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f).get("sm_max_mhz", 1965.0))
+    except (OSError, ValueError):
+        return 1965.0
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -433,6 +441,25 @@ def run_b200(args, rank, world, local_rank):
                 "avg_launch_us": t_cls / max(1, n_cls) / 1e3,
                 "path_C_in_plus_C_out_GBps": path_gbs, "path_frac": path_gbs / peak,
                 "kernel_share": {k: v[0] / max(1.0, sum(x[0] for x in kt.values())) for k, v in kt.items()}}
+
+    # The encoder is issue/latency-bound, not HBM-bound: its
+    # instruction roofline = profiled warp instructions per launch (ncu, same
+    # command, profiles/) / the live event-timed launch time, against the issue
+    # peak (148 SMs x 4 schedulers x max SM clock).
+    ip = os.path.join(ROOT, "profiles", "r1_ncu_summary.json")
+    if cls == "fused" and os.path.exists(ip):
+        with open(ip) as f:
+            prof = json.load(f)
+        modes = [prof[k] for k in ("k_fused_local", "k_fused_raw") if k in prof]
+        if modes:
+            inst = sum(m["inst_executed"] for m in modes) / len(modes)
+            peak_ips = 148 * 4 * measured_clock_mhz() * 1e6
+            achieved_ips = inst / (t_cls / max(1, n_cls) * 1e-9)
+            roofline["instruction_roofline"] = {
+                "warp_inst_per_launch": inst, "achieved_warp_inst_per_s": achieved_ips,
+                "peak_warp_inst_per_s": peak_ips, "frac": achieved_ips / peak_ips,
+                "source": "inst_executed from profiles/r1_ncu_summary.json (mean of the two encoder modes); "
+                          "peak = 148 SMs x 4 schedulers x sm_max_mhz"}
 
     fidelity = None
     if not args.skip_fidelity:

@@ -73,7 +73,8 @@ for line in out:
         fname = r[1].split("/")[-1]
         continue
     if r[0] == "Function Name":
-        func = "LOCAL" if r[1].endswith("(int)1>(qcs::FusedArgs)") else "RAW"
+        func = ("LOCAL" if r[1].endswith("(int)1>(qcs::FusedArgs)") else
+                "RAW" if "k_fused" in r[1] else r[1].split("(")[0].replace("<unnamed>::", ""))
         continue
     if r[0] == "Line No":
         hdr = r
