@@ -128,6 +128,10 @@ class TorchComm:
         self._p2p(send=n_send, recv=n_recv, peer=peer)
         recv = torch.empty(int(n_recv.item()), dtype=torch.uint8, device=dev)
         self._p2p(send=send, recv=recv, peer=peer)
+        if nccl:
+            # the engine reads the image on its own stream: wait on the host
+            # until the receive (ordered on torch's stream by wait()) landed
+            torch.cuda.current_stream().synchronize()
         return recv if nccl else recv.to(obj.device)
 
     def _p2p(self, send, recv, peer):
