@@ -41,3 +41,37 @@ def test_fullsize_matches_reference(reference, cfg):
     got = st.to_amplitudes()
     assert got.tobytes() == ref_amps.tobytes()
     assert st.compressed_bytes() == int(summ["compressed_bytes"])
+
+
+def test_grid_c4_shape_matches_reference(reference):
+    """C4-shaped (BASELINE configs[3], the seeded random grid family) at a size
+    one GPU and the CPU reference both finish: a 4x5 grid (20 qubits), depth
+    20 (CZ patterns + sqrt X / sqrt Y / T), 2^14-amplitude strides, bound
+    mapped from eps = 1e-2 — every record, the amplitudes and the compressed
+    size identical to the unmodified reference."""
+    n, s, basis, eps = 20, 14, 0, 1e-2
+    prog = cc.build_grid(4, 5, 20, 2024)
+    ladder = [cc.pow2_bound(eps, n)]
+    ref_csv, ref_amps, summ = reference.run(cc.print_circuit(prog), s, basis, ladder, 1.0, workers=0)
+    st, csv = _gpu(prog, s, basis, ladder, len(prog.gates))
+    want = mm.strip_elapsed(ref_csv)
+    assert csv == want, first_diff(want, csv)
+    assert st.to_amplitudes().tobytes() == ref_amps.tobytes()
+    assert st.compressed_bytes() == int(summ["compressed_bytes"])
+
+
+def test_sharded_qft_c5_shape_matches_reference(reference):
+    """C5-shaped (BASELINE configs[4]: the top qubits index the GPU, their gates
+    exchange compressed strides): QFT-20 with 2^14-amplitude strides on 4
+    shards (ranks as threads sharing this GPU; the exchange moves device stride
+    images), against the unmodified single-process reference bit for bit."""
+    from paper_1811_05140_b200.distributed import GpuBackend, ShardGeometry, run_thread_cluster
+    n, s, basis, eps = 20, 14, 552808, 1e-3
+    prog = cc.build_qft(n)
+    ladder = [cc.pow2_bound(eps, n)]
+    ref_csv, ref_amps, _ = reference.run(cc.print_circuit(prog), s, basis, ladder, 1.0, workers=0)
+    amp, recs = run_thread_cluster(prog, ShardGeometry(n, s, 2), lambda r: GpuBackend(0), basis, ladder, 1.0)
+    want = mm.strip_elapsed(ref_csv)
+    got = mm.emit_csv(recs, with_elapsed=False)
+    assert got == want, first_diff(want, got)
+    assert amp.tobytes() == ref_amps.tobytes()
