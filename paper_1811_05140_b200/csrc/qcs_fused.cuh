@@ -49,6 +49,7 @@ struct FusedSharedT {
     double s[2];  // exact running sum of squares per stride
     uint64_t mvmax;
     uint64_t bar[4];  // per-plane mbarrier of the payload bulk copy (MODE_LOCAL)
+    uint8_t repaired[NT];  // lane's codes rewritten by a repair pass (resync chain)
 };
 
 // code rows padded to 34 int16 (17 words) so the lanes' row accesses (32-bit
@@ -277,8 +278,9 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
                 const int k = kb + i;
                 if (k < k0 || k >= n_it) continue;
                 const double y = tsq_g<LPL>(xs, 0, k) * to_units;
+                const double ry = rint(y);
                 // a tie (or an element beyond the binade) saturates the total
-                loc = sat_add(loc, (y >= 9007199254740992.0 || y - floor(y) == 0.5) ? SAT : (uint64_t)rint(y));
+                loc = sat_add(loc, (y >= 9007199254740992.0 || fabs(y - ry) == 0.5) ? SAT : (uint64_t)ry);
             }
             uint64_t inc = loc;
             for (int o = 1; o < 32; o <<= 1) {
@@ -305,11 +307,12 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
                 const int k = kb + i;
                 if (k < k0 || k >= n_it) continue;
                 const double y = tsq_g<LPL>(xs, 0, k) * to_units;
-                if (y >= 9007199254740992.0 || y - floor(y) == 0.5) {
+                const double ry = rint(y);
+                if (y >= 9007199254740992.0 || fabs(y - ry) == 0.5) {
                     mine = k;
                     break;
                 }
-                const uint64_t c = (uint64_t)rint(y);
+                const uint64_t c = (uint64_t)ry;
                 if (ms + run + c >= (1ull << 53)) {
                     mine = k;
                     break;
@@ -688,6 +691,7 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL >
                 }
             }
             double used = __longlong_as_double(0x7ff8000000000000ll);  // entry of the last run
+            S.repaired[tid] = 0;
             for (int round = 0;; ++round) {
                 double aval = 0.0;
                 const long long aidx = fscan_last<WPL>(cnt > 0 ? ev_idx : -1, ev_val, S, pl, aval);
@@ -725,6 +729,7 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL >
                         long long li;
                         double lv;
                         const double Pn = lane_chain(cp, xl, cl, cnt, want, true, S.entryP[tid], sy, li, lv);
+                        S.repaired[tid] = 1;
                         S.entryP[tid] = want;
                         if (!sy) S.exitP[tid] = Pn;
                     }
@@ -743,6 +748,7 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL >
                         const double Pn = lane_chain(cp, xs + id * XS_STRIDE, code + id * CODE_STRIDE, c2, want, true,
                                                      S.entryP[id], sy, li, lv);
                         S.entryP[id] = want;
+                        S.repaired[id] = 1;
                         if (!sy) S.exitP[id] = Pn;
                     }
                 }
@@ -752,12 +758,27 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL >
             QCS_PHASE(1);
             if (lane == 0 && active > 0) C.Pnext = S.exitP[pl * LPL + active - 1];
             if (cnt > 0) {  // the reference's reconstructed predictors from the codes
-                double P = S.entryP[tid];
-                for (int i = 0; i < cnt; ++i) {
-                    const int16_t co = cl[i];
-                    if (co == WCODE16) P = xl[i];
-                    else if (co != 0) P = __dadd_rn(P, __dmul_rn(cp.td, (double)co));
-                    xl[i] = P;
+                const double P0 = S.entryP[tid];
+                if (cp.pow2 && ev_idx < 0 && !S.repaired[tid]) {
+                    // the lane's last chain had no event: every step was a
+                    // proven lattice step from its entry (lane_chain), so the
+                    // predictor after element i is exactly entry + 2d*M_i with
+                    // M_i the integer prefix of the codes — independent
+                    // products and sums instead of a serial FP chain
+                    int M = 0;
+#pragma unroll 8
+                    for (int i = 0; i < cnt; ++i) {
+                        M += cl[i];
+                        xl[i] = __dadd_rn(P0, __dmul_rn(cp.td, (double)M));
+                    }
+                } else {
+                    double P = P0;
+                    for (int i = 0; i < cnt; ++i) {
+                        const int16_t co = cl[i];
+                        if (co == WCODE16) P = xl[i];
+                        else if (co != 0) P = __dadd_rn(P, __dmul_rn(cp.td, (double)co));
+                        xl[i] = P;
+                    }
                 }
             }
             __syncthreads();
