@@ -1409,7 +1409,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
         d.pool = 1;
         st->wave = d.NS;
         d.arena_cap = pool_b;
-        TRY(dalloc(st, &d.arena[0], d.arena_cap));
+        TRY(dalloc(st, &d.arena[0], d.arena_cap + 64));  // +64: word-window reads past a last block
         d.arena[1] = d.arena[0];
     } else {
         const uint64_t per_slot = 16 * d.L + 2 * d.slot_cap + 2 * d.nsub * sizeof(SideEntry);
@@ -1433,7 +1433,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
             return set_err(QCS_E_NOMEM, "not enough device memory for a %d-qubit state with %d stride bits", n, s);
         }
         d.arena_cap = cap;
-        TRY(dalloc(st, &d.arena[0], d.arena_cap));
+        TRY(dalloc(st, &d.arena[0], d.arena_cap + 64));  // +64: word-window reads past a last block
         d.arena[1] = nullptr;
         TRY(dalloc(st, &st->mv_src, 2 * d.NS));
         TRY(dalloc(st, &st->mv_dst, 2 * d.NS));
