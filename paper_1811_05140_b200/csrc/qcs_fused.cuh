@@ -325,7 +325,13 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
             __syncthreads();
             long long kstar = LLONG_MAX;
             for (int i = 0; i < GW; ++i) kstar = min(kstar, S.wmin[i]);
-            if (mine == kstar && kstar != LLONG_MAX) S.s[0] = __dadd_rn((double)(ms + run) / to_units, tsq_g<LPL>(xs, 0, (int)kstar));
+            if (mine == kstar && kstar != LLONG_MAX) {
+                S.s[0] = __dadd_rn((double)(ms + run) / to_units, tsq_g<LPL>(xs, 0, (int)kstar));
+                if (counters) {
+                    const double y = tsq_g<LPL>(xs, 0, (int)kstar) * to_units;
+                    atomicAdd(&counters[(y < 9007199254740992.0 && fabs(y - rint(y)) == 0.5) ? 6 : 7], 1ull);
+                }
+            }
             __syncthreads();
             s = S.s[0];
             k0 = (int)kstar + 1;
