@@ -122,6 +122,11 @@ int qcs_apply_gate_ex(qcs_dev_state_t st, const qcs_gate_desc* gate, const doubl
  * through the ordinary commit path. */
 int qcs_pack_strides(qcs_dev_state_t st, int bit, int value, void* dev_buf, uint64_t cap,
                      uint64_t* len);
+/* qcs_pack_strides restricted to the strides whose position among those with
+ * bit `bit` == value is in [first, first + count): an exchange streamed in
+ * chunks, so a 37-qubit shard's half-state never needs one image buffer. */
+int qcs_pack_strides_range(qcs_dev_state_t st, int bit, int value, uint64_t first, uint64_t count,
+                           void* dev_buf, uint64_t cap, uint64_t* len);
 int qcs_unpack_strides(qcs_dev_state_t st, const void* dev_buf, uint64_t len, uint64_t xor_mask);
 /* Per-stride amplitude sums (stride_amplitude_sum, gate.cpp:303-311) of the
  * decompressed, scaled strides: partial[2j] = re, partial[2j+1] = im. */

@@ -220,8 +220,12 @@ class OracleState:
         sc, ss, _, _ = self.stride_info(j)
         return self.export_blocks(j), sc, ss
 
-    def pack(self, bit: int, value: int):
-        return [(j, *self.export(j)) for j in range(1 << (self.n - self.s)) if ((j >> bit) & 1) == value]
+    def pack(self, bit: int, value: int, first: int = 0, count: int = 1 << 62):
+        sel = [j for j in range(1 << (self.n - self.s)) if ((j >> bit) & 1) == value][first:first + count]
+        return [(j, *self.export(j)) for j in sel]
+
+    def image_bytes(self, bit: int, value: int) -> int:
+        return sum(len(b) + 16 for _, b, _, _ in self.pack(bit, value))
 
     def unpack(self, payload, xor_mask: int):
         for (j, blob, sc, ss) in payload:

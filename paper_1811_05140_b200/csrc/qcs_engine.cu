@@ -1974,6 +1974,12 @@ __global__ void k_unpack_finish(Dev d, const PackEntry* ent, uint64_t i0, uint64
 
 int qcs_pack_strides(qcs_dev_state_t st, int bit, int value, void* dev_buf, uint64_t cap, uint64_t* len)
 {
+    return qcs_pack_strides_range(st, bit, value, 0, UINT64_MAX, dev_buf, cap, len);
+}
+
+int qcs_pack_strides_range(qcs_dev_state_t st, int bit, int value, uint64_t first, uint64_t count, void* dev_buf,
+                           uint64_t cap, uint64_t* len)
+{
     if (!st || !len) return set_err(QCS_E_INVALID, "null argument");
     Dev& d = st->d;
     if (bit < 0 || (bit < 63 && (1ull << bit) >= d.NS)) return set_err(QCS_E_RANGE, "stride bit out of range");
@@ -1990,8 +1996,11 @@ int qcs_pack_strides(qcs_dev_state_t st, int bit, int value, void* dev_buf, uint
     CU(cudaMemcpy(sc.data(), d.scale, 8 * d.NS, cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(ss.data(), d.sum_sq, 8 * d.NS, cudaMemcpyDeviceToHost));
     std::vector<PackEntry> ent;
+    uint64_t rank_in_set = 0;  // position among the strides with bit == value
     for (uint64_t j = 0; j < d.NS; ++j)
         if ((int)((j >> bit) & 1) == (value ? 1 : 0)) {
+            const uint64_t r = rank_in_set++;
+            if (r < first || r - first >= count) continue;
             PackEntry e{};
             e.j = j;
             e.scale = sc[j];

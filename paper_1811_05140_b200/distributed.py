@@ -27,6 +27,7 @@ backend in oracle/oracle.py (CPU tests with gloo).
 from __future__ import annotations
 
 import math
+import os
 import pickle
 import struct
 import threading
@@ -229,16 +230,24 @@ class _GpuShard:
         from .engine import _check, lib
         _check(lib().qcs_import_blocks(self.h, j, blob, len(blob), scale, ssq))
 
-    def pack(self, bit: int, value: int):
-        """Device image of the strides with stride bit `bit` == value."""
+    def pack(self, bit: int, value: int, first: int = 0, count: int = (1 << 64) - 1):
+        """Device image of the strides with stride bit `bit` == value (those at
+        positions [first, first + count) among them)."""
         import ctypes as C
         import torch
         from .engine import _check, lib
         n = C.c_uint64()
-        _check(lib().qcs_pack_strides(self.h, bit, value, None, 0, C.byref(n)))
+        _check(lib().qcs_pack_strides_range(self.h, bit, value, first, count, None, 0, C.byref(n)))
         t = torch.empty(n.value, dtype=torch.uint8, device=torch.device("cuda", self.device))
-        _check(lib().qcs_pack_strides(self.h, bit, value, t.data_ptr(), n.value, C.byref(n)))
+        _check(lib().qcs_pack_strides_range(self.h, bit, value, first, count, t.data_ptr(), n.value, C.byref(n)))
         return t
+
+    def image_bytes(self, bit: int, value: int) -> int:
+        import ctypes as C
+        from .engine import _check, lib
+        n = C.c_uint64()
+        _check(lib().qcs_pack_strides(self.h, bit, value, None, 0, C.byref(n)))
+        return n.value
 
     def unpack(self, img, xor_mask: int):
         from .engine import _check, lib
@@ -295,6 +304,8 @@ class ShardedState:
         self.last_use = [-1] * nb                   # logical bit -> last gate index
         self.exchanges = 0
         self.next_target = None                     # schedule: per logical bit, sorted gate indices
+        # exchange images are streamed in chunks of at most this many bytes
+        self.exchange_chunk_bytes = int(os.environ.get("QCS_EXCHANGE_CHUNK_BYTES", str(2 << 30)))
 
     def set_schedule(self, gates) -> None:
         """Future target uses of every stride qubit, so an eviction can drop the
@@ -330,13 +341,24 @@ class ShardedState:
     def _swap(self, b: int, qb: int):
         """All ranks (the layout is global).  The lo rank of each pair sends its
         strides with local bit qb = 1, the hi rank those with qb = 0; each lands
-        at j ^ 2^qb on the other side."""
+        at j ^ 2^qb on the other side.  Streamed in chunks of strides (the same
+        chunking on every rank: the smallest choice) so the images stay
+        below exchange_chunk_bytes: received chunk c overwrites exactly the
+        positions sent in chunk c."""
         r = self.r
         peer = r ^ (1 << b)
         send_bit = 0 if (r >> b) & 1 else 1
-        payload = self.local.pack(qb, send_bit)
-        got = self.comm.exchange(peer, payload, device=getattr(self.local, "device_images", False))
-        self.local.unpack(got, 1 << qb)
+        device = getattr(self.local, "device_images", False)
+        half = self.geom.local_strides // 2
+        k = half
+        if hasattr(self.local, "image_bytes") and self.exchange_chunk_bytes:
+            per = max(1, self.local.image_bytes(qb, send_bit) // max(1, half))
+            k = max(1, min(half, self.exchange_chunk_bytes // per))
+        k = min(self.comm.allgather(k))  # every rank streams the same number of chunks
+        for first in range(0, half, k):
+            payload = self.local.pack(qb, send_bit, first, k)
+            got = self.comm.exchange(peer, payload, device=device)
+            self.local.unpack(got, 1 << qb)
         self.exchanges += 1
 
     def _make_local(self, p: int, keep: Optional[int], index: int) -> int:
@@ -505,3 +527,41 @@ def run_thread_cluster(program, geom: ShardGeometry, backend_factory, basis: int
     if errs:
         raise errs[0]
     return out[0]
+
+
+def plan_exchanges(program, geom: ShardGeometry, belady: bool = True) -> List[int]:
+    """Gate indices at which the lazy qubit permutation exchanges strides
+    between partner ranks, for `program` on `geom` — the same decisions
+    ShardedState makes, without any data (for sizing multi-GPU runs, e.g.
+    BASELINE's 37-qubit QFT on 8 GPUs)."""
+
+    class _Plan(ShardedState):
+        def __init__(self):  # no communicator, no local engine
+            self.geom, self.r = geom, 0
+            nb = geom.n_qubits - geom.stride_bits
+            self.pi, self.inv = list(range(nb)), list(range(nb))
+            self.last_use = [-1] * nb
+            self.exchanges = 0
+            self.next_target = None
+            self.at = []
+
+        def _swap(self, b, qb):
+            self.exchanges += 1
+
+    st = _Plan()
+    if belady:
+        st.set_schedule(program.gates)
+    s = geom.stride_bits
+    out = []
+    for i, g in enumerate(program.gates):
+        if g.kind in (KIND_SINGLE, KIND_CONTROLLED) and g.target >= s:
+            ctl = st.pi[g.control - s] if (g.kind == KIND_CONTROLLED and g.control >= s) else None
+            nloc = geom.local_qubits - s
+            before = st.exchanges
+            st._make_local(g.target - s, ctl if (ctl is not None and ctl < nloc) else None, i)
+            st.last_use[g.target - s] = i
+            if g.kind == KIND_CONTROLLED and g.control >= s:
+                st.last_use[g.control - s] = i
+            if st.exchanges != before:
+                out.append(i)
+    return out

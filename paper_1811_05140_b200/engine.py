@@ -71,6 +71,8 @@ def lib() -> C.CDLL:
         L.qcs_scale_all.argtypes = [C.c_void_p, C.c_double]
         L.qcs_pack_strides.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_uint64,
                                        C.POINTER(C.c_uint64)]
+        L.qcs_pack_strides_range.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
+                                             C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
         L.qcs_unpack_strides.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64]
         L.qcs_apply_gate.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_double), C.c_int,
                                      C.c_double, C.c_void_p, C.POINTER(C.c_uint64),

@@ -34,9 +34,14 @@ def _single(oracle, prog, s, basis, lad, theta):
     return st.amplitudes(), csv
 
 
+@pytest.mark.parametrize("chunk", [None, "1"])
 @pytest.mark.parametrize("ranks", [2, 4])
 @pytest.mark.parametrize("case", _cases(), ids=lambda c: c[0])
-def test_thread_cluster_oracle(oracle, case, ranks):
+def test_thread_cluster_oracle(oracle, monkeypatch, case, ranks, chunk):
+    """chunk="1": every exchange streamed one stride per chunk
+    (QCS_EXCHANGE_CHUNK_BYTES), same bits."""
+    if chunk:
+        monkeypatch.setenv("QCS_EXCHANGE_CHUNK_BYTES", chunk)
     from oracle import OracleBackend
     name, prog, s, basis, lad, theta = case
     rb = ranks.bit_length() - 1
@@ -119,7 +124,8 @@ def test_rank_geometry_errors(oracle):
 @pytest.mark.gpu
 @pytest.mark.parametrize("ranks", [2, 4])
 @pytest.mark.parametrize("case", _cases(), ids=lambda c: c[0])
-def test_thread_cluster_gpu(oracle, case, ranks):
+def test_thread_cluster_gpu(oracle, monkeypatch, case, ranks):
+    monkeypatch.setenv("QCS_EXCHANGE_CHUNK_BYTES", "4096")  # several chunks per exchange
     name, prog, s, basis, lad, theta = case
     rb = ranks.bit_length() - 1
     if prog.n_qubits - rb < s + 2:
@@ -245,6 +251,8 @@ def test_lazy_permutation_one_exchange_per_rank_qubit_gate(oracle):
             t.join()
         ex, rg = res[0]
         assert ex == rg  # exactly one exchange per gate that found its target on a rank bit
+        from paper_1811_05140_b200.distributed import plan_exchanges
+        assert len(plan_exchanges(prog, geom)) == ex  # the data-free planner makes the same decisions
         naive = sum(1 for g in prog.gates if g.kind in (0, 1) and g.target >= geom.local_qubits)
         assert ex <= 2 * naive // 2 + naive // 2, (ex, naive)  # at most 1.5 per rank-qubit gate
         assert ex < 2 * naive
