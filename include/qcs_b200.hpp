@@ -263,14 +263,16 @@ public:
     /// save (aalc.cpp:466-494): QCKP v1, byte-identical to the reference's.
     void save(const std::string& path, std::uint64_t ladder_fingerprint) const
     {
-        std::vector<std::uint8_t> out{'Q', 'C', 'K', 'P', 1};
+        // header: "QCKP", version 1, n u32, s u32, fingerprint u64, strides u64 (29 bytes)
+        std::uint8_t hdr[29] = {'Q', 'C', 'K', 'P', 1};
         const std::uint32_t n = static_cast<std::uint32_t>(geom_.n_qubits);
         const std::uint32_t s = static_cast<std::uint32_t>(geom_.stride_bits);
         const std::uint64_t ns = geom_.n_strides();
-        detail::put_le(out, &n, 4);
-        detail::put_le(out, &s, 4);
-        detail::put_le(out, &ladder_fingerprint, 8);
-        detail::put_le(out, &ns, 8);
+        std::memcpy(hdr + 5, &n, 4);
+        std::memcpy(hdr + 9, &s, 4);
+        std::memcpy(hdr + 13, &ladder_fingerprint, 8);
+        std::memcpy(hdr + 21, &ns, 8);
+        std::vector<std::uint8_t> out(hdr, hdr + sizeof hdr);
         std::vector<std::uint8_t> blocks;
         for (std::uint64_t j = 0; j < ns; ++j) {
             std::uint64_t len = 0;

@@ -256,7 +256,7 @@ static int decompress_lossless(const uint8_t* in, uint64_t len, double* out, uin
             for (uint64_t k = 0; k < run; ++k) out[produced++] = 0.0;
         } else {
             for (uint64_t k = 0; k < run; ++k) {
-                uint64_t w;
+                uint64_t w = 0;
                 rc = get_word(in, len, &pos, &w);
                 if (rc) return rc;
                 out[produced++] = from_bits(w);
@@ -298,7 +298,7 @@ static int decompress_lossy(const uint8_t* in, uint64_t len, double delta, doubl
                 if (arg == 0 || arg > n - produced)
                     return fail(QO_E_BAD_VALUE, "escape-run length inconsistent");
                 for (uint64_t k = 0; k < arg; ++k) {
-                    uint64_t w;
+                    uint64_t w = 0;
                     rc = get_word(in, len, &pos, &w);
                     if (rc) return rc;
                     pred = from_bits(w);
