@@ -129,6 +129,7 @@ struct Dev {
     double* slot_sum;      // [NS]
     uint64_t* job_stride;  // [NS]
     uint8_t* pending;      // [NS]
+    uint8_t* im_zero;      // [NS] per slot: output im plane provably zero (zero-imaginary-plane mode)
     int64_t* slot_of;      // [NS] generation<<32 | slot
     qcs_stride_report* reports;  // [NS]
     uint64_t* new_off;     // [2NS]
@@ -205,6 +206,36 @@ __global__ void k_chain_policy(Dev d, unsigned long long threshold)
     } else if (delta >= threshold) {
         sc->chain_on = 1;
         sc->chain_left = CHAIN_SPAN;
+    }
+}
+
+// Zero-imaginary-plane mode: slot s gets im_zero = 1 when the
+// gate is real and the im plane of every input stride of its unit is the
+// one-token encoding of an all-zero plane (so the output im plane is all
+// zeros too, after snap_zeros).  Pair units: both slots need both planes.
+__device__ __forceinline__ bool plane_is_zero(const Dev& d, uint64_t g)
+{
+    const int codec = d.p_codec[g];
+    const uint64_t tok = codec == 1 ? (d.L << 2) : (d.L << 1);  // run of L zeros
+    const uint64_t len = d.p_len[g];
+    if (len != (uint64_t)varint_len(tok)) return false;
+    const uint8_t* in = d.arena[d.sc->cur] + d.p_off[g];
+    uint64_t pos = 0;
+    return get_varint(in, pos) == tok;
+}
+
+__global__ void k_imz_flags(Dev d, Plan p, uint64_t n_slots)
+{
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        bool z;
+        if (p.pair) {
+            const uint64_t lo = d.job_stride[s & ~1ull], hi = d.job_stride[s | 1ull];
+            z = plane_is_zero(d, 2 * lo + 1) && plane_is_zero(d, 2 * hi + 1);
+        } else {
+            z = plane_is_zero(d, 2 * d.job_stride[s] + 1);
+        }
+        d.im_zero[s] = z ? 1 : 0;
     }
 }
 
@@ -766,6 +797,7 @@ struct qcs_dev_state {
     // serial-chain mode for non-power-of-two bounds (QCS_SERIAL_CHAIN=0 turns
     // it off): codes/predictor scratch for `chain_levels` ladder levels
     int serial_chain = 1;
+    int imz = 1;  // zero-imaginary-plane mode (QCS_IMZ=0 turns it off)
     int chain_levels = 0;
     int16_t* chain_codes = nullptr;
     double* chain_preds = nullptr;
@@ -1143,8 +1175,17 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
 
     prof_start(st, 5);
     k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen, st->lt, lad[0] > 0.0 ? 1 : 0, lad[0]);
-    prof_stop(st);
     ++st->launches;
+    // zero-imaginary-plane mode: real gates (single / controlled with a real
+    // unitary, phase flips) on strides whose im planes are all zero
+    const bool real_gate = p.kind == 2 || (p.kind <= 1 && g->u[1] == 0.0 && g->u[3] == 0.0 && g->u[5] == 0.0 &&
+                                           g->u[7] == 0.0);
+    const bool imz = real_gate && st->imz;
+    if (imz) {
+        k_imz_flags<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots);
+        ++st->launches;
+    }
+    prof_stop(st);
     if (p.reflect && given_mean) {  // sharded run: mean combined across ranks
         k_set_mean<<<1, 1, 0, s>>>(d, given_mean[0], given_mean[1]);
         ++st->launches;
@@ -1243,6 +1284,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         a.sumsq = d.slot_sum;
         a.cp = make_params(delta);
         a.counters = d.counters;
+        a.im_zero = imz ? d.im_zero : nullptr;
         return a;
     };
     const uint64_t spu = p.pair ? 2 : 1;                        // slots per unit
@@ -1372,6 +1414,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     st->device = device;
     if (const char* e = getenv("QCS_SPLIT_LOCAL")) st->split_local = atoi(e);
     if (const char* e = getenv("QCS_SERIAL_CHAIN")) st->serial_chain = atoi(e);
+    if (const char* e = getenv("QCS_IMZ")) st->imz = atoi(e);
     if (const char* e = getenv("QCS_MAX_ROUNDS")) st->max_rounds = std::max(1, atoi(e));
     cudaSetDevice(device);
     int rc = 0;
@@ -1453,6 +1496,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     TRY(dalloc(st, &d.slot_sum, d.NS));
     TRY(dalloc(st, &d.job_stride, d.NS));
     TRY(dalloc(st, &d.pending, d.NS));
+    TRY(dalloc(st, &d.im_zero, d.NS));
     TRY(dalloc(st, &d.slot_of, d.NS));
     TRY(dalloc(st, &d.reports, d.NS));
     TRY(dalloc(st, &d.new_off, 2 * d.NS));

@@ -88,6 +88,11 @@ struct FusedArgs {
                                   // every sub-chunk [slot][plane][nsub]
                                   // (k_serial_chain); no event rounds
     const int* chain_on;          // device flag gating pre_codes (null = always)
+    // zero-imaginary-plane mode: per global slot, 1 = the slot's output im
+    // plane is identically zero (real gate, zero input im planes); the CTA
+    // then encodes the re plane with all its lanes and writes the im plane's
+    // one-token encoding directly (null = off)
+    const uint8_t* im_zero;
     // ---- gate ----
     double u[8];
     int kind;                     // GateKind
@@ -229,17 +234,19 @@ __device__ __forceinline__ long long fscan_last(long long idx, double val, FS& S
 // group g = planes (2g, 2g+1), threads [g*GT, (g+1)*GT), GT = 2*LPL; each thread
 // owns 16 consecutive elements of the chunk.  Same algorithm as
 // the integer-sum argument of DESIGN.md §4, restricted to the group's warps.
-template <int LPL>
+// IMZ: the im plane is identically zero (re^2 + 0*0, the reference's sum)
+template <int LPL, bool IMZ = false>
 __device__ __forceinline__ double tsq_g(double* xs, int g, int k)
 {
-    const double r = xrow<LPL>(xs, 2 * g, k), i = xrow<LPL>(xs, 2 * g + 1, k);
+    const double r = xrow<LPL>(xs, 2 * g, k);
+    const double i = IMZ ? 0.0 : xrow<LPL>(xs, 2 * g + 1, k);
     return __dadd_rn(__dmul_rn(r, r), __dmul_rn(i, i));
 }
 
-template <int LPL, typename FS>
+template <int LPL, bool IMZ, typename FS>
 __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigned long long* counters)
 {
-    constexpr int GT = 2 * LPL;            // threads (the CTA: one stride)
+    constexpr int GT = IMZ ? LPL : 2 * LPL;  // threads (the CTA: one stride)
     constexpr int GW = GT / 32;            // warps
     constexpr int PER = (LPL * SUB) / GT;  // 16 elements per thread
     constexpr uint64_t SAT = 1ull << 62;
@@ -258,7 +265,7 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
         if (tid == 0) {
             double acc = 0.0;
 #pragma unroll 4
-            for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, tsq_g<LPL>(xs, 0, k));
+            for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, tsq_g<LPL, IMZ>(xs, 0, k));
             S.s[0] = acc;
         }
         __syncthreads();
@@ -277,7 +284,7 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
             for (int i = 0; i < PER; ++i) {
                 const int k = kb + i;
                 if (k < k0 || k >= n_it) continue;
-                const double y = tsq_g<LPL>(xs, 0, k) * to_units;
+                const double y = tsq_g<LPL, IMZ>(xs, 0, k) * to_units;
                 const double ry = rint(y);
                 // a tie (or an element beyond the binade) saturates the total
                 loc = sat_add(loc, (y >= 9007199254740992.0 || fabs(y - ry) == 0.5) ? SAT : (uint64_t)ry);
@@ -306,7 +313,7 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
             for (int i = 0; i < PER && mine == LLONG_MAX; ++i) {
                 const int k = kb + i;
                 if (k < k0 || k >= n_it) continue;
-                const double y = tsq_g<LPL>(xs, 0, k) * to_units;
+                const double y = tsq_g<LPL, IMZ>(xs, 0, k) * to_units;
                 const double ry = rint(y);
                 if (y >= 9007199254740992.0 || fabs(y - ry) == 0.5) {
                     mine = k;
@@ -326,9 +333,9 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
             long long kstar = LLONG_MAX;
             for (int i = 0; i < GW; ++i) kstar = min(kstar, S.wmin[i]);
             if (mine == kstar && kstar != LLONG_MAX) {
-                S.s[0] = __dadd_rn((double)(ms + run) / to_units, tsq_g<LPL>(xs, 0, (int)kstar));
+                S.s[0] = __dadd_rn((double)(ms + run) / to_units, tsq_g<LPL, IMZ>(xs, 0, (int)kstar));
                 if (counters) {
-                    const double y = tsq_g<LPL>(xs, 0, (int)kstar) * to_units;
+                    const double y = tsq_g<LPL, IMZ>(xs, 0, (int)kstar) * to_units;
                     atomicAdd(&counters[(y < 9007199254740992.0 && fabs(y - rint(y)) == 0.5) ? 6 : 7], 1ull);
                 }
             }
@@ -338,7 +345,7 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
         } else if (state == 1) {  // 0 + t = t exactly: the first non-zero term starts the sum
             for (int i = 0; i < PER; ++i) {
                 const int k = kb + i;
-                if (k >= k0 && k < n_it && tsq_g<LPL>(xs, 0, k) != 0.0) {
+                if (k >= k0 && k < n_it && tsq_g<LPL, IMZ>(xs, 0, k) != 0.0) {
                     mine = k;
                     break;
                 }
@@ -351,10 +358,10 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
             long long kstar = LLONG_MAX;
             for (int i = 0; i < GW; ++i) kstar = min(kstar, S.wmin[i]);
             if (kstar == LLONG_MAX) break;  // all zero: s stays 0
-            s = tsq_g<LPL>(xs, 0, (int)kstar);
+            s = tsq_g<LPL, IMZ>(xs, 0, (int)kstar);
             k0 = (int)kstar + 1;
         } else {  // far below any practical state: one term at a time, in order
-            s = __dadd_rn(s, tsq_g<LPL>(xs, 0, k0));
+            s = __dadd_rn(s, tsq_g<LPL, IMZ>(xs, 0, k0));
             ++k0;
         }
     }
@@ -467,8 +474,12 @@ __device__ __forceinline__ double lane_chain(const CodecParams& cp, const double
         }                                                                    \
     } while (0)
 
-template <bool LOSSY, int NPL, int LPL, int MODE>
-__global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL > 128 ? 2 : 4))) k_fused(FusedArgs a)
+// The encoder body.  IMZ (zero-imaginary-plane mode): NPL = 1 and the CTA's
+// LPL lanes all work on the re plane of a stride whose im plane is zero
+// before and after the gate; the im plane's encoding (one zero-run token) is
+// written directly.
+template <bool LOSSY, int NPL, int LPL, int MODE, bool IMZ>
+__device__ __forceinline__ void fused_body(const FusedArgs& a)
 {
     unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long ph_t = clock64();
@@ -482,6 +493,7 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL >
     const uint64_t slot = (uint64_t)b;
     const int comp = pl;
     const uint64_t gslot = a.slot_base + slot;  // global slot (tables)
+    const uint64_t row = IMZ ? 2 * slot : (uint64_t)b * NPL + pl;  // launch-local plane row (X, scratch)
     if (a.pending && !a.pending[a.slot_base + (uint64_t)b]) return;
 
     extern __shared__ __align__(16) unsigned char smem[];
@@ -517,7 +529,7 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL >
     const SideEntry* in_side = nullptr;
     const double* xg = nullptr;
     if (MODE == MODE_RAW) {
-        xg = a.X + (uint64_t)b * NPL * a.x_plane_stride + (uint64_t)pl * a.x_plane_stride;
+        xg = a.X + row * a.x_plane_stride;
     } else {
         in_stride = a.job_stride[gslot];
         const uint64_t gpl = 2 * in_stride + comp;
@@ -619,20 +631,25 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL >
                         const int i0 = (int)((((uint64_t)q & ~lo_mask) << 1) | ((uint64_t)q & lo_mask));
                         const int i1 = i0 | (int)hb;
                         if (a.local_ctl >= 0 && !(((base + i0) >> a.local_ctl) & 1)) continue;
-                        pair_update(m8, xrow<LPL>(xs, 0, i0), xrow<LPL>(xs, 1, i0), xrow<LPL>(xs, 0, i1),
-                                    xrow<LPL>(xs, 1, i1));
+                        if (IMZ) {  // the reference's arithmetic with zero im inputs
+                            double z0 = 0.0, z1 = 0.0;
+                            pair_update(m8, xrow<LPL>(xs, 0, i0), z0, xrow<LPL>(xs, 0, i1), z1);
+                        } else {
+                            pair_update(m8, xrow<LPL>(xs, 0, i0), xrow<LPL>(xs, 1, i0), xrow<LPL>(xs, 0, i1),
+                                        xrow<LPL>(xs, 1, i1));
+                        }
                     }
                 } else if (a.kind == 2) {
                     if (tid == 0 && a.flip_off >= base && a.flip_off < base + n_it) {
                         const int k = (int)(a.flip_off - base);
                         xrow<LPL>(xs, 0, k) = -xrow<LPL>(xs, 0, k);
-                        xrow<LPL>(xs, 1, k) = -xrow<LPL>(xs, 1, k);
+                        if (!IMZ) xrow<LPL>(xs, 1, k) = -xrow<LPL>(xs, 1, k);
                     }
                 } else {
                     const double mr2 = 2.0 * a.mean[0], mi2 = 2.0 * a.mean[1];
                     for (int i = tid; i < n_it; i += NPL * LPL) {
                         xrow<LPL>(xs, 0, i) = __dsub_rn(mr2, xrow<LPL>(xs, 0, i));
-                        xrow<LPL>(xs, 1, i) = __dsub_rn(mi2, xrow<LPL>(xs, 1, i));
+                        if (!IMZ) xrow<LPL>(xs, 1, i) = __dsub_rn(mi2, xrow<LPL>(xs, 1, i));
                     }
                 }
             }
@@ -642,7 +659,7 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL >
             for (int i = 0; i < cnt; ++i) xl[i] = snap(xl[i]);
         }
         if (MODE == MODE_LOCAL && a.dump_x) {  // serial-chain mode: input only
-            double* dx = a.dump_x + ((uint64_t)b * NPL + pl) * n + e0;
+            double* dx = a.dump_x + row * n + e0;
             for (int i = 0; i < cnt; ++i) dx[i] = xl[i];
             __syncthreads();
             continue;
@@ -655,7 +672,6 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL >
             // serial-chain mode: the codes and sub-chunk entry predictors of
             // the reference chain were computed by k_serial_chain
             if (cnt > 0) {
-                const uint64_t row = (uint64_t)b * NPL + pl;
                 const int16_t* pc = a.pre_codes + row * n + e0;
                 for (int i = 0; i < cnt; ++i) cl[i] = pc[i];
                 const double P0 = a.pre_pred[row * a.nsub + e0 / SUB];
@@ -796,7 +812,7 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL >
 
         QCS_PHASE(2);
         // 5. stored sum of squares per stride
-        if (a.sumsq) fused_sumsq<LPL>(xs, n_it, S, a.counters);
+        if (a.sumsq) fused_sumsq<LPL, IMZ>(xs, n_it, S, a.counters);
 
         QCS_PHASE(3);
         // 6. run summary of each lane (bitmasks) and the run entering it
@@ -1003,6 +1019,46 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL >
         for (int i = 0; i < 8; ++i) a.cta_trace[8 * (a.slot_base + (uint64_t)b) + i] = ph_acc[i];
     if (lane == 0) a.out_len[2 * gslot + comp] = C.out_pos;
     if (a.sumsq && tid == 0) a.sumsq[gslot] = S.s[0];
+    if (IMZ) {
+        // the im plane: all zeros -> one zero run of n elements (lossless
+        // codec.cpp:129-145 / lossy :224-247 both emit a single run token);
+        // every sub-chunk starts inside it with predictor 0
+        uint8_t* out1;
+        SideEntry* side1;
+        if (a.pool) {
+            const uint64_t g1 = 2 * a.job_stride[gslot] + 1;
+            const int ls1 = (int)((a.p_off[g1] / a.cap) & 1);
+            out1 = a.out + (2 * g1 + 1 - ls1) * a.cap;
+            side1 = a.side + (2 * g1 + 1 - ls1) * a.nsub;
+        } else {
+            out1 = a.out + (2 * slot + 1) * a.cap;
+            side1 = a.side + (2 * slot + 1) * a.nsub;
+        }
+        const uint64_t tok = run_token(LOSSY, TY_Z, n);
+        if (tid == 0) {
+            put_varint(out1, tok);
+            a.out_len[2 * gslot + 1] = (uint64_t)varint_len(tok);
+        }
+        const uint64_t nsub_n = (n + SUB - 1) / SUB;
+        for (uint64_t sc = tid; sc < nsub_n; sc += NPL * LPL) {
+            SideEntry se;
+            se.off = 0;
+            se.skip = (uint32_t)(sc * SUB);
+            se.pred = 0.0;
+            side1[sc] = se;
+        }
+    }
+}
+
+template <bool LOSSY, int NPL, int LPL, int MODE>
+__global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL > 128 ? 2 : 4))) k_fused(FusedArgs a)
+{
+    // a stride whose im plane stays zero gets all of the CTA's lanes for its
+    // re plane (same thread count and shared-memory layout)
+    if (NPL == 2 && a.im_zero && a.im_zero[a.slot_base + blockIdx.x])
+        fused_body<LOSSY, 1, NPL * LPL, MODE, true>(a);
+    else
+        fused_body<LOSSY, NPL, LPL, MODE, false>(a);
 }
 
 // The reference chain of compress_lossy (codec.cpp:206-250) for bounds whose

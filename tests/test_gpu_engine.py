@@ -159,3 +159,49 @@ def test_engine_serial_chain_modes(q, oracle, monkeypatch, mode, kind, n, s, bas
     res, got = gpu_run(prog, s, basis, ladder, theta)
     assert got == want, first_diff(want, got)
     assert res.state.to_amplitudes().tobytes() == st.amplitudes().tobytes()
+
+
+IMZ_CASES = [
+    ("grover_gates", 12, 9, 0, [2.0 ** -20], 1.0),
+    ("grover_gates", 11, 3, 0, [0.0, 2.0 ** -22, 1e-4], 64.0),    # 8-amplitude strides, ladder
+    ("grover_ref", 10, 6, 0, [0.0, 1e-6, 1e-4], 32.0),            # reflect_mean gates stay two-plane
+    ("real_random", 11, 7, 5, [0.0, 2.0 ** -18], 4.0),
+]
+
+
+def _real_random(n, seed):
+    """Random gates from a real set (H, X, Z, CX, CZ, CP(pi)), seeded."""
+    import random
+    rng = random.Random(seed)
+    p = cc.CircuitProgram(n, [], "real-random")
+    U = [cc.Unitary2x2.hadamard(), cc.Unitary2x2.pauli_x(), cc.Unitary2x2.pauli_z()]
+    for _ in range(120):
+        t = rng.randrange(n)
+        if rng.random() < 0.4:
+            c = rng.randrange(n - 1)
+            c = c + 1 if c >= t else c
+            p.gates.append(cc.GateOp.controlled(U[rng.randrange(1, 3)], c, t, f"c {c} {t}"))
+        else:
+            p.gates.append(cc.GateOp.single(U[rng.randrange(3)], t, f"u {t}"))
+    return p
+
+
+@pytest.mark.parametrize("imz", ["0", "1"])
+@pytest.mark.parametrize("big", [False, True])
+@pytest.mark.parametrize("kind,n,s,basis,ladder,theta", IMZ_CASES)
+def test_engine_zero_imaginary_plane_mode(q, oracle, monkeypatch, imz, big, kind, n, s, basis, ladder, theta):
+    """Real gates on strides whose im planes are zero: the CTA encodes the re
+    plane with all its lanes and writes the im plane's one-token encoding
+    (QCS_IMZ=1, default) — bit-identical to the two-plane path and the oracle,
+    in both layouts."""
+    monkeypatch.setenv("QCS_IMZ", imz)
+    if big:
+        monkeypatch.setenv("QCS_FORCE_BIG", "1")
+        monkeypatch.setenv("QCS_WAVE_SLOTS", "3")
+    prog = _real_random(n, 9) if kind == "real_random" else _prog(kind, n)
+    st, want = oracle_run(oracle, prog, s, basis, ladder, theta)
+    res, got = gpu_run(prog, s, basis, ladder, theta)
+    assert got == want, first_diff(want, got)
+    assert res.state.to_amplitudes().tobytes() == st.amplitudes().tobytes()
+    for j in range(1 << (n - s)):
+        assert res.state.export_blocks(j)[0] == st.export_blocks(j)
