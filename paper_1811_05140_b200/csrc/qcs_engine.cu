@@ -174,7 +174,10 @@ __device__ __forceinline__ SideEntry* side_of(const Dev& d, uint64_t g)
     return d.pool ? d.side + (2 * g + pool_sel(d, g)) * d.nsub : d.side + g * d.nsub;
 }
 
-__global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen, LevelTag lt, int codec0, double delta0)
+__device__ __forceinline__ bool plane_is_zero(const Dev& d, uint64_t g);
+
+__global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen, LevelTag lt, int codec0, double delta0,
+                            int imz)
 {
     if (blockIdx.x == 0 && threadIdx.x == 0) d.sc->gate_cin = 0;  // the commits accumulate it
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
@@ -185,6 +188,14 @@ __global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen, Level
         d.slot_of[j] = (int64_t)((gen << 32) | s);
         lt.slot_codec[s] = (int8_t)codec0;  // ladder level 0
         lt.slot_delta[s] = delta0;
+        if (imz) {  // zero-imaginary-plane flags (see k_imz_flags)
+            bool z;
+            if (p.pair)
+                z = plane_is_zero(d, 2 * slot_stride(p, s & ~1ull) + 1) && plane_is_zero(d, 2 * slot_stride(p, s | 1ull) + 1);
+            else
+                z = plane_is_zero(d, 2 * j + 1);
+            d.im_zero[s] = z ? 1 : 0;
+        }
     }
 }
 
@@ -222,21 +233,6 @@ __device__ __forceinline__ bool plane_is_zero(const Dev& d, uint64_t g)
     const uint8_t* in = d.arena[d.sc->cur] + d.p_off[g];
     uint64_t pos = 0;
     return get_varint(in, pos) == tok;
-}
-
-__global__ void k_imz_flags(Dev d, Plan p, uint64_t n_slots)
-{
-    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
-         s += (uint64_t)gridDim.x * blockDim.x) {
-        bool z;
-        if (p.pair) {
-            const uint64_t lo = d.job_stride[s & ~1ull], hi = d.job_stride[s | 1ull];
-            z = plane_is_zero(d, 2 * lo + 1) && plane_is_zero(d, 2 * hi + 1);
-        } else {
-            z = plane_is_zero(d, 2 * d.job_stride[s] + 1);
-        }
-        d.im_zero[s] = z ? 1 : 0;
-    }
 }
 
 struct DecodeJob {
@@ -283,7 +279,7 @@ constexpr int DG_HALF = 8 * DG_R;
 constexpr size_t DG_SMEM = sizeof(double) * DG_R * XS_STRIDE;
 
 __global__ void __launch_bounds__(DG_R) k_decode_gate(Dev d, Plan p, GateParams gp, int mode,
-                                                    uint64_t chunks, uint64_t slot_base)
+                                                    uint64_t chunks, uint64_t slot_base, const uint8_t* imz)
 {
     if (d.sc->err) return;
     extern __shared__ __align__(16) unsigned char dg_smem[];
@@ -316,9 +312,17 @@ __global__ void __launch_bounds__(DG_R) k_decode_gate(Dev d, Plan p, GateParams 
     const uint64_t j = d.job_stride[slot_base + slot];
     const uint64_t g = 2 * j + comp;
     const int cnt = (int)umin64(SUB, L - umin64(e0, L));
-    if (cnt > 0)
-        decode_sub(d.arena[d.sc->cur] + d.p_off[g], d.p_codec[g], 2.0 * d.p_delta[g],
-                   side_of(d, g)[e0 / SUB], cnt, xs + tid * XS_STRIDE, d.scale[j]);
+    // zero-imaginary-plane mode: a zero im plane needs no decode (and its
+    // gated values, zeros, are not written: the encoder reads only re)
+    const bool zim = imz && imz[slot_base + slot];
+    if (cnt > 0) {
+        if (zim && comp == 1) {
+            for (int i = 0; i < cnt; ++i) xs[tid * XS_STRIDE + i] = 0.0;
+        } else {
+            decode_sub(d.arena[d.sc->cur] + d.p_off[g], d.p_codec[g], 2.0 * d.p_delta[g],
+                       side_of(d, g)[e0 / SUB], cnt, xs + tid * XS_STRIDE, d.scale[j]);
+        }
+    }
     __syncthreads();
     double m[8];
 #pragma unroll
@@ -361,6 +365,7 @@ __global__ void __launch_bounds__(DG_R) k_decode_gate(Dev d, Plan p, GateParams 
                 e_base = far_lo(c * DG_HALF) + ((q >> 1) ? hb : 0);
             }
         }
+        if (ocomp == 1 && imz && imz[slot_base + oslot]) continue;
         double* dst = d.X + (2 * oslot + ocomp) * L + e_base;
         const double* rows = xs + (uint64_t)q * (seg / SUB) * XS_STRIDE;
         const int m = (int)umin64((uint64_t)seg, L - umin64(e_base, L));
@@ -1174,17 +1179,14 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     const uint64_t gen = ++st->gen;
 
     prof_start(st, 5);
-    k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen, st->lt, lad[0] > 0.0 ? 1 : 0, lad[0]);
-    ++st->launches;
     // zero-imaginary-plane mode: real gates (single / controlled with a real
     // unitary, phase flips) on strides whose im planes are all zero
     const bool real_gate = p.kind == 2 || (p.kind <= 1 && g->u[1] == 0.0 && g->u[3] == 0.0 && g->u[5] == 0.0 &&
                                            g->u[7] == 0.0);
     const bool imz = real_gate && st->imz;
-    if (imz) {
-        k_imz_flags<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots);
-        ++st->launches;
-    }
+    k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen, st->lt, lad[0] > 0.0 ? 1 : 0, lad[0],
+                                                            imz ? 1 : 0);
+    ++st->launches;
     prof_stop(st);
     if (p.reflect && given_mean) {  // sharded run: mean combined across ranks
         k_set_mean<<<1, 1, 0, s>>>(d, given_mean[0], given_mean[1]);
@@ -1297,7 +1299,8 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
                                                   : (dg == DG_FAR ? d.L / (2 * DG_HALF) : d.L / DG_IN_CH);
             const uint64_t units = dg == DG_PAIR ? (u1 - u0) : nw;
             prof_start(st, 0);
-            k_decode_gate<<<(unsigned)(units * chunks), DG_R, DG_SMEM, s>>>(d, p, gp, dg, chunks, s0);
+            k_decode_gate<<<(unsigned)(units * chunks), DG_R, DG_SMEM, s>>>(d, p, gp, dg, chunks, s0,
+                                                                          imz ? d.im_zero : nullptr);
             prof_stop(st);
             ++st->launches;
         }
