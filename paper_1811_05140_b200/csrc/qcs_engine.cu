@@ -803,6 +803,7 @@ struct qcs_dev_state {
     // it off): codes/predictor scratch for `chain_levels` ladder levels
     int serial_chain = 1;
     int imz = 1;  // zero-imaginary-plane mode (QCS_IMZ=0 turns it off)
+    int imz_split = 0;  // QCS_IMZ_SPLIT=1: real gates take the split path (measured slower on C2)
     int chain_levels = 0;
     int16_t* chain_codes = nullptr;
     double* chain_preds = nullptr;
@@ -1203,8 +1204,13 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     int dg = -1;
     if (p.pair) dg = DG_PAIR;
     else if (p.kind <= 1 && (1ull << p.t) >= (uint64_t)fused_span()) dg = DG_FAR;
-    else if (p.kind <= 1 && st->split_local && (1ull << p.t) >= DG_HALF) dg = DG_FAR;
-    else if (p.kind <= 1 && st->split_local && d.L >= DG_IN_CH) dg = DG_IN;
+    // in-chunk partners take the split path too when asked (QCS_SPLIT_LOCAL) and
+    // for real gates under the zero-imaginary-plane mode: a whole-CTA re plane
+    // decodes 8192 elements per iteration, more payload than the in-kernel
+    // staging holds, while k_decode_gate decodes it at full occupancy
+    const bool split_in = st->split_local || (imz && st->imz_split);
+    if (dg < 0 && p.kind <= 1 && split_in && (1ull << p.t) >= DG_HALF) dg = DG_FAR;
+    else if (dg < 0 && p.kind <= 1 && split_in && d.L >= DG_IN_CH) dg = DG_IN;
     static const int force_wide = [] {
         const char* e = getenv("QCS_WIDE");
         return e ? atoi(e) : -1;
@@ -1418,6 +1424,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     if (const char* e = getenv("QCS_SPLIT_LOCAL")) st->split_local = atoi(e);
     if (const char* e = getenv("QCS_SERIAL_CHAIN")) st->serial_chain = atoi(e);
     if (const char* e = getenv("QCS_IMZ")) st->imz = atoi(e);
+    if (const char* e = getenv("QCS_IMZ_SPLIT")) st->imz_split = atoi(e);
     if (const char* e = getenv("QCS_MAX_ROUNDS")) st->max_rounds = std::max(1, atoi(e));
     cudaSetDevice(device);
     int rc = 0;
