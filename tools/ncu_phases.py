@@ -24,7 +24,7 @@ def source(name):
 
 
 src = source("qcs_fused.cuh")
-kstart = next(i + 1 for i, l in enumerate(src) if "k_fused(FusedArgs a)" in l)
+kstart = next(i + 1 for i, l in enumerate(src) if "void fused_body(" in l or "k_fused(FusedArgs a)" in l)
 marks = [(i + 1, int(m.group(1))) for i, l in enumerate(src) for m in [re.search(r"QCS_PHASE\((\d)\);", l)] if m]
 names = {-1: "0 input", 0: "1 rounds", 1: "2 final", 2: "3 sum", 3: "4 tokcount", 4: "5 write", 5: "6 carry", 6: "7 tail"}
 funcs = [(i + 1, m.group(1)) for i, l in enumerate(src)
