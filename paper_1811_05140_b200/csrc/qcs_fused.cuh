@@ -599,8 +599,25 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
             // varint and the words it owns for this iteration's elements.
             const uint8_t* src = in_bytes;
             if (MODE == MODE_LOCAL) {
-                constexpr uint64_t STAGE = sizeof(int16_t) * ITP;  // bytes per plane
-                uint8_t* stage = reinterpret_cast<uint8_t*>(code + pl * LPL * CODE_STRIDE);
+                // staging room: everything dead between an iteration's end
+                // and its decode — the code rows, and the per-iteration lane
+                // arrays at the head of S (entryP .. runw).  One plane in the
+                // CTA: all of it; two: the code rows for plane 0, the lane
+                // arrays for plane 1
+                uint8_t* const lane_arrays = reinterpret_cast<uint8_t*>(&S.entryP[0]);
+                uint8_t* const lane_end = reinterpret_cast<uint8_t*>(&S.ftype[0]);
+                uint8_t* stage;
+                uint64_t STAGE;
+                if (NPL == 1) {
+                    stage = reinterpret_cast<uint8_t*>(code);
+                    STAGE = (uint64_t)(lane_end - stage) & ~uint64_t(15);
+                } else if (pl == 0) {
+                    stage = reinterpret_cast<uint8_t*>(code);
+                    STAGE = LY::CODE_BYTES & ~size_t(15);
+                } else {
+                    stage = lane_arrays;
+                    STAGE = (uint64_t)(lane_end - lane_arrays) & ~uint64_t(15);
+                }
                 const uint64_t sc0 = base / SUB;
                 const uint64_t lo = in_side[sc0].off & ~uint64_t(15);
                 uint64_t hi;
