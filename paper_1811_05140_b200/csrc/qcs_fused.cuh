@@ -239,7 +239,8 @@ template <int LPL, bool IMZ = false>
 __device__ __forceinline__ double tsq_g(double* xs, int g, int k)
 {
     const double r = xrow<LPL>(xs, 2 * g, k);
-    const double i = IMZ ? 0.0 : xrow<LPL>(xs, 2 * g + 1, k);
+    if (IMZ) return __dmul_rn(r, r);  // fl(r*r + 0*0) == fl(r*r): r*r >= +0
+    const double i = xrow<LPL>(xs, 2 * g + 1, k);
     return __dadd_rn(__dmul_rn(r, r), __dmul_rn(i, i));
 }
 
