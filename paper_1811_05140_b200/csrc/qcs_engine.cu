@@ -381,6 +381,78 @@ __global__ void __launch_bounds__(DG_R) k_decode_gate(Dev d, Plan p, GateParams 
     }
 }
 
+// k_decode_gate for a state whose every im plane is zero (a real state: the
+// host tracks it, all_im_zero) and a real gate, cross-chunk partners
+// (DG_FAR / DG_PAIR): all DG_R threads decode re rows — DG_R/2 per side, so
+// a CTA covers DG_RE_CH = 16 * DG_R elements per side — the gate runs on
+// (re, 0) pairs with the reference's arithmetic, and only re is written (the
+// encoder's zero-imaginary-plane mode writes the im plane itself).
+constexpr int DG_RE_CH = 16 * DG_R;
+
+__global__ void __launch_bounds__(DG_R) k_decode_gate_re(Dev d, Plan p, GateParams gp, int mode, uint64_t chunks,
+                                                       uint64_t slot_base)
+{
+    if (d.sc->err) return;
+    extern __shared__ __align__(16) unsigned char dg_smem[];
+    double* xs = reinterpret_cast<double*>(dg_smem);
+    const uint64_t u = blockIdx.x / chunks, c = blockIdx.x % chunks;
+    const int tid = threadIdx.x;
+    const uint64_t L = d.L;
+    const uint64_t hb = 1ull << (p.pair ? 0 : p.t);
+    constexpr int RH = DG_R / 2;
+    auto far_lo = [&](uint64_t e) { return ((e >> p.t) << (p.t + 1)) | (e & (hb - 1)); };
+    const int side = tid / RH;  // 0 lo / A, 1 hi / B
+    const uint64_t sub = (uint64_t)(tid % RH) * SUB;
+    uint64_t slot, e0;
+    if (mode == DG_PAIR) {
+        slot = 2 * u + side;
+        e0 = c * DG_RE_CH + sub;
+    } else {
+        slot = u;
+        e0 = far_lo(c * DG_RE_CH) + (side ? hb : 0) + sub;
+    }
+    const uint64_t j = d.job_stride[slot_base + slot];
+    const uint64_t g = 2 * j;  // re plane
+    const int cnt = (int)umin64(SUB, L - umin64(e0, L));
+    if (cnt > 0)
+        decode_sub(d.arena[d.sc->cur] + d.p_off[g], d.p_codec[g], 2.0 * d.p_delta[g], side_of(d, g)[e0 / SUB], cnt,
+                   xs + tid * XS_STRIDE, d.scale[j]);
+    __syncthreads();
+    double m[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = gp.u[i];
+    auto at = [&](int row_base, int k) -> double& { return xs[(row_base + (k >> 5)) * XS_STRIDE + (k & 31)]; };
+    for (int i = tid; i < DG_RE_CH; i += DG_R) {
+        const uint64_t gi = (mode == DG_PAIR ? c * DG_RE_CH : far_lo(c * DG_RE_CH)) + i;
+        if (p.local_ctl >= 0 && !((gi >> p.local_ctl) & 1)) continue;
+        double z0 = 0.0, z1 = 0.0;  // the im inputs, exactly zero
+        pair_update(m, at(0, i), z0, at(RH, i), z1);
+    }
+    __syncthreads();
+    for (int q = 0; q < 2; ++q) {
+        uint64_t oslot, e_base;
+        if (mode == DG_PAIR) {
+            oslot = 2 * u + q;
+            e_base = c * DG_RE_CH;
+        } else {
+            oslot = u;
+            e_base = far_lo(c * DG_RE_CH) + (q ? hb : 0);
+        }
+        double* dst = d.X + (2 * oslot) * L + e_base;
+        const double* rows = xs + (uint64_t)q * RH * XS_STRIDE;
+        const int mm = (int)umin64((uint64_t)DG_RE_CH, L - umin64(e_base, L));
+        if (mm == DG_RE_CH) {
+            for (int k = 2 * tid; k < DG_RE_CH; k += 2 * DG_R) {
+                const double v0 = snap(rows[(k >> 5) * XS_STRIDE + (k & 31)]);
+                const double v1 = snap(rows[((k + 1) >> 5) * XS_STRIDE + ((k + 1) & 31)]);
+                *reinterpret_cast<double2*>(dst + k) = make_double2(v0, v1);
+            }
+        } else {
+            for (int k = tid; k < mm; k += DG_R) dst[k] = snap(rows[(k >> 5) * XS_STRIDE + (k & 31)]);
+        }
+    }
+}
+
 // stride_amplitude_sum (gate.cpp:303-311) of every scaled stride, straight
 // from the block store: one CTA per stride decodes 4096-element chunks of both
 // planes into shared memory; one thread per plane folds them serially in
@@ -803,6 +875,7 @@ struct qcs_dev_state {
     // it off): codes/predictor scratch for `chain_levels` ladder levels
     int serial_chain = 1;
     int imz = 1;  // zero-imaginary-plane mode (QCS_IMZ=0 turns it off)
+    bool all_im_zero = true;  // every im plane is zero (real state): real gates keep it
     int imz_split = 0;  // QCS_IMZ_SPLIT=1: real gates take the split path (measured slower on C2)
     int chain_levels = 0;
     int16_t* chain_codes = nullptr;
@@ -1305,8 +1378,21 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
                                                   : (dg == DG_FAR ? d.L / (2 * DG_HALF) : d.L / DG_IN_CH);
             const uint64_t units = dg == DG_PAIR ? (u1 - u0) : nw;
             prof_start(st, 0);
-            k_decode_gate<<<(unsigned)(units * chunks), DG_R, DG_SMEM, s>>>(d, p, gp, dg, chunks, s0,
-                                                                          imz ? d.im_zero : nullptr);
+            const bool re_only = imz && st->all_im_zero && dg != DG_IN && d.L >= DG_RE_CH &&
+                                 (dg == DG_PAIR || (1ull << p.t) >= (uint64_t)DG_RE_CH);
+            if (re_only) {
+                static bool attr = false;
+                if (!attr) {
+                    CU(cudaFuncSetAttribute(k_decode_gate_re, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)DG_SMEM));
+                    attr = true;
+                }
+                const uint64_t chunks_re = dg == DG_PAIR ? (d.L + DG_RE_CH - 1) / DG_RE_CH : d.L / (2 * DG_RE_CH);
+                k_decode_gate_re<<<(unsigned)(units * chunks_re), DG_R, DG_SMEM, s>>>(d, p, gp, dg, chunks_re, s0);
+            } else {
+                k_decode_gate<<<(unsigned)(units * chunks), DG_R, DG_SMEM, s>>>(d, p, gp, dg, chunks, s0,
+                                                                              imz ? d.im_zero : nullptr);
+            }
             prof_stop(st);
             ++st->launches;
         }
@@ -1375,6 +1461,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     prof_stop(st);
     ++st->launches;
     CU(cudaGetLastError());
+    if (!real_gate) st->all_im_zero = false;  // a complex gate (or reflect_mean) may fill im planes
     return 0;
 }
 
@@ -1856,6 +1943,7 @@ int qcs_export_blocks(qcs_dev_state_t st, uint64_t j, uint8_t* buf, uint64_t cap
 int qcs_import_blocks(qcs_dev_state_t st, uint64_t j, const uint8_t* buf, uint64_t len,
                       double scale, double ssq)
 {
+    if (st) st->all_im_zero = false;  // arbitrary blocks: no longer known real
     if (!st || !buf) return set_err(QCS_E_INVALID, "null argument");
     if (j >= st->d.NS) return set_err(QCS_E_RANGE, "stride index out of range");
     cudaSetDevice(st->device);
@@ -2096,6 +2184,7 @@ int qcs_pack_strides_range(qcs_dev_state_t st, int bit, int value, uint64_t firs
 
 int qcs_unpack_strides(qcs_dev_state_t st, const void* dev_buf, uint64_t len, uint64_t xor_mask)
 {
+    if (st) st->all_im_zero = false;  // images from another shard: no longer known real
     if (!st || !dev_buf) return set_err(QCS_E_INVALID, "null argument");
     Dev& d = st->d;
     cudaSetDevice(st->device);

@@ -166,6 +166,8 @@ IMZ_CASES = [
     ("grover_gates", 11, 3, 0, [0.0, 2.0 ** -22, 1e-4], 64.0),    # 8-amplitude strides, ladder
     ("grover_ref", 10, 6, 0, [0.0, 1e-6, 1e-4], 32.0),            # reflect_mean gates stay two-plane
     ("real_random", 11, 7, 5, [0.0, 2.0 ** -18], 4.0),
+    ("grover_gates", 14, 12, 0, [2.0 ** -22], 1.0),              # pair units through k_decode_gate_re
+    ("real_random", 14, 13, 3, [0.0, 2.0 ** -20], 8.0),          # in-stride far (t = 12) and pairs
 ]
 
 
