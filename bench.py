@@ -147,22 +147,39 @@ def measured_peaks():
 # ---------------------------------------------------------------------------
 # dense checker for fidelity (torch on the GPU; test-side only)
 # ---------------------------------------------------------------------------
-def dense_state(prog, n_gates, device):
+def dense_apply(psi, n, g):
+    """One gate on a dense complex128 state (the uncompressed checker, after
+    dense.cpp:30-76; torch complex arithmetic, so agreement is to rounding)."""
+    import torch
+    if g.kind == cc.KIND_FLIP:
+        psi[g.flip_index] = -psi[g.flip_index]
+        return
+    if g.kind == cc.KIND_REFLECT:
+        psi.copy_(2.0 * psi.mean() - psi)
+        return
+    u, t = g.unitary, g.target
+    if g.kind == cc.KIND_SINGLE:
+        v = psi.view(1 << (n - t - 1), 2, 1 << t)
+        a0, a1 = v[:, 0, :].clone(), v[:, 1, :].clone()
+        v[:, 0, :] = u.u11 * a0 + u.u12 * a1
+        v[:, 1, :] = u.u21 * a0 + u.u22 * a1
+        return
+    c = g.control
+    hi, lo = max(c, t), min(c, t)
+    v = psi.view(1 << (n - hi - 1), 2, 1 << (hi - lo - 1), 2, 1 << lo)
+    sel = (lambda b, x: v[:, 1, :, b, :]) if c == hi else (lambda b, x: v[:, b, :, 1, :])
+    a0, a1 = sel(0, None).clone(), sel(1, None).clone()
+    sel(0, None).copy_(u.u11 * a0 + u.u12 * a1)
+    sel(1, None).copy_(u.u21 * a0 + u.u22 * a1)
+
+
+def dense_state(prog, n_gates, device, basis=0):
     import torch
     n = prog.n_qubits
     psi = torch.zeros(1 << n, dtype=torch.complex128, device=device)
-    psi[0] = 1.0
+    psi[basis] = 1.0
     for g in prog.gates[:n_gates]:
-        if g.kind == cc.KIND_FLIP:
-            psi[g.flip_index] = -psi[g.flip_index]
-        elif g.kind == cc.KIND_SINGLE:
-            u = g.unitary
-            v = psi.view(1 << (n - g.target - 1), 2, 1 << g.target)
-            a0, a1 = v[:, 0, :].clone(), v[:, 1, :].clone()
-            v[:, 0, :] = u.u11 * a0 + u.u12 * a1
-            v[:, 1, :] = u.u21 * a0 + u.u22 * a1
-        else:
-            raise NotImplementedError("bench dense checker covers the C2 gate set")
+        dense_apply(psi, n, g)
     return psi
 
 
@@ -499,12 +516,43 @@ def run_b200(args, rank, world, local_rank):
 QFT_CONFIGS = {
     "C1": dict(n=20, s=14, eps=1e-3, basis=552808, note="BASELINE configs[0]; basis = mt19937_64(1)() & (2^20-1)"),
     "C3": dict(n=34, s=20, eps=1e-3, basis=None, note="BASELINE configs[2]; 256 GiB uncompressed > one GPU"),
+    # BASELINE configs[3] (6x6 = 36 qubits over 2-8 GPUs) at the largest grid one
+    # B200 also holds uncompressed for the fidelity check: 5x6 = 30 qubits
+    "C4s": dict(n=30, s=20, eps=1e-2, basis=0, grid=(5, 6, 20, 2024),
+                note="BASELINE configs[3] shape (seeded NN-CZ + {sqrt X, sqrt Y, T} grid, depth 20) on 5x6 "
+                     "qubits, one GPU; fidelity against a dense complex128 run on the same GPU"),
 }
 
 
 def qft_basis(name, n):
     c = QFT_CONFIGS[name]
     return c["basis"] if c["basis"] is not None else next(cc.splitmix64(n)) & ((1 << n) - 1)
+
+
+def dense_fidelity(state, prog, n, s, x, device):
+    """Fidelity |<dense|state>| / (|dense| |state|) against a dense complex128
+    run of the same circuit on the GPU (dense.cpp:94-108), streamed stride by
+    stride; also the largest amplitude difference."""
+    import torch
+    psi = dense_state(prog, len(prog.gates), device, basis=x)
+    L, NS = 1 << s, 1 << (n - s)
+    batch = max(1, min(NS, (1 << 28) // (16 * L)))
+    buf = torch.empty(batch * 2 * L, dtype=torch.float64, device=device)
+    ov = torch.zeros((), dtype=torch.complex128, device=device)
+    nrm = torch.zeros((), dtype=torch.float64, device=device)
+    maxerr = torch.zeros((), dtype=torch.float64, device=device)
+    for j0 in range(0, NS, batch):
+        m = min(batch, NS - j0)
+        state.read_strides_device(j0, m, buf.data_ptr())
+        v = buf[: m * 2 * L].view(m, 2, L)
+        a = torch.complex(v[:, 0, :], v[:, 1, :]).reshape(-1)
+        e = psi[j0 * L:(j0 + m) * L]
+        ov += torch.sum(torch.conj(e) * a)
+        nrm += torch.sum(a.real * a.real + a.imag * a.imag)
+        maxerr = torch.maximum(maxerr, torch.max(torch.abs(a - e)))
+    pn = torch.linalg.vector_norm(psi)
+    del psi
+    return float(torch.abs(ov) / (torch.sqrt(nrm) * pn)), float(maxerr)
 
 
 def dft_fidelity(state, n, s, x, device):
@@ -530,7 +578,8 @@ def dft_fidelity(state, n, s, x, device):
         ov += torch.sum(torch.conj(e) * a)
         nrm += torch.sum(a.real * a.real + a.imag * a.imag)
         maxerr = torch.maximum(maxerr, torch.max(torch.abs(a - e)))
-    return float(torch.abs(ov) ** 2 / nrm), float(maxerr)
+    # the reference's fidelity: |<a|b>| / (|a| |b|) (dense.cpp:94-108); |e| = 1
+    return float(torch.abs(ov) / torch.sqrt(nrm)), float(maxerr)
 
 
 def run_qft_config(args, name):
@@ -540,7 +589,7 @@ def run_qft_config(args, name):
     n, s = c["n"], c["s"]
     x = qft_basis(name, n)
     delta = cc.pow2_bound(c["eps"], n)
-    prog = cc.build_qft(n)
+    prog = cc.build_grid(*c["grid"]) if "grid" in c else cc.build_qft(n)
     torch.cuda.set_device(0)
     lad = q.ErrorBoundLadder.make([delta])
     th = q.RatioThreshold(1.0)
@@ -569,7 +618,10 @@ def run_qft_config(args, name):
     wall = time.perf_counter() - t0
     clk = clocks.stop()
     cbytes, min_stride, nsq = state._stats()
-    fid, maxerr = dft_fidelity(state, n, s, x, torch.device("cuda", 0))
+    if "grid" in c:
+        fid, maxerr = dense_fidelity(state, prog, n, s, x, torch.device("cuda", 0))
+    else:
+        fid, maxerr = dft_fidelity(state, n, s, x, torch.device("cuda", 0))
     ctr = state.counters()
     # per-kernel-class device time (CUDA events around every launch): a second,
     # separate pass over the circuit so the events do not touch the timed one
@@ -599,14 +651,15 @@ def run_qft_config(args, name):
     line = {"metric": METRIC, "value": upd / (dev_ns * 1e-9), "unit": UNIT, "n_gpus": 1,
             "steps": 1, "warmup": 0, "ms_per_step": dev_ns * 1e-6, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (generated QFT circuit, seeded basis state)",
-            "config": {"workload": f"{name}: qft-{n} ({len(prog.gates)} gates), 2^{s}-amp strides",
+            "data": "synthetic (generated " + ("seeded grid" if "grid" in c else "QFT") + " circuit, seeded basis state)",
+            "config": {"workload": f"{name}: {prog.name} ({len(prog.gates)} gates), 2^{s}-amp strides",
                        "n_qubits": n, "stride_bits": s, "eps": c["eps"], "delta": delta,
                        "delta_mapping": "largest power of two <= eps*2^-ceil(n/2)", "basis": x,
                        "note": c["note"], "step": "the whole circuit once"},
             "e2e": {"value": upd / wall, "unit": UNIT, "h2d_bytes_per_step": DESC_BYTES * len(prog.gates),
                     "d2h_bytes_per_step": RECORD_BYTES * len(prog.gates)},
-            "fidelity_vs_dft_row": fid, "max_abs_amp_error": maxerr, "pointwise_bound": delta,
+            ("fidelity_vs_dense" if "grid" in c else "fidelity_vs_dft_row"): fid,
+            "max_abs_amp_error": maxerr, "pointwise_bound": delta,
             "norm_sq_tracked": nsq, "min_stride_ratio": min_ratio,
             "final_state_ratio": (16 << n) / cbytes, "final_compressed_bytes": cbytes,
             "bytes_per_amp_update": (cin + cout) / max(1, upd),
@@ -625,8 +678,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-fidelity", action="store_true")
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3"],
-                    help="C2 (default) is the headline workload; C1/C3 run a whole QFT once")
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4s"],
+                    help="C2 (default) is the headline workload; C1/C3 run a whole QFT once, "
+                         "C4s the 30-qubit grid")
     args = ap.parse_args()
     if args.config != "C2":
         return run_qft_config(args, args.config)
