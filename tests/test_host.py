@@ -110,3 +110,17 @@ def test_gate_record_fold_matches_reference(reference, oracle):
         reps, norm = st.apply_gate(g, [0.0, 1e-7, 1e-6, 1e-5, 1e-4, 1e-3], 8.0)
         recs.append(mm.gate_record(i, g.label, reps, norm)[0])
     assert mm.emit_csv(recs, with_elapsed=False) == mm.strip_elapsed(csv_r)
+
+
+def test_bench_dense_checker_matches_oracle_dense(oracle):
+    """bench.py's GPU dense checker (dense_apply, used for the C2 and C4s
+    fidelities) equals the oracle's dense simulator (dense.cpp:30-76) on small
+    circuits of every gate kind (run here on CPU tensors)."""
+    import numpy as np
+    import torch
+    import bench
+    for prog in (cc.build_grid(3, 3, 6, 5), cc.build_qft(7), cc.build_grover(6, 5, 3),
+                 cc.build_grover_gate_form(6, 9, 2)):
+        psi = bench.dense_state(prog, len(prog.gates), torch.device("cpu"), basis=3)
+        ref = oracle.dense(prog.n_qubits, prog.gates, 3)
+        assert np.array_equal(psi.numpy(), ref), prog.name
