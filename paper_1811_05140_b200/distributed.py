@@ -175,7 +175,7 @@ class _GpuShard:
     def __del__(self):
         try:
             from .engine import _lib_handle
-        except ImportError:  # interpreter shutdown
+        except Exception:  # interpreter shutdown: modules already torn down
             return
         if getattr(self, "h", None) and _lib_handle is not None:
             _lib_handle.qcs_state_destroy(self.h)
