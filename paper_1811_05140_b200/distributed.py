@@ -326,10 +326,24 @@ class ShardedState:
 
     # -- index maps -----------------------------------------------------------
     def _phys_to_log(self, jp: np.ndarray) -> np.ndarray:
-        jl = np.zeros_like(jp)
-        for p, q in enumerate(self.pi):
-            jl |= ((jp >> q) & 1) << p
-        return jl
+        return self._p2l_table()[jp]
+
+    def _p2l_table(self) -> np.ndarray:
+        """Physical -> logical global stride index for every stride, cached
+        until the permutation changes (exchanges are rare)."""
+        key = tuple(self.pi)
+        if getattr(self, "_p2l_key", None) != key:
+            jp = np.arange(1 << len(self.pi), dtype=np.int64)
+            jl = np.zeros_like(jp)
+            for p, q in enumerate(self.pi):
+                jl |= ((jp >> q) & 1) << p
+            self._p2l, self._p2l_key = jl, key
+            self._log_order = np.argsort(jl)  # physical indices in logical order
+        return self._p2l
+
+    def _logical_order(self) -> np.ndarray:
+        self._p2l_table()
+        return self._log_order
 
     def _log_to_phys(self, j: int) -> int:
         out = 0
@@ -424,7 +438,7 @@ class ShardedState:
             # in LOGICAL global stride order, divided by the amplitude count
             parts = self.comm.allgather(self.local.stride_sums().tobytes())
             allp = np.concatenate([np.frombuffer(p).reshape(-1, 2) for p in parts])
-            order = np.argsort(self._phys_to_log(np.arange(len(allp), dtype=np.int64)))
+            order = self._logical_order()
             sr = si = 0.0
             for re_, im_ in allp[order].tolist():
                 sr += re_
@@ -456,7 +470,7 @@ class ShardedState:
         # (aalc.cpp:410-419); np.cumsum is a sequential left-to-right fold
         scales = np.concatenate([p_[1:, 8] for p_ in parts])
         sums = np.concatenate([p_[1:, 9] for p_ in parts])
-        order = np.argsort(self._phys_to_log(np.arange(len(scales), dtype=np.int64)))
+        order = self._logical_order()
         scales, sums = scales[order], sums[order]
         total = float(np.cumsum(scales * scales * sums)[-1])
         if total > 0.0:
