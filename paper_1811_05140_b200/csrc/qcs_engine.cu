@@ -830,24 +830,13 @@ int codec_max_rounds()
     return e ? std::max(1, atoi(e)) : 6;
 }
 
-int fused_narrow()
-{
-    static const int narrow = [] {
-        const char* e = getenv("QCS_NARROW");
-        return e ? atoi(e) : 0;
-    }();
-    return narrow;
-}
 // elements per plane per iteration of the usual encoder CTA: in-stride
 // partners closer than this are gated inside it (MODE_LOCAL)
-int fused_span() { return fused_narrow() ? 2048 : 4096; }
+constexpr uint64_t FUSED_SPAN = 4096;
 
 int launch_fused(const FusedArgs& a, int fm, uint64_t grid, cudaStream_t s)
 {
     const bool L = a.cp.lossy != 0;
-    const int narrow = fused_narrow();
-    if (narrow && L && fm == FM_LOCAL) return launch_fused_t<true, 2, 64, MODE_LOCAL>(a, grid, s);
-    if (narrow && L && fm == FM_RAW2) return launch_fused_t<true, 2, 64, MODE_RAW>(a, grid, s);
     switch (fm) {
         case FM_LOCAL: return L ? launch_fused_t<true, 2, 128, MODE_LOCAL>(a, grid, s) : launch_fused_t<false, 2, 128, MODE_LOCAL>(a, grid, s);
         case FM_LOCAL_W: return L ? launch_fused_t<true, 2, 256, MODE_LOCAL>(a, grid, s) : launch_fused_t<false, 2, 256, MODE_LOCAL>(a, grid, s);
@@ -876,7 +865,6 @@ struct qcs_dev_state {
     int serial_chain = 1;
     int imz = 1;  // zero-imaginary-plane mode (QCS_IMZ=0 turns it off)
     bool all_im_zero = true;  // every im plane is zero (real state): real gates keep it
-    int imz_split = 0;  // QCS_IMZ_SPLIT=1: real gates take the split path (measured slower on C2)
     int chain_levels = 0;
     int16_t* chain_codes = nullptr;
     double* chain_preds = nullptr;
@@ -1276,19 +1264,12 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     // gate fully parallel into X, then the encoder reads X (split path)
     int dg = -1;
     if (p.pair) dg = DG_PAIR;
-    else if (p.kind <= 1 && (1ull << p.t) >= (uint64_t)fused_span()) dg = DG_FAR;
-    // in-chunk partners take the split path too when asked (QCS_SPLIT_LOCAL) and
-    // for real gates under the zero-imaginary-plane mode: a whole-CTA re plane
-    // decodes 8192 elements per iteration, more payload than the in-kernel
-    // staging holds, while k_decode_gate decodes it at full occupancy
-    const bool split_in = st->split_local || (imz && st->imz_split);
-    if (dg < 0 && p.kind <= 1 && split_in && (1ull << p.t) >= DG_HALF) dg = DG_FAR;
-    else if (dg < 0 && p.kind <= 1 && split_in && d.L >= DG_IN_CH) dg = DG_IN;
-    static const int force_wide = [] {
-        const char* e = getenv("QCS_WIDE");
-        return e ? atoi(e) : -1;
-    }();
-    const bool wide = force_wide >= 0 ? (force_wide && d.L >= 2 * 4096) : (n_slots < 148 && d.L >= 2 * 4096);
+    else if (p.kind <= 1 && (1ull << p.t) >= FUSED_SPAN) dg = DG_FAR;
+    // in-chunk partners take the split path too when asked (QCS_SPLIT_LOCAL)
+    else if (p.kind <= 1 && st->split_local && (1ull << p.t) >= DG_HALF) dg = DG_FAR;
+    else if (p.kind <= 1 && st->split_local && d.L >= DG_IN_CH) dg = DG_IN;
+    // gates with fewer units than SMs: one 512-thread CTA per stride
+    const bool wide = n_slots < 148 && d.L >= 2 * FUSED_SPAN;
     const int fm = dg >= 0 ? (wide ? FM_RAW2_W : FM_RAW2) : (wide ? FM_LOCAL_W : FM_LOCAL);  // pairs always split
     if (dg >= 0) {
         static bool dg_attr = false;
@@ -1511,7 +1492,6 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     if (const char* e = getenv("QCS_SPLIT_LOCAL")) st->split_local = atoi(e);
     if (const char* e = getenv("QCS_SERIAL_CHAIN")) st->serial_chain = atoi(e);
     if (const char* e = getenv("QCS_IMZ")) st->imz = atoi(e);
-    if (const char* e = getenv("QCS_IMZ_SPLIT")) st->imz_split = atoi(e);
     if (const char* e = getenv("QCS_MAX_ROUNDS")) st->max_rounds = std::max(1, atoi(e));
     cudaSetDevice(device);
     int rc = 0;
