@@ -869,20 +869,59 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
         if (tail_ty != TY_NONE && tail_j == 0 && in_ty == tail_ty) tail_st = in_st;
         const bool tail_closes = lane + 1 < active ? (tail_ty != TY_NONE && next_ft != tail_ty) : final_iter;
 
-        // 7. byte count of the tokens this lane closes
+        // 7. byte count of the tokens this lane closes.  A lane without raw
+        // words (no W element, no carried W run closing here) emits only code
+        // and zero-run tokens, contiguous at its byte offset: it generates them
+        // right here into its own x row (free after the sum; <= 160 bytes) and
+        // the warp copies them out coalesced in step 9
         uint32_t nbytes = 0;
         int closes_open = 0;
         uint64_t close_vlen = 0;
-        nbytes = lm.cbytes;
-        lane_runs(lm, cnt, e0, in_ty, in_st, tail_closes, lane == 0, [&](int t, uint64_t st, uint64_t end) {
-            const uint64_t len = end - st;
-            const int vl = varint_len(run_token(LOSSY, t, len));
-            nbytes += vl + (t == TY_W ? 8u * (uint32_t)len : 0u);
-            if (st < base) {
-                closes_open = 1;
-                close_vlen = vl;
-            }
-        });
+        const bool staged = cnt > 0 && lm.w == 0u && !(lane == 0 && in_ty == TY_W);
+        int rt_rel = -1, rt_vl = 0, rt_sl = 0;  // staged: token of a run begun in an earlier lane
+        if (staged) {
+            uint8_t* const bufp = reinterpret_cast<uint8_t*>(xl);
+            uint32_t rp = 0;
+            lane_tokens(
+                lm, cl, cnt, e0, in_ty, in_st, tail_closes, lane == 0,
+                [&](int t, uint64_t st, uint64_t end) {
+                    const uint64_t v = run_token(LOSSY, t, end - st);
+                    const int vl = varint_len(v);
+                    put_varint(bufp + rp, v);
+                    if (st < e0 && st >= base) {
+                        rt_rel = (int)rp;
+                        rt_vl = vl;
+                        rt_sl = pl * LPL + (int)((st - base) / SUB);
+                    }
+                    if (st < base) {
+                        closes_open = 1;
+                        close_vlen = vl;
+                    }
+                    rp += vl;
+                },
+                [&](int16_t q) {
+                    const int32_t qq = q;
+                    const uint32_t v = ((((uint32_t)qq << 1) ^ (uint32_t)(qq >> 31)) << 2) | 1u;
+                    const uint32_t len = 1u + (v >= 128u) + (v >= 16384u);
+                    uint8_t* o = bufp + rp;
+                    o[0] = (uint8_t)((v & 0x7fu) | (len > 1u ? 0x80u : 0u));
+                    if (len > 1u) o[1] = (uint8_t)(((v >> 7) & 0x7fu) | (len > 2u ? 0x80u : 0u));
+                    if (len > 2u) o[2] = (uint8_t)(v >> 14);
+                    rp += len;
+                });
+            nbytes = rp;
+        } else {
+            nbytes = lm.cbytes;
+            lane_runs(lm, cnt, e0, in_ty, in_st, tail_closes, lane == 0, [&](int t, uint64_t st, uint64_t end) {
+                const uint64_t len = end - st;
+                const int vl = varint_len(run_token(LOSSY, t, len));
+                nbytes += vl + (t == TY_W ? 8u * (uint32_t)len : 0u);
+                if (st < base) {
+                    closes_open = 1;
+                    close_vlen = vl;
+                }
+            });
+        }
         if (closes_open) {
             C.closes_open = 1;
             C.close_vlen = close_vlen;
@@ -934,7 +973,24 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
         }
 
         // 9. write tokens (see qcs_codec.cuh for the placement rules)
+        if (staged && rt_rel >= 0) {
+            S.runtok[rt_sl] = bstart + (uint64_t)rt_rel;
+            S.runw[rt_sl] = bstart + (uint64_t)(rt_rel + rt_vl);
+        }
         {
+            // staged lanes: the warp copies each lane's bytes, 32 consecutive
+            // bytes per store
+            const int wl = tid & 31;
+            const uint32_t my_nb = staged ? nbytes : 0u;
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t nb = __shfl_sync(0xffffffffu, my_nb, j);
+                if (nb == 0) continue;
+                const uint64_t bs = __shfl_sync(0xffffffffu, bstart, j);
+                const uint8_t* src = reinterpret_cast<const uint8_t*>(xs + (uint64_t)((tid & ~31) + j) * XS_STRIDE);
+                for (uint32_t k = wl; k < nb; k += 32) out[bs + k] = src[k];
+            }
+        }
+        if (!staged) {
             uint64_t pos = bstart;
             lane_tokens(
                 lm, cl, cnt, e0, in_ty, in_st, tail_closes, lane == 0,
@@ -965,13 +1021,13 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
                     if (len > 2u) o[2] = (uint8_t)(v >> 14);
                     pos += len;
                 });
-            if (lane + 1 == active && !final_iter && tail_ty != TY_NONE && tail_st >= base) {
-                const uint64_t tokpos = C.out_pos + C.iter_bytes;
-                const uint64_t vmax = tail_ty == TY_W ? varint_len(run_token(LOSSY, TY_W, n - tail_st)) : 0;
-                const int sl = pl * LPL + (int)((tail_st - base) / SUB);
-                S.runtok[sl] = tokpos;
-                S.runw[sl] = tokpos + vmax;
-            }
+        }
+        if (lane + 1 == active && !final_iter && tail_ty != TY_NONE && tail_st >= base) {
+            const uint64_t tokpos = C.out_pos + C.iter_bytes;
+            const uint64_t vmax = tail_ty == TY_W ? varint_len(run_token(LOSSY, TY_W, n - tail_st)) : 0;
+            const int sl = pl * LPL + (int)((tail_st - base) / SUB);
+            S.runtok[sl] = tokpos;
+            S.runw[sl] = tokpos + vmax;
         }
         __syncthreads();
 
