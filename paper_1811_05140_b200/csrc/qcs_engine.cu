@@ -188,7 +188,9 @@ __global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen, Level
         d.slot_of[j] = (int64_t)((gen << 32) | s);
         lt.slot_codec[s] = (int8_t)codec0;  // ladder level 0
         lt.slot_delta[s] = delta0;
-        if (imz) {  // zero-imaginary-plane flags (see k_imz_flags)
+        if (imz == 2) {  // the host knows every im plane is zero (all_im_zero)
+            d.im_zero[s] = 1;
+        } else if (imz) {  // zero-imaginary-plane flags: check the input planes
             bool z;
             if (p.pair)
                 z = plane_is_zero(d, 2 * slot_stride(p, s & ~1ull) + 1) && plane_is_zero(d, 2 * slot_stride(p, s | 1ull) + 1);
@@ -1247,7 +1249,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
                                            g->u[7] == 0.0);
     const bool imz = real_gate && st->imz;
     k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen, st->lt, lad[0] > 0.0 ? 1 : 0, lad[0],
-                                                            imz ? 1 : 0);
+                                                            imz ? (st->all_im_zero ? 2 : 1) : 0);
     ++st->launches;
     prof_stop(st);
     if (p.reflect && given_mean) {  // sharded run: mean combined across ranks
