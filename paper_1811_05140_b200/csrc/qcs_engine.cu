@@ -649,14 +649,18 @@ __device__ double norm_fold(const Dev& d, double f, bool scale_by_f, double* sh_
     for (uint64_t c0 = 0; c0 < d.NS; c0 += NORM_CHUNK) {
         const int m = (int)umin64(NORM_CHUNK, d.NS - c0);
         __syncthreads();
+        // the terms in parallel (the same products as before), then the
+        // reference's serial left-to-right sum on one thread
         for (int i = threadIdx.x; i < m; i += blockDim.x) {
             const double sc = d.scale[c0 + i];
-            sh_a[i] = scale_by_f ? __dmul_rn(sc, f) : sc;
-            sh_b[i] = d.sum_sq[c0 + i];
+            const double a = scale_by_f ? __dmul_rn(sc, f) : sc;
+            sh_a[i] = __dmul_rn(__dmul_rn(a, a), d.sum_sq[c0 + i]);
         }
         __syncthreads();
-        if (threadIdx.x == 0)
-            for (int i = 0; i < m; ++i) total = __dadd_rn(total, __dmul_rn(__dmul_rn(sh_a[i], sh_a[i]), sh_b[i]));
+        if (threadIdx.x == 0) {
+#pragma unroll 8
+            for (int i = 0; i < m; ++i) total = __dadd_rn(total, sh_a[i]);
+        }
     }
     return total;
 }
