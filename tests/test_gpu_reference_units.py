@@ -290,3 +290,17 @@ def test_checkpoint_restores_amplitudes_and_scales(q):  # :376-395
     assert st.to_amplitudes().tobytes() == res.state.to_amplitudes().tobytes()
     for j in range(geom.n_strides()):
         assert st.stride_scale(j) == res.state.stride_scale(j)
+
+
+# ---- test_circuit.cpp ---------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 7])
+def test_qft_equals_the_dft_row_for_every_input(q, n):  # test_circuit.cpp:18-30, :199-209
+    """Through the engine (lossless ladder, s = n // 2): QFT|x> is the DFT row
+    a_y = e^{2 pi i x y / 2^n} / 2^{n/2} for every basis input x."""
+    prog = cc.build_qft(n)
+    y = np.arange(1 << n)
+    for x in range(1 << n):
+        res, _ = gpu_run(prog, n // 2, x, [0.0], 1.0)
+        want = np.exp(2j * math.pi * ((x * y) % (1 << n)) / (1 << n)) / math.sqrt(1 << n)
+        assert np.max(np.abs(res.state.to_amplitudes() - want)) < 1e-12, (n, x)
