@@ -236,6 +236,88 @@ __device__ __forceinline__ void decode_sub(const uint8_t* in, int codec, double 
     }
 }
 
+// 8 bytes starting at byte offset `pos` of an 8-byte-aligned base (two
+// aligned loads + funnel shift; may read up to 15 bytes past pos)
+__device__ __forceinline__ uint64_t load8_at(const uint8_t* base, uint64_t pos)
+{
+    const uint64_t* p = reinterpret_cast<const uint64_t*>(base + (pos & ~7ull));
+    const int r = (int)(pos & 7) * 8;
+    const uint64_t lo = p[0];
+    if (r == 0) return lo;
+    return (lo >> r) | (p[1] << (64 - r));
+}
+
+// decode_sub over a payload staged in SHARED memory (8-byte aligned base):
+// tokens come from a 64-bit byte window, one pair of aligned loads per up to
+// 8 one-byte (2-3 three-byte) tokens, instead of one dependent load per byte.
+__device__ __forceinline__ void decode_sub_win(const uint8_t* in, int codec, double td, SideEntry se, int cnt,
+                                               double* o, double scale)
+{
+    uint64_t pos = se.off;
+    uint64_t w = 0;
+    int avail = 0;
+    uint64_t skip = se.skip;
+    double P = se.pred;
+    int produced = 0;
+    const bool sc = scale != 1.0;
+    int guard = 0;
+    while (produced < cnt) {
+        if (++guard > 4 * SUB + 8) break;  // corrupt side index: never spin
+        if (avail < 5) {
+            w = load8_at(in, pos);
+            avail = 8;
+        }
+        const uint64_t stop = ~w & 0x8080808080808080ull;
+        const int nb = stop ? (__ffsll((long long)stop) >> 3) : 9;
+        uint64_t v;
+        if (nb <= 4 && nb <= avail) {
+            const uint64_t x = w & ((1ull << (8 * nb)) - 1);
+            v = (x & 0x7full) | ((x >> 1) & (0x7full << 7)) | ((x >> 2) & (0x7full << 14)) |
+                ((x >> 3) & (0x7full << 21));
+            pos += nb;
+            avail -= nb;
+            w >>= 8 * nb;
+        } else {  // long varint: byte loop
+            v = get_varint(in, pos);
+            avail = 0;
+        }
+        if (codec == 1) {
+            const unsigned tag = (unsigned)(v & 3u);
+            const uint64_t arg = v >> 2;
+            if (tag == 0) {
+                const uint64_t m = umin64(arg - skip, (uint64_t)(cnt - produced));
+                const double val = sc ? __dmul_rn(P, scale) : P;
+                for (uint64_t i = 0; i < m; ++i) o[produced++] = val;
+            } else if (tag == 1) {
+                P = __dadd_rn(P, __dmul_rn(td, (double)unzigzag(arg)));
+                o[produced++] = sc ? __dmul_rn(P, scale) : P;
+            } else {
+                const uint64_t m = umin64(arg - skip, (uint64_t)(cnt - produced));
+                for (uint64_t i = 0; i < m; ++i) {
+                    P = __longlong_as_double((long long)load8_at(in, pos + 8 * (skip + i)));
+                    o[produced++] = sc ? __dmul_rn(P, scale) : P;
+                }
+                pos += 8 * arg;
+                avail = 0;
+            }
+        } else {
+            const uint64_t run = v >> 1;
+            const uint64_t m = umin64(run - skip, (uint64_t)(cnt - produced));
+            if ((v & 1u) == 0) {
+                for (uint64_t i = 0; i < m; ++i) o[produced++] = 0.0;
+            } else {
+                for (uint64_t i = 0; i < m; ++i) {
+                    const double x = __longlong_as_double((long long)load8_at(in, pos + 8 * (skip + i)));
+                    o[produced++] = sc ? __dmul_rn(x, scale) : x;
+                }
+                pos += 8 * run;
+                avail = 0;
+            }
+        }
+        skip = 0;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Validating serial walk of one payload (decompress_*_into, codec.cpp:260-340):
 // writes the side index and, optionally, the decoded values.  Used for

@@ -599,6 +599,7 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
             // covering the next iteration's first one, plus that token's
             // varint and the words it owns for this iteration's elements.
             const uint8_t* src = in_bytes;
+            bool staged = false;
             if (MODE == MODE_LOCAL) {
                 // staging room: everything dead between an iteration's end
                 // and its decode — the code rows, and the per-iteration lane
@@ -637,9 +638,15 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
                     mbar_wait(&S.bar[pl], stage_phase);
                     stage_phase ^= 1u;
                     src = stage - lo;  // token offsets stay plane-relative
+                    staged = true;
                 }
             }
-            if (cnt > 0) decode_sub(src, in_codec, in_td, in_side[e0 / SUB], cnt, xl, in_scale);
+            if (cnt > 0) {
+                if (staged && !IMZ)  // measured: helps two-plane CTAs (C1), not whole-CTA re planes (C2)
+                    decode_sub_win(src, in_codec, in_td, in_side[e0 / SUB], cnt, xl, in_scale);
+                else
+                    decode_sub(src, in_codec, in_td, in_side[e0 / SUB], cnt, xl, in_scale);
+            }
             __syncthreads();
             // gate (run_plan_unit, gate.cpp:405-454)
             {  // MODE_LOCAL
