@@ -244,8 +244,20 @@ __device__ __forceinline__ double tsq_g(double* xs, int g, int k)
     return __dadd_rn(__dmul_rn(r, r), __dmul_rn(i, i));
 }
 
+// units of 2^(e-52) of one term x*x (tu = 2^(52-e)); a tie or a term beyond
+// the binade saturates
+__device__ __forceinline__ uint64_t sq_units_y(double y)
+{
+    const double ry = rint(y);
+    return (y >= 9007199254740992.0 || fabs(y - ry) == 0.5) ? (1ull << 62) : (uint64_t)ry;
+}
+__device__ __forceinline__ uint64_t sq_units(double x, double tu) { return sq_units_y(__dmul_rn(x, x) * tu); }
+
+// pre_ok: every thread's units over its own elements for the binade of the
+// entering sum are already in pre_loc (IMZ: formed during reconstruction)
 template <int LPL, bool IMZ, typename FS>
-__device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigned long long* counters)
+__device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigned long long* counters,
+                                            bool pre_ok = false, uint64_t pre_loc = 0)
 {
     constexpr int GT = IMZ ? LPL : 2 * LPL;  // threads (the CTA: one stride)
     constexpr int GW = GT / 32;            // warps
@@ -282,13 +294,17 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
             const double to_units = ldexp(1.0, 52 - e);
             const uint64_t ms = (uint64_t)(s * to_units);
             uint64_t loc = 0;
-            for (int i = 0; i < PER; ++i) {
-                const int k = kb + i;
-                if (k < k0 || k >= n_it) continue;
-                const double y = tsq_g<LPL, IMZ>(xs, 0, k) * to_units;
-                const double ry = rint(y);
-                // a tie (or an element beyond the binade) saturates the total
-                loc = sat_add(loc, (y >= 9007199254740992.0 || fabs(y - ry) == 0.5) ? SAT : (uint64_t)ry);
+            if (pre_ok && k0 == 0) {
+                loc = pre_loc;
+            } else {
+                for (int i = 0; i < PER; ++i) {
+                    const int k = kb + i;
+                    if (k < k0 || k >= n_it) continue;
+                    const double y = tsq_g<LPL, IMZ>(xs, 0, k) * to_units;
+                    const double ry = rint(y);
+                    // a tie (or an element beyond the binade) saturates the total
+                    loc = sat_add(loc, (y >= 9007199254740992.0 || fabs(y - ry) == 0.5) ? SAT : (uint64_t)ry);
+                }
             }
             uint64_t inc = loc;
             for (int o = 1; o < 32; o <<= 1) {
@@ -692,6 +708,8 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
         __syncthreads();
 
         QCS_PHASE(0);
+        bool pre_ok = false;   // IMZ: this thread's first-pass sum units ...
+        uint64_t pre_loc = 0;  // ... formed during reconstruction
         // 2-4. codes and exact predictors
         if (LOSSY && MODE == MODE_RAW && a.pre_codes && (!a.chain_on || *a.chain_on)) {
             // serial-chain mode: the codes and sub-chunk entry predictors of
@@ -804,6 +822,16 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
             }
             QCS_PHASE(1);
             if (lane == 0 && active > 0) C.Pnext = S.exitP[pl * LPL + active - 1];
+            // IMZ: the lane's row is its share of the stride's sum of squares
+            // (fused_sumsq's first pass over it, formed here from registers)
+            double tu = 0.0;
+            if (IMZ && a.sumsq) {
+                const double s0 = S.s[0];  // the running sum entering this iteration
+                if (s0 > 0.0 && ilogb(s0) >= -960) {
+                    tu = ldexp(1.0, 52 - ilogb(s0));
+                    pre_ok = true;
+                }
+            }
             if (cnt > 0) {  // the reference's reconstructed predictors from the codes
                 const double P0 = S.entryP[tid];
                 if (cp.pow2 && ev_idx < 0 && !S.repaired[tid]) {
@@ -816,7 +844,9 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
 #pragma unroll 8
                     for (int i = 0; i < cnt; ++i) {
                         M += cl[i];
-                        xl[i] = __dadd_rn(P0, __dmul_rn(cp.td, (double)M));
+                        const double xv = __dadd_rn(P0, __dmul_rn(cp.td, (double)M));
+                        xl[i] = xv;
+                        if (IMZ) pre_loc = sat_add(pre_loc, sq_units(xv, tu));
                     }
                 } else {
                     double P = P0;
@@ -825,6 +855,7 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
                         if (co == WCODE16) P = xl[i];
                         else if (co != 0) P = __dadd_rn(P, __dmul_rn(cp.td, (double)co));
                         xl[i] = P;
+                        if (IMZ) pre_loc = sat_add(pre_loc, sq_units(P, tu));
                     }
                 }
             }
@@ -837,7 +868,7 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
 
         QCS_PHASE(2);
         // 5. stored sum of squares per stride
-        if (a.sumsq) fused_sumsq<LPL, IMZ>(xs, n_it, S, a.counters);
+        if (a.sumsq) fused_sumsq<LPL, IMZ>(xs, n_it, S, a.counters, pre_ok, pre_loc);
 
         QCS_PHASE(3);
         // 6. run summary of each lane (bitmasks) and the run entering it
