@@ -324,41 +324,34 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
                 s = (double)(ms + total) / to_units;  // < 2^53 units: exact
                 break;
             }
-            // find the first event (binade crossing or tie) and add it exactly
+            // An event (binade crossing or tie) lies in this pass.  It is in
+            // the one thread whose inclusive prefix reaches the binade's end
+            // (the threads before it hold neither a tie nor the crossing): that
+            // thread alone walks its elements to it and adds it exactly.
             const uint64_t off = sat_add(pre, wl ? prev : 0);
-            uint64_t run = off;
-            for (int i = 0; i < PER && mine == LLONG_MAX; ++i) {
-                const int k = kb + i;
-                if (k < k0 || k >= n_it) continue;
-                const double y = tsq_g<LPL, IMZ>(xs, 0, k) * to_units;
-                const double ry = rint(y);
-                if (y >= 9007199254740992.0 || fabs(y - ry) == 0.5) {
-                    mine = k;
-                    break;
-                }
-                const uint64_t c = (uint64_t)ry;
-                if (ms + run + c >= (1ull << 53)) {
-                    mine = k;
-                    break;
-                }
-                run = sat_add(run, c);
-            }
-            long long m = mine;
-            for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-            if (wl == 0) S.wmin[w] = m;
-            __syncthreads();
-            long long kstar = LLONG_MAX;
-            for (int i = 0; i < GW; ++i) kstar = min(kstar, S.wmin[i]);
-            if (mine == kstar && kstar != LLONG_MAX) {
-                S.s[0] = __dadd_rn((double)(ms + run) / to_units, tsq_g<LPL, IMZ>(xs, 0, (int)kstar));
-                if (counters) {
-                    const double y = tsq_g<LPL, IMZ>(xs, 0, (int)kstar) * to_units;
-                    atomicAdd(&counters[(y < 9007199254740992.0 && fabs(y - rint(y)) == 0.5) ? 6 : 7], 1ull);
+            const uint64_t LIM = (1ull << 53) - ms;
+            if (off < LIM && sat_add(off, loc) >= LIM) {
+                uint64_t run = off;
+                for (int i = 0; i < PER; ++i) {
+                    const int k = kb + i;
+                    if (k < k0 || k >= n_it) continue;
+                    const double t = tsq_g<LPL, IMZ>(xs, 0, k);
+                    const double y = t * to_units;
+                    const double ry = rint(y);
+                    const bool beyond = y >= 9007199254740992.0;
+                    const bool tie = !beyond && fabs(y - ry) == 0.5;
+                    if (beyond || tie || ms + run + (uint64_t)ry >= (1ull << 53)) {
+                        S.s[0] = __dadd_rn((double)(ms + run) / to_units, t);
+                        S.wmin[0] = k;
+                        if (counters) atomicAdd(&counters[tie ? 6 : 7], 1ull);
+                        break;
+                    }
+                    run += (uint64_t)ry;
                 }
             }
             __syncthreads();
             s = S.s[0];
-            k0 = (int)kstar + 1;
+            k0 = (int)S.wmin[0] + 1;
         } else if (state == 1) {  // 0 + t = t exactly: the first non-zero term starts the sum
             for (int i = 0; i < PER; ++i) {
                 const int k = kb + i;
