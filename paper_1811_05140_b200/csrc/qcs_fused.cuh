@@ -266,7 +266,7 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
     const int tid = threadIdx.x;
     const int wl = tid & 31, w = tid >> 5;
     const int kb = tid * PER;
-    __syncthreads();
+    // (entered right after a CTA barrier: every step-4 branch ends with one)
     double s = S.s[0];  // uniform across the CTA from here on
     int k0 = 0;
     // While s is still 0 the next elements double it again and again (a binade
@@ -1018,7 +1018,15 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
                 if (nb == 0) continue;
                 const uint64_t bs = __shfl_sync(0xffffffffu, bstart, j);
                 const uint8_t* src = reinterpret_cast<const uint8_t*>(xs + (uint64_t)((tid & ~31) + j) * XS_STRIDE);
-                for (uint32_t k = wl; k < nb; k += 32) out[bs + k] = src[k];
+                // <= 160 bytes (32 tokens of <= 5): five predicated rounds,
+                // loads first
+                uint8_t b[5];
+#pragma unroll
+                for (int r = 0; r < 5; ++r) b[r] = wl + 32u * r < nb ? src[wl + 32u * r] : (uint8_t)0;
+#pragma unroll
+                for (int r = 0; r < 5; ++r)
+                    if (wl + 32u * r < nb) out[bs + wl + 32u * r] = b[r];
+                for (uint32_t k = wl + 160u; k < nb; k += 32) out[bs + k] = src[k];
             }
         }
         if (!staged) {
