@@ -327,26 +327,33 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
             // An event (binade crossing or tie) lies in this pass.  It is in
             // the one thread whose inclusive prefix reaches the binade's end
             // (the threads before it hold neither a tie nor the crossing): that
-            // thread alone walks its elements to it and adds it exactly.
+            // thread's warp finds it — one of the thread's elements per lane,
+            // a scan of their units and a ballot — and adds it exactly.
             const uint64_t off = sat_add(pre, wl ? prev : 0);
             const uint64_t LIM = (1ull << 53) - ms;
-            if (off < LIM && sat_add(off, loc) >= LIM) {
-                uint64_t run = off;
-                for (int i = 0; i < PER; ++i) {
-                    const int k = kb + i;
-                    if (k < k0 || k >= n_it) continue;
-                    const double t = tsq_g<LPL, IMZ>(xs, 0, k);
-                    const double y = t * to_units;
-                    const double ry = rint(y);
-                    const bool beyond = y >= 9007199254740992.0;
-                    const bool tie = !beyond && fabs(y - ry) == 0.5;
-                    if (beyond || tie || ms + run + (uint64_t)ry >= (1ull << 53)) {
-                        S.s[0] = __dadd_rn((double)(ms + run) / to_units, t);
-                        S.wmin[0] = k;
-                        if (counters) atomicAdd(&counters[tie ? 6 : 7], 1ull);
-                        break;
-                    }
-                    run += (uint64_t)ry;
+            const unsigned ob = __ballot_sync(0xffffffffu, off < LIM && sat_add(off, loc) >= LIM);
+            if (ob) {
+                const int ol = __ffs(ob) - 1;
+                const uint64_t off_o = __shfl_sync(0xffffffffu, off, ol);
+                const int k = (tid - wl + ol) * PER + wl;  // the owner's element of this lane
+                const bool valid = wl < PER && k >= k0 && k < n_it;
+                const double t = valid ? tsq_g<LPL, IMZ>(xs, 0, k) : 0.0;
+                const double y = t * to_units;
+                const double ry = rint(y);
+                const bool beyond = y >= 9007199254740992.0;
+                const bool tie = valid && !beyond && fabs(y - ry) == 0.5;
+                const uint64_t c = beyond ? (1ull << 53) : (uint64_t)ry;
+                uint64_t incl = c;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (wl >= o) incl += u;
+                }
+                const bool ev = valid && (beyond || tie || ms + off_o + incl >= (1ull << 53));
+                const unsigned eb = __ballot_sync(0xffffffffu, ev);
+                if (eb && wl == __ffs(eb) - 1) {
+                    S.s[0] = __dadd_rn((double)(ms + off_o + (incl - c)) / to_units, t);
+                    S.wmin[0] = k;
+                    if (counters) atomicAdd(&counters[tie ? 6 : 7], 1ull);
                 }
             }
             __syncthreads();
