@@ -111,6 +111,24 @@ __device__ __forceinline__ uint32_t code_token_len16(uint32_t c16)
     return 1u + (v >= 128u) + (v >= 16384u);
 }
 
+// bytes of a lane's code tokens (what lane_masks<true> adds up in cbytes)
+__device__ __forceinline__ uint32_t lane_cbytes(const int16_t* cl, int cnt)
+{
+    const uint32_t* c2 = reinterpret_cast<const uint32_t*>(cl);
+    uint32_t n = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const uint32_t v = c2[j];
+        const uint32_t lo = v & 0xffffu, hi = v >> 16;
+        const bool clo = lo != 0u && lo != 0x8000u && 2 * j < cnt;
+        const bool chi = hi != 0u && hi != 0x8000u && 2 * j + 1 < cnt;
+        n += (clo ? code_token_len16(lo) : 0u) + (chi ? code_token_len16(hi) : 0u);
+    }
+    return n;
+}
+
+// CB = false: cbytes left 0 (callers that generate the tokens count them then)
+template <bool CB = true>
 __device__ __forceinline__ LaneMasks lane_masks(const int16_t* cl, int cnt)
 {
     LaneMasks m{0u, 0u, cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u), 0u};
@@ -123,7 +141,7 @@ __device__ __forceinline__ LaneMasks lane_masks(const int16_t* cl, int cnt)
         m.w |= ((uint32_t)(lo == 0x8000u) << (2 * j)) | ((uint32_t)(hi == 0x8000u) << (2 * j + 1));
         const bool clo = lo != 0u && lo != 0x8000u && 2 * j < cnt;
         const bool chi = hi != 0u && hi != 0x8000u && 2 * j + 1 < cnt;
-        m.cbytes += (clo ? code_token_len16(lo) : 0u) + (chi ? code_token_len16(hi) : 0u);
+        if (CB) m.cbytes += (clo ? code_token_len16(lo) : 0u) + (chi ? code_token_len16(hi) : 0u);
     }
     m.z &= m.valid;
     m.w &= m.valid;

@@ -312,7 +312,8 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
                 if (wl >= o) inc = sat_add(inc, u);
             }
             const uint64_t prev = __shfl_up_sync(0xffffffffu, inc, 1);
-            __syncthreads();
+            // (S.wsum's last readers are behind a barrier already: the
+            // caller's, the serial prefix's, or the previous event's)
             if (wl == 31) S.wsum[w] = inc;
             __syncthreads();
             uint64_t pre = 0, total = 0;
@@ -872,7 +873,7 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
 
         QCS_PHASE(3);
         // 6. run summary of each lane (bitmasks) and the run entering it
-        const LaneMasks lm = cnt > 0 ? lane_masks(cl, cnt) : LaneMasks{0u, 0u, 0u};
+        const LaneMasks lm = cnt > 0 ? lane_masks<false>(cl, cnt) : LaneMasks{0u, 0u, 0u};
         const int t0 = cnt > 0 ? mask_type(lm, 0) : TY_NONE;
         const bool full = cnt > 0 && (lm.z == lm.valid || lm.w == lm.valid);
         S.ftype[pl * (LPL + 1) + lane] = (int8_t)t0;
@@ -949,7 +950,7 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
                 });
             nbytes = rp;
         } else {
-            nbytes = lm.cbytes;
+            nbytes = lane_cbytes(cl, cnt);
             lane_runs(lm, cnt, e0, in_ty, in_st, tail_closes, lane == 0, [&](int t, uint64_t st, uint64_t end) {
                 const uint64_t len = end - st;
                 const int vl = varint_len(run_token(LOSSY, t, len));
