@@ -974,9 +974,7 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
             C.carry_tok = C.out_pos;
             C.mv_bytes = 0;
             C.mv_shift = 0;
-        }
-        __syncthreads();
-        if (lane == 0) {
+            // (same thread: closes_open is visible since fscan_sum's barrier)
             if (C.open_ty != TY_NONE && C.closes_open) {
                 C.carry_w = C.out_pos + C.close_vlen;
                 if (C.open_ty == TY_W && C.open_vmax > C.close_vlen) {
@@ -991,14 +989,10 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
 
         QCS_PHASE(4);
         // 8. slide words of a carried W run left if its varint came out shorter
-        if (tid == 0) {
-            uint64_t mx = 0;
-            for (int p = 0; p < NPL; ++p) mx = max(mx, S.carry[p].mv_bytes);
-            S.mvmax = mx;
-            if (a.counters && mx) atomicAdd(&a.counters[2], (unsigned long long)mx);
-        }
-        __syncthreads();
-        for (uint64_t o = 0; o < S.mvmax; o += LPL * 8) {
+        uint64_t mvmax = 0;
+        for (int p = 0; p < NPL; ++p) mvmax = max(mvmax, S.carry[p].mv_bytes);
+        if (tid == 0 && a.counters && mvmax) atomicAdd(&a.counters[2], (unsigned long long)mvmax);
+        for (uint64_t o = 0; o < mvmax; o += LPL * 8) {
             uint8_t tmp[8];
             const uint64_t src0 = C.out_pos + C.open_vmax + o + lane * 8;
             int m = 0;
