@@ -390,7 +390,10 @@ def run_b200(args, rank, world, local_rank):
     clocks = Clocks(os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out"))
                                  else ".", f"clocks_rank{rank}.csv"))
     launches0 = state.launches()
-    state.profile(True)
+    # live event timing of the dominant kernel (the encoder) only: two events
+    # per launch; events around every kernel cost ~5% of the step.  The other
+    # classes' shares come from one untimed all-class pass after the run.
+    state.profile(2)
     barrier()
     if rank == 0:
         clocks.start()
@@ -489,6 +492,15 @@ def run_b200(args, rank, world, local_rank):
                                                                  torch.linalg.vector_norm(amps)))
             del psi, amps
     cbytes, min_stride, _ = state._stats()
+    # kernel shares of one more (untimed) iteration with every class timed
+    it = (args.warmup + args.steps) % ITERS
+    a, b = step_range(it)
+    state.profile(1)
+    q.apply_program_range(state, prog, a, b, lad, th)
+    kt_all = state.kernel_times()
+    state.profile(False)
+    roofline["kernel_share"] = {k: v[0] / max(1.0, sum(x[0] for x in kt_all.values())) for k, v in kt_all.items()}
+    roofline["kernel_share_source"] = "one untimed iteration after the timed run, events around every kernel"
     cpu = cpu_baseline(prog, delta) if (world == 1 and not args.no_cpu_baseline) else None
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -179,8 +179,10 @@ uint64_t qcs_state_launches(qcs_dev_state_t st);
 /* Per-kernel-class device timing with CUDA events on the engine's stream
  * (bench roofline accounting).  Classes: 0 decode (k_decode_gate, input
  * passes), 1 serial chain (k_serial_chain), 2 encode (k_fused),
- * 3 commit+norm, 4 mean pass, 5 bookkeeping.  Enabling resets the totals;
- * totals cover every gate enqueued while enabled. */
+ * 3 commit+norm, 4 mean pass, 5 bookkeeping.  enable: 0 off, 1 every class,
+ * 2 the encode class only (two events per encoder launch instead of two per
+ * kernel).  Enabling resets the totals; totals cover every gate enqueued
+ * while enabled. */
 int qcs_state_profile(qcs_dev_state_t st, int enable);
 int qcs_state_kernel_time(qcs_dev_state_t st, int kernel_class, double* total_ns,
                           uint64_t* launches);

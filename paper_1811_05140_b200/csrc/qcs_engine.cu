@@ -890,7 +890,8 @@ struct qcs_dev_state {
     std::vector<void*> allocs;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;
     // per-kernel-class profiling (qcs_state_profile)
-    bool prof = false;
+    int prof = 0;            // 0 off, 1 every kernel class, 2 the encoder (class 2) only
+    bool prof_open = false;  // the last prof_start recorded a mark
     struct Mark {
         int cls;
         cudaEvent_t a, b;
@@ -917,16 +918,19 @@ cudaEvent_t pool_event(qcs_dev_state* st)
 
 void prof_start(qcs_dev_state* st, int cls)
 {
-    if (!st->prof) return;
+    st->prof_open = false;
+    if (!st->prof || (st->prof == 2 && cls != 2)) return;
     qcs_dev_state::Mark m{cls, pool_event(st), pool_event(st)};
     cudaEventRecord(m.a, st->stream);
     st->marks.push_back(m);
+    st->prof_open = true;
 }
 
 void prof_stop(qcs_dev_state* st)
 {
-    if (!st->prof || st->marks.empty()) return;
+    if (!st->prof_open || st->marks.empty()) return;
     cudaEventRecord(st->marks.back().b, st->stream);
+    st->prof_open = false;
 }
 
 void prof_collect(qcs_dev_state* st)
@@ -2281,7 +2285,8 @@ int qcs_state_profile(qcs_dev_state_t st, int enable)
     if (!st) return set_err(QCS_E_INVALID, "null state");
     int rc = sync_and_check(st);
     if (rc) return rc;
-    st->prof = enable != 0;
+    st->prof = enable == 2 ? 2 : (enable != 0 ? 1 : 0);
+    st->prof_open = false;
     for (int i = 0; i < 6; ++i) {
         st->cls_ns[i] = 0;
         st->cls_n[i] = 0;

@@ -366,8 +366,9 @@ class CompressedState:
 
     KERNEL_CLASSES = ("decode", "serial_chain", "fused", "commit", "mean", "bookkeeping")
 
-    def profile(self, enable: bool) -> None:
-        _check(lib().qcs_state_profile(self._h, 1 if enable else 0))
+    def profile(self, enable) -> None:
+        """False/0 off, True/1 every kernel class, 2 the encoder class only."""
+        _check(lib().qcs_state_profile(self._h, 2 if enable == 2 else (1 if enable else 0)))
 
     def kernel_times(self) -> dict:
         out = {}
