@@ -47,7 +47,6 @@ struct FusedSharedT {
     long long wmin[NT / 32];
     PlaneCarry carry[4];
     double s[2];  // exact running sum of squares per stride
-    uint64_t mvmax;
     uint64_t bar[4];  // per-plane mbarrier of the payload bulk copy (MODE_LOCAL)
     uint8_t repaired[NT];  // lane's codes rewritten by a repair pass (resync chain)
 };
@@ -1015,20 +1014,27 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
             // bytes per store
             const int wl = tid & 31;
             const uint32_t my_nb = staged ? nbytes : 0u;
-            for (int j = 0; j < 32; ++j) {
+            for (unsigned todo = __ballot_sync(0xffffffffu, my_nb != 0u); todo; todo &= todo - 1u) {
+                const int j = __ffs(todo) - 1;
                 const uint32_t nb = __shfl_sync(0xffffffffu, my_nb, j);
-                if (nb == 0) continue;
                 const uint64_t bs = __shfl_sync(0xffffffffu, bstart, j);
                 const uint8_t* src = reinterpret_cast<const uint8_t*>(xs + (uint64_t)((tid & ~31) + j) * XS_STRIDE);
-                // <= 160 bytes (32 tokens of <= 5): five predicated rounds,
-                // loads first
-                uint8_t b[5];
+                // <= 160 bytes (32 tokens of <= 5): predicated rounds, loads
+                // first; two rounds cover the usual lane (warp-uniform test)
+                if (nb <= 64u) {
+                    const uint8_t b0 = wl < nb ? src[wl] : (uint8_t)0;
+                    const uint8_t b1 = wl + 32u < nb ? src[wl + 32u] : (uint8_t)0;
+                    if (wl < nb) out[bs + wl] = b0;
+                    if (wl + 32u < nb) out[bs + wl + 32u] = b1;
+                } else {
+                    uint8_t b[5];
 #pragma unroll
-                for (int r = 0; r < 5; ++r) b[r] = wl + 32u * r < nb ? src[wl + 32u * r] : (uint8_t)0;
+                    for (int r = 0; r < 5; ++r) b[r] = wl + 32u * r < nb ? src[wl + 32u * r] : (uint8_t)0;
 #pragma unroll
-                for (int r = 0; r < 5; ++r)
-                    if (wl + 32u * r < nb) out[bs + wl + 32u * r] = b[r];
-                for (uint32_t k = wl + 160u; k < nb; k += 32) out[bs + k] = src[k];
+                    for (int r = 0; r < 5; ++r)
+                        if (wl + 32u * r < nb) out[bs + wl + 32u * r] = b[r];
+                    for (uint32_t k = wl + 160u; k < nb; k += 32) out[bs + k] = src[k];
+                }
             }
         }
         if (!staged) {
