@@ -1,32 +1,39 @@
 #!/usr/bin/env python3
 """Benchmark of the per-gate decompress -> gate -> recompress hot path.
 
-Workload (BASELINE.json configs[1]): 24-qubit Grover search in
-gate form, H^24 then 64 x [flip m; H^24; flip 0; H^24] (3224 gates),
-2^16-amplitude strides, error bound eps = 1e-4 mapped to the power-of-two
-absolute bound delta = 2^-26 (circuit.pow2_bound), single-level ladder,
-theta = 1, marked index m seeded (SplitMix64, seed 7).  Synthetic: the
-circuit is generated, no external data.
-
-A *step* is one Grover iteration (50 gates) applied to the resident state;
-the H^24 prologue is untimed setup.  W warm-up steps, then K timed steps;
-the state keeps evolving along the circuit.  L2 is flushed (256 MiB write)
-before every timed step.
+Headline workload (default, `--config C3`; BASELINE.json configs[2], SURVEY.md
+§8d C3 -- the largest configuration that fits one GPU): QFT-34 on a seeded
+basis state, 2^20-amplitude strides (16384 strides, 256 GiB uncompressed),
+eps = 1e-3 mapped to the power-of-two absolute bound delta = 2^-27
+(circuit.pow2_bound, <= SURVEY's eps*2^-17), single-level ladder, theta = 1.
+The state at the start of the QFT's last stage (gate 612 of 646: qubits 0..32
+transformed, qubit 33 still a basis bit -- the late, dense part of the
+circuit) is built from its exact closed form (circuit.qft_stage) and
+compressed by the engine (qcs_load_strides_device) -- untimed setup.  A *step*
+is 2 consecutive gates of that last stage (CP(k, 33) ... H(33)), applied in
+circuit order to the resident state; W warm-up steps, then K timed steps
+(wrapping to the stage's first gate if W + K steps exceed its 34 gates).  The
+state (>= 34 GB) is far larger than L2, so no flush is needed.
 
 value     amplitude updates (sum of bytes_before/16, aalc.cpp:622) per second
-          of DEVICE time (CUDA events on the engine's stream around every gate),
-          state resident in HBM.
+          of DEVICE time (CUDA events on the engine's stream around every gate).
 e2e       same metric through the public C-ABI call (qcs_run_program) from
           host gate descriptors to host GateRecords, host wall clock.
-roofline  dominant kernel class, algorithmic bytes / its event-timed duration
-          vs MEASURED_PEAKS.json hbm_gbs.
-cpu_baseline  the unmodified reference (oracle/_ref/libqcsref.so) on this
-          host's cores, bounded sample of the same circuit.
+roofline  dominant kernel class, algorithmic bytes (C_in + C_out) / its
+          event-timed duration vs MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline / same_shape
+          the unmodified reference (oracle/_ref) on this host's cores at the
+          same shape one size down (QFT-28, 2^20-amp strides, the same delta
+          mapping, the same last-stage window, started from the same
+          closed-form state compressed by the reference's own
+          compress_stride_adaptive and CompressedState::load), and the GPU on
+          exactly that state: both start from bit-identical amplitudes, so
+          their GateRecords are compared field for field.
 
---impl reference runs the reference CPU path on the same workload instead.
-N > 1 (torchrun): the C2 workload weak-scaled to 24 + log2(N) qubits and
-sharded over the ranks (rank = top qubits; gates on rank qubits exchange
-stride images with NCCL send/recv), device time max over ranks.
+--impl reference runs the reference CPU path on that QFT-28 workload.
+--config C2 is round 1's headline (Grover-24 gate form, 2^16-amp strides);
+C1 / C3-full / C4s run a whole circuit once.  N > 1 (torchrun): the C2
+workload weak-scaled to 24 + log2(N) qubits and sharded over the ranks.
 """
 from __future__ import annotations
 
@@ -43,6 +50,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from paper_1811_05140_b200 import circuit as cc  # noqa: E402
+from paper_1811_05140_b200.stage import load_stage_state, stage_fidelity  # noqa: E402
 
 N_QUBITS, STRIDE_BITS, EPS, ITERS, SEED = 24, 16, 1e-4, 64, 7
 GATES_PER_STEP = 2 * N_QUBITS + 2
@@ -56,10 +64,17 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+EPS_MAPPING = "pow2"  # --eps-mapping (C2): "pow2" or "survey"
+
+
+def c2_delta(n):
+    return cc.survey_bound(EPS, n) if EPS_MAPPING == "survey" else cc.pow2_bound(EPS, n)
+
+
 def workload(n=N_QUBITS):
     marked = next(cc.splitmix64(SEED)) & ((1 << n) - 1)
     prog = cc.build_grover_gate_form(n, marked, ITERS)
-    delta = cc.pow2_bound(EPS, n)
+    delta = c2_delta(n)
     return prog, marked, delta
 
 
@@ -67,7 +82,8 @@ def config_dict(marked, delta, parallelism):
     return {
         "workload": "C2: grover-24 gate form, 64 iterations (3224 gates), 2^16-amp strides",
         "n_qubits": N_QUBITS, "stride_bits": STRIDE_BITS, "eps": EPS,
-        "delta": delta, "delta_mapping": "largest power of two <= eps*2^-ceil(n/2)",
+        "delta": delta, "delta_mapping": ("eps*2^-ceil(n/2) (SURVEY.md §8d)" if EPS_MAPPING == "survey"
+                                          else "largest power of two <= eps*2^-ceil(n/2)"),
         "ladder": [delta], "theta": 1.0, "marked": marked, "iterations": ITERS,
         "step": f"one Grover iteration ({GATES_PER_STEP} gates)",
         "l2": "flushed before each timed step (256 MiB write)",
@@ -194,19 +210,21 @@ def reference_lib():
     return Reference(), None
 
 
-def cpu_baseline(prog, delta):
-    """Reference on this host's cores: H^24 prologue + the first iteration
-    (74 gates) of the same circuit, workers = all cores."""
+def cpu_baseline(prog, delta, first_iter):
+    """Reference on this host's cores, on the GPU arm's own step: the H^24
+    prologue and iterations 0..first_iter-1 untimed, then Grover iteration
+    `first_iter` (50 gates) timed, workers = all cores."""
     ref, why = reference_lib()
     if ref is None:
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": why}
     text = cc.print_circuit(prog)
     st = ref.state(text, STRIDE_BITS, 0)
-    last = N_QUBITS + GATES_PER_STEP
-    r = st.apply(0, last, [delta], 1.0, 0)
+    a, b = step_range(first_iter)
+    st.apply(0, a, [delta], 1.0, 0)
+    r = st.apply(a, b, [delta], 1.0, 0)
     return {"value": r["amp_updates"] / (r["gate_ns"] * 1e-9), "unit": UNIT,
             "cores": ref.max_threads(), "kind": "reference",
-            "sample": f"gates 0..{last} of C2 (H^24 prologue + 1 iteration), "
+            "sample": f"Grover iteration {first_iter} of C2 (gates {a}..{b - 1}) after the untimed prologue, "
                       f"{r['amp_updates']:.3e} amplitude updates in {r['gate_ns'] * 1e-9:.1f} s, "
                       "workers = all cores"}
 
@@ -236,27 +254,35 @@ def run_reference(args, rank, world):
     text = cc.print_circuit(prog)
     st = ref.state(text, STRIDE_BITS, 0)
     st.apply(0, n, [delta], 1.0, 0)                            # untimed prologue
-    total = args.warmup + args.steps
     gps = 2 * n + 2
-    g = gps if total <= 12 else max(10, (12 * gps) // total)
-    g = max(4, g >> g_shift(n))
-    pos = n
-    for _ in range(args.warmup):
-        st.apply(pos, pos + g, [delta], 1.0, 0)
-        pos += g
+    if n == N_QUBITS:
+        # the GPU arm's steps: whole Grover iterations after the prologue
+        steps = [(n + (i % ITERS) * gps, n + (i % ITERS + 1) * gps) for i in range(args.warmup + args.steps)]
+        desc = f"{args.steps} Grover iterations ({gps} gates each) after the H^{n} prologue and {args.warmup} warm-up iterations"
+    else:
+        # weak-scaled state (N > 1 arms): bounded windows of consecutive gates
+        total = args.warmup + args.steps
+        g = gps if total <= 12 else max(10, (12 * gps) // total)
+        g = max(4, g >> g_shift(n))
+        steps, pos = [], n
+        for _ in range(total):
+            if pos + g > len(prog.gates):
+                pos = n  # wrap (state keeps evolving; rate is what is measured)
+            steps.append((pos, pos + g))
+            pos += g
+        desc = f"{args.steps} steps x {g} consecutive gates of grover-{n} after the H^{n} prologue"
+    for a, b in steps[: args.warmup]:
+        st.apply(a, b, [delta], 1.0, 0)
     ns = upd = 0.0
     wall0 = time.perf_counter()
-    for _ in range(args.steps):
-        if pos + g > len(prog.gates):
-            pos = n  # wrap (state keeps evolving; rate is what is measured)
-        r = st.apply(pos, pos + g, [delta], 1.0, 0)
-        pos += g
+    for a, b in steps[args.warmup:]:
+        r = st.apply(a, b, [delta], 1.0, 0)
         ns += r["gate_ns"]
         upd += r["amp_updates"]
     wall = time.perf_counter() - wall0
     value = upd / (ns * 1e-9)
     cores = ref.max_threads()
-    sample = f"{args.steps} steps x {g} consecutive gates of grover-{n} after the H^{n} prologue, workers = {cores}"
+    sample = f"{desc}, workers = {cores}"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ns * 1e-6 / max(1, args.steps),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -290,7 +316,7 @@ def run_sharded(args, rank, world, local_rank):
     n = N_QUBITS + g
     marked = next(cc.splitmix64(SEED)) & ((1 << n) - 1)
     prog = cc.build_grover_gate_form(n, marked, ITERS)
-    delta = cc.pow2_bound(EPS, n)
+    delta = c2_delta(n)
     gps = 2 * n + 2
     dev = 0 if os.environ.get("QCS_SAME_DEVICE") else local_rank
     torch.cuda.set_device(dev)
@@ -501,7 +527,7 @@ def run_b200(args, rank, world, local_rank):
     state.profile(False)
     roofline["kernel_share"] = {k: v[0] / max(1.0, sum(x[0] for x in kt_all.values())) for k, v in kt_all.items()}
     roofline["kernel_share_source"] = "one untimed iteration after the timed run, events around every kernel"
-    cpu = cpu_baseline(prog, delta) if (world == 1 and not args.no_cpu_baseline) else None
+    cpu = cpu_baseline(prog, delta, 1) if (world == 1 and not args.no_cpu_baseline) else None
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_max * 1e-6 / max(1, args.steps),
@@ -682,6 +708,262 @@ def run_qft_config(args, name):
     return 0
 
 
+# ---------------------------------------------------------------------------
+# C3 headline: the last stage of QFT-34 on its exact intermediate state
+# ---------------------------------------------------------------------------
+C3 = dict(n=34, s=20, eps=1e-3, ref_n=28, step=2, cpu_gates=12)
+
+
+def c3_setup(n):
+    """QFT-n, its seeded basis (round 1's C3 basis), the first gate of its last
+    stage (CP(0, n-1) ... CP(n-2, n-1), H(n-1)) and the delta mapping."""
+    prog = cc.build_qft(n)
+    x = next(cc.splitmix64(n)) & ((1 << n) - 1)
+    g0 = len(prog.gates) - n
+    return prog, x, g0, cc.pow2_bound(C3["eps"], n)
+
+
+def c3_step(n, g0, i):
+    """Gate range of step i: C3['step'] consecutive gates of the last stage,
+    wrapping to its first gate once the stage is used up."""
+    per = n // C3["step"]
+    a = g0 + (i % per) * C3["step"]
+    return a, a + C3["step"]
+
+
+def ref_csv_records(csv):
+    """emit_csv rows -> (rows without elapsed_ns, sum elapsed_ns, amplitude updates)."""
+    lines = csv.strip().splitlines()
+    head = lines[0].split(",")
+    ie, ib = head.index("elapsed_ns"), head.index("bytes_before")
+    rows, ns, upd = [], 0, 0
+    for ln in lines[1:]:
+        f = ln.split(",")
+        ns += int(f[ie])
+        upd += int(f[ib]) // 16
+        rows.append(",".join(f[:ie] + f[ie + 1:]))
+    return rows, ns, upd
+
+
+def same_shape_c3(q, ref, device, n_gates):
+    """The reference (all host cores) and the GPU on the SAME QFT-28 state
+    (2^20-amp strides, the same delta mapping): the closed-form state at the
+    start of the last stage, compressed by each engine from bit-identical
+    amplitudes, then the first n_gates gates of the stage.  Returns the CPU
+    baseline, the GPU line and whether the GateRecords agree bit for bit."""
+    from paper_1811_05140_b200 import metrics as mm
+    import torch
+    n, s = C3["ref_n"], C3["s"]
+    prog, x, g0, delta = c3_setup(n)
+    tables = cc.stage_tables(n, s, *cc.qft_stage(n, x, g0))
+    path = os.path.join("/tmp", f"qcs_c3_ref{n}_{os.getpid()}.qckp")
+    t0 = time.perf_counter()
+    rst = ref.state_from_tables(cc.print_circuit(prog), s, tables, [delta], 1.0, path)
+    build_s = time.perf_counter() - t0
+    try:
+        os.remove(path)
+    except OSError:
+        pass
+    csv = rst.apply_csv(g0, g0 + n_gates, [delta], 1.0, 0)
+    rows_ref, ns_ref, upd_ref = ref_csv_records(csv)
+    cores = ref.max_threads()
+    del rst
+    lad, th = q.ErrorBoundLadder.make([delta]), q.RatioThreshold(1.0)
+    gst = load_stage_state(q, n, s, x, g0, lad, th, device)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    m = q.apply_program_range(gst, prog, g0, g0 + n_gates, lad, th)
+    wall = time.perf_counter() - w0
+    rows_gpu = mm.emit_csv(m.records, with_elapsed=False).strip().splitlines()[1:]
+    dev_ns = sum(r.elapsed_ns for r in m.records)
+    upd = sum(r.bytes_before // 16 for r in m.records)
+    del gst
+    sample = (f"QFT-{n} (2^{s}-amp strides, delta {delta:g}), the first {n_gates} gates of its last stage "
+              f"from the closed-form state at gate {g0} (compress_stride_adaptive + CompressedState::load, "
+              f"{build_s:.1f} s untimed), workers = {cores}")
+    cpu = {"value": upd_ref / (ns_ref * 1e-9), "unit": UNIT, "cores": cores, "kind": "reference",
+           "sample": sample}
+    gpu = {"value": upd / (dev_ns * 1e-9), "e2e": upd / wall, "unit": UNIT, "n_qubits": n,
+           "gates": n_gates, "records_identical_to_reference": rows_gpu == rows_ref,
+           "ratio_value_vs_reference": (upd / (dev_ns * 1e-9)) / (upd_ref / (ns_ref * 1e-9)),
+           "ratio_e2e_vs_reference": (upd / wall) / (upd_ref / (ns_ref * 1e-9))}
+    if rows_gpu != rows_ref:
+        bad = next(i for i, (a, b) in enumerate(zip(rows_gpu, rows_ref)) if a != b) if len(rows_gpu) == len(rows_ref) else -1
+        log("same-shape records differ at row", bad, rows_gpu[bad] if bad >= 0 else "", rows_ref[bad] if bad >= 0 else "")
+    return cpu, gpu
+
+
+def run_c3(args, rank, world, local_rank):
+    import torch
+    import paper_1811_05140_b200 as q
+    n, s = C3["n"], C3["s"]
+    prog, x, g0, delta = c3_setup(n)
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    os.environ.setdefault("QCS_RESERVE_BYTES", str(8 << 30))  # torch buffers of setup / fidelity
+    lad, th = q.ErrorBoundLadder.make([delta]), q.RatioThreshold(1.0)
+    t0 = time.perf_counter()
+    state = load_stage_state(q, n, s, x, g0, lad, th, dev)
+    setup_s = time.perf_counter() - t0
+    log(f"C3 state at gate {g0} loaded in {setup_s:.1f} s: {state._stats()}")
+    for i in range(args.warmup):
+        a, b = c3_step(n, g0, i)
+        q.apply_program_range(state, prog, a, b, lad, th)
+    clocks = Clocks(os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out"))
+                                 else ".", f"clocks_rank{rank}.csv"))
+    launches0 = state.launches()
+    state.profile(2)          # events around the encoder launches only
+    torch.cuda.synchronize()
+    clocks.start()
+    dev_ns = wall_ns = 0
+    upd = cin = cout = 0
+    min_ratio = math.inf
+    last_gate = g0
+    for i in range(args.warmup, args.warmup + args.steps):
+        a, b = c3_step(n, g0, i)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter_ns()
+        m = q.apply_program_range(state, prog, a, b, lad, th)   # C-ABI: host descs in, records out
+        wall_ns += time.perf_counter_ns() - w0
+        for r in m.records:
+            dev_ns += r.elapsed_ns
+            upd += r.bytes_before // 16
+            cin += r.compressed_in
+            cout += r.bytes_after
+            min_ratio = min(min_ratio, r.min_ratio)
+        last_gate = b
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    kt = state.kernel_times()
+    log("kernel times (ns, launches):", kt)
+    state.profile(False)
+    launches = state.launches() - launches0
+    wrapped = (args.warmup + args.steps) * C3["step"] > n
+    fid = maxerr = None
+    if not args.skip_fidelity and not wrapped:
+        fid, maxerr = stage_fidelity(state, n, s, x, last_gate, dev)
+    cbytes, min_stride, nsq = state._stats()
+    arena, side_b, scratch_b = state.memory()
+    # kernel shares of one more (untimed) step with every class timed
+    state.profile(1)
+    a, b = c3_step(n, g0, args.warmup + args.steps)
+    q.apply_program_range(state, prog, a, b, lad, th)
+    kt_all = state.kernel_times()
+    state.profile(False)
+    del state
+    torch.cuda.empty_cache()
+
+    peak, peak_src = measured_peaks()
+    t_f, n_f = kt["fused"]
+    achieved = (cin + cout) / (t_f * 1e-9) / 1e9 if t_f else 0.0
+    path_gbs = (cin + cout) / (dev_ns * 1e-9) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic_k_fused_c3.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f)["traffic_bytes"]
+    tot_all = max(1.0, sum(v[0] for v in kt_all.values()))
+    roofline = {"bound": "hbm", "kernel": "k_fused", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "traffic_source": "ncu --set full, one launch (profiles/traffic_k_fused_c3.json)" if traffic else None,
+                "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": (cin + cout) / max(1, n_f),
+                "algorithmic_bytes": "C_in + C_out of the gates' rewritten strides, 29-byte headers included "
+                                     "(SURVEY.md §8d), over the k_fused launches of the timed steps",
+                "avg_launch_us": t_f / max(1, n_f) / 1e3,
+                "path_C_in_plus_C_out_GBps": path_gbs, "path_frac": path_gbs / peak,
+                "kernel_share": {k: v[0] / tot_all for k, v in kt_all.items()},
+                "kernel_share_source": "one untimed step after the timed run, events around every kernel"}
+    cpu = same = None
+    if world == 1 and not args.no_cpu_baseline:
+        ref, why = reference_lib()
+        if ref is None:
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": why}
+        else:
+            cpu, same = same_shape_c3(q, ref, dev, C3["cpu_gates"])
+    line = {"metric": METRIC, "value": upd / (dev_ns * 1e-9), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ns * 1e-6 / max(1, args.steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference-built QFT circuit, seeded basis, exact closed-form stage state)",
+            "config": {"workload": f"C3: qft-{n}, last stage (gates {g0}..{len(prog.gates) - 1}) on the "
+                                   f"exact state at gate {g0}, 2^{s}-amp strides, one B200",
+                       "n_qubits": n, "stride_bits": s, "eps": C3["eps"], "delta": delta,
+                       "delta_mapping": "largest power of two <= eps*2^-ceil(n/2) (SURVEY.md: eps*2^-17)",
+                       "ladder": [delta], "theta": 1.0, "basis": x,
+                       "step": f"{C3['step']} consecutive gates of the last stage", "wrapped": wrapped,
+                       "l2": "state (>= 34 GB) larger than L2; no flush", "parallelism": "single GPU",
+                       "setup": f"closed-form state compressed on the GPU ({setup_s:.1f} s, untimed)"},
+            "roofline": roofline, "cpu_baseline": cpu, "same_shape": same,
+            "e2e": {"value": upd / (wall_ns * 1e-9), "unit": UNIT,
+                    "h2d_bytes_per_step": DESC_BYTES * C3["step"],
+                    "d2h_bytes_per_step": RECORD_BYTES * C3["step"]},
+            "gpu_launches": launches, "clocks": clk,
+            "fidelity_vs_exact": fid, "max_abs_amp_error": maxerr, "pointwise_bound": delta,
+            "min_stride_ratio": min_ratio, "final_state_ratio": (16 << n) / cbytes,
+            "compressed_bytes": cbytes, "hbm_bytes": {"arena_in_use": arena, "side_index": side_b,
+                                                      "scratch": scratch_b},
+            "bytes_per_amp_update": (cin + cout) / max(1, upd)}
+    print(json.dumps(line))
+    return 0
+
+
+def run_reference_c3(args, rank, world):
+    """The unmodified reference on this host's cores at the same shape one size
+    down (QFT-28, 2^20-amp strides, the delta mapping of n = 28): the closed-form
+    state at the start of the last stage, compressed by the reference's own
+    compress_stride_adaptive and read by CompressedState::load, then steps of 2
+    consecutive last-stage gates through apply_program_range (rank 0 only)."""
+    if rank != 0:
+        return 0
+    ref, why = reference_lib()
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": why}))
+        return 0
+    n, s = C3["ref_n"], C3["s"]
+    prog, x, g0, delta = c3_setup(n)
+    path = os.path.join("/tmp", f"qcs_c3_ref{n}_{os.getpid()}.qckp")
+    t0 = time.perf_counter()
+    st = ref.state_from_tables(cc.print_circuit(prog), s, cc.stage_tables(n, s, *cc.qft_stage(n, x, g0)),
+                               [delta], 1.0, path)
+    build_s = time.perf_counter() - t0
+    try:
+        os.remove(path)
+    except OSError:
+        pass
+    for i in range(args.warmup):
+        a, b = c3_step(n, g0, i)
+        st.apply(a, b, [delta], 1.0, 0)
+    ns = upd = 0.0
+    wall0 = time.perf_counter()
+    for i in range(args.warmup, args.warmup + args.steps):
+        a, b = c3_step(n, g0, i)
+        r = st.apply(a, b, [delta], 1.0, 0)
+        ns += r["gate_ns"]
+        upd += r["amp_updates"]
+    wall = time.perf_counter() - wall0
+    value = upd / (ns * 1e-9)
+    cores = ref.max_threads()
+    sample = (f"QFT-{n} (2^{s}-amp strides, delta {delta:g}), {args.steps} steps x {C3['step']} gates of the "
+              f"last stage from the closed-form state at gate {g0} (compress_stride_adaptive + "
+              f"CompressedState::load, {build_s:.1f} s untimed), workers = {cores}")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ns * 1e-6 / max(1, args.steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference-built QFT circuit, seeded basis, exact closed-form stage state)",
+            "config": {"workload": f"C3 shape one size down: qft-{n} last stage, 2^{s}-amp strides "
+                                   "(the B200 arm's C3 workload at n = 34 costs the same per amplitude; "
+                                   "SURVEY.md §8d same-shape method)",
+                       "n_qubits": n, "stride_bits": s, "eps": C3["eps"], "delta": delta,
+                       "delta_mapping": "largest power of two <= eps*2^-ceil(n/2)", "ladder": [delta],
+                       "theta": 1.0, "basis": x, "step": f"{C3['step']} consecutive gates of the last stage",
+                       "parallelism": "reference CPU (OpenMP), rank 0 only"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+            "e2e": {"value": upd / wall, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -690,17 +972,26 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-fidelity", action="store_true")
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4s"],
-                    help="C2 (default) is the headline workload; C1/C3 run a whole QFT once, "
-                         "C4s the 30-qubit grid")
+    ap.add_argument("--config", default="C3", choices=["C3", "C2", "C1", "C3-full", "C4s"],
+                    help="C3 (default): the headline, QFT-34's last stage on one GPU; C2: Grover-24 gate "
+                         "form; C1 / C3-full: a whole QFT once; C4s: the 30-qubit grid")
+    ap.add_argument("--eps-mapping", default="pow2", choices=["pow2", "survey"],
+                    help="C2 only: delta = largest power of two <= eps*2^-ceil(n/2) (default) or "
+                         "SURVEY.md's eps*2^-ceil(n/2) itself")
     args = ap.parse_args()
-    if args.config != "C2":
-        return run_qft_config(args, args.config)
-    if args.warmup < 3 and args.impl == "b200":
-        log("warning: timing rules ask for >= 3 warm-up steps")
+    global EPS_MAPPING
+    EPS_MAPPING = args.eps_mapping
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config in ("C1", "C3-full", "C4s"):
+        return run_qft_config(args, "C3" if args.config == "C3-full" else args.config)
+    if args.config == "C3" and world == 1:
+        if args.impl == "reference":
+            return run_reference_c3(args, rank, world)
+        return run_c3(args, rank, world, local_rank)
+    if args.warmup < 3 and args.impl == "b200":
+        log("warning: timing rules ask for >= 3 warm-up steps")
     if world > 1:
         import torch
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")

@@ -101,6 +101,11 @@ int qcs_apply_gate(qcs_dev_state_t st, const qcs_gate_desc* gate, const double* 
                    int n_levels, double theta, qcs_stride_report* reports,
                    uint64_t* n_reports, double* norm_after);
 
+/* Wave layout (states too large for two slots per plane, e.g. C3): a gate's
+ * units are committed wave by wave, so an out-of-memory failure after the
+ * first wave leaves the gate part-applied; the state is then refused by every
+ * later call (QCS_E_RUNTIME).  Every other failure leaves the state unchanged. */
+
 /* qcs_apply_gate with flags, for a state that is one shard of a larger one.
  * QCS_NO_RENORM skips the lazy renormalisation (aalc.cpp:410-419) so the
  * caller renormalises globally from qcs_stride_norms + qcs_scale_all in the
@@ -153,6 +158,17 @@ int qcs_read_stride(qcs_dev_state_t st, uint64_t stride, int apply_scale, double
  * count * 2 * 2^s doubles laid out [stride][re|im][element]. */
 int qcs_read_strides_device(qcs_dev_state_t st, uint64_t first, uint64_t count, int apply_scale,
                             double* dev_out);
+/* Inverse of qcs_read_strides_device: strides [first, first+count) are
+ * replaced by the compression of dev_planes (device memory, count * 2 * 2^s
+ * doubles laid out [stride][re|im][element]) through the ladder, exactly as
+ * compress_stride_adaptive does (aalc.cpp:117-138: the planes are zero-snapped
+ * IN PLACE first, then each level is tried until the ratio reaches theta);
+ * scale 1 and the stored sum of squares of what was stored (aalc.cpp:46-52).
+ * No renormalisation.  The reference has no from-amplitudes constructor; its
+ * equivalent is a QCKP file of compress()ed blocks read by
+ * CompressedState::load (aalc.cpp:496-586). */
+int qcs_load_strides_device(qcs_dev_state_t st, uint64_t first, uint64_t count, double* dev_planes,
+                            const double* ladder, int n_levels, double theta);
 /* to_amplitudes (aalc.cpp:211-223): interleaved re/im, 2^(n+1) doubles. */
 int qcs_to_amplitudes(qcs_dev_state_t st, double* amps);
 /* compressed_bytes / min_stride_ratio / norm_sq_tracked (aalc.cpp:233-259). */

@@ -269,34 +269,46 @@ class Reference:
         if rc:
             raise OracleError(rc, self.lib.ref_last_error().decode())
 
-    def state(self, text: str, stride_bits: int, basis: int):
-        self.lib.ref_state_create.restype = C.c_void_p
-        self.lib.ref_state_create.argtypes = [C.c_char_p, C.c_int, C.c_uint64]
-        self.lib.ref_state_apply.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_double),
-                                             C.c_int, C.c_double, C.c_int, C.POINTER(C.c_double)]
-        self.lib.ref_state_stats.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
-        self.lib.ref_state_destroy.argtypes = [C.c_void_p]
+    def _state_api(self):
+        L = self.lib
+        L.ref_state_create.restype = C.c_void_p
+        L.ref_state_create.argtypes = [C.c_char_p, C.c_int, C.c_uint64]
+        L.ref_state_from_tables.restype = C.c_void_p
+        L.ref_state_from_tables.argtypes = [C.c_char_p, C.c_int] + [C.c_void_p] * 4 + [
+            C.c_double, C.c_uint64, C.c_uint64, C.POINTER(C.c_double), C.c_int, C.c_double,
+            C.c_char_p, C.c_int]
+        L.ref_state_apply.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_double),
+                                      C.c_int, C.c_double, C.c_int, C.POINTER(C.c_double)]
+        L.ref_state_apply_csv.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_double),
+                                          C.c_int, C.c_double, C.c_int, C.c_char_p, C.c_uint64,
+                                          C.POINTER(C.c_uint64)]
+        L.ref_state_amplitudes.argtypes = [C.c_void_p, C.c_void_p]
+        L.ref_state_stats.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+        L.ref_state_destroy.argtypes = [C.c_void_p]
+
+    def state(self, text: str, stride_bits: int, basis: int) -> "RefState":
+        """CompressedState::basis_state of the circuit's geometry."""
+        self._state_api()
         h = self.lib.ref_state_create(text.encode(), stride_bits, C.c_uint64(basis))
         if not h:
             raise OracleError(1, self.lib.ref_last_error().decode())
-        ref = self
+        return RefState(self, h)
 
-        class _S:
-            def apply(s, first, last, ladder, theta, workers=0):
-                lad = (C.c_double * len(ladder))(*ladder)
-                out = (C.c_double * 4)()
-                ref._check(ref.lib.ref_state_apply(h, first, last, lad, len(ladder),
-                                                   C.c_double(theta), workers, out))
-                return dict(gate_ns=out[0], amp_updates=out[1], min_ratio=out[2], norm=out[3])
-
-            def stats(s):
-                out = (C.c_double * 3)()
-                ref.lib.ref_state_stats(h, out)
-                return dict(compressed_bytes=out[0], min_ratio=out[1], norm_sq=out[2])
-
-            def __del__(s):
-                ref.lib.ref_state_destroy(h)
-        return _S()
+    def state_from_tables(self, text: str, stride_bits: int, tables: dict, ladder: Sequence[float],
+                          theta: float, path: str, workers: int = 0) -> "RefState":
+        """A closed-form intermediate state (circuit.stage_tables) compressed by
+        the reference's compress_stride_adaptive, written as a QCKP checkpoint
+        at `path` and read back by CompressedState::load (oracle/ref_capi.cpp)."""
+        self._state_api()
+        arrs = [np.ascontiguousarray(tables[k], dtype=np.float64) for k in ("lo_re", "lo_im", "hi_re", "hi_im")]
+        lad = (C.c_double * len(ladder))(*ladder)
+        h = self.lib.ref_state_from_tables(text.encode(), stride_bits, *[a.ctypes.data for a in arrs],
+                                           C.c_double(tables["amp"]), C.c_uint64(tables["zmask"]),
+                                           C.c_uint64(tables["zval"]), lad, len(ladder), C.c_double(theta),
+                                           path.encode(), workers)
+        if not h:
+            raise OracleError(1, self.lib.ref_last_error().decode())
+        return RefState(self, h)
 
     def max_threads(self) -> int:
         return self.lib.ref_max_threads()
@@ -351,3 +363,44 @@ class Reference:
         amps = np.empty(2 << n_qubits, dtype=np.float64)
         self._check(self.lib.ref_dense(text.encode(), C.c_uint64(basis), _dptr(amps)))
         return amps.view(np.complex128)
+
+
+class RefState:
+    """A persistent reference CompressedState (oracle/ref_capi.cpp)."""
+
+    def __init__(self, ref: Reference, h):
+        self.ref, self.h = ref, h
+
+    def apply(self, first, last, ladder, theta, workers=0):
+        """apply_program_range over gates [first, last): summed GateRecord
+        elapsed_ns, amplitude updates, min ratio, last norm."""
+        lad = (C.c_double * len(ladder))(*ladder)
+        out = (C.c_double * 4)()
+        self.ref._check(self.ref.lib.ref_state_apply(self.h, first, last, lad, len(ladder),
+                                                     C.c_double(theta), workers, out))
+        return dict(gate_ns=out[0], amp_updates=out[1], min_ratio=out[2], norm=out[3])
+
+    def apply_csv(self, first, last, ladder, theta, workers=0) -> str:
+        """apply_program_range, returning emit_csv of the records."""
+        lad = (C.c_double * len(ladder))(*ladder)
+        cap = 256 * (last - first) + 4096
+        buf = C.create_string_buffer(cap)
+        n = C.c_uint64()
+        self.ref._check(self.ref.lib.ref_state_apply_csv(self.h, first, last, lad, len(ladder),
+                                                         C.c_double(theta), workers, buf, cap, C.byref(n)))
+        return buf.value.decode()
+
+    def amplitudes(self, n_qubits: int) -> np.ndarray:
+        a = np.empty(2 << n_qubits, dtype=np.float64)
+        self.ref._check(self.ref.lib.ref_state_amplitudes(self.h, a.ctypes.data))
+        return a.view(np.complex128)
+
+    def stats(self):
+        out = (C.c_double * 3)()
+        self.ref.lib.ref_state_stats(self.h, out)
+        return dict(compressed_bytes=out[0], min_ratio=out[1], norm_sq=out[2])
+
+    def __del__(self):
+        if self.h:
+            self.ref.lib.ref_state_destroy(self.h)
+            self.h = None

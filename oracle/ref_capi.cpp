@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <fstream>
 #include <string>
 #include <vector>
 
@@ -259,6 +260,114 @@ int ref_state_apply(void* h, std::uint64_t first, std::uint64_t last, const doub
         return 0;
     } catch (const std::exception& e) {
         return fail(classify(e), e.what());
+    }
+}
+
+// ref_state_apply plus the per-gate records as emit_csv text (parity tests).
+int ref_state_apply_csv(void* h, std::uint64_t first, std::uint64_t last, const double* ladder,
+                        int n_levels, double theta, int workers, char* csv, std::uint64_t cap,
+                        std::uint64_t* len)
+{
+    try {
+        auto* r = static_cast<RefState*>(h);
+        const qcs::ErrorBoundLadder lad = qcs::ErrorBoundLadder::make(
+            std::vector<double>(ladder, ladder + n_levels));
+        const qcs::RunMetrics m = qcs::apply_program_range(
+            r->state, r->prog, first, last, lad, qcs::RatioThreshold(theta), workers);
+        return copy_text(qcs::emit_csv(m.records), csv, cap, len);
+    } catch (const std::exception& e) {
+        return fail(classify(e), e.what());
+    }
+}
+
+// to_amplitudes of a persistent state (interleaved re/im).
+int ref_state_amplitudes(void* h, double* amps)
+{
+    try {
+        const std::vector<qcs::Amplitude> a = static_cast<RefState*>(h)->state.to_amplitudes();
+        for (std::size_t i = 0; i < a.size(); ++i) {
+            amps[2 * i] = a[i].real();
+            amps[2 * i + 1] = a[i].imag();
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(classify(e), e.what());
+    }
+}
+
+// A persistent state holding a closed-form intermediate state of the circuit
+// (bench.py's late-QFT window, tests/test_gpu_window.py): amplitude
+//   a_y = amp * lo[y mod L] * hi[y / L]   (complex; zero where (y & zmask) != zval)
+// computed with the same IEEE operations, in the same order, as the GPU arm's
+// generator (t = hr*lr - hi*li, u = hr*li + hi*lr, then amp*t, amp*u), so both
+// arms start from bit-identical amplitudes.  Every stride goes through the
+// reference's compress_stride_adaptive (aalc.cpp:117-138); the result is written
+// as a QCKP v1 checkpoint in the reference's format (aalc.cpp:466-494: scale 1,
+// sum_sq = StrideBuffer::sum_sq of the decoded blocks, as stored_sum_sq does,
+// aalc.cpp:46-52) and read back with CompressedState::load (aalc.cpp:496-586).
+void* ref_state_from_tables(const char* circuit_text, int stride_bits, const double* lo_re,
+                            const double* lo_im, const double* hi_re, const double* hi_im,
+                            double amp, std::uint64_t zmask, std::uint64_t zval,
+                            const double* ladder, int n_levels, double theta, const char* path,
+                            int workers)
+{
+    try {
+        auto* r = new RefState();
+        r->prog = qcs::parse_circuit(circuit_text);
+        const qcs::StateGeometry geom = qcs::StateGeometry::make(r->prog.n_qubits, stride_bits);
+        const qcs::ErrorBoundLadder lad = qcs::ErrorBoundLadder::make(
+            std::vector<double>(ladder, ladder + n_levels));
+        const std::uint64_t L = geom.stride_len(), NS = geom.n_strides();
+        std::vector<std::vector<std::uint8_t>> body(NS);
+        const int nt = workers > 0 ? workers : ref_max_threads();
+#pragma omp parallel for schedule(dynamic) num_threads(nt)
+        for (std::int64_t jj = 0; jj < static_cast<std::int64_t>(NS); ++jj) {
+            const std::uint64_t j = static_cast<std::uint64_t>(jj);
+            qcs::StrideBuffer buf(j, L);
+            for (std::uint64_t e = 0; e < L; ++e) {
+                const std::uint64_t y = j * L + e;
+                if ((y & zmask) != zval) continue;  // exact +0.0
+                const double t = hi_re[j] * lo_re[e] - hi_im[j] * lo_im[e];
+                const double u = hi_re[j] * lo_im[e] + hi_im[j] * lo_re[e];
+                buf.re[e] = amp * t;
+                buf.im[e] = amp * u;
+            }
+            const qcs::AdaptiveResult a =
+                qcs::compress_stride_adaptive(buf, lad, qcs::RatioThreshold(theta));
+            qcs::decompress_into(a.re, buf.re);
+            qcs::decompress_into(a.im, buf.im);
+            const double ss = buf.sum_sq();
+            const double one = 1.0;
+            std::vector<std::uint8_t>& o = body[j];
+            for (double v : {one, ss}) {
+                std::uint64_t w;
+                std::memcpy(&w, &v, 8);
+                for (int i = 0; i < 8; ++i) o.push_back(static_cast<std::uint8_t>(w >> (8 * i)));
+            }
+            qcs::serialize_block_append(a.re, o);
+            qcs::serialize_block_append(a.im, o);
+        }
+        {
+            std::ofstream f(path, std::ios::binary | std::ios::trunc);
+            std::vector<std::uint8_t> hdr = {'Q', 'C', 'K', 'P', 1};
+            auto u32 = [&](std::uint32_t v) { for (int i = 0; i < 4; ++i) hdr.push_back(static_cast<std::uint8_t>(v >> (8 * i))); };
+            auto u64 = [&](std::uint64_t v) { for (int i = 0; i < 8; ++i) hdr.push_back(static_cast<std::uint8_t>(v >> (8 * i))); };
+            u32(static_cast<std::uint32_t>(geom.n_qubits));
+            u32(static_cast<std::uint32_t>(geom.stride_bits));
+            u64(lad.fingerprint());
+            u64(NS);
+            f.write(reinterpret_cast<const char*>(hdr.data()), static_cast<std::streamsize>(hdr.size()));
+            for (auto& b : body) {
+                f.write(reinterpret_cast<const char*>(b.data()), static_cast<std::streamsize>(b.size()));
+                std::vector<std::uint8_t>().swap(b);
+            }
+            if (!f) throw std::runtime_error(std::string("cannot write ") + path);
+        }
+        r->state = std::move(qcs::CompressedState::load(path, geom).state);
+        return r;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
     }
 }
 

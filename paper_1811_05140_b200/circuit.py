@@ -446,3 +446,75 @@ def pow2_bound(eps: float, n: int) -> float:
     in binary64)."""
     d = eps * math.ldexp(1.0, -((n + 1) // 2))
     return math.ldexp(1.0, math.frexp(d)[1] - 1)
+
+
+def survey_bound(eps: float, n: int) -> float:
+    """SURVEY.md §8(d)'s mapping itself: delta = eps * 2^-ceil(n/2) (not a
+    power of two for eps = 1e-3 / 1e-4 / 1e-2)."""
+    return eps * math.ldexp(1.0, -((n + 1) // 2))
+
+
+def qft_stage(n: int, x: int, g: int):
+    """Exact state that build_qft(n) (circuit.cpp:274-297) produces from the
+    basis state x after its first g gates.  QFT keeps a product state: a qubit
+    whose Hadamard has run holds (|0> + e^{i phi}|1>)/sqrt2, every other qubit a
+    basis bit, and CP(k, j) only moves phi_k (qubit j is still a basis bit when
+    its ladder runs).  So
+        a_y = 2^(-m/2) exp(2 pi i R(y) / 2^n)  if (y & zmask) == zval, else 0,
+        R(y) = sum_k y_k r[k]  (mod 2^n),
+    with m the number of processed qubits.  Returns (m, r, zmask, zval)."""
+    if not 0 <= g <= len(build_qft(n).gates):
+        raise IndexError("gate index outside the program")
+    b = x
+    done = 0
+    for i in range(n // 2):                 # swap network: CX permutes basis states
+        a, c = i, n - 1 - i
+        for ctl, tgt in ((a, c), (c, a), (a, c)):
+            if done == g:
+                return 0, [0] * n, (1 << n) - 1, b
+            if (b >> ctl) & 1:
+                b ^= 1 << tgt
+            done += 1
+    r = [0] * n
+    processed = 0
+    mod = (1 << n) - 1
+    for j in range(n):
+        for k in range(j):
+            if done == g:
+                break
+            if (b >> j) & 1:                # CP(k, j), theta = pi / 2^(j-k)
+                r[k] = (r[k] + (1 << (n - 1 - (j - k)))) & mod
+            done += 1
+        if done == g:
+            break
+        processed |= 1 << j                 # H(j)
+        r[j] = (r[j] + (((b >> j) & 1) << (n - 1))) & mod
+        done += 1
+    zmask = ((1 << n) - 1) & ~processed
+    return bin(processed).count("1"), r, zmask, b & zmask
+
+
+def stage_tables(n: int, s: int, m: int, r, zmask: int, zval: int):
+    """Factor tables of a qft_stage state for generation stride by stride:
+    a_y = amp * lo[y mod 2^s] * hi[y >> s] (complex), zero where
+    (y & zmask) != zval.  Both benchmark arms (GPU: torch; reference: the C++
+    generator in oracle/ref_capi.cpp) form t = hr*lr - hi*li, u = hr*li + hi*lr,
+    then amp*t, amp*u with the same IEEE operations, so they start from
+    bit-identical amplitudes."""
+    import numpy as np
+    L, NS = 1 << s, 1 << (n - s)
+    mod = np.uint64((1 << n) - 1)
+    w = 2.0 * math.pi / float(1 << n)
+
+    def table(bits0, count):
+        idx = np.arange(count, dtype=np.uint64)
+        R = np.zeros(count, dtype=np.uint64)
+        for k in range(bits0, bits0 + (count.bit_length() - 1)):
+            R = (R + ((idx >> np.uint64(k - bits0)) & np.uint64(1)) * np.uint64(r[k])) & mod
+        ang = R.astype(np.float64) * w
+        return np.cos(ang), np.sin(ang)
+
+    lo_re, lo_im = table(0, L)
+    hi_re, hi_im = table(s, NS)
+    amp = math.ldexp(math.sqrt(0.5) if m & 1 else 1.0, -(m // 2))
+    return dict(lo_re=lo_re, lo_im=lo_im, hi_re=hi_re, hi_im=hi_im, amp=amp, zmask=zmask, zval=zval)

@@ -25,7 +25,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/qcs_b200.h"
@@ -71,7 +73,12 @@ struct Plan {
     int local_ctl;   // in-stride control mask bit (c < s), else -1
     uint64_t flip_off;
     int reflect;
+    uint64_t first;  // LOAD: first stride of the range (0 for gates)
 };
+
+// Plan.kind of qcs_load_strides_device (not a GateKind): the units are the
+// strides [first, first + n_units), their input is the caller's raw planes
+constexpr int KIND_LOAD = 4;
 
 __host__ __device__ inline uint64_t insert_bit(uint64_t j, int pos, int v)
 {
@@ -84,7 +91,7 @@ __host__ __device__ inline uint64_t unit_lo(const Plan& p, uint64_t u)
     if (p.fixed >= 0) return (uint64_t)p.fixed;
     uint64_t j = u;
     for (int i = 0; i < p.npos; ++i) j = insert_bit(j, p.pos[i], p.val[i]);
-    return j;
+    return j + p.first;
 }
 
 // job/slot s -> stride
@@ -811,15 +818,28 @@ CodecParams make_params(double delta)
     return cp;
 }
 
+// cudaFuncSetAttribute is per device context: remember each (kernel,
+// device) pair once, thread-safely (states on several devices, rank threads).
+int set_smem_attr(const void* fn, int bytes)
+{
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& e : done)
+        if (e.first == fn && e.second == dev) return 0;
+    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.emplace_back(fn, dev);
+    return 0;
+}
+
 template <bool L, int NPL, int LPL, int MODE>
 int launch_fused_t(const FusedArgs& a, uint64_t grid, cudaStream_t s)
 {
-    static bool set = false;
-    if (!set) {
-        CU(cudaFuncSetAttribute(k_fused<L, NPL, LPL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)FusedLayout<NPL * LPL>::SMEM));
-        set = true;
-    }
+    if (const int rc = set_smem_attr(reinterpret_cast<const void*>(k_fused<L, NPL, LPL, MODE>),
+                                     (int)FusedLayout<NPL * LPL>::SMEM))
+        return rc;
     if (grid == 0) return 0;
     k_fused<L, NPL, LPL, MODE><<<(unsigned)grid, NPL * LPL, FusedLayout<NPL * LPL>::SMEM, s>>>(a);
     CU(cudaGetLastError());
@@ -879,6 +899,7 @@ struct qcs_dev_state {
     // buffers (slots, side, X) for `wave` slots, per-wave commit placed by the
     // host, in-place compaction through the X buffer.
     int big = 0;
+    bool poisoned = false;       // a wave-layout gate failed after committing some waves
     uint64_t wave = 0;           // slots per wave (== NS in the small layout)
     uint64_t bump = 0;           // wave mode: arena fill (host-authoritative)
     uint64_t compactions = 0;
@@ -1239,13 +1260,26 @@ bool ensure_chain_scratch(qcs_dev_state* st, int levels)
 }
 
 // One gate, fully stream-ordered.  rec_index < 0: no record.
+// load (x_ext != null): the strides [load_first, load_first + load_count)
+// are compressed from the caller's raw device planes x_ext (g unused).
 int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, int nl,
                  double theta, int64_t rec_index, uint64_t gate_index, uint64_t* n_slots_out,
-                 int renorm = 1, const double* given_mean = nullptr)
+                 int renorm = 1, const double* given_mean = nullptr, const double* x_ext = nullptr,
+                 uint64_t load_first = 0, uint64_t load_count = 0)
 {
     Dev& d = st->d;
     cudaStream_t s = st->stream;
-    const Plan p = make_plan(st, g);
+    static const qcs_gate_desc k_load_desc{KIND_LOAD, 0, -1, 0, 0, {1, 0, 0, 0, 0, 0, 1, 0}};
+    if (x_ext) g = &k_load_desc;
+    Plan p = x_ext ? Plan{} : make_plan(st, g);
+    if (x_ext) {
+        p.fixed = -1;
+        p.kind = KIND_LOAD;
+        p.c = -1;
+        p.local_ctl = -1;
+        p.n_units = load_count;
+        p.first = load_first;
+    }
     const uint64_t n_slots = p.pair ? 2 * p.n_units : p.n_units;
     *n_slots_out = n_slots;
     const uint64_t gen = ++st->gen;
@@ -1256,6 +1290,10 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     const bool real_gate = p.kind == 2 || (p.kind <= 1 && g->u[1] == 0.0 && g->u[3] == 0.0 && g->u[5] == 0.0 &&
                                            g->u[7] == 0.0);
     const bool imz = real_gate && st->imz;
+    // a complex gate (or reflect_mean, or a load) may fill im planes: cleared
+    // before the first wave commits, so a gate that fails part-way never
+    // leaves the flag claiming a real state
+    if (!real_gate) st->all_im_zero = false;
     k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen, st->lt, lad[0] > 0.0 ? 1 : 0, lad[0],
                                                             imz ? (st->all_im_zero ? 2 : 1) : 0);
     ++st->launches;
@@ -1282,12 +1320,10 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     const bool wide = n_slots < 148 && d.L >= 2 * FUSED_SPAN;
     const int fm = dg >= 0 ? (wide ? FM_RAW2_W : FM_RAW2) : (wide ? FM_LOCAL_W : FM_LOCAL);  // pairs always split
     if (dg >= 0) {
-        static bool dg_attr = false;
-        if (!dg_attr) {
-            CU(cudaFuncSetAttribute(k_decode_gate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DG_SMEM));
-            dg_attr = true;
-        }
+        if (const int rc = set_smem_attr(reinterpret_cast<const void*>(k_decode_gate), (int)DG_SMEM)) return rc;
+        if (const int rc = set_smem_attr(reinterpret_cast<const void*>(k_decode_gate_re), (int)DG_SMEM)) return rc;
     }
+    if (x_ext) dg = -1;
     GateParams gp;
     for (int i = 0; i < 8; ++i) gp.u[i] = g->u[i];
     // Serial-chain mode: lossy levels whose 2*delta is not a
@@ -1322,7 +1358,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         ++st->launches;
         chain_flag = &d.sc->chain_on;
     }
-    const int fm_lvl = chain ? (wide ? FM_RAW2_W : FM_RAW2) : fm;
+    const int fm_lvl = (chain || x_ext) ? (wide ? FM_RAW2_W : FM_RAW2) : fm;
     auto fused_args = [&](double delta, uint64_t s0) {
         FusedArgs a{};
         a.arena0 = d.arena[0];
@@ -1372,12 +1408,6 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             const bool re_only = imz && st->all_im_zero && dg != DG_IN && d.L >= DG_RE_CH &&
                                  (dg == DG_PAIR || (1ull << p.t) >= (uint64_t)DG_RE_CH);
             if (re_only) {
-                static bool attr = false;
-                if (!attr) {
-                    CU(cudaFuncSetAttribute(k_decode_gate_re, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)DG_SMEM));
-                    attr = true;
-                }
                 const uint64_t chunks_re = dg == DG_PAIR ? (d.L + DG_RE_CH - 1) / DG_RE_CH : d.L / (2 * DG_RE_CH);
                 k_decode_gate_re<<<(unsigned)(units * chunks_re), DG_R, DG_SMEM, s>>>(d, p, gp, dg, chunks_re, s0);
             } else {
@@ -1387,8 +1417,10 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             prof_stop(st);
             ++st->launches;
         }
+        // the wave's raw input planes: the caller's (load) or the scratch X
+        const double* xw = x_ext ? x_ext + s0 * 2 * d.L : d.X;
         if (chain) {
-            if (dg < 0) {  // in-chunk gate: decode + gate + snap into X only
+            if (dg < 0 && !x_ext) {  // in-chunk gate: decode + gate + snap into X only
                 FusedArgs a = fused_args(lad[0], s0);
                 a.dump_x = d.X;
                 prof_start(st, 0);
@@ -1399,7 +1431,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             }
             const uint64_t chains = 2 * nw * (uint64_t)chl.n;
             prof_start(st, 1);
-            k_serial_chain<<<(unsigned)((chains + 127) / 128), 128, 0, s>>>(d.X, 2 * nw, d.L, d.nsub, chl,
+            k_serial_chain<<<(unsigned)((chains + 127) / 128), 128, 0, s>>>(xw, 2 * nw, d.L, d.nsub, chl,
                                                                            st->chain_codes, st->chain_preds,
                                                                            d.pending, s0, chain_flag);
             prof_stop(st);
@@ -1408,9 +1440,9 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         for (int k = 0; k < nl; ++k) {
             FusedArgs a = fused_args(lad[k], s0);
             if (fm_lvl == FM_RAW2 || fm_lvl == FM_RAW2_W) {  // split path: gated, snapped planes in X
-                a.X = d.X;
+                a.X = xw;
                 a.x_plane_stride = d.L;
-                a.snap = 0;
+                a.snap = 0;  // gated planes were snapped; a load's, in place by k_snap
             }
             if (chain && lev_of[k] >= 0) {
                 a.pre_codes = st->chain_codes + (uint64_t)lev_of[k] * 2 * nw * d.L;
@@ -1444,7 +1476,12 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             const int rc = big_commit_wave(st, s0, s1, gate_index, u0);
             prof_stop(st);
             if (rc < 0) break;  // device error word set: k_norm records the gate
-            if (rc) return rc;
+            if (rc) {
+                // waves before this one are committed: the gate is part-applied
+                // (wave layout only, include/qcs_b200.h); refuse further use
+                if (u0 > 0) st->poisoned = true;
+                return rc;
+            }
         }
     }
     prof_start(st, 3);
@@ -1452,7 +1489,6 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     prof_stop(st);
     ++st->launches;
     CU(cudaGetLastError());
-    if (!real_gate) st->all_im_zero = false;  // a complex gate (or reflect_mean) may fill im planes
     return 0;
 }
 
@@ -1621,10 +1657,14 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     memcpy(&w, &one, 8);
     for (int i = 0; i < 8; ++i) hot.push_back((uint8_t)(w >> (8 * i)));
     if (d.L - off - 1) varint(hot, (d.L - off - 1) << 1);
-    std::vector<uint8_t> img(48, 0);
+    // arena image: the zero block at 0, the hot block at 16 (up to 27 bytes:
+    // two varints of up to 9 bytes around the tag and the word), the bump
+    // after it, 16-byte rounded
+    const uint64_t img_bytes = 16 + round16(hot.size());
+    std::vector<uint8_t> img(std::max<uint64_t>(img_bytes, 48), 0);
     memcpy(img.data(), zero.data(), zero.size());
     memcpy(img.data() + 16, hot.data(), hot.size());
-    if (!d.pool) CU(cudaMemcpy(d.arena[0], img.data(), 32 + 16, cudaMemcpyHostToDevice));
+    if (!d.pool) CU(cudaMemcpy(d.arena[0], img.data(), img_bytes, cudaMemcpyHostToDevice));
     std::vector<uint64_t> h_off(2 * d.NS, 0), h_len(2 * d.NS, zero.size());
     std::vector<int8_t> h_codec(2 * d.NS, 0);
     std::vector<double> h_delta(2 * d.NS, 0.0), h_scale(d.NS, 1.0), h_sum(d.NS, 0.0);
@@ -1652,8 +1692,8 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     CU(cudaMemcpy(d.scale, h_scale.data(), 8 * h_scale.size(), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(d.sum_sq, h_sum.data(), 8 * h_sum.size(), cudaMemcpyHostToDevice));
     Dev::Scal sc{};
-    sc.bump = 32;
-    st->bump = 32;
+    sc.bump = img_bytes;
+    st->bump = img_bytes;
     sc.cur = 0;
     sc.err_gate = -1;
     sc.norm_sq = zero_state ? 0.0 : 1.0;
@@ -1707,6 +1747,7 @@ int qcs_apply_gate_ex(qcs_dev_state_t st, const qcs_gate_desc* g, const double* 
 {
     if (!st || !g) return set_err(QCS_E_INVALID, "null argument");
     if ((flags & QCS_GIVEN_MEAN) && !mean) return set_err(QCS_E_INVALID, "null mean");
+    if (st->poisoned) return set_err(QCS_E_RUNTIME, "state unusable: an earlier gate failed part-way (wave layout)");
     int rc = validate_gate(st, g);
     if (rc) return rc;
     rc = validate_ladder(lad, nl, theta);
@@ -1734,6 +1775,7 @@ int qcs_run_program(qcs_dev_state_t st, const qcs_gate_desc* gates, uint64_t n_g
 {
     if (!st || (!gates && n_gates)) return set_err(QCS_E_INVALID, "null argument");
     if (n_done) *n_done = 0;
+    if (st->poisoned) return set_err(QCS_E_RUNTIME, "state unusable: an earlier gate failed part-way (wave layout)");
     int rc = validate_ladder(lad, nl, theta);
     if (rc) return rc;
     for (uint64_t i = 0; i < n_gates; ++i) {
@@ -1763,29 +1805,68 @@ int qcs_run_program(qcs_dev_state_t st, const qcs_gate_desc* gates, uint64_t n_g
     std::vector<cudaEvent_t> ev(n_gates + 1);
     for (auto& e : ev) cudaEventCreate(&e);
     cudaEventRecord(ev[0], st->stream);
+    uint64_t enq = 0;  // gates fully enqueued
     for (uint64_t i = 0; i < n_gates; ++i) {
         uint64_t ns;
         d.rec = rec;
         rc = enqueue_gate(st, &gates[i], lad, nl, theta, (int64_t)i, first_index + i, &ns);
         if (rc) break;
         cudaEventRecord(ev[i + 1], st->stream);
+        enq = i + 1;
     }
+    const std::string enq_err = rc ? g_err : std::string();
     int rc2 = sync_and_check(st);
     std::vector<qcs_gate_record> h(n_gates);
-    if (!rc && !rc2 && n_gates)
-        cudaMemcpy(h.data(), rec, n_gates * sizeof(qcs_gate_record), cudaMemcpyDeviceToHost);
-    uint64_t done = n_gates;
-    if (!rc && !rc2 && st->h_sc->err) done = (uint64_t)std::max(0, st->h_sc->err_gate - (int)first_index);
-    for (uint64_t i = 0; i < done && !rc && !rc2; ++i) {
+    if (!rc2 && enq)
+        cudaMemcpy(h.data(), rec, enq * sizeof(qcs_gate_record), cudaMemcpyDeviceToHost);
+    // gates before an enqueue failure (host-side, e.g. arena exhausted) ran:
+    // their records are returned and counted, like the reference's
+    // apply_program_range keeps the records of the gates before a throw
+    uint64_t done = enq;
+    if (!rc2 && st->h_sc->err) done = std::min<uint64_t>(done, (uint64_t)std::max(0, st->h_sc->err_gate - (int)first_index));
+    for (uint64_t i = 0; i < done && !rc2; ++i) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
         h[i].elapsed_ns = (uint64_t)((double)ms * 1e6);
         if (records) records[i] = h[i];
     }
     for (auto& e : ev) cudaEventDestroy(e);
-    if (rc) return rc;
     if (rc2) return rc2;
     if (n_done) *n_done = done;
+    if (st->h_sc->err) return report_device_error(st);
+    if (rc) {
+        g_err = enq_err;
+        return rc;
+    }
+    return 0;
+}
+
+// compress_stride_adaptive (aalc.cpp:117-138) of caller-provided device planes
+__global__ void k_snap_planes(double* x, uint64_t n)
+{
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        x[i] = snap(x[i]);
+}
+
+int qcs_load_strides_device(qcs_dev_state_t st, uint64_t first, uint64_t count, double* dev_planes,
+                            const double* lad, int nl, double theta)
+{
+    if (!st || (!dev_planes && count)) return set_err(QCS_E_INVALID, "null argument");
+    if (st->poisoned) return set_err(QCS_E_RUNTIME, "state unusable: an earlier gate failed part-way (wave layout)");
+    if (first > st->d.NS || count > st->d.NS - first) return set_err(QCS_E_RANGE, "stride range out of range");
+    int rc = validate_ladder(lad, nl, theta);
+    if (rc) return rc;
+    if (!count) return 0;
+    cudaSetDevice(st->device);
+    const uint64_t nel = count * 2 * st->d.L;
+    k_snap_planes<<<(unsigned)grid_for(nel), 256, 0, st->stream>>>(dev_planes, nel);
+    ++st->launches;
+    uint64_t ns = 0;
+    st->d.rec = nullptr;
+    rc = enqueue_gate(st, nullptr, lad, nl, theta, -1, 0, &ns, 0, nullptr, dev_planes, first, count);
+    if (rc) return rc;
+    rc = sync_and_check(st);
+    if (rc) return rc;
     if (st->h_sc->err) return report_device_error(st);
     return 0;
 }

@@ -83,6 +83,8 @@ def lib() -> C.CDLL:
         L.qcs_read_stride.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]
         L.qcs_read_strides_device.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p]
         L.qcs_to_amplitudes.argtypes = [C.c_void_p, C.c_void_p]
+        L.qcs_load_strides_device.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
+                                              C.POINTER(C.c_double), C.c_int, C.c_double]
         L.qcs_state_stats.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_double),
                                       C.POINTER(C.c_double)]
         L.qcs_stride_info.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_double),
@@ -326,6 +328,14 @@ class CompressedState:
         """Decode strides [first, first+count) into a device buffer (e.g. a
         torch.float64 CUDA tensor's data_ptr()) laid out [stride][re|im][L]."""
         _check(lib().qcs_read_strides_device(self._h, first, count, int(apply_scale), out_ptr))
+
+    def load_strides_device(self, first: int, count: int, planes_ptr: int, ladder: ErrorBoundLadder,
+                            theta: RatioThreshold = RatioThreshold()) -> None:
+        """Replace strides [first, first+count) by the compression of device
+        planes [stride][re|im][L] (snapped in place first, like
+        compress_stride_adaptive, aalc.cpp:117-138)."""
+        _check(lib().qcs_load_strides_device(self._h, first, count, planes_ptr, ladder.c_array(),
+                                             len(ladder.bounds), theta.theta))
 
     def to_amplitudes(self) -> np.ndarray:
         a = np.empty(2 * self._geom.n_amplitudes(), dtype=np.float64)
