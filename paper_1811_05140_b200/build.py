@@ -30,7 +30,8 @@ def needs_build() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or needs_build():
-        cmd = [NVCC] + FLAGS + ["-o", SO] + SOURCES
+        extra = ["-DQCS_WATCHDOG"] if os.environ.get("QCS_WATCHDOG") else []
+        cmd = [NVCC] + FLAGS + extra + ["-o", SO] + SOURCES
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)

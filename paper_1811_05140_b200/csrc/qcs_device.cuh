@@ -69,11 +69,32 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                  : "memory");
 }
 
+#ifdef QCS_WATCHDOG
+#include <cstdio>
+#define QCS_WD(cond, what)                                                                                  \
+    do {                                                                                                    \
+        if (cond) {                                                                                         \
+            printf("[qcs watchdog] %s block %d thread %d\n", what, (int)blockIdx.x, (int)threadIdx.x);     \
+            __trap();                                                                                       \
+        }                                                                                                   \
+    } while (0)
+#else
+#define QCS_WD(cond, what) \
+    do {                   \
+    } while (0)
+#endif
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity)
 {
     const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
     unsigned done = 0;
+#ifdef QCS_WATCHDOG
+    unsigned long long spins = 0;
+#endif
     while (!done) {
+#ifdef QCS_WATCHDOG
+        QCS_WD(++spins > (1ull << 28), "mbar_wait");
+#endif
         asm volatile(
             "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(done)

@@ -890,6 +890,8 @@ struct qcs_dev_state {
     // it off): codes/predictor scratch for `chain_levels` ladder levels
     int serial_chain = 1;
     int imz = 1;  // zero-imaginary-plane mode (QCS_IMZ=0 turns it off)
+    int diag_local = 1;  // diagonal far/pair gates in the fused kernel (QCS_DIAG_LOCAL=0: split path)
+    int debug_sync = 0;  // QCS_DEBUG_SYNC=1: synchronise and log after every kernel of a gate (debugging)
     bool all_im_zero = true;  // every im plane is zero (real state): real gates keep it
     int chain_levels = 0;
     int16_t* chain_codes = nullptr;
@@ -935,6 +937,13 @@ cudaEvent_t pool_event(qcs_dev_state* st)
     cudaEvent_t e;
     cudaEventCreate(&e);
     return e;
+}
+
+void dbg_sync(qcs_dev_state* st, const char* what)
+{
+    if (!st->debug_sync) return;
+    const cudaError_t e = cudaStreamSynchronize(st->stream);
+    fprintf(stderr, "[qcs] %s: %s\n", what, cudaGetErrorString(e));
 }
 
 void prof_start(qcs_dev_state* st, int cls)
@@ -1298,6 +1307,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
                                                             imz ? (st->all_im_zero ? 2 : 1) : 0);
     ++st->launches;
     prof_stop(st);
+    dbg_sync(st, "k_make_jobs");
     if (p.reflect && given_mean) {  // sharded run: mean combined across ranks
         k_set_mean<<<1, 1, 0, s>>>(d, given_mean[0], given_mean[1]);
         ++st->launches;
@@ -1311,7 +1321,14 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     // cross-chunk partners (pair units, in-stride targets >= 2^12): decode +
     // gate fully parallel into X, then the encoder reads X (split path)
     int dg = -1;
-    if (p.pair) dg = DG_PAIR;
+    // diagonal gates (u12 = u21 = 0: CP, CZ, Z, T, phase): every element is
+    // gated on its own (qcs_fused.cuh, FusedArgs::diag), so far partners and
+    // pair units need no partner data and stay in the fused in-chunk kernel;
+    // the plan, the joint pair ladder and the reports are unchanged
+    const bool diag = p.kind <= 1 && g->u[2] == 0.0 && g->u[3] == 0.0 && g->u[4] == 0.0 && g->u[5] == 0.0 &&
+                      st->diag_local && (p.pair || (1ull << p.t) >= FUSED_SPAN);
+    if (diag) dg = -1;
+    else if (p.pair) dg = DG_PAIR;
     else if (p.kind <= 1 && (1ull << p.t) >= FUSED_SPAN) dg = DG_FAR;
     // in-chunk partners take the split path too when asked (QCS_SPLIT_LOCAL)
     else if (p.kind <= 1 && st->split_local && (1ull << p.t) >= DG_HALF) dg = DG_FAR;
@@ -1373,6 +1390,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         a.job_stride = d.job_stride;
         for (int i = 0; i < 8; ++i) a.u[i] = g->u[i];
         a.kind = p.kind;
+        a.diag = diag ? (p.pair ? 2 : 1) : 0;
         a.t = p.t;
         a.local_ctl = p.local_ctl;
         a.flip_off = p.flip_off;
@@ -1416,6 +1434,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             }
             prof_stop(st);
             ++st->launches;
+            dbg_sync(st, "k_decode_gate");
         }
         // the wave's raw input planes: the caller's (load) or the scratch X
         const double* xw = x_ext ? x_ext + s0 * 2 * d.L : d.X;
@@ -1460,6 +1479,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             prof_stop(st);
             if (rc) return rc;
             ++st->launches;
+            dbg_sync(st, "k_fused");
             if (!st->big && k == nl - 1) {  // last level + commit in one kernel
                 prof_start(st, 3);
                 k_ladder_commit<<<(unsigned)((p.n_units + 127) / 128), 128, 0, s>>>(d, st->lt, p, lad[k], theta);
@@ -1488,6 +1508,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     k_norm<<<1, NORM_THREADS, 0, s>>>(d, n_slots, rec_index < 0 ? 0 : (uint64_t)rec_index, gate_index, renorm);
     prof_stop(st);
     ++st->launches;
+    dbg_sync(st, "k_norm");
     CU(cudaGetLastError());
     return 0;
 }
@@ -1538,6 +1559,8 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     if (const char* e = getenv("QCS_SPLIT_LOCAL")) st->split_local = atoi(e);
     if (const char* e = getenv("QCS_SERIAL_CHAIN")) st->serial_chain = atoi(e);
     if (const char* e = getenv("QCS_IMZ")) st->imz = atoi(e);
+    if (const char* e = getenv("QCS_DIAG_LOCAL")) st->diag_local = atoi(e);
+    if (const char* e = getenv("QCS_DEBUG_SYNC")) st->debug_sync = atoi(e);
     if (const char* e = getenv("QCS_MAX_ROUNDS")) st->max_rounds = std::max(1, atoi(e));
     cudaSetDevice(device);
     int rc = 0;

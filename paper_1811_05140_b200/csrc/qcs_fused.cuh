@@ -47,6 +47,7 @@ struct FusedSharedT {
     long long wmin[NT / 32];
     PlaneCarry carry[4];
     double s[2];  // exact running sum of squares per stride
+    double s_pre;  // fused_sumsq's serial prefix (not s[0]: every thread reads s[0] on entry)
     uint64_t bar[4];  // per-plane mbarrier of the payload bulk copy (MODE_LOCAL)
     uint8_t repaired[NT];  // lane's codes rewritten by a repair pass (resync chain)
 };
@@ -95,6 +96,10 @@ struct FusedArgs {
     // ---- gate ----
     double u[8];
     int kind;                     // GateKind
+    // diagonal gate (u12 = u21 = 0) on far partners, MODE_LOCAL: every element
+    // is gated on its own (0 = pairs inside the chunk; 1 = in-stride target,
+    // the side is bit t of the element; 2 = pair unit, the side is the slot's)
+    int diag;
     int t;                        // target (in-stride bit for LOCAL/FAR)
     int local_ctl;                // in-stride control bit, -1 none
     uint64_t flip_off;
@@ -268,23 +273,38 @@ __device__ __forceinline__ void fused_sumsq(double* xs, int n_it, FS& S, unsigne
     // (entered right after a CTA barrier: every step-4 branch ends with one)
     double s = S.s[0];  // uniform across the CTA from here on
     int k0 = 0;
+#ifdef QCS_WATCHDOG
+    if ((tid & 31) == 31 && !(s == 0.0) && n_it <= 512)
+        printf("[qcs watchdog] sumsq entry block %d tid %d s=%a n_it=%d imz=%d\n", (int)blockIdx.x, tid, s, n_it, (int)IMZ);
+#endif
     // While s is still 0 the next elements double it again and again (a binade
     // crossing, i.e. a parallel pass, per doubling): sum the first SERIAL_SUM
     // elements of a stride in the reference's order on one thread instead.
     constexpr int SERIAL_SUM = 512;
     if (s == 0.0) {
         const int m = min(n_it, SERIAL_SUM);
+        // (written to s_pre: a thread still to read s[0] on entry would see
+        // the prefix and skip this branch — a read-after-write race)
         if (tid == 0) {
             double acc = 0.0;
 #pragma unroll 4
             for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, tsq_g<LPL, IMZ>(xs, 0, k));
-            S.s[0] = acc;
+            S.s_pre = acc;
         }
         __syncthreads();
-        s = S.s[0];
+        s = S.s_pre;
         k0 = m;
     }
+#ifdef QCS_WATCHDOG
+    int wd_passes = 0;
+#endif
     while (k0 < n_it) {
+#ifdef QCS_WATCHDOG
+        if (++wd_passes > 100000 && (tid & 31) == 0)
+            printf("[qcs watchdog] fused_sumsq block %d tid %d s=%a k0=%d n_it=%d S.s0=%a imz=%d\n", (int)blockIdx.x, tid, s, k0, n_it,
+                   S.s[0], (int)IMZ);
+        if (wd_passes > 100000) __trap();
+#endif
         if (counters && tid == 0) atomicAdd(&counters[1], 1ull);
         long long mine = LLONG_MAX;  // this thread's event candidate
         const int state = s == 0.0 ? 1 : (ilogb(s) < -960 ? 2 : 3);
@@ -666,7 +686,26 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
             __syncthreads();
             // gate (run_plan_unit, gate.cpp:405-454)
             {  // MODE_LOCAL
-                if (a.kind <= 1) {
+                if (a.kind <= 1 && a.diag) {
+                    // A diagonal unitary's apply_pair (gate.cpp:153-162) adds the
+                    // partner's terms multiplied by exact zeros: for a non-zero
+                    // result they vanish exactly, a zero result is snapped to
+                    // +0.0 (core.cpp:39-47) whatever its sign -- so each side is
+                    // apply_pair with a zero partner, bit for bit after the snap
+                    const int fixed_side = a.diag == 2 ? (int)(gslot & 1) : -1;
+                    for (int i = tid; i < n_it; i += NPL * LPL) {
+                        const uint64_t gi = base + (uint64_t)i;
+                        if (a.local_ctl >= 0 && !((gi >> a.local_ctl) & 1)) continue;
+                        const int side = fixed_side >= 0 ? fixed_side : (int)((gi >> a.t) & 1);
+                        double& xr = xrow<LPL>(xs, 0, i);
+                        double xi_ = IMZ ? 0.0 : xrow<LPL>(xs, 1, i);
+                        double orr, oi;
+                        if (side == 0) pair_lo(m8, xr, xi_, 0.0, 0.0, orr, oi);
+                        else pair_hi(m8, 0.0, 0.0, xr, xi_, orr, oi);
+                        xr = orr;
+                        if (!IMZ) xrow<LPL>(xs, 1, i) = oi;
+                    }
+                } else if (a.kind <= 1) {
                     const uint64_t lo_mask = hb - 1;
                     for (int q = tid; q < n_it / 2; q += NPL * LPL) {
                         const int i0 = (int)((((uint64_t)q & ~lo_mask) << 1) | ((uint64_t)q & lo_mask));
@@ -991,6 +1030,7 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
         uint64_t mvmax = 0;
         for (int p = 0; p < NPL; ++p) mvmax = max(mvmax, S.carry[p].mv_bytes);
         if (tid == 0 && a.counters && mvmax) atomicAdd(&a.counters[2], (unsigned long long)mvmax);
+        QCS_WD(mvmax > (1ull << 32), "slide");
         for (uint64_t o = 0; o < mvmax; o += LPL * 8) {
             uint8_t tmp[8];
             const uint64_t src0 = C.out_pos + C.open_vmax + o + lane * 8;
