@@ -137,6 +137,8 @@ struct Dev {
     uint64_t* job_stride;  // [NS]
     uint8_t* pending;      // [NS]
     uint8_t* im_zero;      // [NS] per slot: output im plane provably zero (zero-imaginary-plane mode)
+    uint8_t* zero_slot;    // [NS] per slot: output stride provably all zero (zero-stride pass)
+    uint32_t* order;       // [NS] dense-first slot order within each wave (k_slot_order)
     int64_t* slot_of;      // [NS] generation<<32 | slot
     qcs_stride_report* reports;  // [NS]
     uint64_t* new_off;     // [2NS]
@@ -183,8 +185,19 @@ __device__ __forceinline__ SideEntry* side_of(const Dev& d, uint64_t g)
 
 __device__ __forceinline__ bool plane_is_zero(const Dev& d, uint64_t g);
 
+// zmode (zero-stride pass): 0 off; 1 a slot's output depends only on its own
+// stride (in-stride gates, flips, diagonal gates on pair units); 2 on both
+// strides of its pair unit.  A stride whose two planes are the one-token zero
+// encoding stays all zero under every gate but reflect_mean (apply_pair of
+// zeros gives signed zeros, snap_zeros makes them +0.0), so its encoder CTA
+// writes the zero encodings directly.
+__device__ __forceinline__ bool stride_is_zero(const Dev& d, uint64_t j)
+{
+    return plane_is_zero(d, 2 * j) && plane_is_zero(d, 2 * j + 1);
+}
+
 __global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen, LevelTag lt, int codec0, double delta0,
-                            int imz)
+                            int imz, int zmode)
 {
     if (blockIdx.x == 0 && threadIdx.x == 0) d.sc->gate_cin = 0;  // the commits accumulate it
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
@@ -204,6 +217,58 @@ __global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen, Level
             else
                 z = plane_is_zero(d, 2 * j + 1);
             d.im_zero[s] = z ? 1 : 0;
+        }
+        bool zs = false;
+        if (zmode == 1) zs = stride_is_zero(d, j);
+        else if (zmode == 2) zs = stride_is_zero(d, slot_stride(p, s & ~1ull)) && stride_is_zero(d, slot_stride(p, s | 1ull));
+        d.zero_slot[s] = zs ? 1 : 0;
+    }
+}
+
+// Dense-first order of the slots of every wave [w*W, (w+1)*W): the encoder
+// CTAs of all-zero strides finish at once, so putting the costly ones first
+// spreads them over the SMs instead of pairing them on half of them.  One CTA,
+// a stable partition per wave by a block scan of the zero flags.
+constexpr int ORDER_THREADS = 1024;
+__global__ void __launch_bounds__(ORDER_THREADS) k_slot_order(Dev d, uint64_t n_slots, uint64_t W)
+{
+    __shared__ uint32_t wsum[ORDER_THREADS / 32];
+    __shared__ uint32_t carry[2];
+    const int tid = threadIdx.x, wl = tid & 31, w = tid >> 5;
+    for (uint64_t w0 = 0; w0 < n_slots; w0 += W) {
+        const uint64_t w1 = umin64(n_slots, w0 + W);
+        // dense count of the wave first
+        uint32_t cnt = 0;
+        for (uint64_t s = w0 + tid; s < w1; s += ORDER_THREADS) cnt += d.zero_slot[s] ? 0u : 1u;
+        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (wl == 0) wsum[w] = cnt;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t t = 0;
+            for (int i = 0; i < ORDER_THREADS / 32; ++i) t += wsum[i];
+            carry[0] = 0;          // dense placed so far
+            carry[1] = t;          // zero slots start after the dense ones
+        }
+        __syncthreads();
+        for (uint64_t c0 = w0; c0 < w1; c0 += ORDER_THREADS) {
+            const uint64_t s = c0 + tid;
+            const bool dense = s < w1 && !d.zero_slot[s];
+            const bool zero = s < w1 && d.zero_slot[s];
+            const unsigned bd = __ballot_sync(0xffffffffu, dense), bz = __ballot_sync(0xffffffffu, zero);
+            if (wl == 0) wsum[w] = (uint32_t)__popc(bd) | ((uint32_t)__popc(bz) << 16);
+            __syncthreads();
+            uint32_t pd = 0, pz = 0, td = 0, tz = 0;
+            for (int i = 0; i < ORDER_THREADS / 32; ++i) {
+                const uint32_t v = wsum[i];
+                if (i < w) pd += v & 0xffffu, pz += v >> 16;
+                td += v & 0xffffu, tz += v >> 16;
+            }
+            const unsigned lt = (1u << wl) - 1u;
+            if (dense) d.order[w0 + carry[0] + pd + __popc(bd & lt)] = (uint32_t)s;
+            if (zero) d.order[w0 + carry[1] + pz + __popc(bz & lt)] = (uint32_t)s;
+            __syncthreads();
+            if (tid == 0) carry[0] += td, carry[1] += tz;
+            __syncthreads();
         }
     }
 }
@@ -288,12 +353,15 @@ constexpr int DG_HALF = 8 * DG_R;
 constexpr size_t DG_SMEM = sizeof(double) * DG_R * XS_STRIDE;
 
 __global__ void __launch_bounds__(DG_R) k_decode_gate(Dev d, Plan p, GateParams gp, int mode,
-                                                    uint64_t chunks, uint64_t slot_base, const uint8_t* imz)
+                                                    uint64_t chunks, uint64_t slot_base, const uint8_t* imz,
+                                                    const uint8_t* zs)
 {
     if (d.sc->err) return;
     extern __shared__ __align__(16) unsigned char dg_smem[];
     double* xs = reinterpret_cast<double*>(dg_smem);
     const uint64_t u = blockIdx.x / chunks, c = blockIdx.x % chunks;
+    // zero-stride pass: the encoder writes these slots without reading X
+    if (zs && zs[slot_base + (mode == DG_PAIR ? 2 * u : u)]) return;
     const int tid = threadIdx.x;
     const uint64_t L = d.L;
     const uint64_t hb = 1ull << (p.pair ? 0 : p.t);
@@ -399,12 +467,13 @@ __global__ void __launch_bounds__(DG_R) k_decode_gate(Dev d, Plan p, GateParams 
 constexpr int DG_RE_CH = 16 * DG_R;
 
 __global__ void __launch_bounds__(DG_R) k_decode_gate_re(Dev d, Plan p, GateParams gp, int mode, uint64_t chunks,
-                                                       uint64_t slot_base)
+                                                       uint64_t slot_base, const uint8_t* zs)
 {
     if (d.sc->err) return;
     extern __shared__ __align__(16) unsigned char dg_smem[];
     double* xs = reinterpret_cast<double*>(dg_smem);
     const uint64_t u = blockIdx.x / chunks, c = blockIdx.x % chunks;
+    if (zs && zs[slot_base + (mode == DG_PAIR ? 2 * u : u)]) return;  // zero-stride pass
     const int tid = threadIdx.x;
     const uint64_t L = d.L;
     const uint64_t hb = 1ull << (p.pair ? 0 : p.t);
@@ -891,6 +960,7 @@ struct qcs_dev_state {
     int serial_chain = 1;
     int imz = 1;  // zero-imaginary-plane mode (QCS_IMZ=0 turns it off)
     int diag_local = 1;  // diagonal far/pair gates in the fused kernel (QCS_DIAG_LOCAL=0: split path)
+    int zero_pass = 1;   // zero strides skip the codec (QCS_ZERO_PASS=0 turns it off)
     int debug_sync = 0;  // QCS_DEBUG_SYNC=1: synchronise and log after every kernel of a gate (debugging)
     bool all_im_zero = true;  // every im plane is zero (real state): real gates keep it
     int chain_levels = 0;
@@ -1303,9 +1373,16 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     // before the first wave commits, so a gate that fails part-way never
     // leaves the flag claiming a real state
     if (!real_gate) st->all_im_zero = false;
+    const bool diag_gate = p.kind <= 1 && g->u[2] == 0.0 && g->u[3] == 0.0 && g->u[4] == 0.0 && g->u[5] == 0.0;
+    const int zmode = !st->zero_pass || p.kind == KIND_LOAD || p.reflect ? 0 : (p.pair && !diag_gate ? 2 : 1);
     k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen, st->lt, lad[0] > 0.0 ? 1 : 0, lad[0],
-                                                            imz ? (st->all_im_zero ? 2 : 1) : 0);
+                                                            imz ? (st->all_im_zero ? 2 : 1) : 0, zmode);
     ++st->launches;
+    if (zmode) {
+        const uint64_t wslots = std::max<uint64_t>(1, st->wave / (p.pair ? 2 : 1)) * (p.pair ? 2 : 1);
+        k_slot_order<<<1, ORDER_THREADS, 0, s>>>(d, n_slots, wslots);
+        ++st->launches;
+    }
     prof_stop(st);
     dbg_sync(st, "k_make_jobs");
     if (p.reflect && given_mean) {  // sharded run: mean combined across ranks
@@ -1325,8 +1402,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     // gated on its own (qcs_fused.cuh, FusedArgs::diag), so far partners and
     // pair units need no partner data and stay in the fused in-chunk kernel;
     // the plan, the joint pair ladder and the reports are unchanged
-    const bool diag = p.kind <= 1 && g->u[2] == 0.0 && g->u[3] == 0.0 && g->u[4] == 0.0 && g->u[5] == 0.0 &&
-                      st->diag_local && (p.pair || (1ull << p.t) >= FUSED_SPAN);
+    const bool diag = diag_gate && st->diag_local && (p.pair || (1ull << p.t) >= FUSED_SPAN);
     if (diag) dg = -1;
     else if (p.pair) dg = DG_PAIR;
     else if (p.kind <= 1 && (1ull << p.t) >= FUSED_SPAN) dg = DG_FAR;
@@ -1411,6 +1487,8 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         a.cp = make_params(delta);
         a.counters = d.counters;
         a.im_zero = imz ? d.im_zero : nullptr;
+        a.zero_slot = zmode ? d.zero_slot : nullptr;
+        a.order = zmode ? d.order : nullptr;
         return a;
     };
     const uint64_t spu = p.pair ? 2 : 1;                        // slots per unit
@@ -1427,10 +1505,12 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
                                  (dg == DG_PAIR || (1ull << p.t) >= (uint64_t)DG_RE_CH);
             if (re_only) {
                 const uint64_t chunks_re = dg == DG_PAIR ? (d.L + DG_RE_CH - 1) / DG_RE_CH : d.L / (2 * DG_RE_CH);
-                k_decode_gate_re<<<(unsigned)(units * chunks_re), DG_R, DG_SMEM, s>>>(d, p, gp, dg, chunks_re, s0);
+                k_decode_gate_re<<<(unsigned)(units * chunks_re), DG_R, DG_SMEM, s>>>(d, p, gp, dg, chunks_re, s0,
+                                                                                      zmode ? d.zero_slot : nullptr);
             } else {
                 k_decode_gate<<<(unsigned)(units * chunks), DG_R, DG_SMEM, s>>>(d, p, gp, dg, chunks, s0,
-                                                                              imz ? d.im_zero : nullptr);
+                                                                              imz ? d.im_zero : nullptr,
+                                                                              zmode ? d.zero_slot : nullptr);
             }
             prof_stop(st);
             ++st->launches;
@@ -1560,6 +1640,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     if (const char* e = getenv("QCS_SERIAL_CHAIN")) st->serial_chain = atoi(e);
     if (const char* e = getenv("QCS_IMZ")) st->imz = atoi(e);
     if (const char* e = getenv("QCS_DIAG_LOCAL")) st->diag_local = atoi(e);
+    if (const char* e = getenv("QCS_ZERO_PASS")) st->zero_pass = atoi(e);
     if (const char* e = getenv("QCS_DEBUG_SYNC")) st->debug_sync = atoi(e);
     if (const char* e = getenv("QCS_MAX_ROUNDS")) st->max_rounds = std::max(1, atoi(e));
     cudaSetDevice(device);
@@ -1602,9 +1683,12 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
         d.arena[1] = d.arena[0];
     } else {
         const uint64_t per_slot = 16 * d.L + 2 * d.slot_cap + 2 * d.nsub * sizeof(SideEntry);
-        uint64_t w = d.NS < 2 ? 1 : std::min<uint64_t>(d.NS, 296);
+        // up to four encoder slots per SM per wave: the hardware backfills
+        // the SMs of all-zero strides (zero-stride pass) with the next
+        // costly ones; at most an eighth of the free memory (C3: 592 slots)
+        uint64_t w = d.NS < 2 ? 1 : std::min<uint64_t>(d.NS, 592);
         if (const char* e = getenv("QCS_WAVE_SLOTS")) w = std::max<uint64_t>(1, std::min<uint64_t>(d.NS, strtoull(e, nullptr, 10)));
-        while (w > 2 && w * per_slot > (12ull << 30)) w /= 2;
+        while (w > 2 && w * per_slot > std::max<uint64_t>(12ull << 30, free_b / 8)) w /= 2;
         w = std::max<uint64_t>(w, std::min<uint64_t>(d.NS, 2));  // a pair unit needs 2 slots
         if (w > 1 && (w & 1)) --w;  // whole pair units per wave
         st->wave = w;
@@ -1643,6 +1727,8 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     TRY(dalloc(st, &d.job_stride, d.NS));
     TRY(dalloc(st, &d.pending, d.NS));
     TRY(dalloc(st, &d.im_zero, d.NS));
+    TRY(dalloc(st, &d.zero_slot, d.NS));
+    TRY(dalloc(st, &d.order, d.NS));
     TRY(dalloc(st, &d.slot_of, d.NS));
     TRY(dalloc(st, &d.reports, d.NS));
     TRY(dalloc(st, &d.new_off, 2 * d.NS));

@@ -93,6 +93,10 @@ struct FusedArgs {
     // then encodes the re plane with all its lanes and writes the im plane's
     // one-token encoding directly (null = off)
     const uint8_t* im_zero;
+    // zero-stride pass: per global slot, 1 = the slot's output stride is all
+    // zero (k_make_jobs); the CTA writes both planes' zero encodings only
+    const uint8_t* zero_slot;
+    const uint32_t* order;        // [slot] CTA -> global slot within each launch (null = identity)
     // ---- gate ----
     double u[8];
     int kind;                     // GateKind
@@ -511,18 +515,51 @@ __device__ __forceinline__ double lane_chain(const CodecParams& cp, const double
         }                                                                    \
     } while (0)
 
+// An all-zero plane's encoding: one zero run of n elements (lossless
+// codec.cpp:129-145 / lossy :224-247 both emit a single run token); every
+// sub-chunk starts inside it with predictor 0.  Written by nt threads.
+template <bool LOSSY>
+__device__ __forceinline__ void write_zero_plane(const FusedArgs& a, uint64_t slot, uint64_t gslot, int comp, int tid,
+                                                 int nt)
+{
+    uint8_t* o;
+    SideEntry* sd;
+    if (a.pool) {
+        const uint64_t g = 2 * a.job_stride[gslot] + comp;
+        const int ls = (int)((a.p_off[g] / a.cap) & 1);
+        o = a.out + (2 * g + 1 - ls) * a.cap;
+        sd = a.side + (2 * g + 1 - ls) * a.nsub;
+    } else {
+        o = a.out + (2 * slot + comp) * a.cap;
+        sd = a.side + (2 * slot + comp) * a.nsub;
+    }
+    const uint64_t n = a.n;
+    const uint64_t tok = run_token(LOSSY, TY_Z, n);
+    if (tid == 0) {
+        put_varint(o, tok);
+        a.out_len[2 * gslot + comp] = (uint64_t)varint_len(tok);
+    }
+    const uint64_t nsub_n = (n + SUB - 1) / SUB;
+    for (uint64_t sc = tid; sc < nsub_n; sc += nt) {
+        SideEntry se;
+        se.off = 0;
+        se.skip = (uint32_t)(sc * SUB);
+        se.pred = 0.0;
+        sd[sc] = se;
+    }
+}
+
 // The encoder body.  IMZ (zero-imaginary-plane mode): NPL = 1 and the CTA's
 // LPL lanes all work on the re plane of a stride whose im plane is zero
 // before and after the gate; the im plane's encoding (one zero-run token) is
 // written directly.
 template <bool LOSSY, int NPL, int LPL, int MODE, bool IMZ>
-__device__ __forceinline__ void fused_body(const FusedArgs& a)
+__device__ __forceinline__ void fused_body(const FusedArgs& a, const int b)
 {
     unsigned long long ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long ph_t = clock64();
     constexpr int ITP = LPL * SUB;   // elements per plane per CTA iteration
     constexpr int WPL = LPL / 32;    // warps per plane
-    const int b = blockIdx.x;
     const int tid = threadIdx.x;
     const int pl = tid / LPL;
     const int lane = tid % LPL;
@@ -1180,46 +1217,31 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a)
         for (int i = 0; i < 8; ++i) a.cta_trace[8 * (a.slot_base + (uint64_t)b) + i] = ph_acc[i];
     if (lane == 0) a.out_len[2 * gslot + comp] = C.out_pos;
     if (a.sumsq && tid == 0) a.sumsq[gslot] = S.s[0];
-    if (IMZ) {
-        // the im plane: all zeros -> one zero run of n elements (lossless
-        // codec.cpp:129-145 / lossy :224-247 both emit a single run token);
-        // every sub-chunk starts inside it with predictor 0
-        uint8_t* out1;
-        SideEntry* side1;
-        if (a.pool) {
-            const uint64_t g1 = 2 * a.job_stride[gslot] + 1;
-            const int ls1 = (int)((a.p_off[g1] / a.cap) & 1);
-            out1 = a.out + (2 * g1 + 1 - ls1) * a.cap;
-            side1 = a.side + (2 * g1 + 1 - ls1) * a.nsub;
-        } else {
-            out1 = a.out + (2 * slot + 1) * a.cap;
-            side1 = a.side + (2 * slot + 1) * a.nsub;
-        }
-        const uint64_t tok = run_token(LOSSY, TY_Z, n);
-        if (tid == 0) {
-            put_varint(out1, tok);
-            a.out_len[2 * gslot + 1] = (uint64_t)varint_len(tok);
-        }
-        const uint64_t nsub_n = (n + SUB - 1) / SUB;
-        for (uint64_t sc = tid; sc < nsub_n; sc += NPL * LPL) {
-            SideEntry se;
-            se.off = 0;
-            se.skip = (uint32_t)(sc * SUB);
-            se.pred = 0.0;
-            side1[sc] = se;
-        }
-    }
+    if (IMZ) write_zero_plane<LOSSY>(a, slot, gslot, 1, tid, NPL * LPL);
 }
 
 template <bool LOSSY, int NPL, int LPL, int MODE>
 __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL > 128 ? 2 : 4))) k_fused(FusedArgs a)
 {
+    // the launch-local slot of this CTA: block order, or the dense-first
+    // permutation of the launch's slots (k_slot_order) so that all-zero
+    // strides do not pile the costly ones onto the same SMs
+    const int b = a.order ? (int)(a.order[a.slot_base + blockIdx.x] - a.slot_base) : (int)blockIdx.x;
+    const uint64_t gslot = a.slot_base + (uint64_t)b;
+    if (a.pending && !a.pending[gslot]) return;
+    // zero-stride pass: an all-zero output stride is its two zero encodings
+    // and a stored sum of squares of +0.0 (core.cpp:30-37 over zeros)
+    if (NPL == 2 && a.zero_slot && a.zero_slot[gslot]) {
+        for (int c = 0; c < 2; ++c) write_zero_plane<LOSSY>(a, (uint64_t)b, gslot, c, threadIdx.x, NPL * LPL);
+        if (a.sumsq && threadIdx.x == 0) a.sumsq[gslot] = 0.0;
+        return;
+    }
     // a stride whose im plane stays zero gets all of the CTA's lanes for its
     // re plane (same thread count and shared-memory layout)
-    if (NPL == 2 && a.im_zero && a.im_zero[a.slot_base + blockIdx.x])
-        fused_body<LOSSY, 1, NPL * LPL, MODE, true>(a);
+    if (NPL == 2 && a.im_zero && a.im_zero[gslot])
+        fused_body<LOSSY, 1, NPL * LPL, MODE, true>(a, b);
     else
-        fused_body<LOSSY, NPL, LPL, MODE, false>(a);
+        fused_body<LOSSY, NPL, LPL, MODE, false>(a, b);
 }
 
 // The reference chain of compress_lossy (codec.cpp:206-250) for bounds whose
