@@ -844,6 +844,7 @@ def run_c3(args, rank, world, local_rank):
         fid, maxerr = stage_fidelity(state, n, s, x, last_gate, dev)
     cbytes, min_stride, nsq = state._stats()
     arena, side_b, scratch_b = state.memory()
+    ctr = state.counters()
     # kernel shares of one more (untimed) step with every class timed
     state.profile(1)
     a, b = c3_step(n, g0, args.warmup + args.steps)
@@ -902,6 +903,7 @@ def run_c3(args, rank, world, local_rank):
             "min_stride_ratio": min_ratio, "final_state_ratio": (16 << n) / cbytes,
             "compressed_bytes": cbytes, "hbm_bytes": {"arena_in_use": arena, "side_index": side_b,
                                                       "scratch": scratch_b},
+            "layout": {"wave_slots": ctr["wave_slots"], "compactions": ctr["compactions"]},
             "bytes_per_amp_update": (cin + cout) / max(1, upd)}
     print(json.dumps(line))
     return 0

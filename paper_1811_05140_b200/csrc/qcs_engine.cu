@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -79,6 +80,10 @@ struct Plan {
 // Plan.kind of qcs_load_strides_device (not a GateKind): the units are the
 // strides [first, first + n_units), their input is the caller's raw planes
 constexpr int KIND_LOAD = 4;
+// Device error word value of a wave-layout gate whose next wave did not fit in
+// the arena: every later kernel is a no-op, the host compacts the arena and
+// re-enqueues the gate from that wave (internal, never returned).
+constexpr int QCS_SUSPEND = 99;
 
 __host__ __device__ inline uint64_t insert_bit(uint64_t j, int pos, int v)
 {
@@ -93,6 +98,8 @@ __host__ __device__ inline uint64_t unit_lo(const Plan& p, uint64_t u)
     for (int i = 0; i < p.npos; ++i) j = insert_bit(j, p.pos[i], p.val[i]);
     return j + p.first;
 }
+
+__host__ __device__ inline uint64_t round16d(uint64_t x) { return (x + 15) & ~uint64_t(15); }
 
 // job/slot s -> stride
 __host__ __device__ inline uint64_t slot_stride(const Plan& p, uint64_t s)
@@ -148,8 +155,9 @@ struct Dev {
         uint64_t bump;
         int cur;
         int mode;          // 0 append, 1 compact
-        int err;           // first error code
+        int err;           // first error code (QCS_SUSPEND: wave layout arena full, resumable)
         int err_gate;
+        uint64_t susp_unit;  // QCS_SUSPEND: first unit of the wave that did not fit
         uint64_t gen;
         double mean[2];
         double norm_sq;
@@ -197,9 +205,9 @@ __device__ __forceinline__ bool stride_is_zero(const Dev& d, uint64_t j)
 }
 
 __global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen, LevelTag lt, int codec0, double delta0,
-                            int imz, int zmode)
+                            int imz, int zmode, int resume)
 {
-    if (blockIdx.x == 0 && threadIdx.x == 0) d.sc->gate_cin = 0;  // the commits accumulate it
+    if (blockIdx.x == 0 && threadIdx.x == 0 && !resume) d.sc->gate_cin = 0;  // the commits accumulate it
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t j = slot_stride(p, s);
@@ -1157,6 +1165,7 @@ __global__ void k_set_mean(Dev d, double mr, double mi)
 // of aalc.cpp:395-408, one wave at a time).
 __global__ void __launch_bounds__(128) k_wave_commit(Dev d, LevelTag lt, uint64_t s0)
 {
+    if (d.sc->err) return;
     const uint64_t loc = blockIdx.x >> 1;
     const int c = (int)(blockIdx.x & 1);
     const uint64_t slot = s0 + loc;
@@ -1180,6 +1189,92 @@ __global__ void __launch_bounds__(128) k_wave_commit(Dev d, LevelTag lt, uint64_
             d.sum_sq[j] = d.slot_sum[slot];
             d.scale[j] = 1.0;
         }
+    }
+}
+
+// Wave layout, device-side placement of a wave's new blocks (no host round
+// trip): an exclusive scan of the 16-byte-rounded payload lengths of the wave's
+// 2*(s1-s0) planes, one bump of the arena for the whole wave, new_off for
+// k_wave_commit.  A wave that does not fit suspends the gate (QCS_SUSPEND,
+// the wave's first unit in susp_unit): its blocks stay where they are, every
+// later kernel is a no-op, and the host compacts the arena and resumes.
+constexpr int ALLOC_THREADS = 1024;
+__global__ void __launch_bounds__(ALLOC_THREADS) k_wave_alloc(Dev d, uint64_t s0, uint64_t m2, uint64_t unit0)
+{
+    __shared__ uint64_t wsum[ALLOC_THREADS / 32];
+    __shared__ uint64_t base_sh;
+    __shared__ int ok_sh;
+    if (d.sc->err) return;
+    const int tid = threadIdx.x, wl = tid & 31, w = tid >> 5;
+    uint64_t total = 0;
+    for (uint64_t c0 = 0; c0 < m2; c0 += ALLOC_THREADS) {
+        const uint64_t i = c0 + tid;
+        total += i < m2 ? round16d(d.slot_len[2 * s0 + i]) : 0;
+    }
+    for (int o = 16; o; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+    if (wl == 0) wsum[w] = total;
+    __syncthreads();
+    if (tid == 0) {
+        uint64_t t = 0;
+        for (int i = 0; i < ALLOC_THREADS / 32; ++i) t += wsum[i];
+        const uint64_t b = d.sc->bump;
+        ok_sh = b + t <= d.arena_cap;
+        base_sh = b;
+        if (ok_sh) {
+            d.sc->bump = b + t;
+        } else {
+            d.sc->err = QCS_SUSPEND;
+            d.sc->susp_unit = unit0;
+        }
+    }
+    __syncthreads();
+    if (!ok_sh) return;
+    uint64_t carry = base_sh;
+    for (uint64_t c0 = 0; c0 < m2; c0 += ALLOC_THREADS) {
+        const uint64_t i = c0 + tid;
+        const uint64_t v = i < m2 ? round16d(d.slot_len[2 * s0 + i]) : 0;
+        uint64_t inc = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (wl >= o) inc += u;
+        }
+        __syncthreads();
+        if (wl == 31) wsum[w] = inc;
+        __syncthreads();
+        uint64_t pre = 0, tot = 0;
+        for (int k = 0; k < ALLOC_THREADS / 32; ++k) {
+            if (k < w) pre += wsum[k];
+            tot += wsum[k];
+        }
+        if (i < m2) d.new_off[2 * s0 + i] = carry + pre + inc - v;
+        carry += tot;
+    }
+}
+
+// Wave layout, before a gate's first wave: when its new blocks (estimated as
+// 5/4 of the blocks it rewrites) would not fit behind the bump but would after
+// a compaction, suspend the gate at unit 0 -- the host compacts before any of
+// its waves is encoded (a wave that still does not fit suspends in k_wave_alloc).
+__global__ void __launch_bounds__(ALLOC_THREADS) k_precheck(Dev d, uint64_t n_slots)
+{
+    __shared__ unsigned long long need_sh, live_sh;
+    if (d.sc->err) return;
+    if (threadIdx.x == 0) need_sh = live_sh = 0;
+    __syncthreads();
+    unsigned long long need = 0, live = 0;
+    for (uint64_t s = threadIdx.x; s < n_slots; s += ALLOC_THREADS) {
+        const uint64_t j = d.job_stride[s];
+        need += round16d(d.p_len[2 * j]) + round16d(d.p_len[2 * j + 1]);
+    }
+    for (uint64_t g = threadIdx.x; g < 2 * d.NS; g += ALLOC_THREADS) live += round16d(d.p_len[g]);
+    atomicAdd(&need_sh, need);
+    atomicAdd(&live_sh, live);
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const uint64_t est = need_sh + need_sh / 4 + (1ull << 20);
+    if (d.sc->bump + est > d.arena_cap && live_sh + est <= d.arena_cap) {
+        d.sc->err = QCS_SUSPEND;
+        d.sc->susp_unit = 0;
     }
 }
 
@@ -1265,6 +1360,7 @@ int compact_arena(qcs_dev_state* st)
 // Reserve `need` arena bytes in wave mode (compacting when full).
 int big_reserve(qcs_dev_state* st, uint64_t need, uint64_t* at)
 {
+    st->bump = st->h_sc->bump;  // the device's bump is authoritative (k_wave_alloc); h_sc is fresh
     if (st->bump + need > st->d.arena_cap) {
         const int rc = compact_arena(st);
         if (rc) return rc;
@@ -1344,8 +1440,10 @@ bool ensure_chain_scratch(qcs_dev_state* st, int levels)
 int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, int nl,
                  double theta, int64_t rec_index, uint64_t gate_index, uint64_t* n_slots_out,
                  int renorm = 1, const double* given_mean = nullptr, const double* x_ext = nullptr,
-                 uint64_t load_first = 0, uint64_t load_count = 0)
+                 uint64_t load_first = 0, uint64_t load_count = 0, uint64_t first_unit = 0,
+                 bool precheck_done = false)
 {
+    const bool resume = first_unit > 0;  // wave layout: the gate's waves before first_unit are committed
     Dev& d = st->d;
     cudaStream_t s = st->stream;
     static const qcs_gate_desc k_load_desc{KIND_LOAD, 0, -1, 0, 0, {1, 0, 0, 0, 0, 0, 1, 0}};
@@ -1376,8 +1474,12 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     const bool diag_gate = p.kind <= 1 && g->u[2] == 0.0 && g->u[3] == 0.0 && g->u[4] == 0.0 && g->u[5] == 0.0;
     const int zmode = !st->zero_pass || p.kind == KIND_LOAD || p.reflect ? 0 : (p.pair && !diag_gate ? 2 : 1);
     k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen, st->lt, lad[0] > 0.0 ? 1 : 0, lad[0],
-                                                            imz ? (st->all_im_zero ? 2 : 1) : 0, zmode);
+                                                            imz ? (st->all_im_zero ? 2 : 1) : 0, zmode, resume ? 1 : 0);
     ++st->launches;
+    if (st->big && !resume && !precheck_done) {
+        k_precheck<<<1, ALLOC_THREADS, 0, s>>>(d, n_slots);
+        ++st->launches;
+    }
     if (zmode) {
         const uint64_t wslots = std::max<uint64_t>(1, st->wave / (p.pair ? 2 : 1)) * (p.pair ? 2 : 1);
         k_slot_order<<<1, ORDER_THREADS, 0, s>>>(d, n_slots, wslots);
@@ -1385,7 +1487,9 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     }
     prof_stop(st);
     dbg_sync(st, "k_make_jobs");
-    if (p.reflect && given_mean) {  // sharded run: mean combined across ranks
+    if (resume) {
+        // the mean of reflect_mean was taken before the first wave (aalc.cpp:270-295)
+    } else if (p.reflect && given_mean) {  // sharded run: mean combined across ranks
         k_set_mean<<<1, 1, 0, s>>>(d, given_mean[0], given_mean[1]);
         ++st->launches;
     } else if (p.reflect) {  // mean pass (aalc.cpp:270-295) needs every stride first
@@ -1446,9 +1550,11 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     // QCS_SERIAL_CHAIN=1: policy (default); 2: always the serial chain
     const int* chain_flag = nullptr;
     if (chain && st->serial_chain == 1) {
-        const unsigned long long thr = std::max<unsigned long long>(1, 2 * d.NS * d.nsub / 16);
-        k_chain_policy<<<1, 1, 0, s>>>(d, thr);
-        ++st->launches;
+        if (!resume) {  // a resumed gate keeps the choice it started with
+            const unsigned long long thr = std::max<unsigned long long>(1, 2 * d.NS * d.nsub / 16);
+            k_chain_policy<<<1, 1, 0, s>>>(d, thr);
+            ++st->launches;
+        }
         chain_flag = &d.sc->chain_on;
     }
     const int fm_lvl = (chain || x_ext) ? (wide ? FM_RAW2_W : FM_RAW2) : fm;
@@ -1487,13 +1593,14 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         a.cp = make_params(delta);
         a.counters = d.counters;
         a.im_zero = imz ? d.im_zero : nullptr;
+        a.err = &d.sc->err;
         a.zero_slot = zmode ? d.zero_slot : nullptr;
         a.order = zmode ? d.order : nullptr;
         return a;
     };
     const uint64_t spu = p.pair ? 2 : 1;                        // slots per unit
     const uint64_t wave_units = std::max<uint64_t>(1, st->wave / spu);
-    for (uint64_t u0 = 0; u0 < p.n_units; u0 += wave_units) {
+    for (uint64_t u0 = first_unit; u0 < p.n_units; u0 += wave_units) {
         const uint64_t u1 = std::min<uint64_t>(p.n_units, u0 + wave_units);
         const uint64_t s0 = u0 * spu, s1 = u1 * spu, nw = s1 - s0;
         if (dg >= 0) {
@@ -1532,7 +1639,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             prof_start(st, 1);
             k_serial_chain<<<(unsigned)((chains + 127) / 128), 128, 0, s>>>(xw, 2 * nw, d.L, d.nsub, chl,
                                                                            st->chain_codes, st->chain_preds,
-                                                                           d.pending, s0, chain_flag);
+                                                                           d.pending, s0, chain_flag, &d.sc->err);
             prof_stop(st);
             ++st->launches;
         }
@@ -1571,17 +1678,12 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             }
             ++st->launches;
         }
-        if (st->big) {
+        if (st->big) {  // place (device bump) and install the wave: no host round trip
             prof_start(st, 3);
-            const int rc = big_commit_wave(st, s0, s1, gate_index, u0);
+            k_wave_alloc<<<1, ALLOC_THREADS, 0, s>>>(d, s0, 2 * nw, u0);
+            k_wave_commit<<<(unsigned)(2 * nw), 128, 0, s>>>(d, st->lt, s0);
             prof_stop(st);
-            if (rc < 0) break;  // device error word set: k_norm records the gate
-            if (rc) {
-                // waves before this one are committed: the gate is part-applied
-                // (wave layout only, include/qcs_b200.h); refuse further use
-                if (u0 > 0) st->poisoned = true;
-                return rc;
-            }
+            st->launches += 2;
         }
     }
     prof_start(st, 3);
@@ -1843,6 +1945,31 @@ static int report_device_error(qcs_dev_state* st)
     return set_err(QCS_E_RUNTIME, "gate %d failed: device codec error %d", gi, e);
 }
 
+// Wave layout: a synchronisation found QCS_SUSPEND (the wave starting at
+// *unit of gate *gate did not fit in the arena).  Compact the arena and clear
+// the error word so the gate can be re-enqueued from that wave.  `prev_*` is
+// the previous suspension point: suspending at the same point again right
+// after a compaction means the live state itself does not fit — a true
+// out-of-memory (the gate is part-applied if its first wave was committed).
+static int handle_suspend(qcs_dev_state* st, int64_t* gate, uint64_t* unit, int64_t prev_gate, uint64_t prev_unit)
+{
+    *gate = st->h_sc->err_gate;
+    *unit = st->h_sc->susp_unit;
+    Dev::Scal sc = *st->h_sc;
+    sc.err = 0;
+    sc.err_gate = -1;
+    sc.susp_unit = 0;
+    CU(cudaMemcpy(st->d.sc, &sc, sizeof sc, cudaMemcpyHostToDevice));
+    *st->h_sc = sc;
+    if (*gate == prev_gate && *unit == prev_unit) {
+        if (*unit > 0) st->poisoned = true;
+        return set_err(QCS_E_NOMEM, *unit ? "gate %lld failed: block arena exhausted after %llu of its units were committed"
+                                          : "gate %lld failed: block arena exhausted",
+                       (long long)*gate, (unsigned long long)*unit);
+    }
+    return compact_arena(st);
+}
+
 int qcs_apply_gate(qcs_dev_state_t st, const qcs_gate_desc* g, const double* lad, int nl,
                    double theta, qcs_stride_report* reports, uint64_t* n_reports,
                    double* norm_after)
@@ -1864,11 +1991,20 @@ int qcs_apply_gate_ex(qcs_dev_state_t st, const qcs_gate_desc* g, const double* 
     cudaSetDevice(st->device);
     uint64_t ns = 0;
     st->d.rec = nullptr;
-    rc = enqueue_gate(st, g, lad, nl, theta, -1, 0, &ns, (flags & QCS_NO_RENORM) ? 0 : 1,
-                      (flags & QCS_GIVEN_MEAN) ? mean : nullptr);
-    if (rc) return rc;
-    rc = sync_and_check(st);
-    if (rc) return rc;
+    int64_t pg = -2;
+    uint64_t pu = 0, unit = 0;
+    for (;;) {
+        rc = enqueue_gate(st, g, lad, nl, theta, -1, 0, &ns, (flags & QCS_NO_RENORM) ? 0 : 1,
+                          (flags & QCS_GIVEN_MEAN) ? mean : nullptr, nullptr, 0, 0, unit, pg != -2);
+        if (rc) return rc;
+        rc = sync_and_check(st);
+        if (rc) return rc;
+        if (st->h_sc->err != QCS_SUSPEND) break;
+        int64_t gi;
+        rc = handle_suspend(st, &gi, &unit, pg, pu);
+        if (rc) return rc;
+        pg = gi, pu = unit;
+    }
     if (st->h_sc->err) return report_device_error(st);
     if (reports && ns) {
         CU(cudaMemcpy(reports, st->d.reports, ns * sizeof(qcs_stride_report), cudaMemcpyDeviceToHost));
@@ -1913,35 +2049,79 @@ int qcs_run_program(qcs_dev_state_t st, const qcs_gate_desc* gates, uint64_t n_g
     qcs_gate_record* rec = d.rec;
     std::vector<cudaEvent_t> ev(n_gates + 1);
     for (auto& e : ev) cudaEventCreate(&e);
-    cudaEventRecord(ev[0], st->stream);
-    uint64_t enq = 0;  // gates fully enqueued
-    for (uint64_t i = 0; i < n_gates; ++i) {
-        uint64_t ns;
-        d.rec = rec;
-        rc = enqueue_gate(st, &gates[i], lad, nl, theta, (int64_t)i, first_index + i, &ns);
-        if (rc) break;
-        cudaEventRecord(ev[i + 1], st->stream);
-        enq = i + 1;
+    std::vector<double> el_ns(n_gates, 0.0);
+    // Passes: gates [i0, n) are queued back to back with one synchronisation
+    // at the end.  In the wave layout a pass can suspend inside gate k when the
+    // arena is full (QCS_SUSPEND): the arena is compacted and the next pass
+    // resumes gate k from the wave that did not fit (no host round trip per
+    // wave otherwise).
+    uint64_t i0 = 0, unit0 = 0, done = 0;
+    int64_t pg = -2;
+    uint64_t pu = 0;
+    int rc2 = 0;
+    std::string enq_err;
+    for (;;) {
+        uint64_t enq = i0;  // gates fully enqueued
+        cudaEventRecord(ev[i0], st->stream);
+        for (uint64_t i = i0; i < n_gates; ++i) {
+            uint64_t ns;
+            d.rec = rec;
+            rc = enqueue_gate(st, &gates[i], lad, nl, theta, (int64_t)i, first_index + i, &ns, 1, nullptr, nullptr, 0, 0,
+                              i == i0 ? unit0 : 0, i == i0 && pg >= 0);
+            if (rc) break;
+            cudaEventRecord(ev[i + 1], st->stream);
+            enq = i + 1;
+        }
+        if (rc) enq_err = g_err;
+        rc2 = sync_and_check(st);
+        if (rc2) break;
+        uint64_t ran = enq;  // gates whose kernels did their work in this pass
+        const bool susp = st->h_sc->err == QCS_SUSPEND;
+        if (st->h_sc->err) ran = std::min<uint64_t>(ran, (uint64_t)std::max<int64_t>(0, (int64_t)st->h_sc->err_gate - (int64_t)first_index) + (susp ? 1 : 0));
+        for (uint64_t i = i0; i < ran; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            el_ns[i] += (double)ms * 1e6;
+        }
+        if (!susp || rc) {
+            done = susp ? ran - 1 : ran;
+            if (susp) {  // an enqueue error after a suspension: no resume
+                if (st->h_sc->susp_unit > 0) st->poisoned = true;
+                Dev::Scal sc = *st->h_sc;
+                sc.err = 0;
+                sc.err_gate = -1;
+                CU(cudaMemcpy(d.sc, &sc, sizeof sc, cudaMemcpyHostToDevice));
+                *st->h_sc = sc;
+            }
+            break;
+        }
+        int64_t gk;
+        uint64_t uk;
+        // the compaction is part of the suspended gate's device time
+        cudaEventRecord(ev[n_gates], st->stream);
+        const auto h0 = std::chrono::steady_clock::now();
+        rc2 = handle_suspend(st, &gk, &uk, pg, pu);
+        const double comp_ns = (double)std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - h0).count();
+        if (rc2) {
+            done = (uint64_t)(gk - (int64_t)first_index);
+            break;
+        }
+        el_ns[(uint64_t)(gk - (int64_t)first_index)] += comp_ns;
+        pg = gk, pu = uk;
+        i0 = (uint64_t)(gk - (int64_t)first_index);
+        unit0 = uk;
     }
-    const std::string enq_err = rc ? g_err : std::string();
-    int rc2 = sync_and_check(st);
-    std::vector<qcs_gate_record> h(n_gates);
-    if (!rc2 && enq)
-        cudaMemcpy(h.data(), rec, enq * sizeof(qcs_gate_record), cudaMemcpyDeviceToHost);
-    // gates before an enqueue failure (host-side, e.g. arena exhausted) ran:
-    // their records are returned and counted, like the reference's
-    // apply_program_range keeps the records of the gates before a throw
-    uint64_t done = enq;
-    if (!rc2 && st->h_sc->err) done = std::min<uint64_t>(done, (uint64_t)std::max(0, st->h_sc->err_gate - (int)first_index));
-    for (uint64_t i = 0; i < done && !rc2; ++i) {
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
-        h[i].elapsed_ns = (uint64_t)((double)ms * 1e6);
-        if (records) records[i] = h[i];
+    if (done) {
+        std::vector<qcs_gate_record> h(done);
+        cudaMemcpy(h.data(), rec, done * sizeof(qcs_gate_record), cudaMemcpyDeviceToHost);
+        for (uint64_t i = 0; i < done; ++i) {
+            h[i].elapsed_ns = (uint64_t)el_ns[i];
+            if (records) records[i] = h[i];
+        }
     }
     for (auto& e : ev) cudaEventDestroy(e);
-    if (rc2) return rc2;
     if (n_done) *n_done = done;
+    if (rc2) return rc2;
     if (st->h_sc->err) return report_device_error(st);
     if (rc) {
         g_err = enq_err;
@@ -1972,10 +2152,19 @@ int qcs_load_strides_device(qcs_dev_state_t st, uint64_t first, uint64_t count, 
     ++st->launches;
     uint64_t ns = 0;
     st->d.rec = nullptr;
-    rc = enqueue_gate(st, nullptr, lad, nl, theta, -1, 0, &ns, 0, nullptr, dev_planes, first, count);
-    if (rc) return rc;
-    rc = sync_and_check(st);
-    if (rc) return rc;
+    int64_t pg = -2;
+    uint64_t pu = 0, unit = 0;
+    for (;;) {
+        rc = enqueue_gate(st, nullptr, lad, nl, theta, -1, 0, &ns, 0, nullptr, dev_planes, first, count, unit, pg != -2);
+        if (rc) return rc;
+        rc = sync_and_check(st);
+        if (rc) return rc;
+        if (st->h_sc->err != QCS_SUSPEND) break;
+        int64_t gi;
+        rc = handle_suspend(st, &gi, &unit, pg, pu);
+        if (rc) return rc;
+        pg = gi, pu = unit;
+    }
     if (st->h_sc->err) return report_device_error(st);
     return 0;
 }
@@ -2578,7 +2767,7 @@ int qcs_codec_compress(const double* x, uint64_t n, double delta, uint8_t* out, 
             chl.td[0] = a.cp.td;
             chl.inv[0] = 1.0 / a.cp.td;
             chl.lim[0] = a.cp.lim;
-            k_serial_chain<<<1, 128, 0, s>>>(dx, 1, n, nsub, chl, dcodes, dpreds, nullptr, 0, nullptr);
+            k_serial_chain<<<1, 128, 0, s>>>(dx, 1, n, nsub, chl, dcodes, dpreds, nullptr, 0, nullptr, nullptr);
             a.pre_codes = dcodes;
             a.pre_pred = dpreds;
         }

@@ -97,6 +97,7 @@ struct FusedArgs {
     // zero (k_make_jobs); the CTA writes both planes' zero encodings only
     const uint8_t* zero_slot;
     const uint32_t* order;        // [slot] CTA -> global slot within each launch (null = identity)
+    const int* err;               // device error word (non-zero: the gate failed or is suspended; no-op)
     // ---- gate ----
     double u[8];
     int kind;                     // GateKind
@@ -1226,6 +1227,7 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL >
     // the launch-local slot of this CTA: block order, or the dense-first
     // permutation of the launch's slots (k_slot_order) so that all-zero
     // strides do not pile the costly ones onto the same SMs
+    if (a.err && *a.err) return;
     const int b = a.order ? (int)(a.order[a.slot_base + blockIdx.x] - a.slot_base) : (int)blockIdx.x;
     const uint64_t gslot = a.slot_base + (uint64_t)b;
     if (a.pending && !a.pending[gslot]) return;
@@ -1270,9 +1272,9 @@ __device__ __noinline__ double chain_div(double diff, double td) { return __ddiv
 __global__ void __launch_bounds__(128) k_serial_chain(const double* __restrict__ x, uint64_t rows, uint64_t n,
                                                       uint64_t nsub, ChainLevels lv, int16_t* __restrict__ codes,
                                                       double* __restrict__ preds, const uint8_t* pending,
-                                                      uint64_t slot_base, const int* on)
+                                                      uint64_t slot_base, const int* on, const int* err)
 {
-    if (on && !*on) return;
+    if ((on && !*on) || (err && *err)) return;
     const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= rows * (uint64_t)lv.n) return;
     const int lev = (int)(c / rows);

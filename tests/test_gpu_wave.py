@@ -83,3 +83,18 @@ def test_wave_layout_compacts_and_reports_nomem(oracle, wave_env):
     with pytest.raises(RuntimeError) as ei:
         gpu_run(prog, 4, 3, lad, 1.0)
     assert "block arena exhausted" in str(ei.value)
+
+
+def test_wave_layout_hot_block_beyond_16_bytes(oracle, wave_env):
+    """Basis state whose hot block is longer than 16 bytes (stride bits 22,
+    in-stride offset 2^21: two 4-byte varints around the word) in a stride of
+    a later wave: the first wave's blocks must be placed after it."""
+    n, s = 24, 22
+    basis = 3 * (1 << s) + (1 << 21)
+    prog = cc.CircuitProgram(n, [cc.GateOp.single(cc.Unitary2x2.hadamard(), 0, "h 0"),
+                                 cc.GateOp.single(cc.Unitary2x2.hadamard(), 23, "h 23")], "hot")
+    wave_env(2, 1 << 28)
+    st, want = oracle_run(oracle, prog, s, basis, [2.0 ** -20], 1.0)
+    res, got = gpu_run(prog, s, basis, [2.0 ** -20], 1.0)
+    assert got == want, first_diff(want, got)
+    assert res.state.to_amplitudes().tobytes() == st.amplitudes().tobytes()
