@@ -518,3 +518,108 @@ def stage_tables(n: int, s: int, m: int, r, zmask: int, zval: int):
     hi_re, hi_im = table(s, NS)
     amp = math.ldexp(math.sqrt(0.5) if m & 1 else 1.0, -(m // 2))
     return dict(lo_re=lo_re, lo_im=lo_im, hi_re=hi_re, hi_im=hi_im, amp=amp, zmask=zmask, zval=zval)
+
+
+class _MT19937_64:
+    """std::mt19937_64 (the standard's parameters), for build_random."""
+
+    def __init__(self, seed: int):
+        self.mt = [0] * 312
+        self.mt[0] = seed & 0xFFFFFFFFFFFFFFFF
+        for i in range(1, 312):
+            prev = self.mt[i - 1]
+            self.mt[i] = (6364136223846793005 * (prev ^ (prev >> 62)) + i) & 0xFFFFFFFFFFFFFFFF
+        self.i = 312
+
+    def __call__(self) -> int:
+        if self.i >= 312:
+            mt = self.mt
+            for k in range(312):
+                y = (mt[k] & 0xFFFFFFFF80000000) | (mt[(k + 1) % 312] & 0x7FFFFFFF)
+                v = mt[(k + 156) % 312] ^ (y >> 1)
+                if y & 1:
+                    v ^= 0xB5026F5AA96619E9
+                mt[k] = v
+            self.i = 0
+        y = self.mt[self.i]
+        self.i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & 0xFFFFFFFFFFFFFFFF
+
+
+def _uniform_int(rng, a: int, b: int) -> int:
+    """libstdc++ uniform_int_distribution over a 64-bit engine (GCC >= 11:
+    Lemire's nearly divisionless method with a 128-bit product)."""
+    urange = (b - a) & 0xFFFFFFFFFFFFFFFF
+    if urange == 0xFFFFFFFFFFFFFFFF:
+        return a + rng()
+    uerange = urange + 1
+    product = rng() * uerange
+    low = product & 0xFFFFFFFFFFFFFFFF
+    if low < uerange:
+        threshold = ((1 << 64) - uerange) % uerange
+        while low < threshold:
+            product = rng() * uerange
+            low = product & 0xFFFFFFFFFFFFFFFF
+    return a + (product >> 64)
+
+
+def _uniform_real(rng, a: float, b: float) -> float:
+    """libstdc++ uniform_real_distribution: generate_canonical<double, 53> over a
+    64-bit engine (one draw / 2^64, clamped below 1), then x * (b - a) + a."""
+    r = float(rng()) / 18446744073709551616.0
+    if r >= 1.0:
+        r = math.nextafter(1.0, 0.0)
+    return r * (b - a) + a
+
+
+def build_random(n: int, gate_count: int, seed: int) -> CircuitProgram:
+    """circuit.cpp:327-387, draw for draw: std::mt19937_64(seed), angles
+    uniform in [0, 2 pi), qubits uniform in [0, n-1], kind uniform in [0, 9]."""
+    if n < 1:
+        raise ValueError("random circuit needs at least one qubit")
+    if gate_count < 0:
+        raise ValueError("gate count must be non-negative")
+    p = CircuitProgram(n, [], f"random-{n}")
+    rng = _MT19937_64(seed)
+    angle = lambda: _uniform_real(rng, 0.0, 2.0 * _PI)  # noqa: E731
+    qubit = lambda: _uniform_int(rng, 0, n - 1)  # noqa: E731
+
+    def random_unitary():
+        th = angle() / 2.0
+        p1 = angle()
+        p2 = angle()
+        c, s = math.cos(th), math.sin(th)
+        return Unitary2x2(complex(c * math.cos(p1), c * math.sin(p1)),
+                          complex(s * math.cos(p2), s * math.sin(p2)),
+                          complex(-s * math.cos(-p2), -s * math.sin(-p2)),
+                          complex(c * math.cos(-p1), c * math.sin(-p1)))
+
+    for i in range(gate_count):
+        kind = _uniform_int(rng, 0, 9)
+        if kind < 4:
+            # GCC evaluates GateOp::single(random_unitary(), qubit(rng), ...)'s
+            # arguments right to left: the target is drawn first
+            t = qubit()
+            p.gates.append(GateOp.single(random_unitary(), t, f"u {i}"))
+        elif kind < 6 and n >= 2:
+            c = qubit()
+            t = qubit()
+            while t == c:
+                t = qubit()
+            p.gates.append(GateOp.controlled(Unitary2x2.pauli_x(), c, t, f"cx {c} {t}"))
+        elif kind < 8 and n >= 2:
+            c = qubit()
+            t = qubit()
+            while t == c:
+                t = qubit()
+            p.gates.append(GateOp.controlled_phase(angle(), c, t, f"cp {c} {t}"))
+        elif kind == 8:
+            p.gates.append(GateOp.phase_flip(_uniform_int(rng, 0, (1 << n) - 1)))
+        else:
+            q = qubit()
+            p.gates.append(GateOp.single(Unitary2x2.hadamard(), q, f"h {q}"))
+    return p

@@ -93,3 +93,59 @@ def strip_elapsed(csv: str) -> str:
         f = line.split(",")
         lines.append(",".join(f[:8] + f[9:]))
     return "\n".join(lines) + "\n"
+
+
+def qubit_gain(min_ratio: float) -> int:
+    """floor(log2(min_ratio)) settled by comparison (core.cpp:72-82)."""
+    if not (min_ratio >= 1.0):
+        raise ValueError("qubit_gain: ratio must be >= 1")
+    k = int(math.floor(math.log2(min_ratio))) if math.isfinite(min_ratio) else 1023
+    while k > 0 and math.ldexp(1.0, k) > min_ratio:
+        k -= 1
+    while math.ldexp(1.0, k + 1) <= min_ratio:
+        k += 1
+    return k
+
+
+@dataclass
+class RunSummary:
+    overall_min_ratio: float = 0.0
+    qubit_gain: int = 0
+    total_elapsed_ns: int = 0
+    reference_elapsed_ns: Optional[int] = None
+    overhead_factor: Optional[float] = None
+    fidelity: Optional[float] = None
+    threshold_violations: int = 0
+
+
+def summarize_run(m: RunMetrics, fidelity: Optional[float] = None,
+                  reference_elapsed_ns: Optional[int] = None) -> RunSummary:
+    """summarize_run / summarize (metrics.cpp:32-90)."""
+    s = RunSummary(fidelity=fidelity, reference_elapsed_ns=reference_elapsed_ns,
+                   threshold_violations=m.threshold_violations)
+    if not m.records:
+        s.overall_min_ratio = m.init_min_ratio
+    else:
+        s.overall_min_ratio = min(r.min_ratio for r in m.records)
+        if m.init_min_ratio:
+            s.overall_min_ratio = min(s.overall_min_ratio, m.init_min_ratio)
+    s.qubit_gain = qubit_gain(s.overall_min_ratio) if s.overall_min_ratio >= 1.0 else 0
+    s.total_elapsed_ns = m.total_elapsed_ns
+    if reference_elapsed_ns:
+        s.overhead_factor = s.total_elapsed_ns / reference_elapsed_ns
+    return s
+
+
+def emit_summary_json(s: RunSummary) -> str:
+    """emit_summary_json (metrics.cpp:123-140): keys sorted (nlohmann's object
+    is a std::map), two-space indent, absent optionals omitted."""
+    import json
+    d = {"overall_min_ratio": s.overall_min_ratio, "qubit_gain": s.qubit_gain,
+         "total_elapsed_ns": s.total_elapsed_ns, "threshold_violations": s.threshold_violations}
+    if s.reference_elapsed_ns is not None:
+        d["reference_elapsed_ns"] = s.reference_elapsed_ns
+    if s.overhead_factor is not None:
+        d["overhead_factor"] = s.overhead_factor
+    if s.fidelity is not None:
+        d["fidelity"] = s.fidelity
+    return json.dumps(d, indent=2, sort_keys=True) + "\n"
