@@ -969,6 +969,7 @@ struct qcs_dev_state {
     int imz = 1;  // zero-imaginary-plane mode (QCS_IMZ=0 turns it off)
     int diag_local = 1;  // diagonal far/pair gates in the fused kernel (QCS_DIAG_LOCAL=0: split path)
     int zero_pass = 1;   // zero strides skip the codec (QCS_ZERO_PASS=0 turns it off)
+    int ladder_exit = 1; // ladder levels give up at the byte budget (QCS_LADDER_EXIT=0 turns it off)
     int debug_sync = 0;  // QCS_DEBUG_SYNC=1: synchronise and log after every kernel of a gate (debugging)
     bool all_im_zero = true;  // every im plane is zero (real state): real gates keep it
     int chain_levels = 0;
@@ -1655,6 +1656,8 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
                 a.pre_pred = st->chain_preds + (uint64_t)lev_of[k] * 2 * nw * d.nsub;
                 a.chain_on = chain_flag;
             }
+            // early exit of levels that cannot reach theta (all but the last)
+            a.ladder_theta = (k < nl - 1 && st->ladder_exit) ? theta : 0.0;
             if (k > 0) {  // level 0 was tagged by k_make_jobs
                 prof_start(st, 5);
                 k_tag_level<<<(unsigned)grid_for(nw), 256, 0, s>>>(d, st->lt, s0, s1, a.cp.lossy ? 1 : 0, lad[k]);
@@ -1743,6 +1746,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     if (const char* e = getenv("QCS_IMZ")) st->imz = atoi(e);
     if (const char* e = getenv("QCS_DIAG_LOCAL")) st->diag_local = atoi(e);
     if (const char* e = getenv("QCS_ZERO_PASS")) st->zero_pass = atoi(e);
+    if (const char* e = getenv("QCS_LADDER_EXIT")) st->ladder_exit = atoi(e);
     if (const char* e = getenv("QCS_DEBUG_SYNC")) st->debug_sync = atoi(e);
     if (const char* e = getenv("QCS_MAX_ROUNDS")) st->max_rounds = std::max(1, atoi(e));
     cudaSetDevice(device);

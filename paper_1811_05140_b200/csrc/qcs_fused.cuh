@@ -98,6 +98,7 @@ struct FusedArgs {
     const uint8_t* zero_slot;
     const uint32_t* order;        // [slot] CTA -> global slot within each launch (null = identity)
     const int* err;               // device error word (non-zero: the gate failed or is suspended; no-op)
+    double ladder_theta;          // > 0: a level before the last; give up once theta is out of reach
     // ---- gate ----
     double u[8];
     int kind;                     // GateKind
@@ -1208,6 +1209,23 @@ __device__ __forceinline__ void fused_body(const FusedArgs& a, const int b)
             C.closes_open = 0;
         }
         __syncthreads();
+        // Ladder early exit (not the last level): the closed tokens are a
+        // lower bound of the final payload, so once 16L / (headers + them)
+        // falls below theta the level can no longer be chosen
+        // (block_pair_ratio, aalc.cpp:37-42; pairs: min of both) -- stop and
+        // leave the unit pending for the next level (uniform over the CTA)
+        if (a.ladder_theta > 0.0 && !final_iter) {
+            uint64_t lb = 2 * HEADER_BYTES;
+            for (int p = 0; p < NPL; ++p) lb += S.carry[p].out_pos;
+            if ((double)(16 * n) / (double)lb < a.ladder_theta) {
+                if (tid == 0) {
+                    a.out_len[2 * gslot] = 1ull << 50;  // ratio ~ 0: the ladder moves on
+                    a.out_len[2 * gslot + 1] = 1ull << 50;
+                    if (a.counters) atomicAdd(&a.counters[15], 1ull);
+                }
+                return;
+            }
+        }
     }
 
     if (MODE == MODE_LOCAL && a.dump_x) return;
