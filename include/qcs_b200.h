@@ -211,6 +211,38 @@ int qcs_state_kernel_time(qcs_dev_state_t st, int kernel_class, double* total_ns
  * token write, tail). */
 int qcs_state_counters(qcs_dev_state_t st, uint64_t* out, int n);
 
+/* ---- Sharded state in one host process ----
+ * The reference has no distribution.  Rank = the top rank_bits
+ * qubits: rank r's strides live in an engine state of n - rank_bits qubits on
+ * devices[r].  A gate whose target is a rank qubit exchanges half of the
+ * partner shards' strides as device stride images (lazy qubit permutation, no
+ * swap back): backend 1 = grouped ncclSend/ncclRecv (ncclCommInitAll, one
+ * device per rank, libnccl.so.2 loaded at run time), backend 0 = loopback
+ * device copies (several ranks may share one GPU: tests).  Renormalisation,
+ * reflect_mean's mean and the GateRecords are folded on the device in the
+ * reference's global stride / unit order, so results are bit-identical to a
+ * single state for any rank count. */
+typedef struct qcs_cluster* qcs_cluster_t;
+int qcs_cluster_create(int n_qubits, int stride_bits, int rank_bits, uint64_t basis, const int* devices,
+                       int n_devices, int backend, qcs_cluster_t* out);
+void qcs_cluster_destroy(qcs_cluster_t c);
+/* The program's gates, so an exchange evicts the local qubit needed furthest
+ * in the future (Belady); without it, the least recently used one. */
+int qcs_cluster_set_schedule(qcs_cluster_t c, const qcs_gate_desc* gates, uint64_t n_gates);
+/* apply_program_range (aalc.cpp:588-634) across the shards: one GateRecord per
+ * gate (elapsed_ns: device time between the gate's fold and the previous one,
+ * exchanges included), one host synchronisation at the end (plus one per gate
+ * for shards in the wave layout, and the exchanges). */
+int qcs_cluster_run_program(qcs_cluster_t c, const qcs_gate_desc* gates, uint64_t n_gates, uint64_t first_index,
+                            const double* ladder, int n_levels, double theta, qcs_gate_record* records,
+                            uint64_t* n_done);
+/* to_amplitudes of the LOGICAL state (interleaved re/im, 2^(n+1) doubles). */
+int qcs_cluster_to_amplitudes(qcs_cluster_t c, double* amps);
+int qcs_cluster_stats(qcs_cluster_t c, uint64_t* exchanges, uint64_t* exchange_bytes, double* exchange_s,
+                      double* norm_sq);
+/* Rank r's shard (owned by the cluster), for per-shard queries. */
+qcs_dev_state_t qcs_cluster_shard(qcs_cluster_t c, int r);
+
 /* Codec plugin (codec.hpp:80-105): compress(x, ErrorBound(delta)) then
  * serialize_block.  out receives the 29-byte QCS1 header + payload; cap may
  * be 0 to query *len. */

@@ -11,7 +11,7 @@ from .circuit import (CircuitProgram, GateOp, ParseError, Unitary2x2, build_grid
                       print_circuit, survey_bound)
 from .metrics import (GateRecord, RunMetrics, RunSummary, emit_csv, emit_summary_json, gate_record,
                       qubit_gain, summarize_run)
-from .engine import (CheckpointError, CodecError, CompressedState, DeviceError, ErrorBoundLadder,
+from .engine import (CheckpointError, Cluster, CodecError, CompressedState, DeviceError, ErrorBoundLadder,
                      GateResult, RatioThreshold, RunOptions, RunResult, StateGeometry,
                      apply_program_range, compress, decompress, run_program, run_program_on)
 

@@ -1436,6 +1436,10 @@ bool ensure_chain_scratch(qcs_dev_state* st, int levels)
 }
 
 // One gate, fully stream-ordered.  rec_index < 0: no record.
+// given_mean == kMeanPreset: reflect_mean uses the mean already stored on the
+// device (the cluster driver folds it across shards, qcs_cluster.cuh)
+const double kMeanPreset[2] = {0.0, 0.0};
+
 // load (x_ext != null): the strides [load_first, load_first + load_count)
 // are compressed from the caller's raw device planes x_ext (g unused).
 int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, int nl,
@@ -1490,6 +1494,8 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     dbg_sync(st, "k_make_jobs");
     if (resume) {
         // the mean of reflect_mean was taken before the first wave (aalc.cpp:270-295)
+    } else if (p.reflect && given_mean == kMeanPreset) {
+        // sharded run (qcs_cluster): the global mean is already in d.sc->mean
     } else if (p.reflect && given_mean) {  // sharded run: mean combined across ranks
         k_set_mean<<<1, 1, 0, s>>>(d, given_mean[0], given_mean[1]);
         ++st->launches;
@@ -2898,3 +2904,5 @@ int qcs_debug_stride_sumsq(const double* re, const double* im, uint64_t n, doubl
 }
 
 }  // extern "C"
+
+#include "qcs_cluster.cuh"

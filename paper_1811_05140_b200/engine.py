@@ -563,3 +563,84 @@ def run_program(program: CircuitProgram, ladder: ErrorBoundLadder, theta: RatioT
     r = run_program_on(st, program, ladder, theta, options)
     r.metrics.total_elapsed_ns += init_ns
     return r
+
+
+# ---------------------------------------------------------------------------
+# sharded state driven by the C++ cluster driver (qcs_cluster_*, include/qcs_b200.h)
+# ---------------------------------------------------------------------------
+class Cluster:
+    """n qubits sharded over 2^rank_bits engine states (rank = top qubits),
+    exchanges by NCCL send/recv (backend "nccl": one device per rank) or device
+    copies (backend "loopback": ranks may share a GPU); renormalisation,
+    reflect_mean's mean and the GateRecords are folded on the device in the
+    reference's global order (bit-identical to one state)."""
+
+    BACKENDS = {"loopback": 0, "nccl": 1}
+
+    def __init__(self, geom: StateGeometry, rank_bits: int, basis: int, devices: Sequence[int],
+                 backend: str = "loopback"):
+        L = lib()
+        L.qcs_cluster_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_int), C.c_int,
+                                         C.c_int, C.POINTER(C.c_void_p)]
+        L.qcs_cluster_destroy.argtypes = [C.c_void_p]
+        L.qcs_cluster_set_schedule.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64]
+        L.qcs_cluster_run_program.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
+                                              C.POINTER(C.c_double), C.c_int, C.c_double, C.c_void_p,
+                                              C.POINTER(C.c_uint64)]
+        L.qcs_cluster_to_amplitudes.argtypes = [C.c_void_p, C.c_void_p]
+        L.qcs_cluster_stats.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.qcs_cluster_shard.argtypes = [C.c_void_p, C.c_int]
+        L.qcs_cluster_shard.restype = C.c_void_p
+        self._geom = geom
+        self.rank_bits = rank_bits
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(L.qcs_cluster_create(geom.n_qubits, geom.stride_bits, rank_bits, basis, devs, len(devices),
+                                    self.BACKENDS[backend], C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib_handle is not None:
+            _lib_handle.qcs_cluster_destroy(h)
+            self._h = None
+
+    def set_schedule(self, program: CircuitProgram) -> None:
+        desc = pack_gates(program.gates)
+        _check(lib().qcs_cluster_set_schedule(self._h, desc, len(program.gates)))
+
+    def apply_program_range(self, program: CircuitProgram, first: int, last: int, ladder: ErrorBoundLadder,
+                            theta: RatioThreshold = RatioThreshold()) -> RunMetrics:
+        gates = program.gates[first:last]
+        metrics = RunMetrics()
+        if not gates:
+            return metrics
+        desc = pack_gates(gates)
+        recs = (Record * len(gates))()
+        done = C.c_uint64()
+        rc = lib().qcs_cluster_run_program(self._h, desc, len(gates), first, ladder.c_array(),
+                                           len(ladder.bounds), theta.theta, recs, C.byref(done))
+        for i in range(done.value):
+            r = recs[i]
+            metrics.records.append(GateRecord(
+                gate_index=first + i, gate_label=gates[i].label, stride_count=r.stride_count,
+                min_ratio=r.min_ratio, mean_ratio=r.mean_ratio, max_chosen_delta=r.max_chosen_delta,
+                bytes_before=r.bytes_before, bytes_after=r.bytes_after, elapsed_ns=r.elapsed_ns,
+                norm_after=r.norm_after))
+            metrics.records[-1].compressed_in = r.compressed_in
+            metrics.threshold_violations += r.threshold_violations
+            metrics.total_elapsed_ns += r.elapsed_ns
+        if rc:
+            _raise(rc)
+        return metrics
+
+    def to_amplitudes(self) -> np.ndarray:
+        a = np.empty(2 << self._geom.n_qubits, dtype=np.float64)
+        _check(lib().qcs_cluster_to_amplitudes(self._h, a.ctypes.data))
+        return a.view(np.complex128)
+
+    def stats(self) -> dict:
+        x, b, t, nsq = C.c_uint64(), C.c_uint64(), C.c_double(), C.c_double()
+        _check(lib().qcs_cluster_stats(self._h, C.byref(x), C.byref(b), C.byref(t), C.byref(nsq)))
+        return {"exchanges": x.value, "exchange_bytes": b.value, "exchange_s": t.value, "norm_sq": nsq.value}
