@@ -701,7 +701,8 @@ def run_qft_config(args, name):
             "norm_sq_tracked": nsq, "min_stride_ratio": min_ratio,
             "final_state_ratio": (16 << n) / cbytes, "final_compressed_bytes": cbytes,
             "bytes_per_amp_update": (cin + cout) / max(1, upd),
-            "layout": {"wave_slots": ctr["wave_slots"], "compactions": ctr["compactions"]},
+            "layout": {"wave_slots": ctr["wave_slots"], "compactions": ctr["compactions"],
+                       "compaction_s": ctr["compaction_ns"] * 1e-9},
             "roofline": roofline, "codec_counters": {k: v for k, v in ctr.items() if k != "phase_cycles"},
             "gpu_launches": state.launches(), "clocks": clk}
     print(json.dumps(line))
@@ -815,6 +816,7 @@ def run_c3(args, rank, world, local_rank):
     state.profile(2)          # events around the encoder launches only
     torch.cuda.synchronize()
     clocks.start()
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include timed/ (launch lists)
     dev_ns = wall_ns = 0
     upd = cin = cout = 0
     min_ratio = math.inf
@@ -833,6 +835,7 @@ def run_c3(args, rank, world, local_rank):
             min_ratio = min(min_ratio, r.min_ratio)
         last_gate = b
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     clk = clocks.stop()
     kt = state.kernel_times()
     log("kernel times (ns, launches):", kt)
@@ -862,11 +865,17 @@ def run_c3(args, rank, world, local_rank):
     tp = os.path.join(ROOT, "profiles", "traffic_k_fused_c3.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f)["traffic_bytes"]
+            tj = json.load(f)
+        # DRAM bytes per algorithmic byte of the captured launch (ncu --set full),
+        # applied to this run's algorithmic bytes per launch
+        if tj.get("traffic_per_algorithmic_byte"):
+            traffic = tj["traffic_per_algorithmic_byte"] * (cin + cout) / max(1, n_f)
     tot_all = max(1.0, sum(v[0] for v in kt_all.values()))
     roofline = {"bound": "hbm", "kernel": "k_fused", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "traffic_source": "ncu --set full, one launch (profiles/traffic_k_fused_c3.json)" if traffic else None,
+                "traffic_source": ("ncu --set full of the encoder on the C3 shape at n = 28 (tools/profile_c3.py, "
+                                   "profiles/traffic_k_fused_c3.json): its DRAM bytes per algorithmic byte "
+                                   "times this run's algorithmic bytes per launch") if traffic else None,
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": (cin + cout) / max(1, n_f),
                 "algorithmic_bytes": "C_in + C_out of the gates' rewritten strides, 29-byte headers included "
@@ -903,7 +912,8 @@ def run_c3(args, rank, world, local_rank):
             "min_stride_ratio": min_ratio, "final_state_ratio": (16 << n) / cbytes,
             "compressed_bytes": cbytes, "hbm_bytes": {"arena_in_use": arena, "side_index": side_b,
                                                       "scratch": scratch_b},
-            "layout": {"wave_slots": ctr["wave_slots"], "compactions": ctr["compactions"]},
+            "layout": {"wave_slots": ctr["wave_slots"], "compactions": ctr["compactions"],
+                       "compaction_s": ctr["compaction_ns"] * 1e-9},
             "bytes_per_amp_update": (cin + cout) / max(1, upd)}
     print(json.dumps(line))
     return 0

@@ -984,6 +984,7 @@ struct qcs_dev_state {
     uint64_t wave = 0;           // slots per wave (== NS in the small layout)
     uint64_t bump = 0;           // wave mode: arena fill (host-authoritative)
     uint64_t compactions = 0;
+    double compact_ns = 0.0;     // host wall time spent compacting (diagnostics)
     uint64_t* mv_src = nullptr;  // [2NS] compaction work lists
     uint64_t* mv_dst = nullptr;
     uint64_t* mv_len = nullptr;
@@ -1297,7 +1298,16 @@ inline uint64_t round16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
 // past its own source end, so it can only overlap sources of blocks already
 // moved (earlier batches) or of its own batch (bounced).  Blocks shared by
 // several planes (basis-state zero block) move once.
+int compact_arena_impl(qcs_dev_state* st);
 int compact_arena(qcs_dev_state* st)
+{
+    const auto t0 = std::chrono::steady_clock::now();
+    const int rc = compact_arena_impl(st);
+    st->compact_ns += (double)std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+    return rc;
+}
+
+int compact_arena_impl(qcs_dev_state* st)
 {
     Dev& d = st->d;
     cudaStream_t s = st->stream;
@@ -2691,6 +2701,7 @@ int qcs_state_counters(qcs_dev_state_t st, uint64_t* out, int n)
     CU(cudaMemcpy(out, st->d.counters, 8 * n, cudaMemcpyDeviceToHost));
     if (n > 4) out[4] = st->compactions;  // host-side: in-place arena compactions
     if (n > 5) out[5] = st->big ? st->wave : 0;
+    if (n > 14) out[14] = (uint64_t)st->compact_ns;  // (replaces the unused 'tail' phase slot)
     return 0;
 }
 

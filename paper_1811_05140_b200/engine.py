@@ -394,8 +394,9 @@ class CompressedState:
         return {"repaired_lanes": buf[0], "sum_passes": buf[1], "slid_bytes": buf[2],
                 "serial_fallback_lanes": buf[3], "compactions": buf[4], "wave_slots": buf[5],
                 "sum_tie_events": buf[6], "sum_crossing_events": buf[7], "ladder_exits": buf[15],
+                "compaction_ns": buf[14],
                 "phase_cycles": {k: buf[8 + i] for i, k in enumerate(
-                    ("input", "rounds", "final", "sum", "tokcount", "write", "tail"))}}
+                    ("input", "rounds", "final", "sum", "tokcount", "write"))}}
 
     def launches(self) -> int:
         return lib().qcs_state_launches(self._h)

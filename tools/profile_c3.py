@@ -28,6 +28,10 @@ st.profile(1)
 t0 = time.perf_counter()
 m = q.apply_program_range(st, prog, g0, g0 + ng, lad, th)
 wall = time.perf_counter() - t0
+import json  # noqa: E402
+with open(os.environ.get("QCS_PROFILE_OUT", "/dev/null"), "w") as f:
+    json.dump([{"gate": r.gate_index, "elapsed_ns": r.elapsed_ns, "c_in": r.compressed_in, "c_out": r.bytes_after,
+                "amp_updates": r.bytes_before // 16} for r in m.records], f)
 for r in m.records:
     print(f"gate {r.gate_index}: {r.elapsed_ns / 1e6:.2f} ms, {r.bytes_before // 16 / (r.elapsed_ns * 1e-9):.3e} amp/s, "
           f"C_in {r.compressed_in} C_out {r.bytes_after}")
