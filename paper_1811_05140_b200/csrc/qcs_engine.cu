@@ -970,6 +970,7 @@ struct qcs_dev_state {
     int diag_local = 1;  // diagonal far/pair gates in the fused kernel (QCS_DIAG_LOCAL=0: split path)
     int zero_pass = 1;   // zero strides skip the codec (QCS_ZERO_PASS=0 turns it off)
     int ladder_exit = 1; // ladder levels give up at the byte budget (QCS_LADDER_EXIT=0 turns it off)
+    int force_wide = 0;  // QCS_WIDE=1: 2 x 256-lane encoder CTAs for every gate (experiments)
     int debug_sync = 0;  // QCS_DEBUG_SYNC=1: synchronise and log after every kernel of a gate (debugging)
     bool all_im_zero = true;  // every im plane is zero (real state): real gates keep it
     int chain_levels = 0;
@@ -1487,7 +1488,17 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     // leaves the flag claiming a real state
     if (!real_gate) st->all_im_zero = false;
     const bool diag_gate = p.kind <= 1 && g->u[2] == 0.0 && g->u[3] == 0.0 && g->u[4] == 0.0 && g->u[5] == 0.0;
-    const int zmode = !st->zero_pass || p.kind == KIND_LOAD || p.reflect ? 0 : (p.pair && !diag_gate ? 2 : 1);
+    // diagonal gates (u12 = u21 = 0: CP, CZ, Z, T, phase): every element is
+    // gated on its own (qcs_fused.cuh, FusedArgs::diag), so far partners and
+    // pair units need no partner data and stay in the fused in-chunk kernel;
+    // the plan, the joint pair ladder and the reports are unchanged.  (With
+    // fewer slots than SMs the split path's chunk-parallel decode keeps every
+    // SM busy, which the per-stride fused kernel cannot: C1.)
+    const bool diag = !x_ext && diag_gate && st->diag_local && (p.pair || (1ull << p.t) >= FUSED_SPAN) &&
+                      n_slots >= 148;
+    // zero-stride pass: a slot's output depends on its own stride alone, or
+    // (pair units on the split path) on both strides of its unit
+    const int zmode = !st->zero_pass || p.kind == KIND_LOAD || p.reflect ? 0 : (p.pair && !diag ? 2 : 1);
     k_make_jobs<<<(unsigned)grid_for(n_slots), 256, 0, s>>>(d, p, n_slots, gen, st->lt, lad[0] > 0.0 ? 1 : 0, lad[0],
                                                             imz ? (st->all_im_zero ? 2 : 1) : 0, zmode, resume ? 1 : 0);
     ++st->launches;
@@ -1495,7 +1506,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         k_precheck<<<1, ALLOC_THREADS, 0, s>>>(d, n_slots);
         ++st->launches;
     }
-    if (zmode) {
+    if (zmode && n_slots > 148) {  // (up to one CTA per SM the order is moot)
         const uint64_t wslots = std::max<uint64_t>(1, st->wave / (p.pair ? 2 : 1)) * (p.pair ? 2 : 1);
         k_slot_order<<<1, ORDER_THREADS, 0, s>>>(d, n_slots, wslots);
         ++st->launches;
@@ -1519,11 +1530,6 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     // cross-chunk partners (pair units, in-stride targets >= 2^12): decode +
     // gate fully parallel into X, then the encoder reads X (split path)
     int dg = -1;
-    // diagonal gates (u12 = u21 = 0: CP, CZ, Z, T, phase): every element is
-    // gated on its own (qcs_fused.cuh, FusedArgs::diag), so far partners and
-    // pair units need no partner data and stay in the fused in-chunk kernel;
-    // the plan, the joint pair ladder and the reports are unchanged
-    const bool diag = diag_gate && st->diag_local && (p.pair || (1ull << p.t) >= FUSED_SPAN);
     if (diag) dg = -1;
     else if (p.pair) dg = DG_PAIR;
     else if (p.kind <= 1 && (1ull << p.t) >= FUSED_SPAN) dg = DG_FAR;
@@ -1531,7 +1537,12 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     else if (p.kind <= 1 && st->split_local && (1ull << p.t) >= DG_HALF) dg = DG_FAR;
     else if (p.kind <= 1 && st->split_local && d.L >= DG_IN_CH) dg = DG_IN;
     // gates with fewer units than SMs: one 512-thread CTA per stride
-    const bool wide = n_slots < 148 && d.L >= 2 * FUSED_SPAN;
+    // 2 x 256-lane CTAs (16 warps, one per SM) when the usual 2 x 128-lane CTAs
+    // would leave SMs at 8 warps: fewer units than SMs, or up to two per SM of
+    // which some may be all-zero strides (zero-stride pass) -- the encoder is
+    // latency-bound and its throughput per SM follows the resident warps.
+    // Real states (zero-imaginary-plane mode) keep the narrow CTAs (measured).
+    const bool wide = (n_slots < 148 || (n_slots <= 296 && !imz) || st->force_wide) && d.L >= 2 * FUSED_SPAN;
     const int fm = dg >= 0 ? (wide ? FM_RAW2_W : FM_RAW2) : (wide ? FM_LOCAL_W : FM_LOCAL);  // pairs always split
     if (dg >= 0) {
         if (const int rc = set_smem_attr(reinterpret_cast<const void*>(k_decode_gate), (int)DG_SMEM)) return rc;
@@ -1612,7 +1623,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         a.im_zero = imz ? d.im_zero : nullptr;
         a.err = &d.sc->err;
         a.zero_slot = zmode ? d.zero_slot : nullptr;
-        a.order = zmode ? d.order : nullptr;
+        a.order = (zmode && n_slots > 148) ? d.order : nullptr;
         return a;
     };
     const uint64_t spu = p.pair ? 2 : 1;                        // slots per unit
@@ -1763,6 +1774,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     if (const char* e = getenv("QCS_DIAG_LOCAL")) st->diag_local = atoi(e);
     if (const char* e = getenv("QCS_ZERO_PASS")) st->zero_pass = atoi(e);
     if (const char* e = getenv("QCS_LADDER_EXIT")) st->ladder_exit = atoi(e);
+    if (const char* e = getenv("QCS_WIDE")) st->force_wide = atoi(e);
     if (const char* e = getenv("QCS_DEBUG_SYNC")) st->debug_sync = atoi(e);
     if (const char* e = getenv("QCS_MAX_ROUNDS")) st->max_rounds = std::max(1, atoi(e));
     cudaSetDevice(device);
