@@ -398,6 +398,9 @@ int cl_make_local(qcs_cluster* c, int p, int keep, uint64_t index, int* out)
         return 0;
     }
     int v = -1;
+    // (when the control holds the only local stride bit it is evicted: it becomes
+    // a rank bit, and a control on a rank bit is the rank-level skip)
+    if (nloc == 1) keep = -1;
     for (int cand = 0; cand < nloc; ++cand) {
         if (cand == keep) continue;
         if (v < 0) {
@@ -411,7 +414,7 @@ int cl_make_local(qcs_cluster* c, int p, int keep, uint64_t index, int* out)
             v = cand;
         }
     }
-    if (v < 0) return set_err(QCS_E_INVALID, "cluster: needs a local stride bit besides the control");
+    if (v < 0) return set_err(QCS_E_INVALID, "cluster: no local stride bit");
     int rc = cl_swap(c, q - nloc, v);
     if (rc) return rc;
     const int pv = c->inv[v];

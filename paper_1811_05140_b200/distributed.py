@@ -10,19 +10,23 @@ single-process semantics exactly:
   qubit turns into "this rank applies the uncontrolled gate or nothing",
   which is what make_stride_plan's control-bit skip does (gate.cpp:351-379);
 * a target on a rank qubit b: partner ranks r and r^(1<<b) swap rank bit b
-  with a local stride bit (half of each rank's strides change hands, blocks
-  moved verbatim with their scale and sum), run the ordinary cross-stride
-  pair unit locally (aalc.cpp:333-382), and swap back;
+  with a local stride bit (half of each rank's strides change hands as
+  device stride images: blocks verbatim with side index, scale and sum), and
+  the ordinary cross-stride pair unit runs locally (aalc.cpp:333-382); the
+  qubit permutation stays (no swap back; Belady eviction over the program);
 * the lazy renormalisation (aalc.cpp:410-419) is global: per-stride
   (scale, sum_sq) are all-gathered and summed serially in global stride
   order, so every world size reproduces the single-GPU bits;
 * GateRecords fold the stride reports in the reference's global unit order
   (aalc.cpp:612-631).
 
-Exchanges go through host memory in this version (export/import of QCS1
-block images); a device-side NCCL exchange is the next step.
-The local engine is pluggable: GpuBackend (this package) or the oracle's
-backend in oracle/oracle.py (CPU tests with gloo).
+Exchanges move device stride images (qcs_pack_strides_range /
+qcs_unpack_strides) point to point: NCCL send/recv over NVLink under
+torch.distributed, staged through host memory on gloo.  The per-gate folds
+(renormalisation, mean, records) are a host round trip here; the C++ driver
+in the library (qcs_cluster_*, csrc/qcs_cluster.cuh) does them on the device
+from one process.  The local engine is pluggable: GpuBackend (this package) or
+the oracle's backend in oracle/oracle.py (CPU tests with gloo).
 """
 from __future__ import annotations
 
@@ -386,7 +390,9 @@ class ShardedState:
             return q
         cands = [v for v in range(nloc) if v != keep]
         if not cands:
-            raise NotImplementedError("needs a local stride bit besides the control")
+            # the control holds the only local stride bit: evict it -- it becomes a
+            # rank bit, and a control on a rank bit is the rank-level skip
+            cands = list(range(nloc))
         if self.next_target is not None:
             v = max(cands, key=lambda v: (self._next_use(self.inv[v], index), -v))
         else:

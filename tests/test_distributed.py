@@ -13,6 +13,7 @@ import pytest
 
 import paper_1811_05140_b200 as q
 from paper_1811_05140_b200 import metrics as mm
+from paper_1811_05140_b200 import circuit as cc
 from paper_1811_05140_b200.distributed import (GpuBackend, ShardGeometry, run_thread_cluster)
 
 from helpers import golden_program, golden_runs, oracle_run, sha
@@ -256,3 +257,20 @@ def test_lazy_permutation_one_exchange_per_rank_qubit_gate(oracle):
         naive = sum(1 for g in prog.gates if g.kind in (0, 1) and g.target >= geom.local_qubits)
         assert ex <= 2 * naive // 2 + naive // 2, (ex, naive)  # at most 1.5 per rank-qubit gate
         assert ex < 2 * naive
+
+
+def test_control_on_the_only_local_stride_bit(oracle):
+    """One local stride bit (n - g = s + 1) and a controlled gate whose control
+    holds it while the target is a rank qubit: the control is evicted to a rank
+    bit (then the rank-level skip applies) -- same bits as one process."""
+    from oracle import OracleBackend
+    n, s, rb = 6, 4, 1
+    U = cc.Unitary2x2
+    prog = cc.CircuitProgram(n, [cc.GateOp.single(U.hadamard(), q, f"h {q}") for q in range(n)] +
+                             [cc.GateOp.controlled(U.sqrt_x(), 4, 5, "c4t5"), cc.GateOp.controlled(U.t_gate(), 5, 4, "c5t4"),
+                              cc.GateOp.controlled(U.pauli_y(), 4, 5, "c4t5y")], "ctl-local")
+    lad, theta = [2.0 ** -14], 1.0
+    want_amp, want_csv = _single(oracle, prog, s, 3, lad, theta)
+    amp, recs = run_thread_cluster(prog, ShardGeometry(n, s, rb), lambda r: OracleBackend(oracle), 3, lad, theta)
+    assert mm.emit_csv(recs, with_elapsed=False) == want_csv
+    assert amp.tobytes() == want_amp.tobytes()

@@ -86,3 +86,20 @@ def test_cluster_nccl_rejects_shared_device():
     import paper_1811_05140_b200 as q
     with pytest.raises(ValueError):
         q.Cluster(q.StateGeometry.make(10, 6), 1, 0, [0, 0], "nccl")
+
+
+def test_cluster_control_on_the_only_local_stride_bit(reference):
+    """n - g = s + 1: the control holding the only local stride bit is evicted
+    to a rank bit for a rank-qubit target (then the rank-level skip applies)."""
+    import paper_1811_05140_b200 as q
+    n, s, g = 6, 4, 1
+    U = cc.Unitary2x2
+    prog = cc.CircuitProgram(n, [cc.GateOp.single(U.hadamard(), k, f"h {k}") for k in range(n)] +
+                             [cc.GateOp.controlled(U.sqrt_x(), 4, 5, "c4t5"), cc.GateOp.controlled(U.t_gate(), 5, 4, "c5t4"),
+                              cc.GateOp.controlled(U.pauli_y(), 4, 5, "c4t5y")], "ctl-local")
+    ladder = [2.0 ** -14]
+    ref_csv, ref_amps, _ = reference.run(cc.print_circuit(prog), s, 3, ladder, 1.0, workers=0)
+    cl = q.Cluster(q.StateGeometry.make(n, s), g, 3, [0, 0], "loopback")
+    m = cl.apply_program_range(prog, 0, len(prog.gates), q.ErrorBoundLadder.make(ladder), q.RatioThreshold(1.0))
+    assert mm.emit_csv(m.records, with_elapsed=False) == mm.strip_elapsed(ref_csv)
+    assert cl.to_amplitudes().tobytes() == ref_amps.tobytes()
