@@ -95,8 +95,10 @@ def test_cluster_control_on_the_only_local_stride_bit(reference):
     n, s, g = 6, 4, 1
     U = cc.Unitary2x2
     prog = cc.CircuitProgram(n, [cc.GateOp.single(U.hadamard(), k, f"h {k}") for k in range(n)] +
-                             [cc.GateOp.controlled(U.sqrt_x(), 4, 5, "c4t5"), cc.GateOp.controlled(U.t_gate(), 5, 4, "c5t4"),
-                              cc.GateOp.controlled(U.pauli_y(), 4, 5, "c4t5y")], "ctl-local")
+                             [cc.GateOp.controlled(U.pauli_x(), 4, 5, "cx 4 5"),
+                              cc.GateOp.controlled_phase(0.7, 5, 4, "cp 5 4"),
+                              cc.GateOp.single(U.pauli_y(), 5, "y 5"),
+                              cc.GateOp.controlled(U.pauli_x(), 4, 5, "cx 4 5")], "ctl-local")
     ladder = [2.0 ** -14]
     ref_csv, ref_amps, _ = reference.run(cc.print_circuit(prog), s, 3, ladder, 1.0, workers=0)
     cl = q.Cluster(q.StateGeometry.make(n, s), g, 3, [0, 0], "loopback")
