@@ -208,7 +208,8 @@ int qcs_state_kernel_time(qcs_dev_state_t st, int kernel_class, double* total_ns
  * [3] lanes finished by the serial chain, [4] in-place arena compactions
  * and [5] slots per wave (wave layout for large states, 0 otherwise),
  * [8..14] cycles per kernel phase (input, rounds, final, sum, token count,
- * token write, tail). */
+ * token write, tail), [17] slots the streaming kernel left to the legacy
+ * encoder, [18] slots it encoded.  n <= 24. */
 int qcs_state_counters(qcs_dev_state_t st, uint64_t* out, int n);
 
 /* ---- Sharded state in one host process ----

@@ -32,7 +32,7 @@
 #include <vector>
 
 #include "../../include/qcs_b200.h"
-#include "qcs_fused.cuh"
+#include "qcs_stream.cuh"
 
 using namespace qcs;
 
@@ -145,6 +145,7 @@ struct Dev {
     uint8_t* pending;      // [NS]
     uint8_t* im_zero;      // [NS] per slot: output im plane provably zero (zero-imaginary-plane mode)
     uint8_t* zero_slot;    // [NS] per slot: output stride provably all zero (zero-stride pass)
+    uint8_t* redo;         // [NS] per slot: the streaming kernel left it to the legacy encoder
     uint32_t* order;       // [NS] dense-first slot order within each wave (k_slot_order)
     int64_t* slot_of;      // [NS] generation<<32 | slot
     qcs_stride_report* reports;  // [NS]
@@ -172,7 +173,7 @@ struct Dev {
     }* sc;
     qcs_gate_record* rec;  // record ring for run_program
     uint64_t rec_cap;
-    unsigned long long* counters;  // [16] device diagnostics
+    unsigned long long* counters;  // [24] device diagnostics
 };
 
 // per-plane codec/delta of the chosen level, kept with the slot
@@ -923,6 +924,25 @@ int launch_fused_t(const FusedArgs& a, uint64_t grid, cudaStream_t s)
     return 0;
 }
 
+template <int LANES>
+int launch_stream_t(const FusedArgs& a, uint8_t* redo, uint64_t grid, cudaStream_t s)
+{
+    if (const int rc = set_smem_attr(reinterpret_cast<const void*>(k_stream<LANES>), (int)sizeof(StreamSharedT<LANES>)))
+        return rc;
+    if (grid == 0) return 0;
+    k_stream<LANES><<<(unsigned)grid, LANES, sizeof(StreamSharedT<LANES>), s>>>(a, redo);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+// streaming kernel (qcs_stream.cuh): CTA width by the slots per SM of the launch
+int launch_stream(const FusedArgs& a, uint8_t* redo, uint64_t grid, cudaStream_t s)
+{
+    if (grid >= 8 * 148) return launch_stream_t<128>(a, redo, grid, s);
+    if (grid >= 4 * 148) return launch_stream_t<256>(a, redo, grid, s);
+    return launch_stream_t<512>(a, redo, grid, s);
+}
+
 // FM_*_W: 2 planes x 256 lanes (one CTA per SM), for gates with fewer units
 // than SMs, where per-stride parallelism is all there is
 enum { FM_LOCAL = 0, FM_LOCAL_W = 1, FM_RAW2_W = 2, FM_RAW1 = 3, FM_RAW2 = 4 };
@@ -967,6 +987,7 @@ struct qcs_dev_state {
     // it off): codes/predictor scratch for `chain_levels` ladder levels
     int serial_chain = 1;
     int imz = 1;  // zero-imaginary-plane mode (QCS_IMZ=0 turns it off)
+    int stream_mode = 1;  // streaming kernel for element-wise gates (QCS_STREAM=0 turns it off; 2: also below one slot per SM)
     int diag_local = 1;  // diagonal far/pair gates in the fused kernel (QCS_DIAG_LOCAL=0: split path)
     int zero_pass = 1;   // zero strides skip the codec (QCS_ZERO_PASS=0 turns it off)
     int ladder_exit = 1; // ladder levels give up at the byte budget (QCS_LADDER_EXIT=0 turns it off)
@@ -1692,7 +1713,22 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
                 ++st->launches;
             }
             prof_start(st, 2);
-            int rc = launch_fused(a, fm_lvl, nw, s);
+            int rc = 0;
+            // element-wise gates at a power-of-two lossy level: the streaming
+            // kernel first; the legacy encoder then only re-encodes the slots
+            // it left (escapes, off-lattice predictors: d.redo)
+            const bool elementwise = (p.kind <= 1 && diag_gate) || p.kind == 2 || p.kind == 3;
+            if (st->stream_mode && elementwise && (fm_lvl == FM_LOCAL || fm_lvl == FM_LOCAL_W) && !a.dump_x &&
+                a.cp.lossy && a.cp.pow2 && d.L >= SUB && d.L <= (1ull << 31) &&
+                (n_slots >= 148 || st->stream_mode >= 2)) {
+                FusedArgs as = a;
+                if (p.kind <= 1) as.diag = p.pair ? 2 : 1;
+                rc = launch_stream(as, d.redo, nw, s);
+                if (rc) return rc;
+                ++st->launches;
+                a.redo_only = d.redo;
+            }
+            rc = launch_fused(a, fm_lvl, nw, s);
             prof_stop(st);
             if (rc) return rc;
             ++st->launches;
@@ -1771,6 +1807,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     if (const char* e = getenv("QCS_SPLIT_LOCAL")) st->split_local = atoi(e);
     if (const char* e = getenv("QCS_SERIAL_CHAIN")) st->serial_chain = atoi(e);
     if (const char* e = getenv("QCS_IMZ")) st->imz = atoi(e);
+    if (const char* e = getenv("QCS_STREAM")) st->stream_mode = atoi(e);
     if (const char* e = getenv("QCS_DIAG_LOCAL")) st->diag_local = atoi(e);
     if (const char* e = getenv("QCS_ZERO_PASS")) st->zero_pass = atoi(e);
     if (const char* e = getenv("QCS_LADDER_EXIT")) st->ladder_exit = atoi(e);
@@ -1862,16 +1899,17 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     TRY(dalloc(st, &d.pending, d.NS));
     TRY(dalloc(st, &d.im_zero, d.NS));
     TRY(dalloc(st, &d.zero_slot, d.NS));
+    TRY(dalloc(st, &d.redo, d.NS));
     TRY(dalloc(st, &d.order, d.NS));
     TRY(dalloc(st, &d.slot_of, d.NS));
     TRY(dalloc(st, &d.reports, d.NS));
     TRY(dalloc(st, &d.new_off, 2 * d.NS));
     TRY(dalloc(st, &d.partial, 2 * d.NS));
     TRY(dalloc(st, &d.sc, 1));
-    TRY(dalloc(st, &d.counters, 16));
+    TRY(dalloc(st, &d.counters, 24));
     if (const char* e = getenv("QCS_CTA_TRACE"))
         if (atoi(e)) TRY(dalloc(st, &st->cta_trace, 8 * d.NS));
-    CU(cudaMemset(d.counters, 0, 128));
+    CU(cudaMemset(d.counters, 0, 192));
     TRY(dalloc(st, &st->lt.slot_codec, d.NS));
     TRY(dalloc(st, &st->lt.slot_delta, d.NS));
     if (cudaMallocHost(&st->h_sc, sizeof(Dev::Scal)) != cudaSuccess ||
@@ -2707,7 +2745,7 @@ int qcs_state_profile(qcs_dev_state_t st, int enable)
 
 int qcs_state_counters(qcs_dev_state_t st, uint64_t* out, int n)
 {
-    if (!st || !out || n < 0 || n > 16) return set_err(QCS_E_INVALID, "bad argument");
+    if (!st || !out || n < 0 || n > 24) return set_err(QCS_E_INVALID, "bad argument");
     int rc = sync_and_check(st);
     if (rc) return rc;
     CU(cudaMemcpy(out, st->d.counters, 8 * n, cudaMemcpyDeviceToHost));

@@ -113,6 +113,7 @@ struct FusedArgs {
     // ---- encoder ----
     uint64_t n;                   // elements per plane (stride length)
     const uint8_t* pending;       // per slot (null = all)
+    const uint8_t* redo_only;     // per slot (null = all): only the slots the streaming kernel left (qcs_stream.cuh)
     int max_rounds;               // event rounds before the neighbour-exit repair (>= 1)
     int pool;                     // small layout: out / side / side_in are the plane
                                   // slot pools (two slots per plane, p_off selects)
@@ -1249,6 +1250,7 @@ __global__ void __launch_bounds__(NPL * LPL, (NPL * LPL > 256 ? 1 : (NPL * LPL >
     const int b = a.order ? (int)(a.order[a.slot_base + blockIdx.x] - a.slot_base) : (int)blockIdx.x;
     const uint64_t gslot = a.slot_base + (uint64_t)b;
     if (a.pending && !a.pending[gslot]) return;
+    if (a.redo_only && !a.redo_only[gslot]) return;
     // zero-stride pass: an all-zero output stride is its two zero encodings
     // and a stored sum of squares of +0.0 (core.cpp:30-37 over zeros)
     if (NPL == 2 && a.zero_slot && a.zero_slot[gslot]) {

@@ -389,12 +389,12 @@ class CompressedState:
         return out
 
     def counters(self) -> dict:
-        buf = (C.c_uint64 * 16)()
-        _check(lib().qcs_state_counters(self._h, buf, 16))
+        buf = (C.c_uint64 * 24)()
+        _check(lib().qcs_state_counters(self._h, buf, 24))
         return {"repaired_lanes": buf[0], "sum_passes": buf[1], "slid_bytes": buf[2],
                 "serial_fallback_lanes": buf[3], "compactions": buf[4], "wave_slots": buf[5],
                 "sum_tie_events": buf[6], "sum_crossing_events": buf[7], "ladder_exits": buf[15],
-                "compaction_ns": buf[14],
+                "compaction_ns": buf[14], "stream_left_slots": buf[17], "stream_slots": buf[18],
                 "phase_cycles": {k: buf[8 + i] for i, k in enumerate(
                     ("input", "rounds", "final", "sum", "tokcount", "write"))}}
 
