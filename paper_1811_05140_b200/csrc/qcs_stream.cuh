@@ -66,126 +66,109 @@ struct StreamSharedT {
     // sum of squares
     double s;
     double ev_s;
+    uint64_t ev_part;
     uint32_t ev_k;
     int ev_any;
+    int ev_owner;
 };
 static_assert(sizeof(StreamSharedT<128>) <= 55 * 1024 + 768, "four 128-lane streaming CTAs per SM");
 static_assert(sizeof(StreamSharedT<256>) <= 112 * 1024, "two 256-lane streaming CTAs per SM");
 static_assert(sizeof(StreamSharedT<512>) <= 226 * 1024, "one 512-lane streaming CTA per SM");
 
 // Sequential reader of one plane's token stream from a side-index entry
-// (decode_sub's walk, one element per call).
+// (decode_sub's walk, one element per call).  `in` is 4-byte aligned; reads
+// up to 7 bytes past a token's first byte.
 struct TokReader {
     const uint8_t* in;
-    uint64_t pos;
-    uint64_t w;
-    int avail;
-    int codec;
+    uint32_t pos;
     uint32_t skip;
     uint32_t zleft, wleft;
+    int codec;
     double td, P;
 
     __device__ __forceinline__ void init(const uint8_t* in_, int codec_, double td_, SideEntry se)
     {
         in = in_;
         pos = se.off;
-        w = 0;
-        avail = 0;
         codec = codec_;
         skip = se.skip;
         zleft = wleft = 0;
         td = td_;
         P = se.pred;
     }
-    __device__ __forceinline__ uint64_t varint()
+    __device__ __forceinline__ uint32_t fetch4(uint32_t at) const
     {
-        if (avail < 5) {
-            w = load8_at(in, pos);
-            avail = 8;
-        }
-        const uint64_t stop = ~w & 0x8080808080808080ull;
-        const int nb = stop ? (__ffsll((long long)stop) >> 3) : 9;
-        if (nb <= 4 && nb <= avail) {
-            const uint32_t x = (uint32_t)w & (0xffffffffu >> (8 * (4 - nb)));
-            const uint32_t v = (x & 0x7fu) | ((x >> 1) & 0x3f80u) | ((x >> 2) & 0x1fc000u) | ((x >> 3) & 0xfe00000u);
-            pos += nb;
-            avail -= nb;
-            w >>= 8 * nb;
-            return v;
-        }
-        avail = 0;
-        return get_varint(in, pos);
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(in + (at & ~3u));
+        return __funnelshift_r(p[0], p[1], (at & 3u) << 3);
     }
     __device__ __forceinline__ double word()
     {
-        const double x = __longlong_as_double((long long)load8_at(in, pos));
+        const uint64_t w = (uint64_t)fetch4(pos) | ((uint64_t)fetch4(pos + 4) << 32);
         pos += 8;
-        avail = 0;
+        return __longlong_as_double((long long)w);
+    }
+    // a run token (value v): zero run or raw words, lossy or lossless
+    __device__ __forceinline__ double run_token(uint64_t v)
+    {
+        const bool words = codec == 1 ? (v & 3u) == 2u : (v & 1u) != 0u;
+        const uint32_t left = (uint32_t)((codec == 1 ? v >> 2 : v >> 1) - skip) - 1u;
+        if (!words) {
+            zleft = left;
+            skip = 0;
+            return codec == 1 ? P : 0.0;
+        }
+        pos += 8u * skip;
+        skip = 0;
+        wleft = left;
+        const double x = word();
+        if (codec == 1) P = x;
         return x;
     }
     // the next element's decoded value (before the stride scale)
     __device__ __forceinline__ double next()
     {
+        if ((zleft | wleft) == 0u) {
+            const uint32_t w = fetch4(pos);
+            const uint32_t m = ~w & 0x80808080u;
+            if (m != 0u) {  // a varint of up to 4 bytes
+                const uint32_t x = w & (m ^ (m - 1u));
+                const uint32_t v = (x & 0x7fu) | ((x >> 1) & 0x3f80u) | ((x >> 2) & 0x1fc000u) | ((x >> 3) & 0xfe00000u);
+                pos += (uint32_t)__ffs((int)m) >> 3;
+                if (codec == 1 && (v & 3u) == 1u) {  // one nonzero code
+                    const uint32_t z = v >> 2;
+                    P = __dadd_rn(P, __dmul_rn(td, (double)((int)(z >> 1) ^ -(int)(z & 1u))));
+                    return P;
+                }
+                return run_token(v);
+            }
+            uint64_t p64 = pos;
+            const uint64_t v = get_varint(in, p64);
+            pos = (uint32_t)p64;
+            if (codec == 1 && (v & 3u) == 1u) {  // (not a valid code: too large; keep the walk defined)
+                P = __dadd_rn(P, __dmul_rn(td, (double)unzigzag(v >> 2)));
+                return P;
+            }
+            return run_token(v);
+        }
         if (zleft) {
             --zleft;
             return codec == 1 ? P : 0.0;
         }
-        if (wleft) {
-            --wleft;
-            const double x = word();
-            if (codec == 1) P = x;
-            return x;
-        }
-        const uint64_t v = varint();
-        if (codec == 1) {
-            const unsigned tag = (unsigned)(v & 3u);
-            const uint64_t arg = v >> 2;
-            if (tag == 1) {
-                P = __dadd_rn(P, __dmul_rn(td, (double)(int)unzigzag(arg)));
-                return P;
-            }
-            const uint32_t left = (uint32_t)(arg - skip) - 1u;
-            if (tag == 0) {
-                zleft = left;
-                skip = 0;
-                return P;
-            }
-            pos += 8ull * skip;
-            skip = 0;
-            wleft = left;
-            P = word();
-            return P;
-        }
-        const uint64_t run = v >> 1;
-        const uint32_t left = (uint32_t)(run - skip) - 1u;
-        if ((v & 1u) == 0) {
-            zleft = left;
-            skip = 0;
-            return 0.0;
-        }
-        pos += 8ull * skip;
-        skip = 0;
-        wleft = left;
-        return word();
+        --wleft;
+        const double x = word();
+        if (codec == 1) P = x;
+        return x;
     }
 };
 
-// code token of q (|q| < 32768): 1..3 bytes at o, returns the length
-__device__ __forceinline__ uint32_t put_code_token(uint8_t* o, int q)
-{
-    const uint32_t v = ((((uint32_t)q << 1) ^ (uint32_t)(q >> 31)) << 2) | 1u;
-    const uint32_t len = 1u + (v >= 128u) + (v >= 16384u);
-    o[0] = (uint8_t)((v & 0x7fu) | (len > 1u ? 0x80u : 0u));
-    if (len > 1u) o[1] = (uint8_t)(((v >> 7) & 0x7fu) | (len > 2u ? 0x80u : 0u));
-    if (len > 2u) o[2] = (uint8_t)(v >> 14);
-    return len;
-}
-
 struct StreamPlaneOut {
-    double M0, x0, Mlast;
-    bool good0, seen, bad;
+    double x0;
+    int M0, Mlast;
+    bool good0, seen;
     int lz1, tz, body;
 };
+
+constexpr uint64_t ST_SAT = 1ull << 62;
 
 template <int ST_LANES>
 __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a, uint8_t* redo)
@@ -211,7 +194,7 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
 
     extern __shared__ __align__(16) unsigned char smem[];
     StreamShared& S = *reinterpret_cast<StreamShared*>(smem);
-    const CodecParams cp = a.cp;
+    const double td = a.cp.td, inv_td = a.cp.inv_td;
     const uint64_t n = a.n;
     const uint64_t in_stride = a.job_stride[gslot];
     const double scale = a.scale[in_stride];
@@ -245,6 +228,8 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
     const int kind = a.kind;
     const int fixed_side = a.diag == 2 ? (int)(gslot & 1) : -1;
     const double mr2 = kind == 3 ? 2.0 * a.mean[0] : 0.0, mi2 = kind == 3 ? 2.0 * a.mean[1] : 0.0;
+    // side and control are constant over a lane's 32 elements when their bits are >= 5
+    const bool gate_const = kind <= 1 && (fixed_side >= 0 || a.t >= 5) && (a.local_ctl < 0 || a.local_ctl >= 5);
 
     if (tid == 0) {
         S.out_pos[0] = S.out_pos[1] = 0;
@@ -289,52 +274,79 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
         const double s_in = S.s;  // the running sum entering this iteration (uniform)
         const bool have_tu = s_in > 0.0 && ilogb(s_in) >= -960;
         const double tu_main = have_tu ? ldexp(1.0, 52 - ilogb(s_in)) : 0.0;
+        // the lane's gate when side and control do not change inside it
+        bool gate_on = true;
+        double gur = 0.0, gui = 0.0;
+        if (gate_const) {
+            gate_on = a.local_ctl < 0 || ((e0 >> a.local_ctl) & 1u);
+            const int sd = fixed_side >= 0 ? fixed_side : (int)((e0 >> a.t) & 1u);
+            gur = sd ? a.u[6] : a.u[0];
+            gui = sd ? a.u[7] : a.u[1];
+        }
 
-        // One walk over the lane's sub-chunk.  PASS 0: the main pass (tokens
-        // into the staging rows, first-element facts into po, sum units under
-        // tu for every element).  PASS 1: sum units under tu for the elements
-        // after k_after only (replay).  PASS 2: the terms t_k of the elements
-        // below ST_SERIAL into tdst (replay).  Returns the units.
-        auto walk = [&](auto pass_tag, StreamPlaneOut* po, double tu, long long k_after, double* tdst) -> uint64_t {
+        // One walk over the lane's sub-chunk: decode, scale, gate, snap, quantize.
+        //  PASS 0  the main pass: tokens into the staging row, first-element
+        //          facts into po, sum units of every element under tu (uA) and
+        //          under the next binade (uB)
+        //  PASS 1  replay: sum units of every element under tu (uA)
+        //  PASS 2  replay: the terms t_k of the elements below ST_SERIAL into tdst
+        //  PASS 3  replay by the lane holding a sum event: from ms + uA units
+        //          (binade of tu) add the elements after k_after until the event,
+        //          add it exactly (S.ev_s, S.ev_k), then the units of the lane's
+        //          remaining elements under the new binade (S.ev_part)
+        // Returns false when a step is neither proven nor a lattice-preserving
+        // reference step (the slot is left to the legacy encoder).
+        uint64_t uA = 0, uB = 0;
+        auto walk = [&](auto pass_tag, StreamPlaneOut* po, double tu, long long k_after, double* tdst,
+                        uint64_t ms) -> bool {
             constexpr int PASS = decltype(pass_tag)::value;
             TokReader rd[2];
 #pragma unroll
             for (int p = 0; p < 2; ++p) rd[p].init(src[p], in_codec[p], in_td[p], in_side[p][e0 / SUB]);
-            double Mprev[2] = {0.0, 0.0};
+            int Mprev[2] = {0, 0};
             int run[2] = {0, 0};
-            uint8_t* rowp[2];
+            uint64_t acc[2] = {0, 0};  // token bytes not yet stored
+            int fill[2] = {0, 0}, woff[2] = {0, 0};
+            uint8_t* rowp[2] = {nullptr, nullptr};
             if (PASS == 0) {
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
                     rowp[p] = S.rows + (size_t)(p * ST_LANES + tid) * ST_ROW + ST_LEAD;
                     po[p].seen = false;
                     po[p].lz1 = 0;
-                    po[p].body = 0;
                 }
             }
-            uint64_t loc = 0;
-            bool bad = false;
+            uint64_t la = PASS == 3 ? uA : 0, lb = 0;
+            bool eva = false, evb = false, bad = false, found = false;
+            double tu2 = 0.0;
+#pragma unroll 2
             for (int k = 0; k < SUB; ++k) {
                 double xr = rd[0].next(), xi = rd[1].next();
                 if (sc) {
                     xr = __dmul_rn(xr, scale);
                     xi = __dmul_rn(xi, scale);
                 }
-                // gate (run_plan_unit, gate.cpp:405-454), every element on its own
-                const uint64_t gi = (uint64_t)e0 + (uint64_t)k;
+                // gate (run_plan_unit, gate.cpp:405-454), every element on its
+                // own: apply_pair with a zero partner, minus its exact-zero
+                // terms (they change a zero's sign at most: snapped)
                 if (kind <= 1) {
-                    if (!(a.local_ctl >= 0 && !((gi >> a.local_ctl) & 1))) {
-                        const int sd = fixed_side >= 0 ? fixed_side : (int)((gi >> a.t) & 1);
-                        // apply_pair with a zero partner, minus its exact-zero
-                        // terms (they change a zero's sign at most: snapped)
-                        const double ur = sd ? a.u[6] : a.u[0], ui = sd ? a.u[7] : a.u[1];
+                    bool on = gate_on;
+                    double ur = gur, ui = gui;
+                    if (!gate_const) {
+                        const uint32_t gi = e0 + (uint32_t)k;
+                        on = a.local_ctl < 0 || ((gi >> a.local_ctl) & 1u);
+                        const int sd = fixed_side >= 0 ? fixed_side : (int)((gi >> a.t) & 1u);
+                        ur = sd ? a.u[6] : a.u[0];
+                        ui = sd ? a.u[7] : a.u[1];
+                    }
+                    if (on) {
                         const double orr = __dsub_rn(__dmul_rn(ur, xr), __dmul_rn(ui, xi));
                         const double oi = __dadd_rn(__dmul_rn(ur, xi), __dmul_rn(ui, xr));
                         xr = orr;
                         xi = oi;
                     }
                 } else if (kind == 2) {
-                    if (gi == a.flip_off) {
+                    if ((uint64_t)e0 + (uint64_t)k == a.flip_off) {
                         xr = -xr;
                         xi = -xi;
                     }
@@ -349,9 +361,9 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
                     const double x = p ? xi : xr;
-                    const double y = __dmul_rn(x, cp.inv_td);
-                    double M = rint(y);
-                    const double fr = fabs(__dsub_rn(y, M));
+                    const double y = __dmul_rn(x, inv_td);
+                    int M = __double2int_rn(y);
+                    const double fr = fabs(__dsub_rn(y, (double)M));
                     bool good = fabs(y) < 1073741824.0 && fr < 0.5 - 1.9073486328125e-06;
                     if (k == 0) {
                         if (PASS == 0) {
@@ -360,64 +372,115 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                             po[p].good0 = good;
                         }
                     } else {
-                        const double q = __dsub_rn(M, Mprev[p]);
-                        good = good && fabs(q) <= 32766.0;
+                        int q = M - Mprev[p];
+                        good = good && (unsigned)(q + 32766) <= 65532u;
                         if (!good) {  // the reference step from the exact predictor
-                            double P = __dadd_rn(0.0, __dmul_rn(cp.td, Mprev[p]));
-                            const int32_t t = ref_step(cp, P, x);
-                            M = __dadd_rn(Mprev[p], (double)t);
-                            if (t == WCODE || !(fabs(M) < 1073741824.0) ||
-                                !same_bits(__dadd_rn(0.0, __dmul_rn(cp.td, M)), P))
+                            double P = __dmul_rn(td, (double)Mprev[p]);
+                            const int32_t t = ref_step(a.cp, P, x);
+                            M = Mprev[p] + t;
+                            q = t;
+                            if (t == WCODE || M <= -1073741824 || M >= 1073741824 ||
+                                !same_bits(__dmul_rn(td, (double)M), P))
                                 bad = true;
                         }
                         if (PASS == 0) {
-                            const int qi = (int)__dsub_rn(M, Mprev[p]);
-                            if (qi == 0) {
+                            if (q == 0) {
                                 ++run[p];
                             } else {
+                                const uint32_t z = ((uint32_t)q << 1) ^ (uint32_t)(q >> 31);
+                                const uint32_t v = (z << 2) | 1u;
+                                uint32_t len = 1u + (v >= 128u) + (v >= 16384u);
+                                uint32_t pk = (v & 0x7fu) | ((v & 0x3f80u) << 1) | ((v & 0x1fc000u) << 2) |
+                                              (len > 1u ? 0x80u : 0u) | (len > 2u ? 0x8000u : 0u);
                                 if (!po[p].seen) {
                                     po[p].seen = true;
                                     po[p].lz1 = run[p];
-                                } else if (run[p] > 0) {
-                                    rowp[p][po[p].body++] = (uint8_t)(run[p] << 2);  // zero run < 32: one byte
+                                } else if (run[p] > 0) {  // the zero run before it (< 32: one byte)
+                                    pk = (pk << 8) | ((uint32_t)run[p] << 2);
+                                    ++len;
                                 }
-                                po[p].body += (int)put_code_token(rowp[p] + po[p].body, qi);
+                                acc[p] |= (uint64_t)pk << (8 * fill[p]);
+                                fill[p] += (int)len;
+                                if (fill[p] >= 4) {
+                                    *reinterpret_cast<uint32_t*>(rowp[p] + woff[p]) = (uint32_t)acc[p];
+                                    acc[p] >>= 32;
+                                    woff[p] += 4;
+                                    fill[p] -= 4;
+                                }
                                 run[p] = 0;
                             }
                         }
                     }
                     Mprev[p] = M;
-                    rv[p] = __dadd_rn(0.0, __dmul_rn(cp.td, M));
+                    rv[p] = __dmul_rn(td, (double)M);
                 }
                 const double t = __dadd_rn(__dmul_rn(rv[0], rv[0]), __dmul_rn(rv[1], rv[1]));
-                if (PASS == 2) {
+                if (PASS == 0 || PASS == 1) {
+                    const double y0 = t * tu;
+                    const double r0 = rint(y0);
+                    eva = eva || y0 >= 9007199254740992.0 || fabs(y0 - r0) == 0.5;
+                    la += (uint64_t)r0;
+                    if (PASS == 0) {
+                        const double y1 = y0 * 0.5;
+                        const double r1 = rint(y1);
+                        evb = evb || y1 >= 9007199254740992.0 || fabs(y1 - r1) == 0.5;
+                        lb += (uint64_t)r1;
+                    }
+                } else if (PASS == 2) {
+                    const uint32_t gi = e0 + (uint32_t)k;
                     if (gi < ST_SERIAL) tdst[gi] = t;
-                } else if ((long long)gi > k_after) {
-                    loc = sat_add(loc, sq_units_y(t * tu));
+                } else {
+                    const long long gi = (long long)e0 + k;
+                    if (gi > k_after) {
+                        const double y = t * (found ? tu2 : tu);
+                        const double ry = rint(y);
+                        const bool beyond = y >= 9007199254740992.0;
+                        const bool tie = !beyond && fabs(y - ry) == 0.5;
+                        const uint64_t c = beyond ? (1ull << 53) : (uint64_t)ry;
+                        if (found) {
+                            evb = evb || beyond || tie;
+                            lb += c;
+                        } else if (beyond || tie || ms + la + c >= (1ull << 53)) {
+                            const double sn = __dadd_rn((double)(ms + la) / tu, t);
+                            S.ev_s = sn;
+                            S.ev_k = (uint32_t)gi;
+                            if (a.counters) atomicAdd(&a.counters[tie ? 6 : 7], 1ull);
+                            found = true;
+                            tu2 = (sn > 0.0 && ilogb(sn) >= -960 && ilogb(sn) < 1000) ? ldexp(1.0, 52 - ilogb(sn)) : 0.0;
+                        } else {
+                            la += c;
+                        }
+                    }
                 }
             }
             if (PASS == 0) {
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
+                    *reinterpret_cast<uint32_t*>(rowp[p] + woff[p]) = (uint32_t)acc[p];
+                    po[p].body = woff[p] + fill[p];
                     po[p].Mlast = Mprev[p];
                     po[p].tz = run[p];
                     if (!po[p].seen) po[p].lz1 = SUB - 1;
                 }
-                po[0].bad = bad;
             }
-            return loc;
+            if (PASS == 0 || PASS == 1) uA = (eva || la > ST_SAT) ? ST_SAT : la;
+            if (PASS == 0) uB = (evb || lb > ST_SAT) ? ST_SAT : lb;
+            if (PASS == 3) {
+                S.ev_part = (evb || lb > ST_SAT) ? ST_SAT : lb;
+                S.ev_any = found ? 1 : 0;
+            }
+            return !bad;
         };
 
         // B. main pass
         StreamPlaneOut po[2];
-        po[0].bad = false;
-        uint64_t loc = 0;
-        if (have) loc = walk(std::integral_constant<int, 0>{}, po, tu_main, have_tu ? -1ll : (long long)n, nullptr);
+        bool ok = true;
+        if (have) ok = walk(std::integral_constant<int, 0>{}, po, tu_main, -1, nullptr, 0);
         if (have) {
-            S.mlast[0][tid] = (int)po[0].Mlast;
-            S.mlast[1][tid] = (int)po[1].Mlast;
+            S.mlast[0][tid] = po[0].Mlast;
+            S.mlast[1][tid] = po[1].Mlast;
         }
-        if (__syncthreads_or(have && po[0].bad)) {
+        if (__syncthreads_or(!ok)) {
             bail = true;
             break;
         }
@@ -425,21 +488,20 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
         // C. first elements, runs across lanes, lead tokens, byte offsets
         uint32_t val[2] = {0, 0};     // start of the lane's trailing zero run, 0: the lane is one zero run
         int q0[2] = {0, 0};
-        double Mleft[2] = {0.0, 0.0};
+        int Mleft[2] = {0, 0};
         bool bad = false;
         if (have) {
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
-                Mleft[p] = (double)(tid > 0 ? S.mlast[p][tid - 1] : S.m_carry[p]);
-                const double q = __dsub_rn(po[p].M0, Mleft[p]);
-                if (po[p].good0 && fabs(q) <= 32766.0) {
-                    q0[p] = (int)q;
+                Mleft[p] = tid > 0 ? S.mlast[p][tid - 1] : S.m_carry[p];
+                const int q = po[p].M0 - Mleft[p];
+                if (po[p].good0 && (unsigned)(q + 32766) <= 65532u) {
+                    q0[p] = q;
                 } else {  // the reference step; must agree with the lattice point the lane continued from
-                    double P = __dadd_rn(0.0, __dmul_rn(cp.td, Mleft[p]));
-                    const int32_t t = ref_step(cp, P, po[p].x0);
-                    if (t == WCODE || !same_bits(__dadd_rn(Mleft[p], (double)t), po[p].M0) ||
-                        !(fabs(po[p].M0) < 1073741824.0) ||
-                        !same_bits(__dadd_rn(0.0, __dmul_rn(cp.td, po[p].M0)), P))
+                    double P = __dmul_rn(td, (double)Mleft[p]);
+                    const int32_t t = ref_step(a.cp, P, po[p].x0);
+                    if (t == WCODE || Mleft[p] + t != po[p].M0 || po[p].M0 <= -1073741824 || po[p].M0 >= 1073741824 ||
+                        !same_bits(__dmul_rn(td, (double)po[p].M0), P))
                         bad = true;
                     q0[p] = (int)t;
                 }
@@ -484,7 +546,15 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                     put_varint(tmp, (uint64_t)E << 2);
                     ll = (uint32_t)varint_len((uint64_t)E << 2);
                 }
-                ll += put_code_token(tmp + ll, q0[p]);
+                {
+                    const int q = q0[p];
+                    const uint32_t v = ((((uint32_t)q << 1) ^ (uint32_t)(q >> 31)) << 2) | 1u;
+                    const uint32_t len = 1u + (v >= 128u) + (v >= 16384u);
+                    tmp[ll] = (uint8_t)((v & 0x7fu) | (len > 1u ? 0x80u : 0u));
+                    if (len > 1u) tmp[ll + 1] = (uint8_t)(((v >> 7) & 0x7fu) | (len > 2u ? 0x80u : 0u));
+                    if (len > 2u) tmp[ll + 2] = (uint8_t)(v >> 14);
+                    ll += len;
+                }
                 if (po[p].seen && po[p].lz1 > 0) tmp[ll++] = (uint8_t)(po[p].lz1 << 2);
             } else if (!full) {
                 const uint64_t v = (uint64_t)(E + 1u + (uint32_t)po[p].lz1) << 2;
@@ -518,13 +588,6 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             }
             if (wl == 31) S.wbytes[p][wp] = inc;
             bst[p] = inc - nbytes[p];
-        }
-        // (the units of the sum ride on the same barrier)
-        {
-            uint64_t u = loc;
-#pragma unroll
-            for (int o = 16; o; o >>= 1) u = sat_add(u, __shfl_xor_sync(0xffffffffu, u, o));
-            if (wl == 0) S.wunits[wp] = u;
         }
         __syncthreads();
         uint64_t bstart[2];
@@ -569,7 +632,7 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                     se.off = (uint32_t)bstart[p] + (ent[p] > 0 ? (uint32_t)varint_len((uint64_t)ent[p] << 2) : 0u);
                     se.skip = 0;
                 }
-                se.pred = __dadd_rn(0.0, __dmul_rn(cp.td, Mleft[p]));
+                se.pred = __dmul_rn(td, (double)Mleft[p]);
                 side[p][e0 / SUB] = se;
             }
         }
@@ -580,21 +643,25 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             for (int p = 0; p < 2; ++p) {
                 const bool full = q0[p] == 0 && !po[p].seen;
                 S.run_start[p] = full ? rs[p] : val[p];
-                S.m_carry[p] = (int)po[p].Mlast;
+                S.m_carry[p] = po[p].Mlast;
                 S.out_pos[p] += iter_bytes[p];
             }
         }
 
-        // D. stored sum of squares
+        // D. stored sum of squares: s plus the units of the lanes after
+        // `owner` (uA, under the binade of s) plus `part` (the rest of owner's
+        // own sub-chunk); hasB: uB holds the same lanes' units one binade up
         if (a.sumsq) {
             double s = s_in;
-            long long k_after = -1;  // elements up to here are in s
-            double* tser = reinterpret_cast<double*>(S.rows);  // (the rows are free: copied out above)
+            long long k_after = -1;
+            int owner = -1;
+            uint64_t part = 0;
+            bool hasB = have_tu;
             if (!have_tu) {
                 // s is still 0: the first terms double it again and again; add
                 // the first ST_SERIAL in the reference's order on one thread
-                __syncthreads();
-                if (have && e0 < ST_SERIAL) walk(std::integral_constant<int, 2>{}, nullptr, 0.0, -1, tser);
+                double* tser = reinterpret_cast<double*>(S.rows);  // (the rows are free: copied out above)
+                if (have && e0 < ST_SERIAL) walk(std::integral_constant<int, 2>{}, nullptr, 0.0, -1, tser, 0);
                 __syncthreads();
                 const int m = (int)umin64(ST_SERIAL, n - base);
                 if (tid == 0) {
@@ -605,26 +672,31 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                 }
                 __syncthreads();
                 s = S.ev_s;
-                k_after = (long long)base + m - 1;
                 if (base != 0 || !(s > 0.0 && ilogb(s) >= -960)) {  // an all-zero or tiny head: the legacy kernel's cases
                     bail = true;
                     break;
                 }
-                loc = 0;
-                if (have && (long long)e0 + SUB - 1 > k_after)
-                    loc = walk(std::integral_constant<int, 1>{}, nullptr, ldexp(1.0, 52 - ilogb(s)), k_after, nullptr);
-                uint64_t u = loc;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) u = sat_add(u, __shfl_xor_sync(0xffffffffu, u, o));
-                __syncthreads();
-                if (wl == 0) S.wunits[wp] = u;
-                __syncthreads();
+                owner = m / SUB - 1;
+                uA = 0;
+                if (have && tid > owner) walk(std::integral_constant<int, 1>{}, nullptr, ldexp(1.0, 52 - ilogb(s)), -1, nullptr, 0);
             }
             for (;;) {
-                const int e = ilogb(s);
-                const double to_units = ldexp(1.0, 52 - e);
+                const double to_units = ldexp(1.0, 52 - ilogb(s));
                 const uint64_t ms = (uint64_t)(s * to_units);
-                uint64_t total = 0, pre = 0;
+                const uint64_t mine = (have && tid > owner) ? uA : 0;
+                uint64_t inc = mine;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (wl >= o) inc = sat_add(inc, t);
+                }
+                uint64_t excl = __shfl_up_sync(0xffffffffu, inc, 1);
+                if (wl == 0) excl = 0;
+                __syncthreads();  // (S.wunits / S.ev_* of the previous round are read)
+                if (wl == 31) S.wunits[wp] = inc;
+                if (tid == 0) S.ev_any = 0;
+                __syncthreads();
+                uint64_t total = part, pre = part;
                 for (int i = 0; i < ST_WARPS; ++i) {
                     if (i < wp) pre = sat_add(pre, S.wunits[i]);
                     total = sat_add(total, S.wunits[i]);
@@ -633,110 +705,43 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                     s = (double)(ms + total) / to_units;
                     break;
                 }
-                // an event (binade crossing or tie) lies in this iteration: the
-                // lane whose inclusive prefix reaches the binade's end walks to
-                // it and adds it exactly; everything after it is re-measured
-                uint64_t inc = loc;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint64_t t = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (wl >= o) inc = sat_add(inc, t);
-                }
+                // an event (binade crossing or tie) lies ahead: in the rest of
+                // owner's sub-chunk, or in the first lane whose inclusive
+                // prefix reaches the binade's end.  That lane walks to it.
                 const uint64_t LIM = (1ull << 53) - ms;
-                if (tid == 0) S.ev_any = 0;
-                __syncthreads();
-                uint64_t excl = __shfl_up_sync(0xffffffffu, inc, 1);
-                if (wl == 0) excl = 0;
+                const bool in_part = part >= LIM;
                 const uint64_t offx = sat_add(pre, excl);
-                if (have && offx < LIM && sat_add(offx, loc) >= LIM) {
-                    // replay this lane's terms up to the event
-                    TokReader rd[2];
-#pragma unroll
-                    for (int p = 0; p < 2; ++p) rd[p].init(src[p], in_codec[p], in_td[p], in_side[p][e0 / SUB]);
-                    double Mprev[2] = {0.0, 0.0};
-                    uint64_t acc = offx;
-                    for (int k = 0; k < SUB; ++k) {
-                        double xr = rd[0].next(), xi = rd[1].next();
-                        if (sc) {
-                            xr = __dmul_rn(xr, scale);
-                            xi = __dmul_rn(xi, scale);
-                        }
-                        const uint64_t gi = (uint64_t)e0 + (uint64_t)k;
-                        if (kind <= 1) {
-                            if (!(a.local_ctl >= 0 && !((gi >> a.local_ctl) & 1))) {
-                                const int sd = fixed_side >= 0 ? fixed_side : (int)((gi >> a.t) & 1);
-                                const double ur = sd ? a.u[6] : a.u[0], ui = sd ? a.u[7] : a.u[1];
-                                const double orr = __dsub_rn(__dmul_rn(ur, xr), __dmul_rn(ui, xi));
-                                const double oi = __dadd_rn(__dmul_rn(ur, xi), __dmul_rn(ui, xr));
-                                xr = orr;
-                                xi = oi;
-                            }
-                        } else if (kind == 2) {
-                            if (gi == a.flip_off) {
-                                xr = -xr;
-                                xi = -xi;
-                            }
-                        } else {
-                            xr = __dsub_rn(mr2, xr);
-                            xi = __dsub_rn(mi2, xi);
-                        }
-                        xr = snap(xr);
-                        xi = snap(xi);
-                        double rv[2];
-#pragma unroll
-                        for (int p = 0; p < 2; ++p) {
-                            const double x = p ? xi : xr;
-                            const double y = __dmul_rn(x, cp.inv_td);
-                            double M = rint(y);
-                            if (k > 0) {
-                                const double fr = fabs(__dsub_rn(y, M));
-                                const double q = __dsub_rn(M, Mprev[p]);
-                                if (!(fabs(y) < 1073741824.0 && fr < 0.5 - 1.9073486328125e-06 && fabs(q) <= 32766.0)) {
-                                    double P = __dadd_rn(0.0, __dmul_rn(cp.td, Mprev[p]));
-                                    const int32_t t = ref_step(cp, P, x);
-                                    M = __dadd_rn(Mprev[p], (double)t);
-                                }
-                            }
-                            Mprev[p] = M;
-                            rv[p] = __dadd_rn(0.0, __dmul_rn(cp.td, M));
-                        }
-                        if ((long long)gi <= k_after) continue;
-                        const double t = __dadd_rn(__dmul_rn(rv[0], rv[0]), __dmul_rn(rv[1], rv[1]));
-                        const double y = t * to_units;
-                        const double ry = rint(y);
-                        const bool beyond = y >= 9007199254740992.0;
-                        const bool tie = !beyond && fabs(y - ry) == 0.5;
-                        const uint64_t c = beyond ? (1ull << 53) : (uint64_t)ry;
-                        if (beyond || tie || ms + acc + c >= (1ull << 53)) {
-                            S.ev_s = __dadd_rn((double)(ms + acc) / to_units, t);
-                            S.ev_k = (uint32_t)gi;
-                            S.ev_any = 1;
-                            if (a.counters) atomicAdd(&a.counters[tie ? 6 : 7], 1ull);
-                            break;
-                        }
-                        acc += c;
-                    }
+                const bool me = in_part ? tid == owner : (have && tid > owner && offx < LIM && sat_add(offx, mine) >= LIM);
+                if (me) {
+                    uA = in_part ? 0 : offx;
+                    walk(std::integral_constant<int, 3>{}, nullptr, to_units, k_after, nullptr, ms);
+                    S.ev_owner = tid;
                 }
                 __syncthreads();
                 if (!S.ev_any) {  // cannot happen; never spin
                     bail = true;
                     break;
                 }
-                s = S.ev_s;
-                k_after = (long long)S.ev_k;
-                if (!(s > 0.0 && ilogb(s) >= -960)) {
+                const double sn = S.ev_s;
+                const int e_old = ilogb(s), e_new = (sn > 0.0) ? ilogb(sn) : -100000;
+                if (!(sn > 0.0 && e_new >= -960 && e_new < 1000)) {
                     bail = true;
                     break;
                 }
-                loc = 0;
-                if (have && (long long)e0 + SUB - 1 > k_after)
-                    loc = walk(std::integral_constant<int, 1>{}, nullptr, ldexp(1.0, 52 - ilogb(s)), k_after, nullptr);
-                uint64_t u = loc;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) u = sat_add(u, __shfl_xor_sync(0xffffffffu, u, o));
-                __syncthreads();
-                if (wl == 0) S.wunits[wp] = u;
-                __syncthreads();
+                owner = S.ev_owner;
+                k_after = (long long)S.ev_k;
+                part = S.ev_part;
+                s = sn;
+                if (e_new == e_old) {
+                    // a tie inside the binade: the later lanes' units stand
+                } else if (e_new == e_old + 1 && hasB) {
+                    uA = uB;
+                    hasB = false;
+                } else {  // re-measure the later lanes under the new binade
+                    hasB = false;
+                    uA = 0;
+                    if (have && tid > owner) walk(std::integral_constant<int, 1>{}, nullptr, ldexp(1.0, 52 - e_new), -1, nullptr, 0);
+                }
             }
             if (tid == 0) S.s = s;
         }
