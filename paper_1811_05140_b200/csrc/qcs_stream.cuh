@@ -79,7 +79,8 @@ static_assert(sizeof(StreamSharedT<512>) <= 226 * 1024, "one 512-lane streaming 
 // (decode_sub's walk, one element per call).  `in` is 4-byte aligned; reads
 // up to 7 bytes past a token's first byte.
 struct TokReader {
-    const uint8_t* in;
+    const uint8_t* in;  // generic pointer to the staged bytes (slow paths)
+    uint32_t sa;        // the same as a shared-window address
     uint32_t pos;
     uint32_t skip;
     uint32_t zleft, wleft;
@@ -89,6 +90,7 @@ struct TokReader {
     __device__ __forceinline__ void init(const uint8_t* in_, int codec_, double td_, SideEntry se)
     {
         in = in_;
+        sa = (uint32_t)__cvta_generic_to_shared(in_);
         pos = se.off;
         codec = codec_;
         skip = se.skip;
@@ -98,8 +100,11 @@ struct TokReader {
     }
     __device__ __forceinline__ uint32_t fetch4(uint32_t at) const
     {
-        const uint32_t* p = reinterpret_cast<const uint32_t*>(in + (at & ~3u));
-        return __funnelshift_r(p[0], p[1], (at & 3u) << 3);
+        uint32_t lo, hi;
+        const uint32_t ad = sa + (at & ~3u);
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(ad));
+        asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(hi) : "r"(ad));
+        return __funnelshift_r(lo, hi, (at & 3u) << 3);
     }
     __device__ __forceinline__ double word()
     {
@@ -127,18 +132,20 @@ struct TokReader {
     // the next element's decoded value (before the stride scale)
     __device__ __forceinline__ double next()
     {
+        // (the window is read speculatively: inside a run it is not a token)
+        const uint32_t w = fetch4(pos);
+        const uint32_t m = ~w & 0x80808080u;
+        const uint32_t x = w & (m ^ (m - 1u));
+        const uint32_t v = (x & 0x7fu) | ((x >> 1) & 0x3f80u) | ((x >> 2) & 0x1fc000u) | ((x >> 3) & 0xfe00000u);
+        if ((zleft | wleft) == 0u && m != 0u && codec == 1 && (v & 3u) == 1u) {  // one nonzero code, <= 4 bytes
+            pos += (uint32_t)__ffs((int)m) >> 3;
+            const uint32_t z = v >> 2;
+            P = __dadd_rn(P, __dmul_rn(td, (double)((int)(z >> 1) ^ -(int)(z & 1u))));
+            return P;
+        }
         if ((zleft | wleft) == 0u) {
-            const uint32_t w = fetch4(pos);
-            const uint32_t m = ~w & 0x80808080u;
-            if (m != 0u) {  // a varint of up to 4 bytes
-                const uint32_t x = w & (m ^ (m - 1u));
-                const uint32_t v = (x & 0x7fu) | ((x >> 1) & 0x3f80u) | ((x >> 2) & 0x1fc000u) | ((x >> 3) & 0xfe00000u);
+            if (m != 0u) {  // a run token of up to 4 bytes
                 pos += (uint32_t)__ffs((int)m) >> 3;
-                if (codec == 1 && (v & 3u) == 1u) {  // one nonzero code
-                    const uint32_t z = v >> 2;
-                    P = __dadd_rn(P, __dmul_rn(td, (double)((int)(z >> 1) ^ -(int)(z & 1u))));
-                    return P;
-                }
                 return run_token(v);
             }
             uint64_t p64 = pos;
@@ -155,9 +162,9 @@ struct TokReader {
             return codec == 1 ? P : 0.0;
         }
         --wleft;
-        const double x = word();
-        if (codec == 1) P = x;
-        return x;
+        const double xw = word();
+        if (codec == 1) P = xw;
+        return xw;
     }
 };
 
@@ -263,14 +270,16 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                 hi = (uint64_t)nx.off + 10 + 8 * (uint64_t)nx.skip;
             }
             const uint64_t nb = hi > lo ? ((hi - lo + 15) & ~uint64_t(15)) : 0;
-            src[p] = in_bytes[p];
+            src[p] = S.in[p] - lo;
             if (nb > 0 && nb <= ST_STAGE) {  // uniform over the CTA
                 if (tid == 0) bulk_g2s(S.in[p], in_bytes[p] + lo, (unsigned)nb, &S.bar[p]);
                 mbar_wait(&S.bar[p], stage_phase[p]);
                 stage_phase[p] ^= 1u;
-                src[p] = S.in[p] - lo;
+            } else {  // more than 3 bytes per element: poorly compressed input, the legacy encoder's
+                bail = true;
             }
         }
+        if (bail) break;
         const double s_in = S.s;  // the running sum entering this iteration (uniform)
         const bool have_tu = s_in > 0.0 && ilogb(s_in) >= -960;
         const double tu_main = have_tu ? ldexp(1.0, 52 - ilogb(s_in)) : 0.0;
@@ -383,32 +392,30 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                                 !same_bits(__dmul_rn(td, (double)M), P))
                                 bad = true;
                         }
-                        if (PASS == 0) {
-                            if (q == 0) {
-                                ++run[p];
-                            } else {
-                                const uint32_t z = ((uint32_t)q << 1) ^ (uint32_t)(q >> 31);
-                                const uint32_t v = (z << 2) | 1u;
-                                uint32_t len = 1u + (v >= 128u) + (v >= 16384u);
-                                uint32_t pk = (v & 0x7fu) | ((v & 0x3f80u) << 1) | ((v & 0x1fc000u) << 2) |
-                                              (len > 1u ? 0x80u : 0u) | (len > 2u ? 0x8000u : 0u);
-                                if (!po[p].seen) {
-                                    po[p].seen = true;
-                                    po[p].lz1 = run[p];
-                                } else if (run[p] > 0) {  // the zero run before it (< 32: one byte)
-                                    pk = (pk << 8) | ((uint32_t)run[p] << 2);
-                                    ++len;
-                                }
-                                acc[p] |= (uint64_t)pk << (8 * fill[p]);
-                                fill[p] += (int)len;
-                                if (fill[p] >= 4) {
-                                    *reinterpret_cast<uint32_t*>(rowp[p] + woff[p]) = (uint32_t)acc[p];
-                                    acc[p] >>= 32;
-                                    woff[p] += 4;
-                                    fill[p] -= 4;
-                                }
-                                run[p] = 0;
-                            }
+                        if (PASS == 0) {  // (branch-free: lanes differ at every step)
+                            const bool nz = q != 0;
+                            const uint32_t z = ((uint32_t)q << 1) ^ (uint32_t)(q >> 31);
+                            const uint32_t v = (z << 2) | 1u;
+                            const bool l2 = v >= 128u, l3 = v >= 16384u;
+                            uint32_t len = 1u + (uint32_t)l2 + (uint32_t)l3;
+                            uint32_t pk = (v & 0x7fu) | ((v & 0x3f80u) << 1) | ((v & 0x1fc000u) << 2) |
+                                          (l2 ? 0x80u : 0u) | (l3 ? 0x8000u : 0u);
+                            // the zero run before it (< 32: one byte), unless it is the lane's leading run
+                            const bool hr = nz && po[p].seen && run[p] > 0;
+                            pk = hr ? (pk << 8) | ((uint32_t)run[p] << 2) : pk;
+                            len += (uint32_t)hr;
+                            po[p].lz1 = (nz && !po[p].seen) ? run[p] : po[p].lz1;
+                            po[p].seen = po[p].seen || nz;
+                            pk = nz ? pk : 0u;
+                            len = nz ? len : 0u;
+                            acc[p] |= (uint64_t)pk << (8 * fill[p]);
+                            fill[p] += (int)len;
+                            const bool fl = fill[p] >= 4;
+                            if (fl) *reinterpret_cast<uint32_t*>(rowp[p] + woff[p]) = (uint32_t)acc[p];
+                            acc[p] = fl ? acc[p] >> 32 : acc[p];
+                            woff[p] += fl ? 4 : 0;
+                            fill[p] -= fl ? 4 : 0;
+                            run[p] = nz ? 0 : run[p] + 1;
                         }
                     }
                     Mprev[p] = M;
@@ -605,23 +612,31 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
         // copy the rows out, 32 consecutive bytes per store, and the side index
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-            const uint32_t my_nb = nbytes[p];
-            const uint32_t my_lead = lead_len[p];
-            for (unsigned todo = __ballot_sync(0xffffffffu, my_nb != 0u); todo; todo &= todo - 1u) {
-                const int j = __ffs(todo) - 1;
-                const uint32_t nb = __shfl_sync(0xffffffffu, my_nb, j);
-                const uint32_t ld = __shfl_sync(0xffffffffu, my_lead, j);
-                const uint64_t bs = __shfl_sync(0xffffffffu, bstart[p], j);
-                const uint8_t* srow = S.rows + (size_t)(p * ST_LANES + (tid & ~31) + j) * ST_ROW + ST_LEAD - ld;
-                uint8_t* dst = out[p] + bs;
-                if (nb <= 64u) {
-                    const uint8_t b0 = wl < nb ? srow[wl] : (uint8_t)0;
-                    const uint8_t b1 = wl + 32u < nb ? srow[wl + 32u] : (uint8_t)0;
-                    if (wl < nb) dst[wl] = b0;
-                    if (wl + 32u < nb) dst[wl + 32u] = b1;
-                } else {
-                    for (uint32_t k = wl; k < nb; k += 32) dst[k] = srow[k];
+            // every lane stores its own bytes: bytes up to the first 4-byte
+            // boundary of the destination, aligned words (one shared word
+            // read and a funnel shift each), bytes again for the tail — the
+            // boundary words are shared with the neighbour lanes' bytes
+            if (nbytes[p] != 0u) {
+                const uint32_t nb = nbytes[p];
+                uint8_t* dst = out[p] + bstart[p];
+                const uint8_t* srow = S.rows + (size_t)(p * ST_LANES + tid) * ST_ROW + ST_LEAD - lead_len[p];
+                uint32_t i = 0;
+                const uint32_t head = min(nb, (uint32_t)((0u - (uint32_t)(uintptr_t)dst) & 3u));
+                for (; i < head; ++i) dst[i] = srow[i];
+                if (i + 4u <= nb) {
+                    const uint32_t sad = (uint32_t)__cvta_generic_to_shared(srow + i);
+                    const uint32_t sh = (sad & 3u) << 3;
+                    uint32_t wa = sad & ~3u, lo;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(wa) : "memory");
+                    for (; i + 4u <= nb; i += 4u) {
+                        uint32_t hi;
+                        wa += 4u;
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi) : "r"(wa) : "memory");
+                        *reinterpret_cast<uint32_t*>(dst + i) = __funnelshift_r(lo, hi, sh);
+                        lo = hi;
+                    }
                 }
+                for (; i < nb; ++i) dst[i] = srow[i];
             }
             if (have) {
                 SideEntry se;
