@@ -135,14 +135,16 @@ struct TokReader {
         // (the window is read speculatively: inside a run it is not a token)
         const uint32_t w = fetch4(pos);
         const uint32_t m = ~w & 0x80808080u;
-        const uint32_t x = w & (m ^ (m - 1u));
-        const uint32_t v = (x & 0x7fu) | ((x >> 1) & 0x3f80u) | ((x >> 2) & 0x1fc000u) | ((x >> 3) & 0xfe00000u);
-        if ((zleft | wleft) == 0u && m != 0u && codec == 1 && (v & 3u) == 1u) {  // one nonzero code, <= 4 bytes
-            pos += (uint32_t)__ffs((int)m) >> 3;
-            const uint32_t z = v >> 2;
+        const uint32_t tm = m ^ (m - 1u);  // the token's bits (m != 0)
+        const uint32_t x = w & tm;
+        // lossy code token (tag 1 in the first byte) of up to 4 bytes, no run pending
+        if (((zleft | wleft) | (uint32_t)(codec ^ 1) | ((w & 3u) ^ 1u)) == 0u && m != 0u) {
+            pos += (uint32_t)__popc(tm & 0x01010101u);
+            const uint32_t z = ((x >> 2) & 0x1fu) | ((x >> 3) & 0xfe0u) | ((x >> 4) & 0x7f000u) | ((x >> 5) & 0x3f80000u);
             P = __dadd_rn(P, __dmul_rn(td, (double)((int)(z >> 1) ^ -(int)(z & 1u))));
             return P;
         }
+        const uint32_t v = (x & 0x7fu) | ((x >> 1) & 0x3f80u) | ((x >> 2) & 0x1fc000u) | ((x >> 3) & 0xfe00000u);
         if ((zleft | wleft) == 0u) {
             if (m != 0u) {  // a run token of up to 4 bytes
                 pos += (uint32_t)__ffs((int)m) >> 3;
@@ -314,13 +316,11 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             for (int p = 0; p < 2; ++p) rd[p].init(src[p], in_codec[p], in_td[p], in_side[p][e0 / SUB]);
             int Mprev[2] = {0, 0};
             int run[2] = {0, 0};
-            uint64_t acc[2] = {0, 0};  // token bytes not yet stored
-            int fill[2] = {0, 0}, woff[2] = {0, 0};
-            uint8_t* rowp[2] = {nullptr, nullptr};
+            uint32_t wa[2] = {0, 0}, wa0[2] = {0, 0};  // shared-window address of the next token byte / the body
             if (PASS == 0) {
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
-                    rowp[p] = S.rows + (size_t)(p * ST_LANES + tid) * ST_ROW + ST_LEAD;
+                    wa0[p] = wa[p] = (uint32_t)__cvta_generic_to_shared(S.rows + (size_t)(p * ST_LANES + tid) * ST_ROW + ST_LEAD);
                     po[p].seen = false;
                     po[p].lz1 = 0;
                 }
@@ -392,30 +392,29 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                                 !same_bits(__dmul_rn(td, (double)M), P))
                                 bad = true;
                         }
-                        if (PASS == 0) {  // (branch-free: lanes differ at every step)
-                            const bool nz = q != 0;
-                            const uint32_t z = ((uint32_t)q << 1) ^ (uint32_t)(q >> 31);
-                            const uint32_t v = (z << 2) | 1u;
-                            const bool l2 = v >= 128u, l3 = v >= 16384u;
-                            uint32_t len = 1u + (uint32_t)l2 + (uint32_t)l3;
-                            uint32_t pk = (v & 0x7fu) | ((v & 0x3f80u) << 1) | ((v & 0x1fc000u) << 2) |
-                                          (l2 ? 0x80u : 0u) | (l3 ? 0x8000u : 0u);
-                            // the zero run before it (< 32: one byte), unless it is the lane's leading run
-                            const bool hr = nz && po[p].seen && run[p] > 0;
-                            pk = hr ? (pk << 8) | ((uint32_t)run[p] << 2) : pk;
-                            len += (uint32_t)hr;
-                            po[p].lz1 = (nz && !po[p].seen) ? run[p] : po[p].lz1;
-                            po[p].seen = po[p].seen || nz;
-                            pk = nz ? pk : 0u;
-                            len = nz ? len : 0u;
-                            acc[p] |= (uint64_t)pk << (8 * fill[p]);
-                            fill[p] += (int)len;
-                            const bool fl = fill[p] >= 4;
-                            if (fl) *reinterpret_cast<uint32_t*>(rowp[p] + woff[p]) = (uint32_t)acc[p];
-                            acc[p] = fl ? acc[p] >> 32 : acc[p];
-                            woff[p] += fl ? 4 : 0;
-                            fill[p] -= fl ? 4 : 0;
-                            run[p] = nz ? 0 : run[p] + 1;
+                        if (PASS == 0) {
+                            if (q == 0) {
+                                ++run[p];
+                            } else {
+                                if (!po[p].seen) {  // the lane's leading zero run goes with the lead tokens
+                                    po[p].seen = true;
+                                    po[p].lz1 = run[p];
+                                } else if (run[p] > 0) {  // a zero run inside the lane (< 32: one byte)
+                                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(wa[p]), "r"((uint32_t)run[p] << 2) : "memory");
+                                    ++wa[p];
+                                }
+                                run[p] = 0;
+                                // the code token, 1..3 bytes
+                                const uint32_t z = ((uint32_t)q << 1) ^ (uint32_t)(q >> 31);
+                                const uint32_t v = (z << 2) | 1u;
+                                const bool l2 = v >= 128u, l3 = v >= 16384u;
+                                asm volatile("st.shared.u8 [%0], %1;" ::"r"(wa[p]), "r"((v & 0x7fu) | (l2 ? 0x80u : 0u)) : "memory");
+                                if (l2)
+                                    asm volatile("st.shared.u8 [%0+1], %1;" ::"r"(wa[p]), "r"(((v >> 7) & 0x7fu) | (l3 ? 0x80u : 0u))
+                                                 : "memory");
+                                if (l3) asm volatile("st.shared.u8 [%0+2], %1;" ::"r"(wa[p]), "r"(v >> 14) : "memory");
+                                wa[p] += 1u + (uint32_t)l2 + (uint32_t)l3;
+                            }
                         }
                     }
                     Mprev[p] = M;
@@ -463,8 +462,7 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             if (PASS == 0) {
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
-                    *reinterpret_cast<uint32_t*>(rowp[p] + woff[p]) = (uint32_t)acc[p];
-                    po[p].body = woff[p] + fill[p];
+                    po[p].body = (int)(wa[p] - wa0[p]);
                     po[p].Mlast = Mprev[p];
                     po[p].tz = run[p];
                     if (!po[p].seen) po[p].lz1 = SUB - 1;
