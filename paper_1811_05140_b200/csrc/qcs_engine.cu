@@ -938,6 +938,10 @@ int launch_stream_t(const FusedArgs& a, uint8_t* redo, uint64_t grid, cudaStream
 // streaming kernel (qcs_stream.cuh): CTA width by the slots per SM of the launch
 int launch_stream(const FusedArgs& a, uint8_t* redo, uint64_t grid, cudaStream_t s)
 {
+    static const int force_t = getenv("QCS_STREAM_LANES") ? atoi(getenv("QCS_STREAM_LANES")) : 0;  // experiments
+    if (force_t == 128) return launch_stream_t<128>(a, redo, grid, s);
+    if (force_t == 256) return launch_stream_t<256>(a, redo, grid, s);
+    if (force_t == 512) return launch_stream_t<512>(a, redo, grid, s);
     if (grid >= 8 * 148) return launch_stream_t<128>(a, redo, grid, s);
     if (grid >= 4 * 148) return launch_stream_t<256>(a, redo, grid, s);
     return launch_stream_t<512>(a, redo, grid, s);
@@ -1184,10 +1188,27 @@ __global__ void k_set_mean(Dev d, double mr, double mi)
     d.sc->mean[1] = mi;
 }
 
+// CTA-wide copy of n16 16-byte words, four independent loads in flight per
+// thread (the plain one-load loop left the copy kernels at ~2 TB/s)
+__device__ __forceinline__ void cta_copy16(uint4* __restrict__ dst, const uint4* __restrict__ src, uint64_t n16)
+{
+    const uint64_t T = blockDim.x;
+    uint64_t i = threadIdx.x;
+    for (; i + 3 * T < n16; i += 4 * T) {
+        const uint4 a = __ldcs(src + i), b = __ldcs(src + i + T), c = __ldcs(src + i + 2 * T), e = __ldcs(src + i + 3 * T);
+        dst[i] = a;
+        dst[i + T] = b;
+        dst[i + 2 * T] = c;
+        dst[i + 3 * T] = e;
+    }
+    for (; i < n16; i += T) dst[i] = __ldcs(src + i);
+}
+
 // Wave mode: install the wave's new blocks at host-chosen arena offsets
 // (new_off), replace the side index, tables, scale and sum (the staged commit
 // of aalc.cpp:395-408, one wave at a time).
-__global__ void __launch_bounds__(128) k_wave_commit(Dev d, LevelTag lt, uint64_t s0)
+constexpr int COPY_THREADS = 256;
+__global__ void __launch_bounds__(COPY_THREADS) k_wave_commit(Dev d, LevelTag lt, uint64_t s0)
 {
     if (d.sc->err) return;
     const uint64_t loc = blockIdx.x >> 1;
@@ -1199,10 +1220,11 @@ __global__ void __launch_bounds__(128) k_wave_commit(Dev d, LevelTag lt, uint64_
     const uint64_t dst_off = d.new_off[2 * slot + c];
     const uint4* s4 = reinterpret_cast<const uint4*>(d.slot_out + (2 * loc + c) * d.slot_cap);
     uint4* d4 = reinterpret_cast<uint4*>(d.arena[0] + dst_off);
-    for (uint64_t i = threadIdx.x; i < (len + 15) / 16; i += blockDim.x) d4[i] = s4[i];
+    cta_copy16(d4, s4, (len + 15) / 16);
     const SideEntry* ss = d.slot_side + (2 * loc + c) * d.nsub;
     SideEntry* ds = d.side + g * d.nsub;
-    for (uint64_t i = threadIdx.x; i < d.nsub; i += blockDim.x) ds[i] = ss[i];
+    static_assert(sizeof(SideEntry) == 16, "side entries copy as 16-byte words");
+    cta_copy16(reinterpret_cast<uint4*>(ds), reinterpret_cast<const uint4*>(ss), d.nsub);
     if (threadIdx.x == 0) {
         atomicAdd((unsigned long long*)&d.sc->gate_cin, (unsigned long long)(HEADER_BYTES + d.p_len[g]));
         d.p_off[g] = dst_off;
@@ -1304,13 +1326,13 @@ __global__ void __launch_bounds__(ALLOC_THREADS) k_precheck(Dev d, uint64_t n_sl
 
 // Byte moves for compaction: item i copies len[i] bytes from src+so[i] to
 // dst+do[i] (16-byte aligned; one CTA per item).
-__global__ void __launch_bounds__(128) k_move(const uint8_t* src, uint8_t* dst, const uint64_t* so,
+__global__ void __launch_bounds__(COPY_THREADS) k_move(const uint8_t* src, uint8_t* dst, const uint64_t* so,
                                               const uint64_t* dof, const uint64_t* len)
 {
     const uint64_t i = blockIdx.x;
     const uint4* s4 = reinterpret_cast<const uint4*>(src + so[i]);
     uint4* d4 = reinterpret_cast<uint4*>(dst + dof[i]);
-    for (uint64_t k = threadIdx.x; k < (len[i] + 15) / 16; k += blockDim.x) d4[k] = s4[k];
+    cta_copy16(d4, s4, (len[i] + 15) / 16);
 }
 
 inline uint64_t round16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
@@ -1351,9 +1373,9 @@ int compact_arena_impl(qcs_dev_state* st)
         CU(cudaMemcpyAsync(st->mv_src, bs.data(), 8 * m, cudaMemcpyHostToDevice, s));
         CU(cudaMemcpyAsync(st->mv_dst, bt.data(), 8 * m, cudaMemcpyHostToDevice, s));
         CU(cudaMemcpyAsync(st->mv_len, bl.data(), 8 * m, cudaMemcpyHostToDevice, s));
-        k_move<<<(unsigned)m, 128, 0, s>>>(d.arena[0], X, st->mv_src, st->mv_dst, st->mv_len);
+        k_move<<<(unsigned)m, COPY_THREADS, 0, s>>>(d.arena[0], X, st->mv_src, st->mv_dst, st->mv_len);
         CU(cudaMemcpyAsync(st->mv_src, bd.data(), 8 * m, cudaMemcpyHostToDevice, s));
-        k_move<<<(unsigned)m, 128, 0, s>>>(X, d.arena[0], st->mv_dst, st->mv_src, st->mv_len);
+        k_move<<<(unsigned)m, COPY_THREADS, 0, s>>>(X, d.arena[0], st->mv_dst, st->mv_src, st->mv_len);
         st->launches += 2;
         CU(cudaGetLastError());
         CU(cudaStreamSynchronize(s));  // the host vectors are reused
@@ -1430,7 +1452,7 @@ int big_commit_wave(qcs_dev_state* st, uint64_t s0, uint64_t s1, uint64_t gate_i
     }
     CU(cudaMemcpyAsync(d.new_off + 2 * s0, nof.data(), 8 * m, cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(&d.sc->bump, &st->bump, 8, cudaMemcpyHostToDevice, s));
-    k_wave_commit<<<(unsigned)m, 128, 0, s>>>(d, st->lt, s0);
+    k_wave_commit<<<(unsigned)m, COPY_THREADS, 0, s>>>(d, st->lt, s0);
     ++st->launches;
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(s));  // nof / bump are host locals
@@ -1747,7 +1769,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         if (st->big) {  // place (device bump) and install the wave: no host round trip
             prof_start(st, 3);
             k_wave_alloc<<<1, ALLOC_THREADS, 0, s>>>(d, s0, 2 * nw, u0);
-            k_wave_commit<<<(unsigned)(2 * nw), 128, 0, s>>>(d, st->lt, s0);
+            k_wave_commit<<<(unsigned)(2 * nw), COPY_THREADS, 0, s>>>(d, st->lt, s0);
             prof_stop(st);
             st->launches += 2;
         }

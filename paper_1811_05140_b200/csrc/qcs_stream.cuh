@@ -328,16 +328,38 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             uint64_t la = PASS == 3 ? uA : 0, lb = 0;
             bool eva = false, evb = false, bad = false, found = false;
             double tu2 = 0.0;
-#pragma unroll 2
-            for (int k = 0; k < SUB; ++k) {
-                double xr = rd[0].next(), xi = rd[1].next();
+            // the next element of both planes: the usual case (both streams at a
+            // nonzero code token) in one straight line, anything else by next()
+            auto next2 = [&](double& xr, double& xi) {
+                const uint32_t w0 = rd[0].fetch4(rd[0].pos), w1 = rd[1].fetch4(rd[1].pos);
+                const uint32_t m0 = ~w0 & 0x80808080u, m1 = ~w1 & 0x80808080u;
+                const uint32_t t0 = m0 ^ (m0 - 1u), t1 = m1 ^ (m1 - 1u);
+                const uint32_t x0 = w0 & t0, x1 = w1 & t1;
+                const uint32_t busy = rd[0].zleft | rd[0].wleft | rd[1].zleft | rd[1].wleft |
+                                      (uint32_t)(rd[0].codec ^ 1) | (uint32_t)(rd[1].codec ^ 1) | ((w0 & 3u) ^ 1u) |
+                                      ((w1 & 3u) ^ 1u);
+                const uint32_t z0 = ((x0 >> 2) & 0x1fu) | ((x0 >> 3) & 0xfe0u) | ((x0 >> 4) & 0x7f000u) | ((x0 >> 5) & 0x3f80000u);
+                const uint32_t z1 = ((x1 >> 2) & 0x1fu) | ((x1 >> 3) & 0xfe0u) | ((x1 >> 4) & 0x7f000u) | ((x1 >> 5) & 0x3f80000u);
+                const double P0 = __dadd_rn(rd[0].P, __dmul_rn(rd[0].td, (double)((int)(z0 >> 1) ^ -(int)(z0 & 1u))));
+                const double P1 = __dadd_rn(rd[1].P, __dmul_rn(rd[1].td, (double)((int)(z1 >> 1) ^ -(int)(z1 & 1u))));
+                if (busy == 0u && m0 != 0u && m1 != 0u) {
+                    rd[0].pos += (uint32_t)__popc(t0 & 0x01010101u);
+                    rd[1].pos += (uint32_t)__popc(t1 & 0x01010101u);
+                    rd[0].P = xr = P0;
+                    rd[1].P = xi = P1;
+                } else {
+                    xr = rd[0].next();
+                    xi = rd[1].next();
+                }
+            };
+            // scale, gate (run_plan_unit, gate.cpp:405-454) and snap of element k:
+            // every element on its own — apply_pair with a zero partner, minus its
+            // exact-zero terms (they change a zero's sign at most: snapped)
+            auto gate_snap = [&](int k, double& xr, double& xi) {
                 if (sc) {
                     xr = __dmul_rn(xr, scale);
                     xi = __dmul_rn(xi, scale);
                 }
-                // gate (run_plan_unit, gate.cpp:405-454), every element on its
-                // own: apply_pair with a zero partner, minus its exact-zero
-                // terms (they change a zero's sign at most: snapped)
                 if (kind <= 1) {
                     bool on = gate_on;
                     double ur = gur, ui = gui;
@@ -348,12 +370,10 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                         ur = sd ? a.u[6] : a.u[0];
                         ui = sd ? a.u[7] : a.u[1];
                     }
-                    if (on) {
-                        const double orr = __dsub_rn(__dmul_rn(ur, xr), __dmul_rn(ui, xi));
-                        const double oi = __dadd_rn(__dmul_rn(ur, xi), __dmul_rn(ui, xr));
-                        xr = orr;
-                        xi = oi;
-                    }
+                    const double orr = __dsub_rn(__dmul_rn(ur, xr), __dmul_rn(ui, xi));
+                    const double oi = __dadd_rn(__dmul_rn(ur, xi), __dmul_rn(ui, xr));
+                    xr = on ? orr : xr;
+                    xi = on ? oi : xi;
                 } else if (kind == 2) {
                     if ((uint64_t)e0 + (uint64_t)k == a.flip_off) {
                         xr = -xr;
@@ -365,62 +385,42 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                 }
                 xr = snap(xr);
                 xi = snap(xi);
-                // quantize on the lattice anchored at 0
-                double rv[2];
-#pragma unroll
-                for (int p = 0; p < 2; ++p) {
-                    const double x = p ? xi : xr;
-                    const double y = __dmul_rn(x, inv_td);
-                    int M = __double2int_rn(y);
-                    const double fr = fabs(__dsub_rn(y, (double)M));
-                    bool good = fabs(y) < 1073741824.0 && fr < 0.5 - 1.9073486328125e-06;
-                    if (k == 0) {
-                        if (PASS == 0) {
-                            po[p].M0 = M;
-                            po[p].x0 = x;
-                            po[p].good0 = good;
-                        }
-                    } else {
-                        int q = M - Mprev[p];
-                        good = good && (unsigned)(q + 32766) <= 65532u;
-                        if (!good) {  // the reference step from the exact predictor
-                            double P = __dmul_rn(td, (double)Mprev[p]);
-                            const int32_t t = ref_step(a.cp, P, x);
-                            M = Mprev[p] + t;
-                            q = t;
-                            if (t == WCODE || M <= -1073741824 || M >= 1073741824 ||
-                                !same_bits(__dmul_rn(td, (double)M), P))
-                                bad = true;
-                        }
-                        if (PASS == 0) {
-                            if (q == 0) {
-                                ++run[p];
-                            } else {
-                                if (!po[p].seen) {  // the lane's leading zero run goes with the lead tokens
-                                    po[p].seen = true;
-                                    po[p].lz1 = run[p];
-                                } else if (run[p] > 0) {  // a zero run inside the lane (< 32: one byte)
-                                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(wa[p]), "r"((uint32_t)run[p] << 2) : "memory");
-                                    ++wa[p];
-                                }
-                                run[p] = 0;
-                                // the code token, 1..3 bytes
-                                const uint32_t z = ((uint32_t)q << 1) ^ (uint32_t)(q >> 31);
-                                const uint32_t v = (z << 2) | 1u;
-                                const bool l2 = v >= 128u, l3 = v >= 16384u;
-                                asm volatile("st.shared.u8 [%0], %1;" ::"r"(wa[p]), "r"((v & 0x7fu) | (l2 ? 0x80u : 0u)) : "memory");
-                                if (l2)
-                                    asm volatile("st.shared.u8 [%0+1], %1;" ::"r"(wa[p]), "r"(((v >> 7) & 0x7fu) | (l3 ? 0x80u : 0u))
-                                                 : "memory");
-                                if (l3) asm volatile("st.shared.u8 [%0+2], %1;" ::"r"(wa[p]), "r"(v >> 14) : "memory");
-                                wa[p] += 1u + (uint32_t)l2 + (uint32_t)l3;
-                            }
-                        }
-                    }
-                    Mprev[p] = M;
-                    rv[p] = __dmul_rn(td, (double)M);
+            };
+            // the reference step of plane p from the exact predictor (a step the lattice test does not prove)
+            auto slow_step = [&](int p, double x, int& M, int& q) {
+                double P = __dmul_rn(td, (double)Mprev[p]);
+                const int32_t t = ref_step(a.cp, P, x);
+                M = Mprev[p] + t;
+                q = t;
+                if (t == WCODE || M <= -1073741824 || M >= 1073741824 || !same_bits(__dmul_rn(td, (double)M), P)) bad = true;
+            };
+            // token(s) of code q of plane p (PASS 0): any case
+            auto emit_any = [&](int p, int q) {
+                if (q == 0) {
+                    ++run[p];
+                    return;
                 }
-                const double t = __dadd_rn(__dmul_rn(rv[0], rv[0]), __dmul_rn(rv[1], rv[1]));
+                if (!po[p].seen) {  // the lane's leading zero run goes with the lead tokens
+                    po[p].seen = true;
+                    po[p].lz1 = run[p];
+                } else if (run[p] > 0) {  // a zero run inside the lane (< 32: one byte)
+                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(wa[p]), "r"((uint32_t)run[p] << 2) : "memory");
+                    ++wa[p];
+                }
+                run[p] = 0;
+                const uint32_t z = ((uint32_t)q << 1) ^ (uint32_t)(q >> 31);
+                const uint32_t v = (z << 2) | 1u;
+                const bool l2 = v >= 128u, l3 = v >= 16384u;
+                asm volatile("st.shared.u8 [%0], %1;" ::"r"(wa[p]), "r"((v & 0x7fu) | (l2 ? 0x80u : 0u)) : "memory");
+                if (l2)
+                    asm volatile("st.shared.u8 [%0+1], %1;" ::"r"(wa[p]), "r"(((v >> 7) & 0x7fu) | (l3 ? 0x80u : 0u)) : "memory");
+                if (l3) asm volatile("st.shared.u8 [%0+2], %1;" ::"r"(wa[p]), "r"(v >> 14) : "memory");
+                wa[p] += 1u + (uint32_t)l2 + (uint32_t)l3;
+            };
+            // sum-of-squares bookkeeping of element k from the lattice indices
+            auto sums = [&](int k, int M0, int M1) {
+                const double r0v = __dmul_rn(td, (double)M0), r1v = __dmul_rn(td, (double)M1);
+                const double t = __dadd_rn(__dmul_rn(r0v, r0v), __dmul_rn(r1v, r1v));
                 if (PASS == 0 || PASS == 1) {
                     const double y0 = t * tu;
                     const double r0 = rint(y0);
@@ -458,6 +458,65 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                         }
                     }
                 }
+            };
+            // element 0: its code needs the left neighbour's last index (step C)
+            {
+                double xr, xi;
+                next2(xr, xi);
+                gate_snap(0, xr, xi);
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const double x = p ? xi : xr;
+                    const double y = __dmul_rn(x, inv_td);
+                    const int M = __double2int_rn(y);
+                    const double fr = fabs(__dsub_rn(y, (double)M));
+                    if (PASS == 0) {
+                        po[p].M0 = M;
+                        po[p].x0 = x;
+                        po[p].good0 = fabs(y) < 1073741824.0 && fr < 0.5 - 1.9073486328125e-06;
+                    }
+                    Mprev[p] = M;
+                }
+                sums(0, Mprev[0], Mprev[1]);
+            }
+#pragma unroll 2
+            for (int k = 1; k < SUB; ++k) {
+                double xr, xi;
+                next2(xr, xi);
+                gate_snap(k, xr, xi);
+                // quantize on the lattice anchored at 0, both planes side by side
+                const double y0 = __dmul_rn(xr, inv_td), y1 = __dmul_rn(xi, inv_td);
+                int M0 = __double2int_rn(y0), M1 = __double2int_rn(y1);
+                const double f0 = fabs(__dsub_rn(y0, (double)M0)), f1 = fabs(__dsub_rn(y1, (double)M1));
+                int q0 = M0 - Mprev[0], q1 = M1 - Mprev[1];
+                const bool g0 = fabs(y0) < 1073741824.0 && f0 < 0.5 - 1.9073486328125e-06 && (unsigned)(q0 + 32766) <= 65532u;
+                const bool g1 = fabs(y1) < 1073741824.0 && f1 < 0.5 - 1.9073486328125e-06 && (unsigned)(q1 + 32766) <= 65532u;
+                if (!(g0 && g1)) {
+                    if (!g0) slow_step(0, xr, M0, q0);
+                    if (!g1) slow_step(1, xi, M1, q1);
+                }
+                if (PASS == 0) {
+                    if (q0 != 0 && q1 != 0 && (run[0] | run[1]) == 0 && po[0].seen && po[1].seen) {
+                        // two code tokens, nothing else: one straight line
+                        const uint32_t z0 = ((uint32_t)q0 << 1) ^ (uint32_t)(q0 >> 31), z1 = ((uint32_t)q1 << 1) ^ (uint32_t)(q1 >> 31);
+                        const uint32_t v0 = (z0 << 2) | 1u, v1 = (z1 << 2) | 1u;
+                        const bool a2 = v0 >= 128u, a3 = v0 >= 16384u, b2 = v1 >= 128u, b3 = v1 >= 16384u;
+                        asm volatile("st.shared.u8 [%0], %1;" ::"r"(wa[0]), "r"((v0 & 0x7fu) | (a2 ? 0x80u : 0u)) : "memory");
+                        asm volatile("st.shared.u8 [%0], %1;" ::"r"(wa[1]), "r"((v1 & 0x7fu) | (b2 ? 0x80u : 0u)) : "memory");
+                        if (a2) asm volatile("st.shared.u8 [%0+1], %1;" ::"r"(wa[0]), "r"(((v0 >> 7) & 0x7fu) | (a3 ? 0x80u : 0u)) : "memory");
+                        if (b2) asm volatile("st.shared.u8 [%0+1], %1;" ::"r"(wa[1]), "r"(((v1 >> 7) & 0x7fu) | (b3 ? 0x80u : 0u)) : "memory");
+                        if (a3) asm volatile("st.shared.u8 [%0+2], %1;" ::"r"(wa[0]), "r"(v0 >> 14) : "memory");
+                        if (b3) asm volatile("st.shared.u8 [%0+2], %1;" ::"r"(wa[1]), "r"(v1 >> 14) : "memory");
+                        wa[0] += 1u + (uint32_t)a2 + (uint32_t)a3;
+                        wa[1] += 1u + (uint32_t)b2 + (uint32_t)b3;
+                    } else {
+                        emit_any(0, q0);
+                        emit_any(1, q1);
+                    }
+                }
+                Mprev[0] = M0;
+                Mprev[1] = M1;
+                sums(k, M0, M1);
             }
             if (PASS == 0) {
 #pragma unroll
