@@ -862,7 +862,8 @@ def run_c3(args, rank, world, local_rank):
     achieved = (cin + cout) / (t_f * 1e-9) / 1e9 if t_f else 0.0
     path_gbs = (cin + cout) / (dev_ns * 1e-9) / 1e9
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic_k_fused_c3.json")
+    streamed = ctr.get("stream_slots", 0) > 0
+    tp = os.path.join(ROOT, "profiles", "traffic_k_stream_c3.json" if streamed else "traffic_k_fused_c3.json")
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f)
@@ -871,15 +872,20 @@ def run_c3(args, rank, world, local_rank):
         if tj.get("traffic_per_algorithmic_byte"):
             traffic = tj["traffic_per_algorithmic_byte"] * (cin + cout) / max(1, n_f)
     tot_all = max(1.0, sum(v[0] for v in kt_all.values()))
-    roofline = {"bound": "hbm", "kernel": "k_fused", "achieved": achieved, "peak": peak, "unit": "GB/s",
+    roofline = {"bound": "hbm", "kernel": "k_stream" if streamed else "k_fused",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "traffic_source": ("ncu --set full of the encoder on the C3 shape at n = 28 (tools/profile_c3.py, "
-                                   "profiles/traffic_k_fused_c3.json): its DRAM bytes per algorithmic byte "
+                "traffic_source": (f"ncu --set full of the encoder on the C3 shape at n = 28 (tools/profile_c3.py, "
+                                   f"profiles/{os.path.basename(tp)}): its DRAM bytes per algorithmic byte "
                                    "times this run's algorithmic bytes per launch") if traffic else None,
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": (cin + cout) / max(1, n_f),
                 "algorithmic_bytes": "C_in + C_out of the gates' rewritten strides, 29-byte headers included "
-                                     "(SURVEY.md §8d), over the k_fused launches of the timed steps",
+                                     "(SURVEY.md §8d), over the encoder launches of the timed steps (one per wave: "
+                                     "the streaming kernel k_stream, then the legacy encoder k_fused for the slots "
+                                     "it left, timed together)",
+                "encoder_slots": {"streamed": ctr.get("stream_slots", 0),
+                                  "left_to_legacy_encoder": ctr.get("stream_left_slots", 0)},
                 "avg_launch_us": t_f / max(1, n_f) / 1e3,
                 "path_C_in_plus_C_out_GBps": path_gbs, "path_frac": path_gbs / peak,
                 "kernel_share": {k: v[0] / tot_all for k, v in kt_all.items()},

@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
     }
     unsigned stage_phase[2] = {0, 0};
     bool bail = false;  // uniform over the CTA
+    int why = 0;        // why the slot was left (counters[19 + why]): 0 input not staged, 1 unproven step, 2 first element, 3 sum head, 4 sum event
     __syncthreads();
 
     for (uint64_t base = 0; base < n; base += ST_ITER) {
@@ -546,6 +547,7 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
         }
         if (__syncthreads_or(!ok)) {
             bail = true;
+            why = 1;
             break;
         }
 
@@ -590,6 +592,7 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
         }
         if (__syncthreads_or(bad)) {
             bail = true;
+            why = 2;
             break;
         }
         uint32_t lead_len[2] = {0, 0}, nbytes[2] = {0, 0}, ent[2] = {0, 0};
@@ -746,6 +749,7 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                 s = S.ev_s;
                 if (base != 0 || !(s > 0.0 && ilogb(s) >= -960)) {  // an all-zero or tiny head: the legacy kernel's cases
                     bail = true;
+                    why = 3;
                     break;
                 }
                 owner = m / SUB - 1;
@@ -792,12 +796,14 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                 __syncthreads();
                 if (!S.ev_any) {  // cannot happen; never spin
                     bail = true;
+                    why = 4;
                     break;
                 }
                 const double sn = S.ev_s;
                 const int e_old = ilogb(s), e_new = (sn > 0.0) ? ilogb(sn) : -100000;
                 if (!(sn > 0.0 && e_new >= -960 && e_new < 1000)) {
                     bail = true;
+                    why = 4;
                     break;
                 }
                 owner = S.ev_owner;
@@ -839,7 +845,10 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
     if (tid == 0) {
         if (bail) {
             redo[gslot] = 1;
-            if (a.counters) atomicAdd(&a.counters[17], 1ull);
+            if (a.counters) {
+                atomicAdd(&a.counters[17], 1ull);
+                atomicAdd(&a.counters[19 + why], 1ull);
+            }
         } else {
             redo[gslot] = 0;
             a.out_len[2 * gslot] = S.out_pos[0];

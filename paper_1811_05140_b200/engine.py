@@ -395,6 +395,8 @@ class CompressedState:
                 "serial_fallback_lanes": buf[3], "compactions": buf[4], "wave_slots": buf[5],
                 "sum_tie_events": buf[6], "sum_crossing_events": buf[7], "ladder_exits": buf[15],
                 "compaction_ns": buf[14], "stream_left_slots": buf[17], "stream_slots": buf[18],
+                "stream_left_why": {k: buf[19 + i] for i, k in enumerate(
+                    ("input_not_staged", "unproven_step", "first_element", "sum_head", "sum_event"))},
                 "phase_cycles": {k: buf[8 + i] for i, k in enumerate(
                     ("input", "rounds", "final", "sum", "tokcount", "write"))}}
 
