@@ -991,7 +991,7 @@ struct qcs_dev_state {
     // it off): codes/predictor scratch for `chain_levels` ladder levels
     int serial_chain = 1;
     int imz = 1;  // zero-imaginary-plane mode (QCS_IMZ=0 turns it off)
-    int stream_mode = 1;  // streaming kernel for element-wise gates (QCS_STREAM=0 turns it off; 2: also below one slot per SM)
+    int stream_mode = 1;  // streaming kernel for element-wise gates (QCS_STREAM=0 turns it off)
     int diag_local = 1;  // diagonal far/pair gates in the fused kernel (QCS_DIAG_LOCAL=0: split path)
     int zero_pass = 1;   // zero strides skip the codec (QCS_ZERO_PASS=0 turns it off)
     int ladder_exit = 1; // ladder levels give up at the byte budget (QCS_LADDER_EXIT=0 turns it off)
@@ -1741,8 +1741,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             // it left (escapes, off-lattice predictors: d.redo)
             const bool elementwise = (p.kind <= 1 && diag_gate) || p.kind == 2 || p.kind == 3;
             if (st->stream_mode && elementwise && (fm_lvl == FM_LOCAL || fm_lvl == FM_LOCAL_W) && !a.dump_x &&
-                a.cp.lossy && a.cp.pow2 && d.L >= SUB && d.L <= (1ull << 31) &&
-                (n_slots >= 148 || st->stream_mode >= 2)) {
+                a.cp.lossy && a.cp.pow2 && d.L >= SUB && d.L <= (1ull << 31)) {
                 FusedArgs as = a;
                 if (p.kind <= 1) as.diag = p.pair ? 2 : 1;
                 rc = launch_stream(as, d.redo, nw, s);
