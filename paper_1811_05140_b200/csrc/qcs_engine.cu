@@ -924,27 +924,28 @@ int launch_fused_t(const FusedArgs& a, uint64_t grid, cudaStream_t s)
     return 0;
 }
 
-template <int LANES>
+template <int LANES, bool RAW>
 int launch_stream_t(const FusedArgs& a, uint8_t* redo, uint64_t grid, cudaStream_t s)
 {
-    if (const int rc = set_smem_attr(reinterpret_cast<const void*>(k_stream<LANES>), (int)sizeof(StreamSharedT<LANES>)))
+    if (const int rc = set_smem_attr(reinterpret_cast<const void*>(k_stream<LANES, RAW>), (int)sizeof(StreamSharedT<LANES>)))
         return rc;
     if (grid == 0) return 0;
-    k_stream<LANES><<<(unsigned)grid, LANES, sizeof(StreamSharedT<LANES>), s>>>(a, redo);
+    k_stream<LANES, RAW><<<(unsigned)grid, LANES, sizeof(StreamSharedT<LANES>), s>>>(a, redo);
     CU(cudaGetLastError());
     return 0;
 }
 
 // streaming kernel (qcs_stream.cuh): CTA width by the slots per SM of the launch
+template <bool RAW>
 int launch_stream(const FusedArgs& a, uint8_t* redo, uint64_t grid, cudaStream_t s)
 {
     static const int force_t = getenv("QCS_STREAM_LANES") ? atoi(getenv("QCS_STREAM_LANES")) : 0;  // experiments
-    if (force_t == 128) return launch_stream_t<128>(a, redo, grid, s);
-    if (force_t == 256) return launch_stream_t<256>(a, redo, grid, s);
-    if (force_t == 512) return launch_stream_t<512>(a, redo, grid, s);
-    if (grid >= 8 * 148) return launch_stream_t<128>(a, redo, grid, s);
-    if (grid >= 4 * 148) return launch_stream_t<256>(a, redo, grid, s);
-    return launch_stream_t<512>(a, redo, grid, s);
+    if (force_t == 128) return launch_stream_t<128, RAW>(a, redo, grid, s);
+    if (force_t == 256) return launch_stream_t<256, RAW>(a, redo, grid, s);
+    if (force_t == 512) return launch_stream_t<512, RAW>(a, redo, grid, s);
+    if (grid >= 8 * 148) return launch_stream_t<128, RAW>(a, redo, grid, s);
+    if (grid >= 4 * 148) return launch_stream_t<256, RAW>(a, redo, grid, s);
+    return launch_stream_t<512, RAW>(a, redo, grid, s);
 }
 
 // FM_*_W: 2 planes x 256 lanes (one CTA per SM), for gates with fewer units
@@ -991,7 +992,7 @@ struct qcs_dev_state {
     // it off): codes/predictor scratch for `chain_levels` ladder levels
     int serial_chain = 1;
     int imz = 1;  // zero-imaginary-plane mode (QCS_IMZ=0 turns it off)
-    int stream_mode = 1;  // streaming kernel for element-wise gates (QCS_STREAM=0 turns it off)
+    int stream_mode = 1;  // streaming kernel for element-wise gates (QCS_STREAM=0 turns it off; bit 2: also as the split path's encoder)
     int diag_local = 1;  // diagonal far/pair gates in the fused kernel (QCS_DIAG_LOCAL=0: split path)
     int zero_pass = 1;   // zero strides skip the codec (QCS_ZERO_PASS=0 turns it off)
     int ladder_exit = 1; // ladder levels give up at the byte budget (QCS_LADDER_EXIT=0 turns it off)
@@ -1740,11 +1741,20 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             // kernel first; the legacy encoder then only re-encodes the slots
             // it left (escapes, off-lattice predictors: d.redo)
             const bool elementwise = (p.kind <= 1 && diag_gate) || p.kind == 2 || p.kind == 3;
-            if (st->stream_mode && elementwise && (fm_lvl == FM_LOCAL || fm_lvl == FM_LOCAL_W) && !a.dump_x &&
-                a.cp.lossy && a.cp.pow2 && d.L >= SUB && d.L <= (1ull << 31)) {
+            const bool stream_level = st->stream_mode && a.cp.lossy && a.cp.pow2 && d.L >= SUB && d.L <= (1ull << 31);
+            if (stream_level && elementwise && (fm_lvl == FM_LOCAL || fm_lvl == FM_LOCAL_W) && !a.dump_x) {
                 FusedArgs as = a;
                 if (p.kind <= 1) as.diag = p.pair ? 2 : 1;
-                rc = launch_stream(as, d.redo, nw, s);
+                rc = launch_stream<false>(as, d.redo, nw, s);
+                if (rc) return rc;
+                ++st->launches;
+                a.redo_only = d.redo;
+            } else if (stream_level && (fm_lvl == FM_RAW2 || fm_lvl == FM_RAW2_W) && !a.pre_codes && (st->stream_mode & 4)) {
+                // split path (or a load): the planes are in X, the streaming walk only encodes them.
+                // Experimental (QCS_STREAM=5): measured slower than the legacy encoder there (C2 2.3e10
+                // against 3.5e10: lane-strided reads of X without a shared-memory transpose, and no
+                // zero-imaginary-plane shortcut)
+                rc = launch_stream<true>(a, d.redo, nw, s);
                 if (rc) return rc;
                 ++st->launches;
                 a.redo_only = d.redo;

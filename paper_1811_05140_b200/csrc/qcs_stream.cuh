@@ -179,7 +179,10 @@ struct StreamPlaneOut {
 
 constexpr uint64_t ST_SAT = 1ull << 62;
 
-template <int ST_LANES>
+// RAW: the planes were decoded, gated and snapped into a.X by the split path
+// (k_decode_gate) or are the caller's (a load): the walk reads them there and
+// only quantizes, emits and sums.
+template <int ST_LANES, bool RAW>
 __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a, uint8_t* redo)
 {
     using StreamShared = StreamSharedT<ST_LANES>;
@@ -206,8 +209,14 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
     const double td = a.cp.td, inv_td = a.cp.inv_td;
     const uint64_t n = a.n;
     const uint64_t in_stride = a.job_stride[gslot];
-    const double scale = a.scale[in_stride];
+    const double scale = RAW ? 1.0 : a.scale[in_stride];
     const bool sc = scale != 1.0;
+    // RAW: this slot's planes in X; a slot flagged zero-imaginary has no im plane there
+    const double* xg[2] = {nullptr, nullptr};
+    if (RAW) {
+        xg[0] = a.X + (2 * slot) * a.x_plane_stride;
+        xg[1] = (a.im_zero && a.im_zero[gslot]) ? nullptr : a.X + (2 * slot + 1) * a.x_plane_stride;
+    }
 
     // input planes and output slots (k_fused's addressing)
     const uint8_t* in_bytes[2];
@@ -261,9 +270,9 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
         const uint64_t sc0 = base / SUB;
 
         // A. stage this iteration's payload bytes of both planes (one TMA bulk copy each)
-        const uint8_t* src[2];
+        const uint8_t* src[2] = {nullptr, nullptr};
 #pragma unroll
-        for (int p = 0; p < 2; ++p) {
+        for (int p = 0; p < 2 && !RAW; ++p) {
             const uint64_t lo = in_side[p][sc0].off & ~uint64_t(15);
             uint64_t hi;
             if (final_iter) {
@@ -313,8 +322,11 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                         uint64_t ms) -> bool {
             constexpr int PASS = decltype(pass_tag)::value;
             TokReader rd[2];
+            if (!RAW) {
 #pragma unroll
-            for (int p = 0; p < 2; ++p) rd[p].init(src[p], in_codec[p], in_td[p], in_side[p][e0 / SUB]);
+                for (int p = 0; p < 2; ++p) rd[p].init(src[p], in_codec[p], in_td[p], in_side[p][e0 / SUB]);
+            }
+            int kx = 0;  // RAW: the next element of the lane's rows in X
             int Mprev[2] = {0, 0};
             int run[2] = {0, 0};
             uint32_t wa[2] = {0, 0}, wa0[2] = {0, 0};  // shared-window address of the next token byte / the body
@@ -332,6 +344,12 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             // the next element of both planes: the usual case (both streams at a
             // nonzero code token) in one straight line, anything else by next()
             auto next2 = [&](double& xr, double& xi) {
+                if (RAW) {
+                    xr = __ldcs(xg[0] + e0 + kx);
+                    xi = xg[1] ? __ldcs(xg[1] + e0 + kx) : 0.0;
+                    ++kx;
+                    return;
+                }
                 const uint32_t w0 = rd[0].fetch4(rd[0].pos), w1 = rd[1].fetch4(rd[1].pos);
                 const uint32_t m0 = ~w0 & 0x80808080u, m1 = ~w1 & 0x80808080u;
                 const uint32_t t0 = m0 ^ (m0 - 1u), t1 = m1 ^ (m1 - 1u);
@@ -357,6 +375,13 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             // every element on its own — apply_pair with a zero partner, minus its
             // exact-zero terms (they change a zero's sign at most: snapped)
             auto gate_snap = [&](int k, double& xr, double& xi) {
+                if (RAW) {  // gated already; snapped already unless the caller asks
+                    if (a.snap) {
+                        xr = snap(xr);
+                        xi = snap(xi);
+                    }
+                    return;
+                }
                 if (sc) {
                     xr = __dmul_rn(xr, scale);
                     xi = __dmul_rn(xi, scale);
