@@ -146,6 +146,7 @@ struct Dev {
     uint8_t* im_zero;      // [NS] per slot: output im plane provably zero (zero-imaginary-plane mode)
     uint8_t* zero_slot;    // [NS] per slot: output stride provably all zero (zero-stride pass)
     uint8_t* redo;         // [NS] per slot: the streaming kernel left it to the legacy encoder
+    uint8_t* committed;    // [NS] per slot: its encoder CTA installed it (wave layout, StreamCommit)
     uint32_t* order;       // [NS] dense-first slot order within each wave (k_slot_order)
     int64_t* slot_of;      // [NS] generation<<32 | slot
     qcs_stride_report* reports;  // [NS]
@@ -170,6 +171,10 @@ struct Dev {
         int chain_on;
         int chain_left;
         unsigned long long fb_prev;
+        // wave layout, encoder-side commit (qcs_stream.cuh, StreamCommit): the wave's worst case is
+        // reserved behind the bump and the CTAs take their bytes from it
+        unsigned long long wave_used;
+        int wave_direct;
     }* sc;
     qcs_gate_record* rec;  // record ring for run_program
     uint64_t rec_cap;
@@ -925,27 +930,27 @@ int launch_fused_t(const FusedArgs& a, uint64_t grid, cudaStream_t s)
 }
 
 template <int LANES, bool RAW>
-int launch_stream_t(const FusedArgs& a, uint8_t* redo, uint64_t grid, cudaStream_t s)
+int launch_stream_t(const FusedArgs& a, uint8_t* redo, const StreamCommit& dc, uint64_t grid, cudaStream_t s)
 {
     if (const int rc = set_smem_attr(reinterpret_cast<const void*>(k_stream<LANES, RAW>), (int)sizeof(StreamSharedT<LANES>)))
         return rc;
     if (grid == 0) return 0;
-    k_stream<LANES, RAW><<<(unsigned)grid, LANES, sizeof(StreamSharedT<LANES>), s>>>(a, redo);
+    k_stream<LANES, RAW><<<(unsigned)grid, LANES, sizeof(StreamSharedT<LANES>), s>>>(a, redo, dc);
     CU(cudaGetLastError());
     return 0;
 }
 
 // streaming kernel (qcs_stream.cuh): CTA width by the slots per SM of the launch
 template <bool RAW>
-int launch_stream(const FusedArgs& a, uint8_t* redo, uint64_t grid, cudaStream_t s)
+int launch_stream(const FusedArgs& a, uint8_t* redo, const StreamCommit& dc, uint64_t grid, cudaStream_t s)
 {
     static const int force_t = getenv("QCS_STREAM_LANES") ? atoi(getenv("QCS_STREAM_LANES")) : 0;  // experiments
-    if (force_t == 128) return launch_stream_t<128, RAW>(a, redo, grid, s);
-    if (force_t == 256) return launch_stream_t<256, RAW>(a, redo, grid, s);
-    if (force_t == 512) return launch_stream_t<512, RAW>(a, redo, grid, s);
-    if (grid >= 8 * 148) return launch_stream_t<128, RAW>(a, redo, grid, s);
-    if (grid >= 4 * 148) return launch_stream_t<256, RAW>(a, redo, grid, s);
-    return launch_stream_t<512, RAW>(a, redo, grid, s);
+    if (force_t == 128) return launch_stream_t<128, RAW>(a, redo, dc, grid, s);
+    if (force_t == 256) return launch_stream_t<256, RAW>(a, redo, dc, grid, s);
+    if (force_t == 512) return launch_stream_t<512, RAW>(a, redo, dc, grid, s);
+    if (grid >= 8 * 148) return launch_stream_t<128, RAW>(a, redo, dc, grid, s);
+    if (grid >= 4 * 148) return launch_stream_t<256, RAW>(a, redo, dc, grid, s);
+    return launch_stream_t<512, RAW>(a, redo, dc, grid, s);
 }
 
 // FM_*_W: 2 planes x 256 lanes (one CTA per SM), for gates with fewer units
@@ -1209,12 +1214,13 @@ __device__ __forceinline__ void cta_copy16(uint4* __restrict__ dst, const uint4*
 // (new_off), replace the side index, tables, scale and sum (the staged commit
 // of aalc.cpp:395-408, one wave at a time).
 constexpr int COPY_THREADS = 256;
-__global__ void __launch_bounds__(COPY_THREADS) k_wave_commit(Dev d, LevelTag lt, uint64_t s0)
+__global__ void __launch_bounds__(COPY_THREADS) k_wave_commit(Dev d, LevelTag lt, uint64_t s0, const uint8_t* committed)
 {
     if (d.sc->err) return;
     const uint64_t loc = blockIdx.x >> 1;
     const int c = (int)(blockIdx.x & 1);
     const uint64_t slot = s0 + loc;
+    if (committed && committed[slot]) return;  // installed by its encoder CTA
     const uint64_t j = d.job_stride[slot];
     const uint64_t g = 2 * j + c;
     const uint64_t len = d.slot_len[2 * slot + c];
@@ -1246,18 +1252,28 @@ __global__ void __launch_bounds__(COPY_THREADS) k_wave_commit(Dev d, LevelTag lt
 // the wave's first unit in susp_unit): its blocks stay where they are, every
 // later kernel is a no-op, and the host compacts the arena and resumes.
 constexpr int ALLOC_THREADS = 1024;
-__global__ void __launch_bounds__(ALLOC_THREADS) k_wave_alloc(Dev d, uint64_t s0, uint64_t m2, uint64_t unit0)
+// committed (null: none): slots their encoder CTAs installed already, inside the
+// block k_wave_reserve set aside — the bump first moves past what they took.
+__global__ void __launch_bounds__(ALLOC_THREADS) k_wave_alloc(Dev d, uint64_t s0, uint64_t m2, uint64_t unit0,
+                                                              const uint8_t* committed)
 {
     __shared__ uint64_t wsum[ALLOC_THREADS / 32];
     __shared__ uint64_t base_sh;
     __shared__ int ok_sh;
     if (d.sc->err) return;
     const int tid = threadIdx.x, wl = tid & 31, w = tid >> 5;
-    uint64_t total = 0;
-    for (uint64_t c0 = 0; c0 < m2; c0 += ALLOC_THREADS) {
-        const uint64_t i = c0 + tid;
-        total += i < m2 ? round16d(d.slot_len[2 * s0 + i]) : 0;
+    auto need_of = [&](uint64_t i) -> uint64_t {
+        if (i >= m2 || (committed && committed[s0 + i / 2])) return 0;
+        return round16d(d.slot_len[2 * s0 + i]);
+    };
+    if (committed && tid == 0 && d.sc->wave_direct) {
+        d.sc->bump += d.sc->wave_used;
+        d.sc->wave_used = 0;
+        d.sc->wave_direct = 0;
     }
+    __syncthreads();
+    uint64_t total = 0;
+    for (uint64_t c0 = 0; c0 < m2; c0 += ALLOC_THREADS) total += need_of(c0 + tid);
     for (int o = 16; o; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
     if (wl == 0) wsum[w] = total;
     __syncthreads();
@@ -1279,7 +1295,7 @@ __global__ void __launch_bounds__(ALLOC_THREADS) k_wave_alloc(Dev d, uint64_t s0
     uint64_t carry = base_sh;
     for (uint64_t c0 = 0; c0 < m2; c0 += ALLOC_THREADS) {
         const uint64_t i = c0 + tid;
-        const uint64_t v = i < m2 ? round16d(d.slot_len[2 * s0 + i]) : 0;
+        const uint64_t v = need_of(i);
         uint64_t inc = v;
         for (int o = 1; o < 32; o <<= 1) {
             const uint64_t u = __shfl_up_sync(0xffffffffu, inc, o);
@@ -1296,6 +1312,16 @@ __global__ void __launch_bounds__(ALLOC_THREADS) k_wave_alloc(Dev d, uint64_t s0
         if (i < m2) d.new_off[2 * s0 + i] = carry + pre + inc - v;
         carry += tot;
     }
+}
+
+// Wave layout, encoder-side commit: set the wave's worst case (every plane at
+// its slot capacity) aside behind the bump when it fits — the CTAs then install
+// their strides themselves (StreamCommit); otherwise the staged path.
+__global__ void k_wave_reserve(Dev d, uint64_t m2)
+{
+    if (d.sc->err) return;
+    d.sc->wave_used = 0;
+    d.sc->wave_direct = (d.sc->bump + m2 * round16d(d.slot_cap) <= d.arena_cap) ? 1 : 0;
 }
 
 // Wave layout, before a gate's first wave: when its new blocks (estimated as
@@ -1453,7 +1479,7 @@ int big_commit_wave(qcs_dev_state* st, uint64_t s0, uint64_t s1, uint64_t gate_i
     }
     CU(cudaMemcpyAsync(d.new_off + 2 * s0, nof.data(), 8 * m, cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(&d.sc->bump, &st->bump, 8, cudaMemcpyHostToDevice, s));
-    k_wave_commit<<<(unsigned)m, COPY_THREADS, 0, s>>>(d, st->lt, s0);
+    k_wave_commit<<<(unsigned)m, COPY_THREADS, 0, s>>>(d, st->lt, s0, nullptr);
     ++st->launches;
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(s));  // nof / bump are host locals
@@ -1670,6 +1696,13 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         a.order = (zmode && n_slots > 148) ? d.order : nullptr;
         return a;
     };
+    // wave layout, single-level ladder, streaming kernel: the encoder CTAs install their strides
+    // (QCS_STREAM_COMMIT=0: always the staged commit)
+    static const bool commit_env = !(getenv("QCS_STREAM_COMMIT") && atoi(getenv("QCS_STREAM_COMMIT")) == 0);
+    const bool wave_direct = commit_env && st->big && nl == 1 && !x_ext && !chain && st->stream_mode &&
+                             ((p.kind <= 1 && diag_gate) || p.kind == 2 || p.kind == 3) &&
+                             (fm_lvl == FM_LOCAL || fm_lvl == FM_LOCAL_W) && make_params(lad[0]).lossy &&
+                             make_params(lad[0]).pow2 && d.L >= SUB && d.L <= (1ull << 31);
     const uint64_t spu = p.pair ? 2 : 1;                        // slots per unit
     const uint64_t wave_units = std::max<uint64_t>(1, st->wave / spu);
     for (uint64_t u0 = first_unit; u0 < p.n_units; u0 += wave_units) {
@@ -1745,7 +1778,25 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             if (stream_level && elementwise && (fm_lvl == FM_LOCAL || fm_lvl == FM_LOCAL_W) && !a.dump_x) {
                 FusedArgs as = a;
                 if (p.kind <= 1) as.diag = p.pair ? 2 : 1;
-                rc = launch_stream<false>(as, d.redo, nw, s);
+                StreamCommit dc{};
+                if (wave_direct) {
+                    k_wave_reserve<<<1, 1, 0, s>>>(d, 2 * nw);
+                    ++st->launches;
+                    dc.direct = &d.sc->wave_direct;
+                    dc.wave_used = &d.sc->wave_used;
+                    dc.bump = &d.sc->bump;
+                    dc.arena = d.arena[0];
+                    dc.side = d.side;
+                    dc.p_off = d.p_off;
+                    dc.p_len = d.p_len;
+                    dc.p_codec = d.p_codec;
+                    dc.p_delta = d.p_delta;
+                    dc.scale = d.scale;
+                    dc.sum_sq = d.sum_sq;
+                    dc.gate_cin = (unsigned long long*)&d.sc->gate_cin;
+                    dc.committed = d.committed;
+                }
+                rc = launch_stream<false>(as, d.redo, dc, nw, s);
                 if (rc) return rc;
                 ++st->launches;
                 a.redo_only = d.redo;
@@ -1754,7 +1805,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
                 // Experimental (QCS_STREAM=5): measured slower than the legacy encoder there (C2 2.3e10
                 // against 3.5e10: lane-strided reads of X without a shared-memory transpose, and no
                 // zero-imaginary-plane shortcut)
-                rc = launch_stream<true>(a, d.redo, nw, s);
+                rc = launch_stream<true>(a, d.redo, StreamCommit{}, nw, s);
                 if (rc) return rc;
                 ++st->launches;
                 a.redo_only = d.redo;
@@ -1777,8 +1828,8 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         }
         if (st->big) {  // place (device bump) and install the wave: no host round trip
             prof_start(st, 3);
-            k_wave_alloc<<<1, ALLOC_THREADS, 0, s>>>(d, s0, 2 * nw, u0);
-            k_wave_commit<<<(unsigned)(2 * nw), COPY_THREADS, 0, s>>>(d, st->lt, s0);
+            k_wave_alloc<<<1, ALLOC_THREADS, 0, s>>>(d, s0, 2 * nw, u0, wave_direct ? d.committed : nullptr);
+            k_wave_commit<<<(unsigned)(2 * nw), COPY_THREADS, 0, s>>>(d, st->lt, s0, wave_direct ? d.committed : nullptr);
             prof_stop(st);
             st->launches += 2;
         }
@@ -1931,6 +1982,7 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     TRY(dalloc(st, &d.im_zero, d.NS));
     TRY(dalloc(st, &d.zero_slot, d.NS));
     TRY(dalloc(st, &d.redo, d.NS));
+    TRY(dalloc(st, &d.committed, d.NS));
     TRY(dalloc(st, &d.order, d.NS));
     TRY(dalloc(st, &d.slot_of, d.NS));
     TRY(dalloc(st, &d.reports, d.NS));

@@ -170,6 +170,75 @@ struct TokReader {
     }
 };
 
+// Wave layout, single-level ladder: the encoder CTA installs its own stride
+// (the staged commit of aalc.cpp:395-408 for that stride) instead of leaving it
+// to k_wave_commit — its copy from the staging slot into the arena then runs
+// under the other CTAs' encoding.  The host reserved the wave's worst case
+// behind the bump (k_wave_reserve sets *direct); a CTA takes its 16-byte-rounded
+// bytes from that block with one atomic, copies payloads and side entries,
+// installs the tables and marks the slot committed.  Slots left to the legacy
+// encoder, and every slot when *direct is 0, keep the staged path.
+struct StreamCommit {
+    const int* direct;             // null: never
+    unsigned long long* wave_used; // bytes taken from the wave's block
+    const uint64_t* bump;          // arena fill before the wave
+    uint8_t* arena;
+    SideEntry* side;               // the block store's side index [2NS][nsub]
+    uint64_t* p_off;
+    uint64_t* p_len;
+    int8_t* p_codec;
+    double* p_delta;
+    double* scale;
+    double* sum_sq;
+    unsigned long long* gate_cin;
+    uint8_t* committed;            // [slot]
+};
+
+__device__ __forceinline__ void stream_copy16(uint4* __restrict__ dst, const uint4* __restrict__ src, uint64_t n16, int tid,
+                                              int nt)
+{
+    uint64_t i = (uint64_t)tid;
+    const uint64_t T = (uint64_t)nt;
+    for (; i + 3 * T < n16; i += 4 * T) {
+        const uint4 a = __ldcs(src + i), b = __ldcs(src + i + T), c = __ldcs(src + i + 2 * T), e = __ldcs(src + i + 3 * T);
+        __stcs(dst + i, a);
+        __stcs(dst + i + T, b);
+        __stcs(dst + i + 2 * T, c);
+        __stcs(dst + i + 3 * T, e);
+    }
+    for (; i < n16; i += T) __stcs(dst + i, __ldcs(src + i));
+}
+
+// install slot `gslot` (stride j) from its staging slot; lens: the planes' payload bytes
+__device__ __forceinline__ void stream_commit(const FusedArgs& a, const StreamCommit& dc, uint64_t slot, uint64_t gslot,
+                                              uint64_t j, uint64_t len0, uint64_t len1, double sumsq, uint64_t* sh_off,
+                                              int tid, int nt)
+{
+    const uint64_t r0 = (len0 + 15) & ~uint64_t(15), r1 = (len1 + 15) & ~uint64_t(15);
+    if (tid == 0) *sh_off = (uint64_t)atomicAdd(dc.wave_used, (unsigned long long)(r0 + r1));
+    __syncthreads();
+    const uint64_t at = *dc.bump + *sh_off;
+    stream_copy16(reinterpret_cast<uint4*>(dc.arena + at), reinterpret_cast<const uint4*>(a.out + (2 * slot) * a.cap), r0 / 16, tid, nt);
+    stream_copy16(reinterpret_cast<uint4*>(dc.arena + at + r0), reinterpret_cast<const uint4*>(a.out + (2 * slot + 1) * a.cap),
+                  r1 / 16, tid, nt);
+    stream_copy16(reinterpret_cast<uint4*>(dc.side + (2 * j) * a.nsub), reinterpret_cast<const uint4*>(a.side + (2 * slot) * a.nsub),
+                  a.nsub, tid, nt);
+    stream_copy16(reinterpret_cast<uint4*>(dc.side + (2 * j + 1) * a.nsub),
+                  reinterpret_cast<const uint4*>(a.side + (2 * slot + 1) * a.nsub), a.nsub, tid, nt);
+    if (tid == 0) {
+        atomicAdd(dc.gate_cin, (unsigned long long)(2 * HEADER_BYTES + dc.p_len[2 * j] + dc.p_len[2 * j + 1]));
+        dc.p_off[2 * j] = at;
+        dc.p_off[2 * j + 1] = at + r0;
+        dc.p_len[2 * j] = len0;
+        dc.p_len[2 * j + 1] = len1;
+        dc.p_codec[2 * j] = dc.p_codec[2 * j + 1] = 1;
+        dc.p_delta[2 * j] = dc.p_delta[2 * j + 1] = a.cp.delta;
+        dc.sum_sq[j] = sumsq;
+        dc.scale[j] = 1.0;
+        dc.committed[gslot] = 1;
+    }
+}
+
 struct StreamPlaneOut {
     double x0;
     int M0, Mlast;
@@ -183,7 +252,7 @@ constexpr uint64_t ST_SAT = 1ull << 62;
 // (k_decode_gate) or are the caller's (a load): the walk reads them there and
 // only quantizes, emits and sums.
 template <int ST_LANES, bool RAW>
-__global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a, uint8_t* redo)
+__global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a, uint8_t* redo, StreamCommit dc)
 {
     using StreamShared = StreamSharedT<ST_LANES>;
     constexpr int ST_WARPS = StreamShared::ST_WARPS;
@@ -195,11 +264,40 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
     const uint64_t gslot = a.slot_base + slot;
     if (a.pending && !a.pending[gslot]) return;
     const int tid = threadIdx.x, wl = tid & 31, wp = tid >> 5;
+    const bool direct = dc.direct && *dc.direct;  // (uniform; the pool layout never sets it)
     if (a.zero_slot && a.zero_slot[gslot]) {
+        if (direct) {
+            // a zero stride already stored as this level's zero encodings (one run token per plane,
+            // side entries {0, 32k, 0.0}: write_zero_plane's) is its own output: only the stride's
+            // scale and sum change, nothing is written or copied
+            const uint64_t j = a.job_stride[gslot];
+            if (dc.p_codec[2 * j] == 1 && dc.p_codec[2 * j + 1] == 1 && dc.p_delta[2 * j] == a.cp.delta &&
+                dc.p_delta[2 * j + 1] == a.cp.delta) {
+                if (tid == 0) {
+                    const uint64_t zl = (uint64_t)varint_len(run_token(1, TY_Z, a.n));
+                    a.out_len[2 * gslot] = a.out_len[2 * gslot + 1] = zl;
+                    if (a.sumsq) a.sumsq[gslot] = 0.0;
+                    redo[gslot] = 0;
+                    atomicAdd(dc.gate_cin, (unsigned long long)(2 * HEADER_BYTES + dc.p_len[2 * j] + dc.p_len[2 * j + 1]));
+                    dc.sum_sq[j] = 0.0;
+                    dc.scale[j] = 1.0;
+                    dc.committed[gslot] = 1;
+                }
+                return;
+            }
+        }
         for (int c = 0; c < 2; ++c) write_zero_plane<true>(a, slot, gslot, c, tid, ST_LANES);
         if (tid == 0) {
             if (a.sumsq) a.sumsq[gslot] = 0.0;
             redo[gslot] = 0;
+        }
+        if (direct) {
+            __shared__ uint64_t zoff;
+            const uint64_t zl = (uint64_t)varint_len(run_token(1, TY_Z, a.n));
+            __syncthreads();  // (the zero encodings above are this CTA's own global writes)
+            stream_commit(a, dc, slot, gslot, a.job_stride[gslot], zl, zl, 0.0, &zoff, tid, ST_LANES);
+        } else if (dc.committed && tid == 0) {
+            dc.committed[gslot] = 0;
         }
         return;
     }
@@ -861,12 +959,19 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                     a.out_len[2 * gslot + 1] = 1ull << 50;
                     if (a.counters) atomicAdd(&a.counters[15], 1ull);
                     redo[gslot] = 0;
+                    if (dc.committed) dc.committed[gslot] = 0;
                 }
                 return;
             }
         }
     }
     __syncthreads();
+    if (direct && !bail) {
+        stream_commit(a, dc, slot, gslot, in_stride, S.out_pos[0], S.out_pos[1], a.sumsq ? S.s : 0.0,
+                      reinterpret_cast<uint64_t*>(&S.ev_part), tid, ST_LANES);
+    } else if (dc.committed && tid == 0) {
+        dc.committed[gslot] = 0;
+    }
     if (tid == 0) {
         if (bail) {
             redo[gslot] = 1;
