@@ -1778,6 +1778,8 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             if (stream_level && elementwise && (fm_lvl == FM_LOCAL || fm_lvl == FM_LOCAL_W) && !a.dump_x) {
                 FusedArgs as = a;
                 if (p.kind <= 1) as.diag = p.pair ? 2 : 1;
+                as.X = d.X;  // (scratch of the sum's serial head: min(512, L) doubles per slot)
+                as.x_plane_stride = d.L;
                 StreamCommit dc{};
                 if (wave_direct) {
                     k_wave_reserve<<<1, 1, 0, s>>>(d, 2 * nw);

@@ -239,6 +239,30 @@ __device__ __forceinline__ void stream_commit(const FusedArgs& a, const StreamCo
     }
 }
 
+// nb bytes from shared memory (any alignment) to dst (generic, any alignment): bytes up to
+// dst's first 4-byte boundary, aligned words (one shared word read and a funnel shift each),
+// bytes again for the tail — the boundary words belong to the neighbours' bytes too
+__device__ __forceinline__ void stream_lane_copy(uint8_t* dst, const uint8_t* srow, uint32_t nb)
+{
+    uint32_t i = 0;
+    const uint32_t head = min(nb, (uint32_t)((0u - (uint32_t)(uintptr_t)dst) & 3u));
+    for (; i < head; ++i) dst[i] = srow[i];
+    if (i + 4u <= nb) {
+        const uint32_t sad = (uint32_t)__cvta_generic_to_shared(srow + i);
+        const uint32_t sh = (sad & 3u) << 3;
+        uint32_t wa = sad & ~3u, lo;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(wa) : "memory");
+        for (; i + 4u <= nb; i += 4u) {
+            uint32_t hi;
+            wa += 4u;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi) : "r"(wa) : "memory");
+            *reinterpret_cast<uint32_t*>(dst + i) = __funnelshift_r(lo, hi, sh);
+            lo = hi;
+        }
+    }
+    for (; i < nb; ++i) dst[i] = srow[i];
+}
+
 struct StreamPlaneOut {
     double x0;
     int M0, Mlast;
@@ -780,7 +804,7 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             bst[p] = inc - nbytes[p];
         }
         __syncthreads();
-        uint64_t bstart[2];
+        uint64_t bstart[2], obase[2];
         uint32_t iter_bytes[2];
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
@@ -790,37 +814,19 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                 tot += S.wbytes[p][i];
             }
             iter_bytes[p] = tot;
-            bstart[p] = S.out_pos[p] + pre + bst[p];
+            obase[p] = S.out_pos[p];
+            bstart[p] = obase[p] + pre + bst[p];
         }
+        // The token bytes leave the rows after the sum (step E): the rows are
+        // packed into the plane's contiguous image first, in the input staging
+        // buffer (dead by then), and stored with 16-byte words.  RAW keeps the
+        // lane-by-lane stores here (its replays read X, the serial head the rows).
+        constexpr bool LATE_COPY = !RAW;
         // copy the rows out, 32 consecutive bytes per store, and the side index
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-            // every lane stores its own bytes: bytes up to the first 4-byte
-            // boundary of the destination, aligned words (one shared word
-            // read and a funnel shift each), bytes again for the tail — the
-            // boundary words are shared with the neighbour lanes' bytes
-            if (nbytes[p] != 0u) {
-                const uint32_t nb = nbytes[p];
-                uint8_t* dst = out[p] + bstart[p];
-                const uint8_t* srow = S.rows + (size_t)(p * ST_LANES + tid) * ST_ROW + ST_LEAD - lead_len[p];
-                uint32_t i = 0;
-                const uint32_t head = min(nb, (uint32_t)((0u - (uint32_t)(uintptr_t)dst) & 3u));
-                for (; i < head; ++i) dst[i] = srow[i];
-                if (i + 4u <= nb) {
-                    const uint32_t sad = (uint32_t)__cvta_generic_to_shared(srow + i);
-                    const uint32_t sh = (sad & 3u) << 3;
-                    uint32_t wa = sad & ~3u, lo;
-                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(wa) : "memory");
-                    for (; i + 4u <= nb; i += 4u) {
-                        uint32_t hi;
-                        wa += 4u;
-                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi) : "r"(wa) : "memory");
-                        *reinterpret_cast<uint32_t*>(dst + i) = __funnelshift_r(lo, hi, sh);
-                        lo = hi;
-                    }
-                }
-                for (; i < nb; ++i) dst[i] = srow[i];
-            }
+            if (!LATE_COPY && nbytes[p] != 0u)
+                stream_lane_copy(out[p] + bstart[p], S.rows + (size_t)(p * ST_LANES + tid) * ST_ROW + ST_LEAD - lead_len[p], nbytes[p]);
             if (have) {
                 SideEntry se;
                 if (q0[p] == 0) {
@@ -858,7 +864,8 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             if (!have_tu) {
                 // s is still 0: the first terms double it again and again; add
                 // the first ST_SERIAL in the reference's order on one thread
-                double* tser = reinterpret_cast<double*>(S.rows);  // (the rows are free: copied out above)
+                // (RAW: the rows are free, copied out above; else this slot's part of the split path's scratch X)
+                double* tser = LATE_COPY ? const_cast<double*>(a.X) + 2 * slot * a.x_plane_stride : reinterpret_cast<double*>(S.rows);
                 if (have && e0 < ST_SERIAL) walk(std::integral_constant<int, 2>{}, nullptr, 0.0, -1, tser, 0);
                 __syncthreads();
                 const int m = (int)umin64(ST_SERIAL, n - base);
@@ -946,8 +953,37 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             }
             if (tid == 0) S.s = s;
         }
-        __syncthreads();
         if (bail) break;
+        // E. token bytes out
+        if (LATE_COPY) {
+            bool packed[2];
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                packed[p] = iter_bytes[p] + 16u <= (uint32_t)ST_STAGE;  // uniform
+                if (nbytes[p] != 0u) {
+                    // the image keeps the destination's 16-byte phase
+                    uint8_t* dst = packed[p] ? S.in[p] + (obase[p] & 15u) + (bstart[p] - obase[p]) : out[p] + bstart[p];
+                    stream_lane_copy(dst, S.rows + (size_t)(p * ST_LANES + tid) * ST_ROW + ST_LEAD - lead_len[p], nbytes[p]);
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                if (!packed[p] || iter_bytes[p] == 0u) continue;
+                const uint8_t* img = S.in[p] + (obase[p] & 15u);
+                uint8_t* dst = out[p] + obase[p];
+                const uint32_t nb = iter_bytes[p];
+                const uint32_t hb = min(nb, (16u - (uint32_t)(obase[p] & 15u)) & 15u);
+                const uint32_t n16 = (nb - hb) / 16u;
+                const uint32_t tb = nb - hb - 16u * n16;
+                if ((uint32_t)tid < hb) dst[tid] = img[tid];
+                const uint4* s4 = reinterpret_cast<const uint4*>(img + hb);
+                uint4* d4 = reinterpret_cast<uint4*>(dst + hb);
+                for (uint32_t i = (uint32_t)tid; i < n16; i += ST_LANES) d4[i] = s4[i];
+                if ((uint32_t)tid < tb) dst[hb + 16u * n16 + tid] = img[hb + 16u * n16 + tid];
+            }
+        }
+        __syncthreads();
 
         // ladder early exit (k_fused's): a level before the last gives up once
         // theta is out of reach of the bytes already closed
