@@ -1397,13 +1397,24 @@ int compact_arena_impl(qcs_dev_state* st)
     auto flush = [&]() -> int {
         if (bs.empty()) return 0;
         const uint64_t m = bs.size();
+        // sources ascend and every later block lies above them: when the batch's destinations end
+        // at or below its first source, no destination byte is a source still to be read — one
+        // pass inside the arena instead of the bounce through X (the usual case after a few gates:
+        // the live blocks are the newest, at the top)
+        bool direct = true;
+        for (uint64_t i = 0; i < m && direct; ++i) direct = bd[i] + round16(bl[i]) <= bs[0];
         CU(cudaMemcpyAsync(st->mv_src, bs.data(), 8 * m, cudaMemcpyHostToDevice, s));
-        CU(cudaMemcpyAsync(st->mv_dst, bt.data(), 8 * m, cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(st->mv_dst, (direct ? bd : bt).data(), 8 * m, cudaMemcpyHostToDevice, s));
         CU(cudaMemcpyAsync(st->mv_len, bl.data(), 8 * m, cudaMemcpyHostToDevice, s));
-        k_move<<<(unsigned)m, COPY_THREADS, 0, s>>>(d.arena[0], X, st->mv_src, st->mv_dst, st->mv_len);
-        CU(cudaMemcpyAsync(st->mv_src, bd.data(), 8 * m, cudaMemcpyHostToDevice, s));
-        k_move<<<(unsigned)m, COPY_THREADS, 0, s>>>(X, d.arena[0], st->mv_dst, st->mv_src, st->mv_len);
-        st->launches += 2;
+        if (direct) {
+            k_move<<<(unsigned)m, COPY_THREADS, 0, s>>>(d.arena[0], d.arena[0], st->mv_src, st->mv_dst, st->mv_len);
+            st->launches += 1;
+        } else {
+            k_move<<<(unsigned)m, COPY_THREADS, 0, s>>>(d.arena[0], X, st->mv_src, st->mv_dst, st->mv_len);
+            CU(cudaMemcpyAsync(st->mv_src, bd.data(), 8 * m, cudaMemcpyHostToDevice, s));
+            k_move<<<(unsigned)m, COPY_THREADS, 0, s>>>(X, d.arena[0], st->mv_dst, st->mv_src, st->mv_len);
+            st->launches += 2;
+        }
         CU(cudaGetLastError());
         CU(cudaStreamSynchronize(s));  // the host vectors are reused
         bs.clear(), bt.clear(), bd.clear(), bl.clear();
