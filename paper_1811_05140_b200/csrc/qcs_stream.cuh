@@ -440,6 +440,7 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
         // Returns false when a step is neither proven nor a lattice-preserving
         // reference step (the slot is left to the legacy encoder).
         uint64_t uA = 0, uB = 0;
+        uint64_t ownB = ST_SAT;  // PASS 3: the walking lane's own next-binade units of the whole sub-chunk (ST_SAT: unknown)
         auto walk = [&](auto pass_tag, StreamPlaneOut* po, double tu, long long k_after, double* tdst,
                         uint64_t ms) -> bool {
             constexpr int PASS = decltype(pass_tag)::value;
@@ -461,7 +462,8 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                 }
             }
             uint64_t la = PASS == 3 ? uA : 0, lb = 0;
-            bool eva = false, evb = false, bad = false, found = false;
+            uint64_t lbp = 0;  // PASS 3: next-binade units of the elements up to the event
+            bool eva = false, evb = false, bad = false, found = false, stop = false;
             double tu2 = 0.0;
             // the next element of both planes: the usual case (both streams at a
             // nonzero code token) in one straight line, anything else by next()
@@ -591,6 +593,10 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                         const bool beyond = y >= 9007199254740992.0;
                         const bool tie = !beyond && fabs(y - ry) == 0.5;
                         const uint64_t c = beyond ? (1ull << 53) : (uint64_t)ry;
+                        // the same element one binade up (exact halving), for the shortcut below
+                        const double yb = y * 0.5;
+                        const double rb = rint(yb);
+                        const bool oddb = yb >= 9007199254740992.0 || fabs(yb - rb) == 0.5;
                         if (found) {
                             evb = evb || beyond || tie;
                             lb += c;
@@ -601,8 +607,16 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                             if (a.counters) atomicAdd(&a.counters[tie ? 6 : 7], 1ull);
                             found = true;
                             tu2 = (sn > 0.0 && ilogb(sn) >= -960 && ilogb(sn) < 1000) ? ldexp(1.0, 52 - ilogb(sn)) : 0.0;
+                            // a plain crossing into the next binade: the rest of the sub-chunk is the
+                            // lane's next-binade units of the main pass minus those walked — stop here
+                            if (ownB < ST_SAT && !oddb && tu2 == tu * 0.5 && k_after < (long long)e0) {
+                                lb = ownB - lbp - (uint64_t)rb;
+                                stop = true;
+                            }
                         } else {
                             la += c;
+                            lbp += (uint64_t)rb;
+                            if (oddb) ownB = ST_SAT;  // (a tie or overflow one binade up: no shortcut)
                         }
                     }
                 }
@@ -629,6 +643,7 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             }
 #pragma unroll 2
             for (int k = 1; k < SUB; ++k) {
+                if (PASS == 3 && stop) break;
                 double xr, xi;
                 next2(xr, xi);
                 gate_snap(k, xr, xi);
@@ -919,6 +934,7 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                 const uint64_t offx = sat_add(pre, excl);
                 const bool me = in_part ? tid == owner : (have && tid > owner && offx < LIM && sat_add(offx, mine) >= LIM);
                 if (me) {
+                    ownB = (hasB && !in_part && uB < ST_SAT) ? uB : ST_SAT;
                     uA = in_part ? 0 : offx;
                     walk(std::integral_constant<int, 3>{}, nullptr, to_units, k_after, nullptr, ms);
                     S.ev_owner = tid;
