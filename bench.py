@@ -679,7 +679,7 @@ def run_qft_config(args, name):
     t_f, n_f = kt["fused"]
     t_f_run = t_f
     achieved = (cin + cout) / (t_f_run * 1e-9) / 1e9 if t_f_run else 0.0
-    roofline = {"bound": "hbm", "kernel": "k_fused", "achieved": achieved, "peak": peak, "unit": "GB/s",
+    roofline = {"bound": "hbm", "kernel": "encoder (k_stream, k_fused)", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": (cin + cout) / max(1, n_f),
                 "avg_launch_us": t_f_run / max(1, n_f) / 1e3,
