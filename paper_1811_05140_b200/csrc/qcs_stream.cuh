@@ -818,6 +818,14 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             if (wl == 31) S.wbytes[p][wp] = inc;
             bst[p] = inc - nbytes[p];
         }
+        // (the warps' sum units of the main pass ride on the same barrier: an
+        // iteration without a sum event needs nothing more, step D)
+        {
+            uint64_t u = have ? uA : 0;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) u = sat_add(u, __shfl_xor_sync(0xffffffffu, u, o));
+            if (wl == 0) S.wunits[wp] = u;
+        }
         __syncthreads();
         uint64_t bstart[2], obase[2];
         uint32_t iter_bytes[2];
@@ -856,15 +864,21 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             }
         }
         // the carry is read above by every lane: update it behind a barrier
-        __syncthreads();
-        if (tid + 1 == active) {
+        // (the packing barrier of step E when the copy is late)
+        auto carry_update = [&]() {
+            if (tid + 1 == active) {
 #pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                const bool full = q0[p] == 0 && !po[p].seen;
-                S.run_start[p] = full ? rs[p] : val[p];
-                S.m_carry[p] = po[p].Mlast;
-                S.out_pos[p] += iter_bytes[p];
+                for (int p = 0; p < 2; ++p) {
+                    const bool full = q0[p] == 0 && !po[p].seen;
+                    S.run_start[p] = full ? rs[p] : val[p];
+                    S.m_carry[p] = po[p].Mlast;
+                    S.out_pos[p] += iter_bytes[p];
+                }
             }
+        };
+        if (!LATE_COPY) {
+            __syncthreads();
+            carry_update();
         }
 
         // D. stored sum of squares: s plus the units of the lanes after
@@ -901,7 +915,18 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                 uA = 0;
                 if (have && tid > owner) walk(std::integral_constant<int, 1>{}, nullptr, ldexp(1.0, 52 - ilogb(s)), -1, nullptr, 0);
             }
-            for (;;) {
+            bool summed = false;
+            if (have_tu) {  // the usual iteration: no event, the totals of step C are all it takes
+                const double to_units = ldexp(1.0, 52 - ilogb(s));
+                const uint64_t ms = (uint64_t)(s * to_units);
+                uint64_t total = 0;
+                for (int i = 0; i < ST_WARPS; ++i) total = sat_add(total, S.wunits[i]);
+                if (ms + total < (1ull << 53)) {
+                    s = (double)(ms + total) / to_units;
+                    summed = true;
+                }
+            }
+            while (!summed) {
                 const double to_units = ldexp(1.0, 52 - ilogb(s));
                 const uint64_t ms = (uint64_t)(s * to_units);
                 const uint64_t mine = (have && tid > owner) ? uA : 0;
@@ -983,6 +1008,7 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                 }
             }
             __syncthreads();
+            carry_update();
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
                 if (!packed[p] || iter_bytes[p] == 0u) continue;
