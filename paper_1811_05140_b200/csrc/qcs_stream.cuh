@@ -31,9 +31,18 @@
 // run has its side offset at the lane's own first byte.
 //
 // Stored sum of squares (aalc.cpp:46-52, core.cpp:30-37): the integer-units
-// argument of fused_sumsq; an iteration holding a binade crossing or a tie
-// replays the lanes after it (decode + gate + quantize again) under the new
-// binade instead of re-reading stored values.
+// argument of fused_sumsq without stored values — every lane accumulates its
+// units under the binade of the running sum and under the next one while it
+// walks; an iteration without event is one CTA reduction; at a binade crossing
+// or tie the lane whose prefix reaches the binade's end replays its sub-chunk
+// (decode + gate + quantize again) up to the event, adds it exactly, and the
+// lanes after it switch to their next-binade units.
+//
+// Iteration = steps A (TMA staging of both planes' payload bytes), B (the
+// walk), C (first elements, runs across lanes, lead tokens, byte scan, side
+// index), D (stored sum), E (rows packed into the plane's contiguous image in
+// the dead staging buffer, 16-byte stores).  In the wave layout with a
+// single-level ladder the CTA finally installs its own stride (StreamCommit).
 #pragma once
 
 #include "qcs_fused.cuh"
