@@ -84,6 +84,9 @@ constexpr int KIND_LOAD = 4;
 // the arena: every later kernel is a no-op, the host compacts the arena and
 // re-enqueues the gate from that wave (internal, never returned).
 constexpr int QCS_SUSPEND = 99;
+// susp_unit of a gate suspended inside the persistent streaming kernel: the flag, plus the
+// strides installed so far (progress: the same value twice means the state does not fit)
+constexpr uint64_t SUSP_PERSIST = 1ull << 62;
 
 __host__ __device__ inline uint64_t insert_bit(uint64_t j, int pos, int v)
 {
@@ -175,6 +178,10 @@ struct Dev {
         // reserved behind the bump and the CTAs take their bytes from it
         unsigned long long wave_used;
         int wave_direct;
+        // persistent streaming kernel (k_stream_persist): slot queue head, strides installed so far
+        unsigned long long q_head;
+        unsigned long long persist_done;
+        int persist_susp;  // the suspension was raised inside the persistent kernel (not by k_precheck)
     }* sc;
     qcs_gate_record* rec;  // record ring for run_program
     uint64_t rec_cap;
@@ -213,7 +220,8 @@ __device__ __forceinline__ bool stride_is_zero(const Dev& d, uint64_t j)
 __global__ void k_make_jobs(Dev d, Plan p, uint64_t n_slots, uint64_t gen, LevelTag lt, int codec0, double delta0,
                             int imz, int zmode, int resume)
 {
-    if (blockIdx.x == 0 && threadIdx.x == 0 && !resume) d.sc->gate_cin = 0;  // the commits accumulate it
+    // the commits accumulate it (a gate queued behind a suspended one leaves the suspended gate's sum alone)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && !resume && !d.sc->err) d.sc->gate_cin = 0;
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < n_slots;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t j = slot_stride(p, s);
@@ -953,6 +961,29 @@ int launch_stream(const FusedArgs& a, uint8_t* redo, const StreamCommit& dc, uin
     return launch_stream_t<512, RAW>(a, redo, dc, grid, s);
 }
 
+template <int LANES>
+int launch_stream_persist_t(const FusedArgs& a, uint8_t* redo, const StreamCommit& dc, uint64_t n_slots,
+                            unsigned long long* q_head, uint64_t grid, cudaStream_t s)
+{
+    if (const int rc = set_smem_attr(reinterpret_cast<const void*>(k_stream_persist<LANES>), (int)sizeof(StreamSharedT<LANES>)))
+        return rc;
+    if (grid == 0) return 0;
+    k_stream_persist<LANES><<<(unsigned)grid, LANES, sizeof(StreamSharedT<LANES>), s>>>(a, redo, dc, n_slots, q_head);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+// persistent streaming kernel: one CTA per staging slot, width by the CTAs per SM
+int launch_stream_persist(const FusedArgs& a, uint8_t* redo, const StreamCommit& dc, uint64_t n_slots,
+                          unsigned long long* q_head, uint64_t grid, cudaStream_t s)
+{
+    static const int force_t = getenv("QCS_STREAM_LANES") ? atoi(getenv("QCS_STREAM_LANES")) : 0;  // experiments
+    const int lanes = force_t ? force_t : (grid >= 4 * 148 ? 128 : (grid >= 2 * 148 ? 256 : 512));
+    if (lanes == 128) return launch_stream_persist_t<128>(a, redo, dc, n_slots, q_head, grid, s);
+    if (lanes == 256) return launch_stream_persist_t<256>(a, redo, dc, n_slots, q_head, grid, s);
+    return launch_stream_persist_t<512>(a, redo, dc, n_slots, q_head, grid, s);
+}
+
 // FM_*_W: 2 planes x 256 lanes (one CTA per SM), for gates with fewer units
 // than SMs, where per-stride parallelism is all there is
 enum { FM_LOCAL = 0, FM_LOCAL_W = 1, FM_RAW2_W = 2, FM_RAW1 = 3, FM_RAW2 = 4 };
@@ -1324,6 +1355,32 @@ __global__ void k_wave_reserve(Dev d, uint64_t m2)
     d.sc->wave_direct = (d.sc->bump + m2 * round16d(d.slot_cap) <= d.arena_cap) ? 1 : 0;
 }
 
+// Persistent streaming kernel, around its launch: reset the slot queue (and, for a gate's first
+// attempt, the installed flags and their count); afterwards a suspension inside it is tagged for
+// the host (SUSP_PERSIST + progress).
+__global__ void k_persist_begin(Dev d, uint64_t n_slots, int resume)
+{
+    // (a gate queued behind a suspended one must not touch the suspended gate's flags)
+    if (d.sc->err) return;
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i == 0) {
+        d.sc->q_head = 0;
+        d.sc->persist_susp = 0;
+        if (!resume) d.sc->persist_done = 0;
+    }
+    if (!resume && i < n_slots) {
+        d.committed[i] = 0;
+        d.redo[i] = 0;
+    }
+}
+__global__ void k_persist_end(Dev d, int64_t gate_index)
+{
+    if (d.sc->err == QCS_SUSPEND && d.sc->persist_susp && d.sc->err_gate < 0) {
+        d.sc->err_gate = (int)gate_index;
+        d.sc->susp_unit = SUSP_PERSIST | d.sc->persist_done;
+    }
+}
+
 // Wave layout, before a gate's first wave: when its new blocks (estimated as
 // 5/4 of the blocks it rewrites) would not fit behind the bump but would after
 // a compaction, suspend the gate at unit 0 -- the host compacts before any of
@@ -1540,7 +1597,10 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
                  uint64_t load_first = 0, uint64_t load_count = 0, uint64_t first_unit = 0,
                  bool precheck_done = false)
 {
-    const bool resume = first_unit > 0;  // wave layout: the gate's waves before first_unit are committed
+    // wave layout: the gate's waves before first_unit are committed; a gate suspended inside the
+    // persistent streaming kernel resumes with every slot not installed yet (SUSP_PERSIST)
+    const bool resume = first_unit > 0;
+    if (first_unit & SUSP_PERSIST) first_unit = 0;  // (the low bits count installed strides: progress only)
     Dev& d = st->d;
     cudaStream_t s = st->stream;
     static const qcs_gate_desc k_load_desc{KIND_LOAD, 0, -1, 0, 0, {1, 0, 0, 0, 0, 0, 1, 0}};
@@ -1714,6 +1774,42 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
                              ((p.kind <= 1 && diag_gate) || p.kind == 2 || p.kind == 3) &&
                              (fm_lvl == FM_LOCAL || fm_lvl == FM_LOCAL_W) && make_params(lad[0]).lossy &&
                              make_params(lad[0]).pow2 && d.L >= SUB && d.L <= (1ull << 31);
+    // ... and from one persistent kernel over the whole gate instead of a launch per wave
+    // (QCS_STREAM_PERSIST=0: waves)
+    static const bool persist_env = !(getenv("QCS_STREAM_PERSIST") && atoi(getenv("QCS_STREAM_PERSIST")) == 0);
+    const bool persist = wave_direct && persist_env;
+    if (persist) {
+        FusedArgs as = fused_args(lad[0], 0);
+        as.diag = p.kind <= 1 ? (p.pair ? 2 : 1) : 0;
+        as.X = d.X;  // (scratch of the sum's serial head: min(512, L) doubles per staging slot)
+        as.x_plane_stride = d.L;
+        as.ladder_theta = 0.0;
+        StreamCommit dc{};
+        dc.bump_rw = (unsigned long long*)&d.sc->bump;
+        dc.arena_cap = d.arena_cap;
+        dc.err_rw = &d.sc->err;
+        dc.persist_done = &d.sc->persist_done;
+        dc.persist_susp = &d.sc->persist_susp;
+        dc.arena = d.arena[0];
+        dc.side = d.side;
+        dc.p_off = d.p_off;
+        dc.p_len = d.p_len;
+        dc.p_codec = d.p_codec;
+        dc.p_delta = d.p_delta;
+        dc.scale = d.scale;
+        dc.sum_sq = d.sum_sq;
+        dc.gate_cin = (unsigned long long*)&d.sc->gate_cin;
+        dc.committed = d.committed;
+        const uint64_t grid = std::min<uint64_t>(n_slots, st->wave);
+        prof_start(st, 2);
+        k_persist_begin<<<(unsigned)grid_for(std::max<uint64_t>(n_slots, 1)), 256, 0, s>>>(d, n_slots, resume ? 1 : 0);
+        const int rc = launch_stream_persist(as, d.redo, dc, n_slots, &d.sc->q_head, grid, s);
+        if (rc) return rc;
+        k_persist_end<<<1, 1, 0, s>>>(d, (int64_t)gate_index);
+        prof_stop(st);
+        st->launches += 3;
+        dbg_sync(st, "k_stream_persist");
+    }
     const uint64_t spu = p.pair ? 2 : 1;                        // slots per unit
     const uint64_t wave_units = std::max<uint64_t>(1, st->wave / spu);
     for (uint64_t u0 = first_unit; u0 < p.n_units; u0 += wave_units) {
@@ -1786,7 +1882,11 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
             // it left (escapes, off-lattice predictors: d.redo)
             const bool elementwise = (p.kind <= 1 && diag_gate) || p.kind == 2 || p.kind == 3;
             const bool stream_level = st->stream_mode && a.cp.lossy && a.cp.pow2 && d.L >= SUB && d.L <= (1ull << 31);
-            if (stream_level && elementwise && (fm_lvl == FM_LOCAL || fm_lvl == FM_LOCAL_W) && !a.dump_x) {
+            if (persist) {
+                // the persistent kernel encoded and installed the slots; what it left (d.redo) is
+                // re-encoded here and goes through the staged commit
+                a.redo_only = d.redo;
+            } else if (stream_level && elementwise && (fm_lvl == FM_LOCAL || fm_lvl == FM_LOCAL_W) && !a.dump_x) {
                 FusedArgs as = a;
                 if (p.kind <= 1) as.diag = p.pair ? 2 : 1;
                 as.X = d.X;  // (scratch of the sum's serial head: min(512, L) doubles per slot)
@@ -2125,13 +2225,15 @@ static int handle_suspend(qcs_dev_state* st, int64_t* gate, uint64_t* unit, int6
     sc.err = 0;
     sc.err_gate = -1;
     sc.susp_unit = 0;
+    sc.persist_susp = 0;
     CU(cudaMemcpy(st->d.sc, &sc, sizeof sc, cudaMemcpyHostToDevice));
     *st->h_sc = sc;
     if (*gate == prev_gate && *unit == prev_unit) {
-        if (*unit > 0) st->poisoned = true;
-        return set_err(QCS_E_NOMEM, *unit ? "gate %lld failed: block arena exhausted after %llu of its units were committed"
-                                          : "gate %lld failed: block arena exhausted",
-                       (long long)*gate, (unsigned long long)*unit);
+        const uint64_t done = *unit & ~SUSP_PERSIST;  // waves' units, or strides of the persistent kernel
+        if (done > 0) st->poisoned = true;
+        return set_err(QCS_E_NOMEM, done ? "gate %lld failed: block arena exhausted after %llu of its units were committed"
+                                         : "gate %lld failed: block arena exhausted",
+                       (long long)*gate, (unsigned long long)done);
     }
     return compact_arena(st);
 }
@@ -2252,7 +2354,7 @@ int qcs_run_program(qcs_dev_state_t st, const qcs_gate_desc* gates, uint64_t n_g
         if (!susp || rc) {
             done = susp ? ran - 1 : ran;
             if (susp) {  // an enqueue error after a suspension: no resume
-                if (st->h_sc->susp_unit > 0) st->poisoned = true;
+                if ((st->h_sc->susp_unit & ~SUSP_PERSIST) > 0) st->poisoned = true;
                 Dev::Scal sc = *st->h_sc;
                 sc.err = 0;
                 sc.err_gate = -1;

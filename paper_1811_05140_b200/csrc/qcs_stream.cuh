@@ -191,6 +191,14 @@ struct StreamCommit {
     const int* direct;             // null: never
     unsigned long long* wave_used; // bytes taken from the wave's block
     const uint64_t* bump;          // arena fill before the wave
+    // persistent kernel (k_stream_persist): no wave, every stride takes its bytes from the
+    // arena's bump itself; a stride that does not fit suspends the gate (the slots installed
+    // so far stay, `committed`; the host compacts and the gate resumes with the others)
+    unsigned long long* bump_rw;   // non-null: persistent mode
+    uint64_t arena_cap;
+    int* err_rw;
+    int* persist_susp;             // set with the error word: the suspension is this kernel's
+    unsigned long long* persist_done;
     uint8_t* arena;
     SideEntry* side;               // the block store's side index [2NS][nsub]
     uint64_t* p_off;
@@ -224,9 +232,31 @@ __device__ __forceinline__ void stream_commit(const FusedArgs& a, const StreamCo
                                               int tid, int nt)
 {
     const uint64_t r0 = (len0 + 15) & ~uint64_t(15), r1 = (len1 + 15) & ~uint64_t(15);
-    if (tid == 0) *sh_off = (uint64_t)atomicAdd(dc.wave_used, (unsigned long long)(r0 + r1));
-    __syncthreads();
-    const uint64_t at = *dc.bump + *sh_off;
+    uint64_t at;
+    if (dc.bump_rw) {
+        if (tid == 0) {
+            const unsigned long long need = (unsigned long long)(r0 + r1);
+            unsigned long long off = atomicAdd(dc.bump_rw, need);
+            if (off + need > dc.arena_cap) {
+                // arena full: suspend the gate.  (The bump stays where it is — taking the bytes back
+                // could pull it under a block another CTA placed meanwhile; the compaction that
+                // follows recomputes it from the live blocks.)
+                *dc.persist_susp = 1;
+                __threadfence();
+                atomicCAS(dc.err_rw, 0, 99 /* QCS_SUSPEND */);
+                off = ~0ull;
+                dc.committed[gslot] = 0;
+            }
+            *sh_off = (uint64_t)off;
+        }
+        __syncthreads();
+        if (*sh_off == ~uint64_t(0)) return;
+        at = *sh_off;
+    } else {
+        if (tid == 0) *sh_off = (uint64_t)atomicAdd(dc.wave_used, (unsigned long long)(r0 + r1));
+        __syncthreads();
+        at = *dc.bump + *sh_off;
+    }
     stream_copy16(reinterpret_cast<uint4*>(dc.arena + at), reinterpret_cast<const uint4*>(a.out + (2 * slot) * a.cap), r0 / 16, tid, nt);
     stream_copy16(reinterpret_cast<uint4*>(dc.arena + at + r0), reinterpret_cast<const uint4*>(a.out + (2 * slot + 1) * a.cap),
                   r1 / 16, tid, nt);
@@ -245,6 +275,7 @@ __device__ __forceinline__ void stream_commit(const FusedArgs& a, const StreamCo
         dc.sum_sq[j] = sumsq;
         dc.scale[j] = 1.0;
         dc.committed[gslot] = 1;
+        if (dc.persist_done) atomicAdd(dc.persist_done, 1ull);
     }
 }
 
@@ -284,20 +315,19 @@ constexpr uint64_t ST_SAT = 1ull << 62;
 // RAW: the planes were decoded, gated and snapped into a.X by the split path
 // (k_decode_gate) or are the caller's (a load): the walk reads them there and
 // only quantizes, emits and sums.
+// One slot: `slot` is the CTA's staging slot (out / side / X scratch), `gslot` the
+// gate's slot (tables, flags).  The mbarriers are initialised by the kernel;
+// stage_phase carries their parity from slot to slot.
 template <int ST_LANES, bool RAW>
-__global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a, uint8_t* redo, StreamCommit dc)
+__device__ __forceinline__ void stream_slot(const FusedArgs& a, uint8_t* redo, const StreamCommit& dc, const uint64_t slot,
+                                            const uint64_t gslot, unsigned (&stage_phase)[2])
 {
     using StreamShared = StreamSharedT<ST_LANES>;
     constexpr int ST_WARPS = StreamShared::ST_WARPS;
     constexpr int ST_STAGE = StreamShared::ST_STAGE;
     constexpr int ST_ITER = ST_LANES * SUB;  // elements per plane per iteration
-    if (a.err && *a.err) return;
-    const int b = a.order ? (int)(a.order[a.slot_base + blockIdx.x] - a.slot_base) : (int)blockIdx.x;
-    const uint64_t slot = (uint64_t)b;
-    const uint64_t gslot = a.slot_base + slot;
-    if (a.pending && !a.pending[gslot]) return;
     const int tid = threadIdx.x, wl = tid & 31, wp = tid >> 5;
-    const bool direct = dc.direct && *dc.direct;  // (uniform; the pool layout never sets it)
+    const bool direct = dc.bump_rw || (dc.direct && *dc.direct);  // (uniform; the pool layout never sets it)
     if (a.zero_slot && a.zero_slot[gslot]) {
         if (direct) {
             // a zero stride already stored as this level's zero encodings (one run token per plane,
@@ -315,6 +345,7 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
                     dc.sum_sq[j] = 0.0;
                     dc.scale[j] = 1.0;
                     dc.committed[gslot] = 1;
+                    if (dc.persist_done) atomicAdd(dc.persist_done, 1ull);
                 }
                 return;
             }
@@ -380,15 +411,13 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
     // side and control are constant over a lane's 32 elements when their bits are >= 5
     const bool gate_const = kind <= 1 && (fixed_side >= 0 || a.t >= 5) && (a.local_ctl < 0 || a.local_ctl >= 5);
 
+    __syncthreads();  // (a persistent CTA: the previous slot's readers of S are done)
     if (tid == 0) {
         S.out_pos[0] = S.out_pos[1] = 0;
         S.run_start[0] = S.run_start[1] = 0;
         S.m_carry[0] = S.m_carry[1] = 0;
         S.s = 0.0;
-        mbar_init(&S.bar[0], 1);
-        mbar_init(&S.bar[1], 1);
     }
-    unsigned stage_phase[2] = {0, 0};
     bool bail = false;  // uniform over the CTA
     int why = 0;        // why the slot was left (counters[19 + why]): 0 input not staged, 1 unproven step, 2 first element, 3 sum head, 4 sum event
     __syncthreads();
@@ -1073,6 +1102,54 @@ __global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a
             if (a.sumsq) a.sumsq[gslot] = S.s;
             if (a.counters) atomicAdd(&a.counters[18], 1ull);
         }
+    }
+}
+
+// one CTA per slot of the launch (a wave, or the whole gate in the small layout)
+template <int ST_LANES, bool RAW>
+__global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream(FusedArgs a, uint8_t* redo, StreamCommit dc)
+{
+    if (a.err && *a.err) return;
+    const int b = a.order ? (int)(a.order[a.slot_base + blockIdx.x] - a.slot_base) : (int)blockIdx.x;
+    const uint64_t gslot = a.slot_base + (uint64_t)b;
+    if (a.pending && !a.pending[gslot]) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    StreamSharedT<ST_LANES>& S = *reinterpret_cast<StreamSharedT<ST_LANES>*>(smem);
+    if (threadIdx.x == 0) {
+        mbar_init(&S.bar[0], 1);
+        mbar_init(&S.bar[1], 1);
+    }
+    unsigned stage_phase[2] = {0, 0};
+    stream_slot<ST_LANES, RAW>(a, redo, dc, (uint64_t)b, gslot, stage_phase);
+}
+
+// Persistent form (wave layout, single-level ladder): as many CTAs as staging
+// slots, each taking the gate's slots one after the other from a queue — no
+// waves, no kernel boundary between them, and the CTAs' end-of-stride copies
+// fall at different times.  A CTA's staging slot is its own (blockIdx.x): free
+// again once its stride is installed.  Slots already installed (a resumed
+// gate) are skipped.
+template <int ST_LANES>
+__global__ void __launch_bounds__(ST_LANES, 512 / ST_LANES) k_stream_persist(FusedArgs a, uint8_t* redo, StreamCommit dc,
+                                                                             uint64_t n_slots, unsigned long long* q_head)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    StreamSharedT<ST_LANES>& S = *reinterpret_cast<StreamSharedT<ST_LANES>*>(smem);
+    __shared__ unsigned long long s_idx;
+    if (threadIdx.x == 0) {
+        mbar_init(&S.bar[0], 1);
+        mbar_init(&S.bar[1], 1);
+    }
+    unsigned stage_phase[2] = {0, 0};
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_idx = (a.err && *reinterpret_cast<const volatile int*>(a.err)) ? ~0ull : atomicAdd(q_head, 1ull);
+        __syncthreads();
+        const unsigned long long idx = s_idx;
+        if (idx >= n_slots) break;
+        const uint64_t gslot = a.order ? (uint64_t)a.order[idx] : (uint64_t)idx;
+        if ((a.pending && !a.pending[gslot]) || dc.committed[gslot]) continue;
+        stream_slot<ST_LANES, false>(a, redo, dc, (uint64_t)blockIdx.x, gslot, stage_phase);
     }
 }
 

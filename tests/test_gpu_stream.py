@@ -112,3 +112,40 @@ def test_stream_default_threshold_of_slots(oracle, monkeypatch):
     n, s = 14, 6
     ctr = _check(oracle, _diag_program(random.Random(13), n, 24), s, 99, [cc.pow2_bound(1e-3, n)], 1.0)
     assert ctr["stream_slots"] > 0
+
+
+def test_stream_persistent_kernel_suspends_and_resumes(oracle, monkeypatch):
+    # wave layout, single-level ladder: the persistent kernel installs the strides itself; an arena
+    # of about 1.5x the dense compressed state fills inside gates, which suspend, compact and resume
+    # with the slots not installed yet
+    monkeypatch.setenv("QCS_FORCE_BIG", "1")
+    monkeypatch.setenv("QCS_WAVE_SLOTS", "8")
+    n, s = 13, 7
+    monkeypatch.setenv("QCS_ARENA_BYTES", str(int(1.5 * 4.5 * (1 << n))))
+    ctr = _check(oracle, _diag_program(random.Random(17), n, 30), s, 321, [cc.pow2_bound(1e-3, n)], 1.0)
+    assert ctr["stream_slots"] > 0
+    assert ctr["compactions"] > 0
+
+
+def test_stream_persistent_kernel_reports_nomem(oracle, monkeypatch):
+    import paper_1811_05140_b200 as q
+    monkeypatch.setenv("QCS_FORCE_BIG", "1")
+    monkeypatch.setenv("QCS_WAVE_SLOTS", "8")
+    n, s = 13, 7
+    monkeypatch.setenv("QCS_ARENA_BYTES", str(3 * (1 << n)))  # less than the dense state at ~4.5 B per amplitude
+    with pytest.raises(RuntimeError) as ei:
+        gpu_run(_diag_program(random.Random(17), n, 30), s, 321, [cc.pow2_bound(1e-3, n)], 1.0)
+    assert "block arena exhausted" in str(ei.value)
+
+
+def test_stream_persistent_kernel_behind_a_precheck_suspension(oracle, monkeypatch):
+    # an arena large enough for the pre-gate check to act (it keeps 1 MiB of slack): gates queued in
+    # one pass suspend at unit 0 before the persistent kernel starts, compact and start over — the
+    # installed flags of the gate before must not leak into the restarted one
+    monkeypatch.setenv("QCS_FORCE_BIG", "1")
+    monkeypatch.setenv("QCS_WAVE_SLOTS", "64")
+    n, s = 17, 8
+    monkeypatch.setenv("QCS_ARENA_BYTES", str(int(2.5 * (1 << 20))))
+    ctr = _check(oracle, _diag_program(random.Random(23), n, 16), s, 4321, [cc.pow2_bound(1e-3, n)], 1.0)
+    assert ctr["stream_slots"] > 0
+    assert ctr["compactions"] > 0
