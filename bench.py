@@ -872,7 +872,8 @@ def run_c3(args, rank, world, local_rank):
         if tj.get("traffic_per_algorithmic_byte"):
             traffic = tj["traffic_per_algorithmic_byte"] * (cin + cout) / max(1, n_f)
     tot_all = max(1.0, sum(v[0] for v in kt_all.values()))
-    roofline = {"bound": "hbm", "kernel": "k_stream" if streamed else "k_fused",
+    # (wave layout, single-level ladder: the persistent form of the streaming kernel)
+    roofline = {"bound": "hbm", "kernel": ("k_stream_persist" if ctr["wave_slots"] else "k_stream") if streamed else "k_fused",
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "traffic_source": (f"ncu --set full of the encoder on the C3 shape at n = 28 (tools/profile_c3.py, "
@@ -881,9 +882,9 @@ def run_c3(args, rank, world, local_rank):
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": (cin + cout) / max(1, n_f),
                 "algorithmic_bytes": "C_in + C_out of the gates' rewritten strides, 29-byte headers included "
-                                     "(SURVEY.md §8d), over the encoder launches of the timed steps (one per wave: "
-                                     "the streaming kernel k_stream, then the legacy encoder k_fused for the slots "
-                                     "it left, timed together)",
+                                     "(SURVEY.md §8d), over the encoder launches of the timed steps (per gate one "
+                                     "persistent launch of the streaming kernel, then per wave the legacy encoder k_fused "
+                                     "for the slots it left, timed together)",
                 "encoder_slots": {"streamed": ctr.get("stream_slots", 0),
                                   "left_to_legacy_encoder": ctr.get("stream_left_slots", 0)},
                 "avg_launch_us": t_f / max(1, n_f) / 1e3,
