@@ -150,6 +150,8 @@ struct Dev {
     uint8_t* zero_slot;    // [NS] per slot: output stride provably all zero (zero-stride pass)
     uint8_t* redo;         // [NS] per slot: the streaming kernel left it to the legacy encoder
     uint8_t* committed;    // [NS] per slot: its encoder CTA installed it (wave layout, StreamCommit)
+    uint64_t* p_cap;       // [2NS] capacity of a block placed by the persistent kernel, valid while
+    uint64_t* p_capoff;    // [2NS] ... p_off still is the offset it was placed at (qcs_stream.cuh)
     uint32_t* order;       // [NS] dense-first slot order within each wave (k_slot_order)
     int64_t* slot_of;      // [NS] generation<<32 | slot
     qcs_stride_report* reports;  // [NS]
@@ -1501,6 +1503,7 @@ int compact_arena_impl(qcs_dev_state* st)
     int rc = flush();
     if (rc) return rc;
     CU(cudaMemcpy(d.p_off, nof.data(), 8 * np, cudaMemcpyHostToDevice));
+    CU(cudaMemset(d.p_capoff, 0xff, 8 * np));  // packed by length: no block keeps its slack
     st->bump = at;
     CU(cudaMemcpy(&d.sc->bump, &st->bump, 8, cudaMemcpyHostToDevice));
     ++st->compactions;
@@ -1790,6 +1793,8 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         dc.err_rw = &d.sc->err;
         dc.persist_done = &d.sc->persist_done;
         dc.persist_susp = &d.sc->persist_susp;
+        dc.p_cap = d.p_cap;
+        dc.p_capoff = d.p_capoff;
         dc.arena = d.arena[0];
         dc.side = d.side;
         dc.p_off = d.p_off;
@@ -2096,6 +2101,9 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     TRY(dalloc(st, &d.zero_slot, d.NS));
     TRY(dalloc(st, &d.redo, d.NS));
     TRY(dalloc(st, &d.committed, d.NS));
+    TRY(dalloc(st, &d.p_cap, 2 * d.NS));
+    TRY(dalloc(st, &d.p_capoff, 2 * d.NS));
+    CU(cudaMemset(d.p_capoff, 0xff, 16 * d.NS));
     TRY(dalloc(st, &d.order, d.NS));
     TRY(dalloc(st, &d.slot_of, d.NS));
     TRY(dalloc(st, &d.reports, d.NS));

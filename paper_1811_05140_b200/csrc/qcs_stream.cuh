@@ -199,6 +199,14 @@ struct StreamCommit {
     int* err_rw;
     int* persist_susp;             // set with the error word: the suspension is this kernel's
     unsigned long long* persist_done;
+    // block capacities: a block this kernel places gets a little slack (1/256 + 64 bytes); the
+    // stride's next encoding goes over it in place when both planes fit — by then the CTA has read
+    // the old blocks to their end and nobody else reads them — so a state whose strides keep
+    // their size needs no new arena bytes and no compaction.  p_capoff[g] is the offset p_cap[g]
+    // belongs to: any other installer (staged commit, import, compaction) moves p_off and so
+    // invalidates the capacity.
+    uint64_t* p_cap;
+    uint64_t* p_capoff;
     uint8_t* arena;
     SideEntry* side;               // the block store's side index [2NS][nsub]
     uint64_t* p_off;
@@ -232,10 +240,28 @@ __device__ __forceinline__ void stream_commit(const FusedArgs& a, const StreamCo
                                               int tid, int nt)
 {
     const uint64_t r0 = (len0 + 15) & ~uint64_t(15), r1 = (len1 + 15) & ~uint64_t(15);
-    uint64_t at;
+    uint64_t at, at1;
+    bool fresh = true;
+    uint64_t c0 = r0, c1 = r1;  // capacities of freshly placed blocks
     if (dc.bump_rw) {
+        __shared__ uint64_t sh_at1;
+        __shared__ int sh_fresh;
+        c0 = (r0 + (r0 >> 8) + 64 + 15) & ~uint64_t(15);
+        c1 = (r1 + (r1 >> 8) + 64 + 15) & ~uint64_t(15);
         if (tid == 0) {
-            const unsigned long long need = (unsigned long long)(r0 + r1);
+            const uint64_t g0 = 2 * j, g1 = 2 * j + 1;
+            const bool reuse = dc.p_capoff[g0] == dc.p_off[g0] && dc.p_capoff[g1] == dc.p_off[g1] && r0 <= dc.p_cap[g0] &&
+                               r1 <= dc.p_cap[g1];
+            sh_fresh = reuse ? 0 : 1;
+            if (reuse) {
+                *sh_off = dc.p_off[g0];
+                sh_at1 = dc.p_off[g1];
+            }
+        }
+        __syncthreads();
+        fresh = sh_fresh != 0;
+        if (tid == 0 && fresh) {
+            const unsigned long long need = (unsigned long long)(c0 + c1);
             unsigned long long off = atomicAdd(dc.bump_rw, need);
             if (off + need > dc.arena_cap) {
                 // arena full: suspend the gate.  (The bump stays where it is — taking the bytes back
@@ -248,17 +274,20 @@ __device__ __forceinline__ void stream_commit(const FusedArgs& a, const StreamCo
                 dc.committed[gslot] = 0;
             }
             *sh_off = (uint64_t)off;
+            sh_at1 = (uint64_t)off + c0;
         }
         __syncthreads();
         if (*sh_off == ~uint64_t(0)) return;
         at = *sh_off;
+        at1 = sh_at1;
     } else {
         if (tid == 0) *sh_off = (uint64_t)atomicAdd(dc.wave_used, (unsigned long long)(r0 + r1));
         __syncthreads();
         at = *dc.bump + *sh_off;
+        at1 = at + r0;
     }
     stream_copy16(reinterpret_cast<uint4*>(dc.arena + at), reinterpret_cast<const uint4*>(a.out + (2 * slot) * a.cap), r0 / 16, tid, nt);
-    stream_copy16(reinterpret_cast<uint4*>(dc.arena + at + r0), reinterpret_cast<const uint4*>(a.out + (2 * slot + 1) * a.cap),
+    stream_copy16(reinterpret_cast<uint4*>(dc.arena + at1), reinterpret_cast<const uint4*>(a.out + (2 * slot + 1) * a.cap),
                   r1 / 16, tid, nt);
     stream_copy16(reinterpret_cast<uint4*>(dc.side + (2 * j) * a.nsub), reinterpret_cast<const uint4*>(a.side + (2 * slot) * a.nsub),
                   a.nsub, tid, nt);
@@ -267,7 +296,13 @@ __device__ __forceinline__ void stream_commit(const FusedArgs& a, const StreamCo
     if (tid == 0) {
         atomicAdd(dc.gate_cin, (unsigned long long)(2 * HEADER_BYTES + dc.p_len[2 * j] + dc.p_len[2 * j + 1]));
         dc.p_off[2 * j] = at;
-        dc.p_off[2 * j + 1] = at + r0;
+        dc.p_off[2 * j + 1] = at1;
+        if (dc.bump_rw && fresh) {
+            dc.p_cap[2 * j] = c0;
+            dc.p_cap[2 * j + 1] = c1;
+            dc.p_capoff[2 * j] = at;
+            dc.p_capoff[2 * j + 1] = at1;
+        }
         dc.p_len[2 * j] = len0;
         dc.p_len[2 * j + 1] = len1;
         dc.p_codec[2 * j] = dc.p_codec[2 * j + 1] = 1;

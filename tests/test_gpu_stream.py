@@ -149,3 +149,42 @@ def test_stream_persistent_kernel_behind_a_precheck_suspension(oracle, monkeypat
     ctr = _check(oracle, _diag_program(random.Random(23), n, 16), s, 4321, [cc.pow2_bound(1e-3, n)], 1.0)
     assert ctr["stream_slots"] > 0
     assert ctr["compactions"] > 0
+
+
+def test_stream_persistent_kernel_reuses_blocks_in_place(oracle, monkeypatch):
+    # wave layout: a block the persistent kernel placed has a little slack, and the stride's next
+    # encoding goes over it in place — a run of diagonal gates on a dense state must not grow the
+    # arena (no compaction), where each gate used to leave the whole state behind as garbage
+    import paper_1811_05140_b200 as q
+    from paper_1811_05140_b200 import metrics as mm
+    monkeypatch.setenv("QCS_FORCE_BIG", "1")
+    monkeypatch.setenv("QCS_WAVE_SLOTS", "16")
+    n, s = 16, 7  # (512 strides: pair-unit targets take the fused path also under a stride-bit control)
+    monkeypatch.setenv("QCS_ARENA_BYTES", str(int(3.2 * 4.5 * (1 << n))))
+    rng = random.Random(29)
+    U = cc.Unitary2x2
+    prog = cc.CircuitProgram(n, [], "reuse")
+    for t in range(n):
+        prog.gates.append(cc.GateOp.single(U.hadamard(), t, f"h{t}"))
+        prog.gates.append(cc.GateOp.single(U.phase(0.1 + 0.3 * t), t, f"p{t}"))
+    n_prep = len(prog.gates)
+    diag = [U.t_gate(), U.s_gate(), U.pauli_z(), U.phase(0.37)]
+    for _ in range(40):
+        t = rng.randrange(n)
+        c = rng.randrange(n - 1)
+        c = c + 1 if c >= t else c
+        prog.gates.append(cc.GateOp.controlled(rng.choice(diag), c, t, f"c{c}t{t}") if rng.random() < 0.5
+                          else cc.GateOp.single(rng.choice(diag), t, f"d{t}"))
+    delta = cc.pow2_bound(1e-3, n)
+    st, want = oracle_run(oracle, prog, s, 77, [delta], 1.0)
+    lad, th = q.ErrorBoundLadder.make([delta]), q.RatioThreshold(1.0)
+    gst = q.CompressedState.basis_state(q.StateGeometry.make(n, s), 77)
+    m1 = q.apply_program_range(gst, prog, 0, n_prep + 2, lad, th)   # (two diagonal gates place the slack blocks)
+    c1 = gst.counters()["compactions"]
+    m2 = q.apply_program_range(gst, prog, n_prep + 2, len(prog.gates), lad, th)
+    assert gst.counters()["compactions"] == c1
+    got = mm.emit_csv(list(m1.records) + list(m2.records), with_elapsed=False)
+    assert got == want, first_diff(want, got)
+    assert gst.to_amplitudes().tobytes() == st.amplitudes().tobytes()
+    for j in range(1 << (n - s)):
+        assert gst.export_blocks(j)[0] == st.export_blocks(j), j
