@@ -103,6 +103,9 @@ __host__ __device__ inline uint64_t unit_lo(const Plan& p, uint64_t u)
 }
 
 __host__ __device__ inline uint64_t round16d(uint64_t x) { return (x + 15) & ~uint64_t(15); }
+// capacity of a freshly placed block of r (16-byte-rounded) bytes: 1/256 + 64 bytes of slack, so
+// that the stride's next encodings fit it in place (StreamCommit in qcs_stream.cuh uses the same)
+__host__ __device__ inline uint64_t slack16(uint64_t r) { return (r + (r >> 8) + 64 + 15) & ~uint64_t(15); }
 
 // job/slot s -> stride
 __host__ __device__ inline uint64_t slot_stride(const Plan& p, uint64_t s)
@@ -150,6 +153,7 @@ struct Dev {
     uint8_t* zero_slot;    // [NS] per slot: output stride provably all zero (zero-stride pass)
     uint8_t* redo;         // [NS] per slot: the streaming kernel left it to the legacy encoder
     uint8_t* committed;    // [NS] per slot: its encoder CTA installed it (wave layout, StreamCommit)
+    int inplace;           // blocks are rewritten in place when they fit (QCS_INPLACE=0 turns it off)
     uint64_t* p_cap;       // [2NS] capacity of a block placed by the persistent kernel, valid while
     uint64_t* p_capoff;    // [2NS] ... p_off still is the offset it was placed at (qcs_stream.cuh)
     uint32_t* order;       // [NS] dense-first slot order within each wave (k_slot_order)
@@ -1247,7 +1251,9 @@ __device__ __forceinline__ void cta_copy16(uint4* __restrict__ dst, const uint4*
 // (new_off), replace the side index, tables, scale and sum (the staged commit
 // of aalc.cpp:395-408, one wave at a time).
 constexpr int COPY_THREADS = 256;
-__global__ void __launch_bounds__(COPY_THREADS) k_wave_commit(Dev d, LevelTag lt, uint64_t s0, const uint8_t* committed)
+// slack: the offsets are k_wave_alloc's (new blocks carry slack16); 0: host-placed, exact size
+__global__ void __launch_bounds__(COPY_THREADS) k_wave_commit(Dev d, LevelTag lt, uint64_t s0, const uint8_t* committed,
+                                                             int slack)
 {
     if (d.sc->err) return;
     const uint64_t loc = blockIdx.x >> 1;
@@ -1267,6 +1273,10 @@ __global__ void __launch_bounds__(COPY_THREADS) k_wave_commit(Dev d, LevelTag lt
     cta_copy16(reinterpret_cast<uint4*>(ds), reinterpret_cast<const uint4*>(ss), d.nsub);
     if (threadIdx.x == 0) {
         atomicAdd((unsigned long long*)&d.sc->gate_cin, (unsigned long long)(HEADER_BYTES + d.p_len[g]));
+        if (dst_off != d.p_off[g]) {  // a new block (in place: offset and capacity stay)
+            d.p_cap[g] = slack ? slack16(round16d(len)) : round16d(len);
+            d.p_capoff[g] = dst_off;
+        }
         d.p_off[g] = dst_off;
         d.p_len[g] = len;
         d.p_codec[g] = lt.slot_codec[slot];
@@ -1295,9 +1305,17 @@ __global__ void __launch_bounds__(ALLOC_THREADS) k_wave_alloc(Dev d, uint64_t s0
     __shared__ int ok_sh;
     if (d.sc->err) return;
     const int tid = threadIdx.x, wl = tid & 31, w = tid >> 5;
+    // a plane whose new block fits the capacity of its current one (a block placed with slack,
+    // p_cap / p_capoff, qcs_stream.cuh) is rewritten in place: by the commit every read of this
+    // wave's inputs is over; any other gets a new block with slack
+    auto plane_of = [&](uint64_t i) -> uint64_t { return 2 * d.job_stride[s0 + i / 2] + (i & 1); };
+    auto in_place = [&](uint64_t i) -> bool {
+        const uint64_t g = plane_of(i);
+        return d.inplace && d.p_capoff[g] == d.p_off[g] && round16d(d.slot_len[2 * s0 + i]) <= d.p_cap[g];
+    };
     auto need_of = [&](uint64_t i) -> uint64_t {
-        if (i >= m2 || (committed && committed[s0 + i / 2])) return 0;
-        return round16d(d.slot_len[2 * s0 + i]);
+        if (i >= m2 || (committed && committed[s0 + i / 2]) || in_place(i)) return 0;
+        return slack16(round16d(d.slot_len[2 * s0 + i]));
     };
     if (committed && tid == 0 && d.sc->wave_direct) {
         d.sc->bump += d.sc->wave_used;
@@ -1342,7 +1360,9 @@ __global__ void __launch_bounds__(ALLOC_THREADS) k_wave_alloc(Dev d, uint64_t s0
             if (k < w) pre += wsum[k];
             tot += wsum[k];
         }
-        if (i < m2) d.new_off[2 * s0 + i] = carry + pre + inc - v;
+        if (i < m2) d.new_off[2 * s0 + i] = (v == 0 && !(committed && committed[s0 + i / 2]) && in_place(i))
+                                                ? d.p_off[plane_of(i)]
+                                                : carry + pre + inc - v;
         carry += tot;
     }
 }
@@ -1550,7 +1570,7 @@ int big_commit_wave(qcs_dev_state* st, uint64_t s0, uint64_t s1, uint64_t gate_i
     }
     CU(cudaMemcpyAsync(d.new_off + 2 * s0, nof.data(), 8 * m, cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(&d.sc->bump, &st->bump, 8, cudaMemcpyHostToDevice, s));
-    k_wave_commit<<<(unsigned)m, COPY_THREADS, 0, s>>>(d, st->lt, s0, nullptr);
+    k_wave_commit<<<(unsigned)m, COPY_THREADS, 0, s>>>(d, st->lt, s0, nullptr, 0);
     ++st->launches;
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(s));  // nof / bump are host locals
@@ -1793,7 +1813,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         dc.err_rw = &d.sc->err;
         dc.persist_done = &d.sc->persist_done;
         dc.persist_susp = &d.sc->persist_susp;
-        dc.p_cap = d.p_cap;
+        dc.p_cap = d.inplace ? d.p_cap : nullptr;
         dc.p_capoff = d.p_capoff;
         dc.arena = d.arena[0];
         dc.side = d.side;
@@ -1947,7 +1967,7 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
         if (st->big) {  // place (device bump) and install the wave: no host round trip
             prof_start(st, 3);
             k_wave_alloc<<<1, ALLOC_THREADS, 0, s>>>(d, s0, 2 * nw, u0, wave_direct ? d.committed : nullptr);
-            k_wave_commit<<<(unsigned)(2 * nw), COPY_THREADS, 0, s>>>(d, st->lt, s0, wave_direct ? d.committed : nullptr);
+            k_wave_commit<<<(unsigned)(2 * nw), COPY_THREADS, 0, s>>>(d, st->lt, s0, wave_direct ? d.committed : nullptr, 1);
             prof_stop(st);
             st->launches += 2;
         }
@@ -2104,6 +2124,8 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     TRY(dalloc(st, &d.p_cap, 2 * d.NS));
     TRY(dalloc(st, &d.p_capoff, 2 * d.NS));
     CU(cudaMemset(d.p_capoff, 0xff, 16 * d.NS));
+    d.inplace = 1;
+    if (const char* e = getenv("QCS_INPLACE")) d.inplace = atoi(e);
     TRY(dalloc(st, &d.order, d.NS));
     TRY(dalloc(st, &d.slot_of, d.NS));
     TRY(dalloc(st, &d.reports, d.NS));

@@ -246,12 +246,12 @@ __device__ __forceinline__ void stream_commit(const FusedArgs& a, const StreamCo
     if (dc.bump_rw) {
         __shared__ uint64_t sh_at1;
         __shared__ int sh_fresh;
-        c0 = (r0 + (r0 >> 8) + 64 + 15) & ~uint64_t(15);
+        c0 = (r0 + (r0 >> 8) + 64 + 15) & ~uint64_t(15);  // (slack16 of qcs_engine.cu)
         c1 = (r1 + (r1 >> 8) + 64 + 15) & ~uint64_t(15);
         if (tid == 0) {
             const uint64_t g0 = 2 * j, g1 = 2 * j + 1;
-            const bool reuse = dc.p_capoff[g0] == dc.p_off[g0] && dc.p_capoff[g1] == dc.p_off[g1] && r0 <= dc.p_cap[g0] &&
-                               r1 <= dc.p_cap[g1];
+            const bool reuse = dc.p_cap && dc.p_capoff[g0] == dc.p_off[g0] && dc.p_capoff[g1] == dc.p_off[g1] &&
+                               r0 <= dc.p_cap[g0] && r1 <= dc.p_cap[g1];
             sh_fresh = reuse ? 0 : 1;
             if (reuse) {
                 *sh_off = dc.p_off[g0];
@@ -297,7 +297,7 @@ __device__ __forceinline__ void stream_commit(const FusedArgs& a, const StreamCo
         atomicAdd(dc.gate_cin, (unsigned long long)(2 * HEADER_BYTES + dc.p_len[2 * j] + dc.p_len[2 * j + 1]));
         dc.p_off[2 * j] = at;
         dc.p_off[2 * j + 1] = at1;
-        if (dc.bump_rw && fresh) {
+        if (dc.bump_rw && fresh && dc.p_cap) {
             dc.p_cap[2 * j] = c0;
             dc.p_cap[2 * j + 1] = c1;
             dc.p_capoff[2 * j] = at;

@@ -120,6 +120,7 @@ def test_stream_persistent_kernel_suspends_and_resumes(oracle, monkeypatch):
     # with the slots not installed yet
     monkeypatch.setenv("QCS_FORCE_BIG", "1")
     monkeypatch.setenv("QCS_WAVE_SLOTS", "8")
+    monkeypatch.setenv("QCS_INPLACE", "0")  # (no in-place rewrite: the arena fills inside gates)
     n, s = 13, 7
     monkeypatch.setenv("QCS_ARENA_BYTES", str(int(1.5 * 4.5 * (1 << n))))
     ctr = _check(oracle, _diag_program(random.Random(17), n, 30), s, 321, [cc.pow2_bound(1e-3, n)], 1.0)
@@ -144,6 +145,7 @@ def test_stream_persistent_kernel_behind_a_precheck_suspension(oracle, monkeypat
     # installed flags of the gate before must not leak into the restarted one
     monkeypatch.setenv("QCS_FORCE_BIG", "1")
     monkeypatch.setenv("QCS_WAVE_SLOTS", "64")
+    monkeypatch.setenv("QCS_INPLACE", "0")  # (every gate leaves its old blocks behind: the arena does fill)
     n, s = 17, 8
     monkeypatch.setenv("QCS_ARENA_BYTES", str(int(2.5 * (1 << 20))))
     ctr = _check(oracle, _diag_program(random.Random(23), n, 16), s, 4321, [cc.pow2_bound(1e-3, n)], 1.0)
@@ -158,6 +160,7 @@ def test_stream_persistent_kernel_reuses_blocks_in_place(oracle, monkeypatch):
     import paper_1811_05140_b200 as q
     from paper_1811_05140_b200 import metrics as mm
     monkeypatch.setenv("QCS_FORCE_BIG", "1")
+    monkeypatch.setenv("QCS_INPLACE", "1")
     monkeypatch.setenv("QCS_WAVE_SLOTS", "16")
     n, s = 16, 7  # (512 strides: pair-unit targets take the fused path also under a stride-bit control)
     monkeypatch.setenv("QCS_ARENA_BYTES", str(int(3.2 * 4.5 * (1 << n))))

@@ -13,10 +13,14 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture
 def wave_env(monkeypatch):
-    def set_(wave, arena):
+    def set_(wave, arena, inplace="0"):
+        # (inplace 0: every rewritten stride gets a new block, so these small arenas fill, suspend
+        # and compact as they are meant to; test_wave_layout_in_place runs the same cases with the
+        # default in-place rewrite)
         monkeypatch.setenv("QCS_FORCE_BIG", "1")
         monkeypatch.setenv("QCS_WAVE_SLOTS", str(wave))
         monkeypatch.setenv("QCS_ARENA_BYTES", str(arena))
+        monkeypatch.setenv("QCS_INPLACE", inplace)
     return set_
 
 
@@ -53,6 +57,19 @@ def test_wave_layout_matches_oracle(oracle, wave_env, kind, n, s, basis, ladder,
     c = res.state.counters()
     w = max(min(wave, 1 << (n - s)), min(1 << (n - s), 2))
     assert c["wave_slots"] == (w - 1 if w > 1 and w & 1 else w)
+    for j in range(1 << (n - s)):
+        assert res.state.export_blocks(j)[0] == st.export_blocks(j)
+
+
+@pytest.mark.parametrize("kind,n,s,basis,ladder,theta,wave,arena", CASES)
+def test_wave_layout_in_place(oracle, wave_env, kind, n, s, basis, ladder, theta, wave, arena):
+    # blocks rewritten in place when they fit (the default): same results, every path
+    wave_env(wave, arena, inplace="1")
+    prog = _prog(kind, n)
+    st, want = oracle_run(oracle, prog, s, basis, ladder, theta)
+    res, got = gpu_run(prog, s, basis, ladder, theta)
+    assert got == want, first_diff(want, got)
+    assert res.state.to_amplitudes().tobytes() == st.amplitudes().tobytes()
     for j in range(1 << (n - s)):
         assert res.state.export_blocks(j)[0] == st.export_blocks(j)
 
