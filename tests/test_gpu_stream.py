@@ -118,6 +118,7 @@ def test_stream_persistent_kernel_suspends_and_resumes(oracle, monkeypatch):
     # wave layout, single-level ladder: the persistent kernel installs the strides itself; an arena
     # of about 1.5x the dense compressed state fills inside gates, which suspend, compact and resume
     # with the slots not installed yet
+    monkeypatch.setenv("QCS_STREAM_PERSIST", "1")
     monkeypatch.setenv("QCS_FORCE_BIG", "1")
     monkeypatch.setenv("QCS_WAVE_SLOTS", "8")
     monkeypatch.setenv("QCS_INPLACE", "0")  # (no in-place rewrite: the arena fills inside gates)
@@ -129,6 +130,7 @@ def test_stream_persistent_kernel_suspends_and_resumes(oracle, monkeypatch):
 
 
 def test_stream_persistent_kernel_reports_nomem(oracle, monkeypatch):
+    monkeypatch.setenv("QCS_STREAM_PERSIST", "1")
     import paper_1811_05140_b200 as q
     monkeypatch.setenv("QCS_FORCE_BIG", "1")
     monkeypatch.setenv("QCS_WAVE_SLOTS", "8")
@@ -143,6 +145,7 @@ def test_stream_persistent_kernel_behind_a_precheck_suspension(oracle, monkeypat
     # an arena large enough for the pre-gate check to act (it keeps 1 MiB of slack): gates queued in
     # one pass suspend at unit 0 before the persistent kernel starts, compact and start over — the
     # installed flags of the gate before must not leak into the restarted one
+    monkeypatch.setenv("QCS_STREAM_PERSIST", "1")
     monkeypatch.setenv("QCS_FORCE_BIG", "1")
     monkeypatch.setenv("QCS_WAVE_SLOTS", "64")
     monkeypatch.setenv("QCS_INPLACE", "0")  # (every gate leaves its old blocks behind: the arena does fill)
@@ -157,6 +160,7 @@ def test_stream_persistent_kernel_reuses_blocks_in_place(oracle, monkeypatch):
     # wave layout: a block the persistent kernel placed has a little slack, and the stride's next
     # encoding goes over it in place — a run of diagonal gates on a dense state must not grow the
     # arena (no compaction), where each gate used to leave the whole state behind as garbage
+    monkeypatch.setenv("QCS_STREAM_PERSIST", "1")
     import paper_1811_05140_b200 as q
     from paper_1811_05140_b200 import metrics as mm
     monkeypatch.setenv("QCS_FORCE_BIG", "1")
