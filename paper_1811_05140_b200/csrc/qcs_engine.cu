@@ -1034,6 +1034,8 @@ struct qcs_dev_state {
     // it off): codes/predictor scratch for `chain_levels` ladder levels
     int serial_chain = 1;
     int imz = 1;  // zero-imaginary-plane mode (QCS_IMZ=0 turns it off)
+    int stream_commit = 1;   // wave layout: the streaming kernel's CTAs install their strides (QCS_STREAM_COMMIT=0: staged)
+    int stream_persist = 1;  // ... from one persistent launch per gate (QCS_STREAM_PERSIST=0: a launch per wave)
     int stream_mode = 1;  // streaming kernel for element-wise gates (QCS_STREAM=0 turns it off; bit 2: also as the split path's encoder)
     int diag_local = 1;  // diagonal far/pair gates in the fused kernel (QCS_DIAG_LOCAL=0: split path)
     int zero_pass = 1;   // zero strides skip the codec (QCS_ZERO_PASS=0 turns it off)
@@ -1792,15 +1794,13 @@ int enqueue_gate(qcs_dev_state* st, const qcs_gate_desc* g, const double* lad, i
     };
     // wave layout, single-level ladder, streaming kernel: the encoder CTAs install their strides
     // (QCS_STREAM_COMMIT=0: always the staged commit)
-    static const bool commit_env = !(getenv("QCS_STREAM_COMMIT") && atoi(getenv("QCS_STREAM_COMMIT")) == 0);
-    const bool wave_direct = commit_env && st->big && nl == 1 && !x_ext && !chain && st->stream_mode &&
+    const bool wave_direct = st->stream_commit && st->big && nl == 1 && !x_ext && !chain && st->stream_mode &&
                              ((p.kind <= 1 && diag_gate) || p.kind == 2 || p.kind == 3) &&
                              (fm_lvl == FM_LOCAL || fm_lvl == FM_LOCAL_W) && make_params(lad[0]).lossy &&
                              make_params(lad[0]).pow2 && d.L >= SUB && d.L <= (1ull << 31);
     // ... and from one persistent kernel over the whole gate instead of a launch per wave
     // (QCS_STREAM_PERSIST=0: waves)
-    static const bool persist_env = !(getenv("QCS_STREAM_PERSIST") && atoi(getenv("QCS_STREAM_PERSIST")) == 0);
-    const bool persist = wave_direct && persist_env;
+    const bool persist = wave_direct && st->stream_persist;
     if (persist) {
         FusedArgs as = fused_args(lad[0], 0);
         as.diag = p.kind <= 1 ? (p.pair ? 2 : 1) : 0;
@@ -2028,6 +2028,8 @@ int qcs_state_create(int n, int s, uint64_t basis, int device, qcs_dev_state_t* 
     if (const char* e = getenv("QCS_SERIAL_CHAIN")) st->serial_chain = atoi(e);
     if (const char* e = getenv("QCS_IMZ")) st->imz = atoi(e);
     if (const char* e = getenv("QCS_STREAM")) st->stream_mode = atoi(e);
+    if (const char* e = getenv("QCS_STREAM_COMMIT")) st->stream_commit = atoi(e);
+    if (const char* e = getenv("QCS_STREAM_PERSIST")) st->stream_persist = atoi(e);
     if (const char* e = getenv("QCS_DIAG_LOCAL")) st->diag_local = atoi(e);
     if (const char* e = getenv("QCS_ZERO_PASS")) st->zero_pass = atoi(e);
     if (const char* e = getenv("QCS_LADDER_EXIT")) st->ladder_exit = atoi(e);
